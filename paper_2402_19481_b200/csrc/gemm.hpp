@@ -1,0 +1,94 @@
+// Host interface of the sm_100a tcgen05 GEMM / implicit-GEMM conv kernel.
+//
+// One persistent, warp-specialised kernel serves every tensor-core op on the
+// hot path:
+//   * conv2d_region  (proj/src/tensor.cpp:79-130)  -> implicit GEMM, A operand
+//     gathered by 5-D TMA boxes straight out of the halo-padded NHWC band,
+//     M = output pixels, N = C_out, K = 9 * C_in (tap-major, channel-minor);
+//   * linear         (proj/src/tensor.cpp:139-161) -> plain GEMM;
+//   * attention      (proj/src/tensor.cpp:163-199) -> S = Q K^T and O = P V^T.
+// Operands are staged by TMA into 128B-swizzled shared memory, multiplied by
+// tcgen05.mma (kind::f16 for bf16, kind::tf32 for the fp32 mode) into a
+// double-buffered TMEM accumulator, and drained by four epilogue warps that
+// add bias / residual and store NHWC rows (or fp32 split-K partials).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace pp {
+
+enum class Elem : int { BF16 = 0, F32 = 1 };  // F32: fp32 storage, TF32 tensor-core multiply
+
+inline size_t elem_bytes(Elem e) { return e == Elem::BF16 ? 2 : 4; }
+
+struct GemmArgs {
+    int mode;                 // 0 = plain row-major A (2-D map), 1 = conv stride 1, 2 = conv stride 2
+    int rows_box, w_box;      // conv: output rows / cols covered by one 128-row M tile
+    int tiles_y, tiles_x;     // M-tile grid (plain: tiles_y = ceil(M/128), tiles_x = 1)
+    int out_rows, out_w;      // valid output extent in pixels (plain: M, 1)
+    int n_tiles, block_n;     // N tiling (block_n % 16 == 0, <= 256)
+    int cin_chunks;           // conv: channel chunks of 128 B per tap; plain: k_blocks
+    int k_blocks;             // total 128-byte K blocks
+    int splits, kb_per_split; // split-K
+    int stages;               // smem pipeline depth
+    uint32_t idesc;           // tcgen05 instruction descriptor
+    // epilogue
+    void* out;                // output base (already offset to pixel 0 of the band)
+    long long out_ld;         // elements between consecutive output pixels / rows
+    int n_valid;              // columns actually stored
+    int out_f32;              // 1: fp32 output, 0: bf16 (bf16 mode) ; fp32 mode always fp32
+    int round_tf32;           // fp32 mode: round stored values to tf32 (they feed another GEMM)
+    const float* bias;        // [n] or null
+    const void* residual;     // same element type/layout as out (ld = res_ld) or null
+    long long res_ld;
+    float* partial;           // split-K workspace: [splits][m_pix][n_pad] fp32
+    int m_pix, n_pad;
+    float scale;              // multiplier applied to the accumulator before bias (1 = none)
+};
+
+struct GemmPlan {
+    CUtensorMap tmA;
+    CUtensorMap tmB;
+    GemmArgs a;
+    int grid = 0;
+    size_t smem = 0;
+    Elem elem = Elem::BF16;
+    // split-K reduce epilogue
+    bool needs_reduce = false;
+    double flops = 0;         // algorithmic 2*M*N*K of the layer (for rooflines)
+};
+
+struct EpilogueSpec {
+    void* out = nullptr;
+    long long out_ld = 0;
+    int n_valid = 0;
+    bool out_f32 = false;
+    bool round_tf32 = false;
+    const float* bias = nullptr;
+    const void* residual = nullptr;
+    long long res_ld = 0;
+    float scale = 1.0f;
+};
+
+// Conv over a halo-padded NHWC band: in = [rows_in + 2][W][C_in_pad] (row 0 = the halo
+// row above the band, row rows_in + 1 = the halo row below). weights = [n_pad][9][C_in_pad]
+// (K-major). Output pixel (oy, ox) of the band is stored at out + (oy*out_w + ox)*out_ld.
+void plan_conv(GemmPlan& p, Elem e, const void* in, int rows_in, int W, int C_in_pad, int stride,
+               const void* weights, int n_pad, const EpilogueSpec& ep, float* workspace,
+               size_t workspace_bytes, int num_sms, int force_splits = 0, int force_block_n = 0);
+
+// Plain GEMM: D[M][N] = A[M][K] * B[N][K]^T (both K-major, leading dims in elements).
+void plan_gemm(GemmPlan& p, Elem e, const void* A, int M, int K, long long lda, const void* B,
+               int N, long long ldb, const EpilogueSpec& ep, float* workspace,
+               size_t workspace_bytes, int num_sms, int force_splits = 0, int force_block_n = 0);
+
+void launch_gemm(const GemmPlan& p, cudaStream_t s);
+
+size_t gemm_workspace_bytes(const GemmPlan& p);
+
+int device_sm_count();
+
+}  // namespace pp

@@ -1,0 +1,579 @@
+// sm_100a tcgen05 GEMM / implicit-GEMM 3x3 conv (see gemm.hpp for the contract).
+//
+// Warp roles (192 threads, 1 CTA per SM, persistent over output tiles):
+//   warp 0      TMA producer (one lane): A box + B box per 128-byte K block
+//   warp 1      TMEM owner + MMA issuer (one lane): 4 x tcgen05.mma per K block
+//   warps 2..5  epilogue: tcgen05.ld -> bias/residual -> NHWC stores
+// Pipelines: smem ring (full/empty mbarriers, TMA <-> MMA) and a 2-deep TMEM
+// accumulator ring (tmem_full/tmem_empty, MMA <-> epilogue), so the epilogue of
+// tile i overlaps the main loop of tile i+1.
+#include "gemm.hpp"
+#include "ptx.cuh"
+#include "util.hpp"
+
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+namespace pp {
+
+namespace {
+
+constexpr int kThreads = 192;
+constexpr int kTileM = 128;
+constexpr int kBlockBytes = 128;   // K block = 128 bytes of each operand row
+constexpr int kTmemCols = 512;     // 2 accumulators x 256 columns
+constexpr int kSmemBudget = 232448 - 1024;
+
+__device__ __forceinline__ float round_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+struct TileCoord {
+    int ty, tx, nt, split;
+};
+
+__device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int t) {
+    TileCoord c;
+    c.split = t % a.splits;
+    int rest = t / a.splits;
+    c.nt = rest % a.n_tiles;
+    int m = rest / a.n_tiles;
+    c.tx = m % a.tiles_x;
+    c.ty = m / a.tiles_x;
+    return c;
+}
+
+template <bool kTF32>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const GemmArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-align the dynamic smem base (SWIZZLE_128B atoms are 1024 B).
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int stages = a.stages;
+    const uint32_t a_stage_bytes = kTileM * kBlockBytes;
+    const uint32_t b_stage_bytes = uint32_t(a.block_n) * kBlockBytes;
+    const uint32_t stage_bytes = a_stage_bytes + b_stage_bytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(stages) * stage_bytes);
+    uint64_t* full_bar = bars;
+    uint64_t* empty_bar = bars + stages;
+    uint64_t* tfull_bar = bars + 2 * stages;
+    uint64_t* tempty_bar = bars + 2 * stages + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 4);
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+        for (int s = 0; s < stages; ++s) {
+            ptx::mbar_init(&full_bar[s], 1);
+            ptx::mbar_init(&empty_bar[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            ptx::mbar_init(&tfull_bar[s], 1);
+            ptx::mbar_init(&tempty_bar[s], 4);
+        }
+        ptx::fence_barrier_init();
+        ptx::fence_proxy_async();
+    }
+    if (warp == 1) ptx::tmem_alloc(tmem_slot, kTmemCols);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int total_tiles = a.tiles_y * a.tiles_x * a.n_tiles * a.splits;
+    const int conv = a.mode != 0;
+    const int a_box_bytes = conv ? a.rows_box * a.w_box * kBlockBytes : a_stage_bytes;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ===== TMA producer =====
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+                const TileCoord tc = decode_tile(a, t);
+                const int kb0 = tc.split * a.kb_per_split;
+                const int kb1 = min(kb0 + a.kb_per_split, a.k_blocks);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+                    uint8_t* sa = smem + size_t(stage) * stage_bytes;
+                    uint8_t* sb = sa + a_stage_bytes;
+                    ptx::mbar_arrive_expect_tx(&full_bar[stage], a_box_bytes + b_stage_bytes);
+                    const int kel = kTF32 ? 32 : 64;  // elements per 128-byte K block
+                    if (!conv) {
+                        ptx::tma_load_2d(sa, &tmA, &full_bar[stage], kb * kel, tc.ty * kTileM);
+                    } else {
+                        const int tap = kb / a.cin_chunks;
+                        const int chunk = kb - tap * a.cin_chunks;
+                        const int ky = tap / 3, kx = tap - 3 * (tap / 3);
+                        const int oy0 = tc.ty * a.rows_box, ox0 = tc.tx * a.w_box;
+                        if (a.mode == 1) {
+                            ptx::tma_load_5d(sa, &tmA, &full_bar[stage], chunk * kel, 0,
+                                             ox0 + kx - 1, 0, oy0 + ky);
+                        } else {
+                            ptx::tma_load_5d(sa, &tmA, &full_bar[stage], chunk * kel,
+                                             kx == 1 ? 0 : 1, ox0 + (kx == 0 ? -1 : 0),
+                                             ky == 1 ? 1 : 0, oy0 + (ky == 2 ? 1 : 0));
+                        }
+                    }
+                    ptx::tma_load_2d(sb, &tmB, &full_bar[stage], kb * kel, tc.nt * a.block_n);
+                    if (++stage == stages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ===== MMA issuer =====
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+                const TileCoord tc = decode_tile(a, t);
+                const int kb0 = tc.split * a.kb_per_split;
+                const int kb1 = min(kb0 + a.kb_per_split, a.k_blocks);
+                ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + uint32_t(acc * 256);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    ptx::mbar_wait(&full_bar[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t sa = ptx::smem_u32(smem + size_t(stage) * stage_bytes);
+                    const uint32_t sb = sa + a_stage_bytes;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint64_t da = ptx::smem_desc_sw128(sa + k * 32);
+                        const uint64_t db = ptx::smem_desc_sw128(sb + k * 32);
+                        const uint32_t accum = (kb > kb0 || k > 0) ? 1u : 0u;
+                        if (kTF32)
+                            ptx::mma_tf32(d_tmem, da, db, a.idesc, accum);
+                        else
+                            ptx::mma_bf16(d_tmem, da, db, a.idesc, accum);
+                    }
+                    ptx::mma_commit(&empty_bar[stage]);
+                    if (++stage == stages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                ptx::mma_commit(&tfull_bar[acc]);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ===== epilogue (warps 2..5; TMEM lane quarter = warp % 4) =====
+        const int quarter = warp & 3;
+        const int r = quarter * 32 + lane;  // tile row owned by this thread
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+            const TileCoord tc = decode_tile(a, t);
+            long long p;
+            bool valid;
+            if (conv) {
+                const int ry = r / a.w_box, rx = r - ry * a.w_box;
+                const int oy = tc.ty * a.rows_box + ry, ox = tc.tx * a.w_box + rx;
+                valid = r < a.rows_box * a.w_box && oy < a.out_rows && ox < a.out_w;
+                p = (long long)oy * a.out_w + ox;
+            } else {
+                p = (long long)tc.ty * kTileM + r;
+                valid = p < a.out_rows;
+            }
+            ptx::mbar_wait(&tfull_bar[acc], acc_phase);
+            ptx::tc_fence_after();
+            const uint32_t t_row = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * 256);
+            const int nbase = tc.nt * a.block_n;
+            for (int c0 = 0; c0 < a.block_n; c0 += 16) {
+                float v[16];
+                ptx::tmem_ld16(t_row + c0, v);
+                const int n0 = nbase + c0;
+                if (!valid) continue;
+                if (a.splits > 1) {
+                    float* dst = a.partial + ((size_t)tc.split * a.m_pix + p) * a.n_pad + n0;
+#pragma unroll
+                    for (int j = 0; j < 16; j += 4)
+                        *reinterpret_cast<float4*>(dst + j) =
+                            make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                    continue;
+                }
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    float x = v[j] * a.scale;
+                    if (a.bias && n0 + j < a.n_valid) x += a.bias[n0 + j];
+                    v[j] = x;
+                }
+                const bool full = n0 + 16 <= a.n_valid;
+                if (kTF32 || a.out_f32) {
+                    float* dst = reinterpret_cast<float*>(a.out) + p * a.out_ld + n0;
+                    const float* res = a.residual
+                                           ? reinterpret_cast<const float*>(a.residual) + p * a.res_ld + n0
+                                           : nullptr;
+                    if (full && (a.out_ld % 4) == 0 && (!res || (a.res_ld % 4) == 0)) {
+#pragma unroll
+                        for (int j = 0; j < 16; j += 4) {
+                            float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                            if (res) {
+                                const float4 q = *reinterpret_cast<const float4*>(res + j);
+                                o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+                            }
+                            if (a.round_tf32) {
+                                o.x = round_tf32(o.x); o.y = round_tf32(o.y);
+                                o.z = round_tf32(o.z); o.w = round_tf32(o.w);
+                            }
+                            *reinterpret_cast<float4*>(dst + j) = o;
+                        }
+                    } else {
+                        for (int j = 0; j < 16 && n0 + j < a.n_valid; ++j) {
+                            float o = v[j] + (res ? res[j] : 0.0f);
+                            dst[j] = a.round_tf32 ? round_tf32(o) : o;
+                        }
+                    }
+                } else {
+                    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(a.out) + p * a.out_ld + n0;
+                    const __nv_bfloat16* res =
+                        a.residual ? reinterpret_cast<const __nv_bfloat16*>(a.residual) + p * a.res_ld + n0
+                                   : nullptr;
+                    if (full && (a.out_ld % 8) == 0 && (!res || (a.res_ld % 8) == 0)) {
+#pragma unroll
+                        for (int j = 0; j < 16; j += 8) {
+                            float w8[8];
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) w8[i] = v[j + i];
+                            if (res) {
+                                const uint4 q = *reinterpret_cast<const uint4*>(res + j);
+                                const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    const float2 f = __bfloat1622float2(q2[i]);
+                                    // the pre-add value is rounded like the reference's
+                                    // separate layer output (bf16 storage here)
+                                    w8[2 * i] = __bfloat162float(__float2bfloat16(w8[2 * i])) + f.x;
+                                    w8[2 * i + 1] = __bfloat162float(__float2bfloat16(w8[2 * i + 1])) + f.y;
+                                }
+                            }
+                            uint4 o;
+                            __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) o2[i] = __floats2bfloat162_rn(w8[2 * i], w8[2 * i + 1]);
+                            *reinterpret_cast<uint4*>(dst + j) = o;
+                        }
+                    } else {
+                        for (int j = 0; j < 16 && n0 + j < a.n_valid; ++j) {
+                            float o = v[j];
+                            if (res) o = __bfloat162float(__float2bfloat16(o)) + __bfloat162float(res[j]);
+                            dst[j] = __float2bfloat16(o);
+                        }
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, kTmemCols);
+    }
+}
+
+// Deterministic split-K reduction: sum partials in split order, then scale, bias,
+// residual, store.  Same pixel mapping as the main epilogue.
+template <bool kTF32>
+__global__ void splitk_reduce_kernel(const GemmArgs a) {
+    const long long total = (long long)a.m_pix * a.n_valid;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long p = i / a.n_valid;
+        const int n = int(i - p * a.n_valid);
+        float s = 0.0f;
+        for (int k = 0; k < a.splits; ++k) s += a.partial[((size_t)k * a.m_pix + p) * a.n_pad + n];
+        float x = s * a.scale;
+        if (a.bias) x += a.bias[n];
+        if (kTF32 || a.out_f32) {
+            float* dst = reinterpret_cast<float*>(a.out) + p * a.out_ld + n;
+            if (a.residual) x += reinterpret_cast<const float*>(a.residual)[p * a.res_ld + n];
+            *dst = a.round_tf32 ? round_tf32(x) : x;
+        } else {
+            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(a.out) + p * a.out_ld + n;
+            if (a.residual)
+                x = __bfloat162float(__float2bfloat16(x)) +
+                    __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(a.residual)[p * a.res_ld + n]);
+            *dst = __float2bfloat16(x);
+        }
+    }
+}
+
+// ---- host side ------------------------------------------------------------------------------
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess)
+            throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+void encode(CUtensorMap* m, Elem e, int rank, const void* base, const uint64_t* dims,
+            const uint64_t* strides_bytes, const uint32_t* box) {
+    uint32_t estr[5] = {1, 1, 1, 1, 1};
+    const CUresult r = get_encode()(
+        m, e == Elem::BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+        rank, const_cast<void*>(base), dims, strides_bytes, box, estr,
+        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+}
+
+uint32_t make_idesc(Elem e, int n) {
+    uint32_t d = 0;
+    d |= 1u << 4;                               // D format f32
+    const uint32_t fmt = e == Elem::BF16 ? 1u : 2u;  // BF16 / TF32
+    d |= fmt << 7;                              // A format
+    d |= fmt << 10;                             // B format
+    d |= uint32_t(n >> 3) << 17;                // N
+    d |= uint32_t(kTileM >> 4) << 24;           // M = 128
+    return d;
+}
+
+int stages_for(int block_n) {
+    const int stage = kTileM * kBlockBytes + block_n * kBlockBytes;
+    const int barriers = 1024;  // align slack + barriers + tmem slot
+    return std::max(2, std::min(8, (kSmemBudget - barriers) / stage));
+}
+
+size_t smem_for(int block_n, int stages) {
+    return size_t(stages) * (kTileM * kBlockBytes + block_n * kBlockBytes) + 1024 +
+           size_t(2 * stages + 4) * 8 + 16;
+}
+
+// Pick block_n and split-K from a simple cost model: per 128-byte K block a tile costs
+// max(MMA cycles, L2 feed cycles); waves are quantised over the SM count.
+void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int force_splits,
+                   int force_block_n, int& block_n, int& splits) {
+    double best = 1e300;
+    block_n = 16;
+    splits = 1;
+    for (int bn = 256; bn >= 16; bn -= 16) {
+        if (force_block_n && bn != force_block_n) continue;
+        if (n_pad % bn) continue;
+        const int nt = n_pad / bn;
+        for (int s : {1, 2, 3, 4, 6, 8, 12, 16}) {
+            if (force_splits && s != force_splits) continue;
+            if (s > 1 && k_blocks / s < 4 && !force_splits) continue;
+            if (s > k_blocks) continue;
+            const long long tiles = (long long)m_tiles * nt * s;
+            const double waves = std::ceil(double(tiles) / num_sms);
+            const double per_kb = std::max(2.0 * bn, (16384.0 + 128.0 * bn) / 42.0);
+            const double kbs = std::ceil(double(k_blocks) / s);
+            double cost = waves * (kbs * per_kb + 600.0);
+            if (s > 1) cost += 0.02 * m_tiles * 128.0 * n_pad * s / num_sms;  // reduce pass
+            if (cost < best * 0.999) {
+                best = cost;
+                block_n = bn;
+                splits = s;
+            }
+        }
+    }
+    if (force_block_n) block_n = force_block_n;
+}
+
+void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const EpilogueSpec& ep,
+                 float* ws, size_t ws_bytes, int num_sms, int force_splits, int force_block_n) {
+    int bn, splits;
+    choose_tiling(m_tiles, n_pad, k_blocks, num_sms, force_splits, force_block_n, bn, splits);
+    GemmArgs& a = p.a;
+    a.block_n = bn;
+    a.n_tiles = n_pad / bn;
+    a.k_blocks = k_blocks;
+    a.n_pad = n_pad;
+    while (splits > 1 &&
+           (size_t)splits * a.m_pix * n_pad * sizeof(float) > ws_bytes)
+        --splits;
+    a.splits = splits;
+    a.kb_per_split = (k_blocks + splits - 1) / splits;
+    a.splits = (k_blocks + a.kb_per_split - 1) / a.kb_per_split;
+    a.stages = stages_for(bn);
+    a.idesc = make_idesc(p.elem, bn);
+    a.out = ep.out;
+    a.out_ld = ep.out_ld;
+    a.n_valid = ep.n_valid;
+    a.out_f32 = ep.out_f32 ? 1 : 0;
+    a.round_tf32 = ep.round_tf32 ? 1 : 0;
+    a.bias = ep.bias;
+    a.residual = ep.residual;
+    a.res_ld = ep.res_ld;
+    a.scale = ep.scale;
+    a.partial = a.splits > 1 ? ws : nullptr;
+    p.needs_reduce = a.splits > 1;
+    const int tiles = m_tiles * a.n_tiles * a.splits;
+    p.grid = std::min(tiles, num_sms);
+    p.smem = smem_for(bn, a.stages);
+}
+
+}  // namespace
+
+int device_sm_count() {
+    int dev = 0, n = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    CUDA_CHECK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    return n;
+}
+
+void plan_conv(GemmPlan& p, Elem e, const void* in, int rows_in, int W, int C_in_pad, int stride,
+               const void* weights, int n_pad, const EpilogueSpec& ep, float* workspace,
+               size_t workspace_bytes, int num_sms, int force_splits, int force_block_n) {
+    std::memset(&p, 0, sizeof(p));
+    p.elem = e;
+    const size_t eb = elem_bytes(e);
+    const int kel = int(kBlockBytes / eb);
+    if (C_in_pad % kel) throw std::invalid_argument("plan_conv: C_in_pad must fill 128-byte blocks");
+    if (n_pad % 16) throw std::invalid_argument("plan_conv: n_pad % 16 != 0");
+    if (stride != 1 && stride != 2) throw std::invalid_argument("plan_conv: stride must be 1 or 2");
+    GemmArgs& a = p.a;
+    a.mode = stride == 1 ? 1 : 2;
+    const int out_w = stride == 1 ? W : W / 2;
+    const int out_rows = stride == 1 ? rows_in : rows_in / 2;
+    if (stride == 2 && ((W % 2) || (rows_in % 2)))
+        throw std::invalid_argument("plan_conv: stride-2 band must have even rows and width");
+    int wb = 1;
+    for (int d = std::min(out_w, kTileM); d >= 1; --d)
+        if (out_w % d == 0) {
+            wb = d;
+            break;
+        }
+    a.w_box = wb;
+    a.rows_box = std::min(kTileM / wb, out_rows);
+    a.tiles_x = out_w / wb;
+    a.tiles_y = (out_rows + a.rows_box - 1) / a.rows_box;
+    a.out_rows = out_rows;
+    a.out_w = out_w;
+    a.cin_chunks = C_in_pad / kel;
+    a.m_pix = out_rows * out_w;
+    const int k_blocks = 9 * a.cin_chunks;
+
+    // A: 5-D view of the padded band [rows_in+2][W][C_in_pad]
+    const int rows_pad = rows_in + 2;
+    uint64_t dims[5], strides[4];
+    uint32_t box[5];
+    const uint64_t pix = uint64_t(C_in_pad) * eb;
+    if (stride == 1) {
+        dims[0] = C_in_pad; dims[1] = 1; dims[2] = W; dims[3] = 1; dims[4] = rows_pad;
+        strides[0] = pix; strides[1] = pix; strides[2] = pix * W; strides[3] = pix * W;
+    } else {
+        dims[0] = C_in_pad; dims[1] = 2; dims[2] = W / 2; dims[3] = 2; dims[4] = rows_pad / 2;
+        strides[0] = pix; strides[1] = 2 * pix; strides[2] = pix * W; strides[3] = 2 * pix * W;
+    }
+    box[0] = kel; box[1] = 1; box[2] = wb; box[3] = 1; box[4] = a.rows_box;
+    encode(&p.tmA, e, 5, in, dims, strides, box);
+    finish_plan(p, a.tiles_y * a.tiles_x, n_pad, k_blocks, ep, workspace, workspace_bytes, num_sms,
+                force_splits, force_block_n);
+    // B: weights [n_pad][9*C_in_pad]
+    uint64_t bd[2] = {uint64_t(9) * C_in_pad, uint64_t(n_pad)};
+    uint64_t bs[1] = {uint64_t(9) * C_in_pad * eb};
+    uint32_t bb[2] = {uint32_t(kel), uint32_t(a.block_n)};
+    encode(&p.tmB, e, 2, weights, bd, bs, bb);
+    p.flops = 2.0 * a.m_pix * double(ep.n_valid) * 9.0 * C_in_pad;
+}
+
+void plan_gemm(GemmPlan& p, Elem e, const void* A, int M, int K, long long lda, const void* B,
+               int N, long long ldb, const EpilogueSpec& ep, float* workspace,
+               size_t workspace_bytes, int num_sms, int force_splits, int force_block_n) {
+    std::memset(&p, 0, sizeof(p));
+    p.elem = e;
+    const size_t eb = elem_bytes(e);
+    const int kel = int(kBlockBytes / eb);
+    if (K % kel) throw std::invalid_argument("plan_gemm: K must fill 128-byte blocks");
+    GemmArgs& a = p.a;
+    a.mode = 0;
+    a.tiles_y = (M + kTileM - 1) / kTileM;
+    a.tiles_x = 1;
+    a.out_rows = M;
+    a.out_w = 1;
+    a.rows_box = kTileM;
+    a.w_box = 1;
+    a.cin_chunks = K / kel;
+    a.m_pix = M;
+    const int n_pad = (N + 15) / 16 * 16;
+    uint64_t ad[2] = {uint64_t(K), uint64_t(M)};
+    uint64_t as[1] = {uint64_t(lda) * eb};
+    uint32_t ab[2] = {uint32_t(kel), uint32_t(kTileM)};
+    encode(&p.tmA, e, 2, A, ad, as, ab);
+    finish_plan(p, a.tiles_y, n_pad, K / kel, ep, workspace, workspace_bytes, num_sms,
+                force_splits, force_block_n);
+    uint64_t bd[2] = {uint64_t(K), uint64_t(N)};
+    uint64_t bs[1] = {uint64_t(ldb) * eb};
+    uint32_t bb[2] = {uint32_t(kel), uint32_t(a.block_n)};
+    encode(&p.tmB, e, 2, B, bd, bs, bb);
+    p.flops = 2.0 * double(M) * N * K;
+}
+
+size_t gemm_workspace_bytes(const GemmPlan& p) {
+    return p.needs_reduce ? size_t(p.a.splits) * p.a.m_pix * p.a.n_pad * sizeof(float) : 0;
+}
+
+void launch_gemm(const GemmPlan& p, cudaStream_t s) {
+    if (p.elem == Elem::BF16) {
+        static bool attr = false;
+        if (!attr) {
+            CUDA_CHECK(cudaFuncSetAttribute(gemm_kernel<false>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+            attr = true;
+        }
+        gemm_kernel<false><<<p.grid, kThreads, p.smem, s>>>(p.tmA, p.tmB, p.a);
+    } else {
+        static bool attr = false;
+        if (!attr) {
+            CUDA_CHECK(cudaFuncSetAttribute(gemm_kernel<true>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+            attr = true;
+        }
+        gemm_kernel<true><<<p.grid, kThreads, p.smem, s>>>(p.tmA, p.tmB, p.a);
+    }
+    CUDA_CHECK(cudaGetLastError());
+    if (p.needs_reduce) {
+        const long long total = (long long)p.a.m_pix * p.a.n_valid;
+        const int blocks = int(std::min<long long>((total + 255) / 256, 148 * 8));
+        if (p.elem == Elem::BF16)
+            splitk_reduce_kernel<false><<<blocks, 256, 0, s>>>(p.a);
+        else
+            splitk_reduce_kernel<true><<<blocks, 256, 0, s>>>(p.a);
+        CUDA_CHECK(cudaGetLastError());
+    }
+}
+
+}  // namespace pp

@@ -1,0 +1,624 @@
+// HBM-bound kernels (see kernels.hpp).  128-bit vectorised NHWC access; all
+// reductions are fixed-order (no float atomics) so every run is bit-deterministic.
+#include "kernels.hpp"
+#include "util.hpp"
+
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+
+namespace pp {
+
+namespace {
+
+using bf16 = __nv_bfloat16;
+
+__device__ __forceinline__ float rtf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+template <class T>
+struct Vec {
+    static constexpr int N = 16 / sizeof(T);
+};
+
+template <class T>
+__device__ __forceinline__ void load_vec(const T* p, float* f);
+template <>
+__device__ __forceinline__ void load_vec<float>(const float* p, float* f) {
+    const float4 v = *reinterpret_cast<const float4*>(p);
+    f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w;
+}
+template <>
+__device__ __forceinline__ void load_vec<bf16>(const bf16* p, float* f) {
+    const uint4 v = *reinterpret_cast<const uint4*>(p);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 t = __bfloat1622float2(h[i]);
+        f[2 * i] = t.x;
+        f[2 * i + 1] = t.y;
+    }
+}
+template <class T>
+__device__ __forceinline__ void store_vec(T* p, const float* f, bool round_tf32);
+template <>
+__device__ __forceinline__ void store_vec<float>(float* p, const float* f, bool r) {
+    float4 v = make_float4(f[0], f[1], f[2], f[3]);
+    if (r) {
+        v.x = rtf32(v.x); v.y = rtf32(v.y); v.z = rtf32(v.z); v.w = rtf32(v.w);
+    }
+    *reinterpret_cast<float4*>(p) = v;
+}
+template <>
+__device__ __forceinline__ void store_vec<bf16>(bf16* p, const float* f, bool) {
+    uint4 v;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    *reinterpret_cast<uint4*>(p) = v;
+}
+template <class T>
+__device__ __forceinline__ T from_float(float x, bool r);
+template <>
+__device__ __forceinline__ float from_float<float>(float x, bool r) { return r ? rtf32(x) : x; }
+template <>
+__device__ __forceinline__ bf16 from_float<bf16>(float x, bool) { return __float2bfloat16(x); }
+__device__ __forceinline__ float to_float(float x) { return x; }
+__device__ __forceinline__ float to_float(bf16 x) { return __bfloat162float(x); }
+
+int grid_for(long long n, int threads) {
+    long long b = (n + threads - 1) / threads;
+    return int(std::max<long long>(1, std::min<long long>(b, 148LL * 16)));
+}
+
+// ---------------------------------------------------------------- GroupNorm stats
+constexpr int kGnThreads = 256;
+constexpr int kGnPixels = 64;
+
+template <class T>
+__global__ void gn_partial_kernel(const T* __restrict__ x, long long pix, int C, int ld, int G,
+                                  double* __restrict__ partial) {
+    constexpr int VEC = Vec<T>::N;
+    extern __shared__ unsigned char sm_raw[];
+    const int nvec = C / VEC;
+    const int L = max(1, kGnThreads / nvec);
+    float* s_sum = reinterpret_cast<float*>(sm_raw);
+    float* s_sq = s_sum + L * C;
+    double* c_sum = reinterpret_cast<double*>(s_sq + L * C + (((L * C) & 1) ? 1 : 0));
+    double* c_sq = c_sum + C;
+    const long long p0 = (long long)blockIdx.x * kGnPixels;
+    const long long p1 = min(p0 + kGnPixels, pix);
+    for (int idx = threadIdx.x; idx < L * nvec; idx += blockDim.x) {
+        const int pl = idx / nvec, v = idx - pl * nvec;
+        float a[VEC], b[VEC];
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) a[i] = b[i] = 0.0f;
+        for (long long p = p0 + pl; p < p1; p += L) {
+            float f[VEC];
+            load_vec<T>(x + p * ld + v * VEC, f);
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) {
+                a[i] += f[i];
+                b[i] = fmaf(f[i], f[i], b[i]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) {
+            s_sum[pl * C + v * VEC + i] = a[i];
+            s_sq[pl * C + v * VEC + i] = b[i];
+        }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+        double a = 0.0, b = 0.0;
+        for (int pl = 0; pl < L; ++pl) {
+            a += double(s_sum[pl * C + c]);
+            b += double(s_sq[pl * C + c]);
+        }
+        c_sum[c] = a;
+        c_sq[c] = b;
+    }
+    __syncthreads();
+    const int cpg = C / G;
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+        double a = 0.0, b = 0.0;
+        for (int c = g * cpg; c < (g + 1) * cpg; ++c) {
+            a += c_sum[c];
+            b += c_sq[c];
+        }
+        partial[((long long)blockIdx.x * G + g) * 2] = a;
+        partial[((long long)blockIdx.x * G + g) * 2 + 1] = b;
+    }
+}
+
+__global__ void gn_finalize_kernel(const double* __restrict__ partial, int blocks, int G,
+                                   double count, double* __restrict__ out) {
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+        double a = 0.0, b = 0.0;
+        for (int k = 0; k < blocks; ++k) {
+            a += partial[((long long)k * G + g) * 2];
+            b += partial[((long long)k * G + g) * 2 + 1];
+        }
+        out[g * 2] = a / count;
+        out[g * 2 + 1] = b / count;
+    }
+}
+
+// Device-order weighted mean (collectives.cpp:150-172), no FMA contraction.
+__device__ void weighted_mean(const double* all, int n, const double* w, int G, int g, double& m,
+                              double& q) {
+    if (n == 1) {
+        m = all[g * 2];
+        q = all[g * 2 + 1];
+        return;
+    }
+    double tw = 0.0;
+    for (int d = 0; d < n; ++d) tw = __dadd_rn(tw, w[d]);
+    double a = 0.0, b = 0.0;
+    for (int d = 0; d < n; ++d) {
+        a = __dadd_rn(a, __dmul_rn(w[d], all[((long long)d * G + g) * 2]));
+        b = __dadd_rn(b, __dmul_rn(w[d], all[((long long)d * G + g) * 2 + 1]));
+    }
+    m = __ddiv_rn(a, tw);
+    q = __ddiv_rn(b, tw);
+}
+
+__global__ void gn_combine_kernel(int mode, const double* __restrict__ fresh,
+                                  const double* __restrict__ all_cur,
+                                  const double* __restrict__ all_prev, int n, int rank,
+                                  const double* __restrict__ w, int G, float eps,
+                                  float* __restrict__ use, int* err) {
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+        double m = fresh[g * 2], q = fresh[g * 2 + 1];
+        if (mode == GN_USE_GLOBAL) {
+            weighted_mean(all_cur, n, w, G, g, m, q);
+        } else if (mode == GN_USE_STALE) {
+            weighted_mean(all_prev, n, w, G, g, m, q);
+        } else if (mode == GN_USE_CORRECTED) {
+            // corrected_gn_stats (runtime.cpp:85-106)
+            const double lm = all_prev[((long long)rank * G + g) * 2];
+            const double lq = all_prev[((long long)rank * G + g) * 2 + 1];
+            double gm, gq;
+            weighted_mean(all_prev, n, w, G, g, gm, gq);
+            if (!(gm == lm && gq == lq)) {
+                const double cm = __dadd_rn(gm, __dsub_rn(m, lm));
+                const double cq = __dadd_rn(gq, __dsub_rn(q, lq));
+                if (!(__dsub_rn(cq, __dmul_rn(cm, cm)) < 0.0)) {
+                    m = cm;
+                    q = cq;
+                }
+            }
+        }
+        const double var = __dsub_rn(q, __dmul_rn(m, m));
+        if (var < 0.0) atomicExch(err, 1);  // group_norm_apply contract (tensor.cpp:256-259)
+        const double inv = 1.0 / sqrt(__dadd_rn(fmax(var, 0.0), double(eps)));
+        use[g * 2] = float(m);
+        use[g * 2 + 1] = float(inv);
+    }
+}
+
+template <class T>
+__global__ void gn_apply_kernel(const T* __restrict__ x, T* __restrict__ y, long long pix, int C,
+                                int ld, int G, const float* __restrict__ use,
+                                const float* __restrict__ gamma, const float* __restrict__ beta,
+                                int do_silu, const float* __restrict__ temb,
+                                const T* __restrict__ skip, int round_tf32) {
+    constexpr int VEC = Vec<T>::N;
+    __shared__ float s_use[2 * 1024];
+    for (int i = threadIdx.x; i < 2 * G; i += blockDim.x) s_use[i] = use[i];
+    __syncthreads();
+    const int nvec = ld / VEC;
+    const int cpg = C / G;
+    const long long total = pix * nvec;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long p = idx / nvec;
+        const int c0 = int(idx - p * nvec) * VEC;
+        float f[VEC];
+        load_vec<T>(x + p * ld + c0, f);
+        float sk[VEC];
+        if (skip) load_vec<T>(skip + p * ld + c0, sk);
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) {
+            const int c = c0 + i;
+            if (c < C) {
+                const int g = c / cpg;
+                float v = (f[i] - s_use[2 * g]) * s_use[2 * g + 1] * gamma[c] + beta[c];
+                if (do_silu) v = v / (1.0f + expf(-v));
+                if (temb) v = v + temb[c];
+                if (skip) v = v + sk[i];
+                f[i] = v;
+            } else {
+                f[i] = 0.0f;
+            }
+        }
+        store_vec<T>(y + p * ld + c0, f, round_tf32 != 0);
+    }
+}
+
+// ---------------------------------------------------------------- pointwise
+template <class T>
+__global__ void silu_kernel(const T* __restrict__ x, T* __restrict__ y, long long nv, int r) {
+    constexpr int VEC = Vec<T>::N;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nv;
+         i += (long long)gridDim.x * blockDim.x) {
+        float f[VEC];
+        load_vec<T>(x + i * VEC, f);
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) f[k] = f[k] / (1.0f + expf(-f[k]));
+        store_vec<T>(y + i * VEC, f, r != 0);
+    }
+}
+
+template <class T>
+__global__ void add_kernel(const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ o,
+                           long long nv, int r) {
+    constexpr int VEC = Vec<T>::N;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nv;
+         i += (long long)gridDim.x * blockDim.x) {
+        float a[VEC], b[VEC];
+        load_vec<T>(x + i * VEC, a);
+        load_vec<T>(y + i * VEC, b);
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) a[k] = a[k] + b[k];
+        store_vec<T>(o + i * VEC, a, r != 0);
+    }
+}
+
+template <class T>
+__global__ void add_channel_kernel(const T* __restrict__ x, const float* __restrict__ vec,
+                                   const T* __restrict__ skip, T* __restrict__ o, long long pix,
+                                   int ld, int r) {
+    constexpr int VEC = Vec<T>::N;
+    const int nvec = ld / VEC;
+    const long long total = pix * nvec;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int c0 = int(i % nvec) * VEC;
+        float a[VEC];
+        if (x) {
+            load_vec<T>(x + i * VEC, a);
+        } else {
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) a[k] = 0.0f;
+        }
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) a[k] = x ? a[k] + vec[c0 + k] : vec[c0 + k];
+        if (skip) {
+            float b[VEC];
+            load_vec<T>(skip + i * VEC, b);
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) a[k] = a[k] + b[k];
+        }
+        store_vec<T>(o + i * VEC, a, r != 0);
+    }
+}
+
+template <class T>
+__global__ void upsample_kernel(const T* __restrict__ x, T* __restrict__ y, int rows, int W,
+                                int ld) {
+    constexpr int VEC = Vec<T>::N;
+    const int nvec = ld / VEC;
+    const long long total = (long long)rows * W * nvec;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int v = int(i % nvec);
+        const long long p = i / nvec;
+        const int xx = int(p % W), yy = int(p / W);
+        const uint4 val = *reinterpret_cast<const uint4*>(x + p * ld + v * VEC);
+        const long long W2 = 2LL * W;
+        const long long o00 = ((2LL * yy) * W2 + 2 * xx) * ld + v * VEC;
+        *reinterpret_cast<uint4*>(y + o00) = val;
+        *reinterpret_cast<uint4*>(y + o00 + ld) = val;
+        *reinterpret_cast<uint4*>(y + o00 + W2 * ld) = val;
+        *reinterpret_cast<uint4*>(y + o00 + W2 * ld + ld) = val;
+    }
+}
+
+// ---------------------------------------------------------------- attention helpers
+template <class T>
+__global__ void softmax_kernel(const float* __restrict__ S, int ns, long long lds, float scale,
+                               T* __restrict__ P, long long ldp) {
+    const int row = blockIdx.x;
+    const float* s = S + (long long)row * lds;
+    __shared__ float red[32];
+    float mx = -INFINITY;
+    for (int j = threadIdx.x; j < ns; j += blockDim.x) mx = fmaxf(mx, s[j] * scale);
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : -INFINITY;
+        for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    mx = red[0];
+    __syncthreads();
+    float sum = 0.0f;
+    for (int j = threadIdx.x; j < ns; j += blockDim.x) sum += expf(s[j] * scale - mx);
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    const float inv = 1.0f / red[0];
+    T* pr = P + (long long)row * ldp;
+    for (int j = threadIdx.x; j < ns; j += blockDim.x)
+        pr[j] = from_float<T>(expf(s[j] * scale - mx) * inv, true);
+}
+
+template <class T>
+__global__ void transpose_kernel(const T* __restrict__ V, int ns, int C, long long ldv,
+                                 T* __restrict__ Vt, long long ldt) {
+    __shared__ T tile[32][33];
+    const int j0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int j = j0 + k, c = c0 + threadIdx.x;
+        if (j < ns && c < C) tile[k][threadIdx.x] = V[(long long)j * ldv + c];
+    }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int c = c0 + k, j = j0 + threadIdx.x;
+        if (j < ns && c < C) Vt[(long long)c * ldt + j] = tile[threadIdx.x][k];
+    }
+}
+
+// ---------------------------------------------------------------- embeddings / projections
+__global__ void time_projection_kernel(const TembLayer* __restrict__ layers, int dim, int t) {
+    extern __shared__ float emb[];
+    const int half = dim / 2;
+    for (int i = threadIdx.x; i < half; i += blockDim.x) {
+        const double freq = pow(10000.0, -2.0 * i / double(dim));
+        emb[i] = float(sin(t * freq));
+        emb[half + i] = float(cos(t * freq));
+    }
+    __syncthreads();
+    const TembLayer L = layers[blockIdx.y];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int nw = blockDim.x / 32;
+    for (int c = blockIdx.x * nw + warp; c < L.C; c += gridDim.x * nw) {
+        double acc = 0.0;
+        for (int i = lane; i < dim; i += 32) acc += double(emb[i]) * double(L.W[(long long)c * dim + i]);
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) L.out[c] = float(acc + double(L.b[c]));
+    }
+}
+
+__global__ void gemv_f64_kernel(const float* __restrict__ W, const float* __restrict__ b,
+                                const float* __restrict__ x, int rows, int cols,
+                                float* __restrict__ out) {
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int nw = blockDim.x / 32;
+    for (int r = blockIdx.x * nw + warp; r < rows; r += gridDim.x * nw) {
+        double acc = 0.0;
+        for (int i = lane; i < cols; i += 32) acc += double(x[i]) * double(W[(long long)r * cols + i]);
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) out[r] = float(acc + double(b[r]));
+    }
+}
+
+// ---------------------------------------------------------------- sampler / layout
+template <class T>
+__global__ void ddim_kernel(const float* __restrict__ x, const float* __restrict__ eps,
+                            float* __restrict__ xo, long long n, int C, double sa, double s1,
+                            double sn, double s1n, T* __restrict__ stem, int stem_ld) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double e = double(eps[i]);
+        const double x0 = __ddiv_rn(__dsub_rn(double(x[i]), __dmul_rn(s1, e)), sa);
+        const float v = float(__dadd_rn(__dmul_rn(sn, x0), __dmul_rn(s1n, e)));
+        xo[i] = v;
+        if (stem) {
+            const long long p = i / C;
+            stem[p * stem_ld + (i - p * C)] = from_float<T>(v, true);
+        }
+    }
+}
+
+template <class T>
+__global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, int C, int H, int W, int r0,
+                                    int rows, T* __restrict__ dst, int ld, int r) {
+    const long long total = (long long)rows * W * C;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int c = int(i % C);
+        const long long p = i / C;
+        const int xx = int(p % W), yy = int(p / W);
+        dst[p * ld + c] = from_float<T>(src[((long long)c * H + r0 + yy) * W + xx], r != 0);
+    }
+}
+
+template <class T>
+__global__ void nhwc_to_nchw_kernel(const T* __restrict__ src, int ld, int C, int rows, int W,
+                                    float* __restrict__ dst, int* nonfinite) {
+    const long long total = (long long)rows * W * C;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int xx = int(i % W);
+        const long long rest = i / W;
+        const int yy = int(rest % rows), c = int(rest / rows);
+        const float v = to_float(src[((long long)yy * W + xx) * ld + c]);
+        dst[i] = v;
+        if (nonfinite && !isfinite(v)) atomicExch(nonfinite, 1);
+    }
+}
+
+template <class T>
+__global__ void f32_to_elem_kernel(const float* __restrict__ s, T* __restrict__ d, long long n, int r) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        d[i] = from_float<T>(s[i], r != 0);
+}
+template <class T>
+__global__ void elem_to_f32_kernel(const T* __restrict__ s, float* __restrict__ d, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        d[i] = to_float(s[i]);
+}
+
+#define DISPATCH(e, ...)                          \
+    do {                                          \
+        if ((e) == Elem::BF16) {                  \
+            using T = bf16;                       \
+            __VA_ARGS__;                          \
+        } else {                                  \
+            using T = float;                      \
+            __VA_ARGS__;                          \
+        }                                         \
+    } while (0)
+
+}  // namespace
+
+int gn_stats_blocks(long long pix) { return int((pix + kGnPixels - 1) / kGnPixels); }
+
+void gn_partial_stats(Elem e, const void* x, long long pix, int C, int ld, int groups,
+                      double* partial, cudaStream_t s) {
+    const int VEC = e == Elem::BF16 ? 8 : 4;
+    if (C % VEC || ld % VEC || C % groups)
+        throw std::invalid_argument("group_stats: channels must be a multiple of the vector width");
+    const int nvec = C / VEC;
+    const int L = std::max(1, kGnThreads / nvec);
+    const size_t smem = size_t(2) * L * C * 4 + 8 + size_t(2) * C * 8;
+    DISPATCH(e, gn_partial_kernel<T><<<gn_stats_blocks(pix), kGnThreads, smem, s>>>(
+                    static_cast<const T*>(x), pix, C, ld, groups, partial));
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void gn_finalize(const double* partial, int blocks, int groups, double count, double* out,
+                 cudaStream_t s) {
+    gn_finalize_kernel<<<1, std::min(1024, std::max(32, groups)), 0, s>>>(partial, blocks, groups,
+                                                                         count, out);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void gn_combine(int mode, const double* fresh, const double* all_cur, const double* all_prev,
+                int n_dev, int rank, const double* weights, int groups, float eps, float* use,
+                int* err, cudaStream_t s) {
+    gn_combine_kernel<<<1, std::min(1024, std::max(32, groups)), 0, s>>>(
+        mode, fresh, all_cur, all_prev, n_dev, rank, weights, groups, eps, use, err);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void gn_apply(Elem e, const void* x, void* y, long long pix, int C, int ld, int groups,
+              const float* use, const float* gamma, const float* beta, bool do_silu,
+              const float* temb, const void* skip, bool round_tf32, cudaStream_t s) {
+    if (groups > 1024) throw std::invalid_argument("group_norm_apply: too many groups");
+    const int VEC = e == Elem::BF16 ? 8 : 4;
+    DISPATCH(e, gn_apply_kernel<T><<<grid_for(pix * (ld / VEC), 256), 256, 0, s>>>(
+                    static_cast<const T*>(x), static_cast<T*>(y), pix, C, ld, groups, use, gamma,
+                    beta, do_silu ? 1 : 0, temb, static_cast<const T*>(skip), round_tf32 ? 1 : 0));
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void silu(Elem e, const void* x, void* y, long long n, bool r, cudaStream_t s) {
+    const int VEC = e == Elem::BF16 ? 8 : 4;
+    DISPATCH(e, silu_kernel<T><<<grid_for(n / VEC, 256), 256, 0, s>>>(
+                    static_cast<const T*>(x), static_cast<T*>(y), n / VEC, r ? 1 : 0));
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void add(Elem e, const void* x, const void* y, void* o, long long n, bool r, cudaStream_t s) {
+    const int VEC = e == Elem::BF16 ? 8 : 4;
+    DISPATCH(e, add_kernel<T><<<grid_for(n / VEC, 256), 256, 0, s>>>(
+                    static_cast<const T*>(x), static_cast<const T*>(y), static_cast<T*>(o),
+                    n / VEC, r ? 1 : 0));
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void add_channel(Elem e, const void* x, const float* vec, const void* skip, void* o,
+                 long long pix, int ld, bool, bool r, cudaStream_t s) {
+    const int VEC = e == Elem::BF16 ? 8 : 4;
+    DISPATCH(e, add_channel_kernel<T><<<grid_for(pix * ld / VEC, 256), 256, 0, s>>>(
+                    static_cast<const T*>(x), vec, static_cast<const T*>(skip), static_cast<T*>(o),
+                    pix, ld, r ? 1 : 0));
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void upsample2x(Elem e, const void* x, void* y, int rows, int W, int ld, cudaStream_t s) {
+    const int VEC = e == Elem::BF16 ? 8 : 4;
+    DISPATCH(e, upsample_kernel<T><<<grid_for((long long)rows * W * ld / VEC, 256), 256, 0, s>>>(
+                    static_cast<const T*>(x), static_cast<T*>(y), rows, W, ld));
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void softmax_rows(Elem e, const float* S, int m, int ns, long long lds, float scale, void* P,
+                  long long ldp, cudaStream_t s) {
+    DISPATCH(e, softmax_kernel<T><<<m, 256, 0, s>>>(S, ns, lds, scale, static_cast<T*>(P), ldp));
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void transpose(Elem e, const void* V, int ns, int C, long long ldv, void* Vt, long long ldt,
+               cudaStream_t s) {
+    dim3 grid((ns + 31) / 32, (C + 31) / 32), block(32, 8);
+    DISPATCH(e, transpose_kernel<T><<<grid, block, 0, s>>>(static_cast<const T*>(V), ns, C, ldv,
+                                                          static_cast<T*>(Vt), ldt));
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void time_projection(const TembLayer* layers_dev, int n_layers, int max_c, int dim, int t,
+                     cudaStream_t s) {
+    if (n_layers == 0) return;
+    dim3 grid(std::max(1, std::min(64, (max_c + 7) / 8)), n_layers);
+    time_projection_kernel<<<grid, 256, dim * sizeof(float), s>>>(layers_dev, dim, t);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void gemv_f64(const float* W, const float* b, const float* x, int rows, int cols, float* out,
+              cudaStream_t s) {
+    gemv_f64_kernel<<<std::max(1, std::min(148, (rows + 7) / 8)), 256, 0, s>>>(W, b, x, rows, cols,
+                                                                              out);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void ddim_update(const float* x, const float* eps, float* xo, long long n, int C, double abar_t,
+                 double abar_n, Elem e, void* stem, int stem_ld, cudaStream_t s) {
+    const double sa = std::sqrt(abar_t), s1 = std::sqrt(1.0 - abar_t);
+    const double sn = std::sqrt(abar_n), s1n = std::sqrt(1.0 - abar_n);
+    DISPATCH(e, ddim_kernel<T><<<grid_for(n, 256), 256, 0, s>>>(x, eps, xo, n, C, sa, s1, sn, s1n,
+                                                                static_cast<T*>(stem), stem_ld));
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void nchw_to_nhwc(const float* src, int C, int H, int W, int r0, int rows, Elem e, void* dst,
+                  int ld, bool r, cudaStream_t s) {
+    DISPATCH(e, nchw_to_nhwc_kernel<T><<<grid_for((long long)rows * W * C, 256), 256, 0, s>>>(
+                    src, C, H, W, r0, rows, static_cast<T*>(dst), ld, r ? 1 : 0));
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void nhwc_to_nchw(Elem e, const void* src, int ld, int C, int rows, int W, float* dst,
+                  int* nonfinite, cudaStream_t s) {
+    DISPATCH(e, nhwc_to_nchw_kernel<T><<<grid_for((long long)rows * W * C, 256), 256, 0, s>>>(
+                    static_cast<const T*>(src), ld, C, rows, W, dst, nonfinite));
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void nhwc_f32_to_nchw(const float* src, int C, int rows, int W, float* dst, int* nonfinite,
+                      cudaStream_t s) {
+    nhwc_to_nchw_kernel<float><<<grid_for((long long)rows * W * C, 256), 256, 0, s>>>(
+        src, C, C, rows, W, dst, nonfinite);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void f32_to_elem(const float* src, Elem e, void* dst, long long n, bool r, cudaStream_t s) {
+    DISPATCH(e, f32_to_elem_kernel<T><<<grid_for(n, 256), 256, 0, s>>>(src, static_cast<T*>(dst), n,
+                                                                       r ? 1 : 0));
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void elem_to_f32(Elem e, const void* src, float* dst, long long n, cudaStream_t s) {
+    DISPATCH(e, elem_to_f32_kernel<T><<<grid_for(n, 256), 256, 0, s>>>(static_cast<const T*>(src),
+                                                                       dst, n));
+    CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace pp

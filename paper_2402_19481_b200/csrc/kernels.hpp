@@ -1,0 +1,90 @@
+// HBM-bound kernels on the hot path (everything that is not a tensor-core GEMM).
+// All activations are NHWC bands: `pix` pixels x `ld` channels (ld >= C, padded
+// channels hold zeros), element type bf16 (bf16 mode) or fp32 (fp32 mode).
+#pragma once
+#include "gemm.hpp"
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace pp {
+
+// ---- GroupNorm (proj/src/tensor.cpp:203-277, proj/src/runtime.cpp:85-106) ----------------
+// Stage 1: per-block fp32 partial sums -> per-group fp64 partials [blocks][G][2].
+int gn_stats_blocks(long long pix);
+void gn_partial_stats(Elem e, const void* x, long long pix, int C, int ld, int groups,
+                      double* partial, cudaStream_t s);
+// Stage 2: fixed-order fp64 reduction of the partials into the local (mean, mean_sq),
+// written to stats_out[groups][2].
+void gn_finalize(const double* partial, int blocks, int groups, double count, double* stats_out,
+                 cudaStream_t s);
+
+// Combine rule applied on the device (one thread per group):
+//   GN_USE_LOCAL      use = fresh local                (N == 1 sync, or scheme Separate)
+//   GN_USE_GLOBAL     use = weighted device-order mean of all ranks' locals (sync, N > 1)
+//   GN_USE_CORRECTED  use = corrected_gn_stats(fresh, prev_local, prev_global)
+//   GN_USE_STALE      use = prev_global
+// `all_cur` / `all_prev` are [n_dev][groups][2] (mean, mean_sq) tables; weights are the
+// per-device pixel counts (collectives.cpp:150-172 weighting).
+enum GnUse : int { GN_USE_LOCAL = 0, GN_USE_GLOBAL = 1, GN_USE_CORRECTED = 2, GN_USE_STALE = 3 };
+void gn_combine(int mode, const double* fresh_local, const double* all_cur, const double* all_prev,
+                int n_dev, int rank, const double* weights, int groups, float eps,
+                float* use_out /*[groups][2] = (mean, inv_std)*/, int* err_flag, cudaStream_t s);
+
+// y = GN(x) [-> SiLU] [+ temb[c]] [+ skip]  (fused GroupNorm / SiLU / AddTimeEmb / AddSkip)
+void gn_apply(Elem e, const void* x, void* y, long long pix, int C, int ld, int groups,
+              const float* use, const float* gamma, const float* beta, bool silu,
+              const float* temb, const void* skip, bool round_tf32, cudaStream_t s);
+
+// ---- pointwise (proj/src/tensor.cpp:297-334, model.cpp:278-298) ---------------------------
+void silu(Elem e, const void* x, void* y, long long n, bool round_tf32, cudaStream_t s);
+void add(Elem e, const void* x, const void* y, void* out, long long n, bool round_tf32,
+         cudaStream_t s);
+// out[p][c] = x[p][c] + vec[c]   (AddTimeEmb / CrossAttn broadcast, with optional skip)
+void add_channel(Elem e, const void* x, const float* vec, const void* skip, void* out,
+                 long long pix, int ld, bool vec_first, bool round_tf32, cudaStream_t s);
+void upsample2x(Elem e, const void* x, void* y, int rows, int W, int ld, cudaStream_t s);
+
+// ---- attention helpers (proj/src/tensor.cpp:163-199) -------------------------------------
+// P[i][j] = softmax_j(S[i][j] * scale) written as T with row stride ldp (cols >= S zeroed).
+void softmax_rows(Elem e, const float* S, int m, int ns, long long lds, float scale, void* P,
+                  long long ldp, cudaStream_t s);
+// Vt[c][j] = V[j][c] for j < ns (ld of V = ldv, ld of Vt = ldt)
+void transpose(Elem e, const void* V, int ns, int C, long long ldv, void* Vt, long long ldt,
+               cudaStream_t s);
+
+// ---- time embedding / condition projection ----------------------------------------------
+// emb = timestep_embedding(t, dim) (model.cpp:220-231); proj[l][c] for every AddTimeEmb
+// layer in one launch: proj = W_l emb + b_l (fp64 accumulate, fp32 result).
+struct TembLayer {
+    const float* W;   // [C][dim] fp32 (reference layout)
+    const float* b;   // [C]
+    float* out;       // [ld] fp32 (padding stays 0)
+    int C;
+};
+void time_projection(const TembLayer* layers_dev, int n_layers, int max_c, int dim, int t,
+                     cudaStream_t s);
+// v[c] = W[c][:] . cond + b[c] in fp64 (project_condition value half, model.cpp:252-263)
+void gemv_f64(const float* W, const float* b, const float* x, int rows, int cols, float* out,
+              cudaStream_t s);
+
+// ---- sampler / layout conversion -----------------------------------------------------------
+// x_nhwc (fp32 band) <- DDIM-eta0 update with eps (sampler.cpp:46-61, fp64 math) and the
+// next step's stem input (T, NHWC, ld channels) refreshed in the same pass.
+void ddim_update(const float* x, const float* eps, float* x_out, long long n, int C,
+                 double abar_t, double abar_n, Elem e, void* stem, int stem_ld, cudaStream_t s);
+// NCHW fp32 rows [r0, r0+rows) of a (C, H, W) image -> NHWC band (T or fp32) with ld.
+void nchw_to_nhwc(const float* src, int C, int H, int W, int r0, int rows, Elem e, void* dst,
+                  int ld, bool round_tf32, cudaStream_t s);
+// NHWC band (T or fp32) -> NCHW fp32 band (C, rows, W); sets *nonfinite if any value is
+// not finite (require_finite, tensor.cpp:36-42).
+void nhwc_to_nchw(Elem e, const void* src, int ld, int C, int rows, int W, float* dst,
+                  int* nonfinite, cudaStream_t s);
+void nhwc_f32_to_nchw(const float* src, int C, int rows, int W, float* dst, int* nonfinite,
+                      cudaStream_t s);
+void f32_to_elem(const float* src, Elem e, void* dst, long long n, bool round_tf32,
+                 cudaStream_t s);
+void elem_to_f32(Elem e, const void* src, float* dst, long long n, cudaStream_t s);
+
+}  // namespace pp

@@ -1,0 +1,118 @@
+// B200 host runtime for displaced patch parallelism.
+//
+// Replaces PatchRunner (proj/include/patchsim/runtime.hpp:57-108,
+// proj/src/runtime.cpp:110-476).  Each row band ("device" in the reference) is a
+// Program: the layer graph compiled for that band's geometry into fused
+// sm_100a launches on the band's CUDA device, with its own compute stream and
+// comm stream.  Context exchange follows the reference's step semantics
+// exactly (posted at layer l of step s, consumed at layer l of step s+1 in
+// displaced steps; posted and consumed in the same step in synchronous ones),
+// but moves only what the operators read:
+//   Conv / DownConv  -> one halo row from each neighbour (DownConv: the row above);
+//   SelfAttn         -> the full K/V map (all-gather of the bands);
+//   GroupNorm        -> per-group (mean, mean_sq) of every band (all-gather).
+// Stale context lives in parity double buffers indexed by step % 2.
+#pragma once
+#include "gemm.hpp"
+#include "kernels.hpp"
+#include "model.hpp"
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+namespace pp {
+
+enum RunMode : int { MODE_REFERENCE = 0, MODE_NAIVE = 1, MODE_SYNC = 2, MODE_DISPLACED = 3 };
+enum GnScheme : int { GN_CORRECTED = 0, GN_STALE = 1, GN_SEPARATE = 2 };
+enum StepEntry : int { STEP_RUN = 0, STEP_REFERENCE = 1, STEP_NAIVE = 2, STEP_SYNC = 3, STEP_DISPLACED = 4 };
+
+struct RunnerOptions {
+    int mode = MODE_REFERENCE;
+    int n_devices = 1;
+    int warmup = 4;
+    int gn_scheme = GN_CORRECTED;
+    Elem elem = Elem::BF16;
+    int world = 1, rank = 0;          // world > 1: one band per process, NCCL exchange
+    std::vector<uint8_t> nccl_id;     // 128-byte ncclUniqueId (world > 1)
+    int device = 0;                   // CUDA device of band 0 / of this rank
+    bool profile = false;
+};
+
+struct CommVolumes {
+    uint64_t allgather_recv = 0, allgather_sent = 0;
+    uint64_t halo_recv = 0, halo_sent = 0;
+    uint64_t statreduce_recv = 0, statreduce_sent = 0;
+};
+
+struct ProfileTotals {
+    double conv_ms = 0, conv_flops = 0, gemm_ms = 0, gemm_flops = 0, gn_ms = 0, other_ms = 0;
+    long launches = 0;
+};
+
+struct DeviceWeights;  // packed weights on one CUDA device
+struct Program;        // one band compiled for one CUDA device
+class Transport;
+
+class Runner {
+public:
+    Runner(const Model& m, const std::vector<float>& cond, int h, int w, const RunnerOptions& o);
+    ~Runner();
+    Runner(const Runner&) = delete;
+    Runner& operator=(const Runner&) = delete;
+
+    // run_step / step_* (runtime.cpp:382-476): full NCHW host x and eps.
+    void step(int entry, const float* x, int t, int step_index, float* eps);
+    // sample() (sampler.cpp:76-95) with the DDIM update on the GPU.
+    void sample(const float* x_T, const int* timesteps, int num_steps, const double* abar,
+                int schedule_steps, float* x0, float* trajectory);
+
+    const PatchSpec& patch_spec(int device) const;
+    long cached_input(int device, int layer, float* dst, int* nchw4);
+    uint64_t total_macs() const { return total_macs_; }
+    std::vector<uint64_t> step_device_macs(int step) const;
+    CommVolumes volumes() const { return volumes_; }
+    ProfileTotals profile() const { return prof_; }
+    long launches() const { return launches_; }
+    int n_devices() const { return n_dev_; }
+
+private:
+    friend struct Program;
+    friend class Transport;
+    void check_displaced_ready(int step_index) const;
+    void run_bands(int t, int step_index, bool displaced);   // eps left on the devices
+    void run_naive_patches(int t, int step_index);           // naive: eps_full_ on device 0
+    void load_x(const float* x_host_nchw);                    // x -> every band's stem input
+    void store_eps(float* eps_host_nchw);                     // band eps -> host NCHW
+    void check_flags(const char* who);
+    void count_macs(int step_index, bool naive);
+    void begin_profile();
+    void end_profile();
+
+    const Model& m_;
+    std::vector<float> cond_;
+    RunnerOptions o_;
+    int h_, w_, n_dev_;
+    std::vector<PatchSpec> specs_;
+    std::vector<std::unique_ptr<DeviceWeights>> weights_;   // one per CUDA device used
+    std::vector<std::unique_ptr<Program>> bands_;            // local bands
+    std::vector<std::unique_ptr<Program>> naive_rows_, naive_cols_;
+    std::unique_ptr<Transport> transport_;
+    std::vector<int> posted_;      // per layer: last step whose gather exchange was posted
+    std::vector<int> gn_posted_;   // per layer: last step whose GN stats were posted
+    uint64_t total_macs_ = 0;
+    std::vector<std::vector<uint64_t>> step_device_macs_;
+    CommVolumes volumes_;
+    ProfileTotals prof_;
+    long launches_ = 0;
+    // host staging (pinned)
+    float* h_x_ = nullptr;      // full NCHW image
+    float* h_eps_ = nullptr;    // full NCHW image
+    int* h_flags_ = nullptr;
+};
+
+}  // namespace pp
