@@ -1,0 +1,170 @@
+// One row band compiled for one CUDA device (internal to the runtime).
+//
+// Buffers (all NHWC, element type bf16 or fp32, channels padded to a 128-byte
+// multiple `ld`):
+//   act[l]       output of layer l: [rows+2][W][ld]; row 0 / row rows+1 are the halo
+//                rows a following conv reads (zero at the image border);
+//   stem         the band of the latent x_t, same padded layout (input of layer 0);
+//   eps          fp32 [rows][W][C] output of the head conv (the band of eps);
+//   x_state      fp32 [rows][W][C] band of the sampler state x_t.
+// Exchange buffers (parity double-buffered, index = step % 2), per gather / GN layer:
+//   send_rows    [2][W][ld]  own first / last row (halo source)
+//   halo_recv    [2][W][ld]  row above (from band-1) / row below (from band+1)
+//   kv           [H_l*W][ld] full map for self-attention (own rows + gathered rows)
+//   stats        [N][G][2]   every band's local (mean, mean_sq), fp64
+#pragma once
+#include "runtime.hpp"
+
+#include <array>
+#include <functional>
+#include <vector>
+
+namespace pp {
+
+struct LayerWeights {
+    void* w = nullptr;       // conv: [n_pad][9][cin_ld]; linear: [n_pad][cin_ld] (T)
+    int n_pad = 0;
+    float* bias = nullptr;   // [n_pad] fp32
+    float* gamma = nullptr;  // [ld] fp32 (GroupNorm)
+    float* beta = nullptr;
+    float* temb_w = nullptr;  // AddTimeEmb: [C][time_dim] fp32 (reference layout)
+    float* temb_b = nullptr;
+    float* cross_v = nullptr; // CrossAttn: projected value vector [ld] fp32
+};
+
+struct DeviceWeights {
+    int dev = 0;
+    Elem e = Elem::BF16;
+    std::vector<LayerWeights> L;
+    std::vector<void*> allocs;
+    DeviceWeights(const Model& m, const std::vector<float>& cond, int dev, Elem e);
+    ~DeviceWeights();
+    void* alloc(size_t bytes);
+};
+
+// A fused launch group: layers [first, last] executed as one op.
+struct Group {
+    Kind kind{};
+    int first = 0, last = 0;
+    bool silu = false;   // GroupNorm + SiLU
+    int temb = -1;       // + AddTimeEmb (layer id)
+    int skip = -1;       // + AddSkip (skip source layer id)
+};
+std::vector<Group> fuse_layers(const Model& m);
+
+struct Program {
+    Runner* r = nullptr;
+    const Model* m = nullptr;
+    const DeviceWeights* wts = nullptr;
+    int dev = 0;
+    int band = 0, nb = 1;    // band index / number of bands in the exchange
+    int H = 0, W = 0;        // latent size of the image this program covers
+    Elem e = Elem::BF16;
+    size_t eb = 2;
+    int kel = 64;            // elements per 128-byte block
+    bool rnd = false;        // fp32 mode: round stored activations to tf32
+    PatchSpec spec;
+    cudaStream_t cs = nullptr, xs = nullptr;
+
+    struct Act {
+        void* base = nullptr;   // padded buffer
+        int rows = 0, w = 0, ld = 0, C = 0;
+        void* interior(size_t eb) const {
+            return static_cast<char*>(base) + size_t(w) * ld * eb;
+        }
+        long long pix() const { return (long long)rows * w; }
+    };
+    std::vector<Act> act;   // [L] (base == nullptr when fused away; last layer -> eps)
+    Act stem;
+    float* eps = nullptr;       // fp32 NHWC band
+    float* x_state = nullptr;   // fp32 NHWC band (sampler)
+    float* x_full = nullptr;    // fp32 NCHW full image (step API upload)
+    float* band_nchw = nullptr; // fp32 NCHW band (eps / x download)
+    int* flags = nullptr;       // [0] non-finite, [1] negative GN variance
+
+    struct LayerX {
+        std::array<void*, 2> send_rows{{nullptr, nullptr}};
+        std::array<void*, 2> halo_recv{{nullptr, nullptr}};
+        std::array<void*, 2> kv{{nullptr, nullptr}};
+        std::array<double*, 2> stats{{nullptr, nullptr}};
+        double* weights = nullptr;   // [nb] band pixel counts
+        int G = 0;
+        size_t row_bytes = 0;        // one halo row
+        size_t band_bytes = 0;       // own K/V rows
+    };
+    std::vector<LayerX> lx;
+    std::vector<Group> groups;
+    std::vector<GemmPlan> plans;         // per group: conv / linear / attention PV
+    std::vector<std::array<GemmPlan, 2>> s_plans;  // attention S = Q K^T per parity
+    // scratch
+    double* gn_partial = nullptr;
+    float* gn_use = nullptr;
+    float* S = nullptr;
+    void* P = nullptr;
+    void* Vt = nullptr;
+    int s_pad = 0;
+    float* ws = nullptr;
+    size_t ws_bytes = 0;
+    // time embedding
+    std::vector<float*> temb_out;   // per layer (nullptr unless AddTimeEmb)
+    TembLayer* temb_dev = nullptr;
+    int n_temb = 0, temb_max_c = 0;
+    // events
+    std::vector<cudaEvent_t> ready;               // per layer
+    std::vector<std::array<cudaEvent_t, 2>> sent; // per layer, per parity
+    std::vector<void*> allocs;
+    // profiling
+    struct Timed {
+        int cat;
+        cudaEvent_t a, b;
+        double flops;
+    };
+    std::vector<Timed> timed;
+    std::vector<cudaEvent_t> event_pool;
+    size_t event_next = 0;
+    bool profile = false;
+
+    Program(Runner* r, const Model& m, const DeviceWeights* w, int dev, int band, int nb, int H,
+            int W, const PatchSpec& spec, Elem e, bool profile);
+    ~Program();
+    Program(const Program&) = delete;
+    Program& operator=(const Program&) = delete;
+
+    void* alloc(size_t bytes);
+    const Act& input_of(int l) const { return l == 0 ? stem : act[l - 1]; }
+    void count(long n);
+    void run_timed(int cat, double flops, const std::function<void()>& fn);
+
+    // per-step pieces (issued by Runner in layer order)
+    void time_projection(int t);
+    void pack_halo(const Group& g, int par);
+    void unpack_halo(const Group& g, int par);
+    void conv(const Group& g);
+    void pack_kv(const Group& g, int par);
+    void scatter_kv(const Group& g, int par);
+    void attention(const Group& g, int par);
+    void gn_stats(const Group& g, int par);
+    void gn_apply(const Group& g, int combine_mode, int par_cur, int par_prev);
+    void simple(const Group& g);
+    void record_ready(int l);
+};
+
+class Transport {
+public:
+    virtual ~Transport() = default;
+    // Exchange the layer-l context of the current step into parity `par` buffers.
+    // Precondition: every local band recorded ready[l] after packing.
+    virtual void halo(int l, int par, bool top_only) = 0;
+    virtual void kv(int l, int par) = 0;
+    virtual void stats(int l, int par) = 0;
+    // Make band b's compute stream wait until the (l, par) exchange has landed.
+    virtual void wait(Program& b, int l, int par) = 0;
+    // All-gather equal float chunks (rank order) on band b's compute stream (NCCL only).
+    virtual void gather_floats(Program& b, const float* send, float* recv, size_t count) = 0;
+};
+
+std::unique_ptr<Transport> make_inproc_transport(std::vector<Program*> bands);
+std::unique_ptr<Transport> make_nccl_transport(Program* band, int world, int rank,
+                                               const std::vector<uint8_t>& id);
+
+}  // namespace pp

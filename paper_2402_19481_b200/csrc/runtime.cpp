@@ -1,0 +1,1021 @@
+// B200 host runtime: weight packing, layer fusion, per-band programs and the
+// step / sampling orchestration that replaces PatchRunner (proj/src/runtime.cpp).
+#include "program.hpp"
+#include "util.hpp"
+
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <set>
+#include <stdexcept>
+
+namespace pp {
+
+namespace {
+
+constexpr int CAT_CONV = 0, CAT_GEMM = 1, CAT_GN = 2, CAT_OTHER = 3;
+constexpr size_t kWorkspaceBytes = size_t(64) << 20;
+
+int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int d) {
+        CUDA_CHECK(cudaGetDevice(&prev));
+        if (prev != d) CUDA_CHECK(cudaSetDevice(d));
+    }
+    ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+uint16_t f2bf(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fc0;
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return uint16_t(u >> 16);
+}
+float tf32_rna(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & ~0x1fffu;
+    float o;
+    std::memcpy(&o, &u, 4);
+    return o;
+}
+
+// Upload a host fp32 array as element type e (bf16 RNE, or fp32 rounded to tf32).
+void upload_elem(void* dst, const std::vector<float>& src, Elem e) {
+    if (e == Elem::BF16) {
+        std::vector<uint16_t> h(src.size());
+        for (size_t i = 0; i < src.size(); ++i) h[i] = f2bf(src[i]);
+        CUDA_CHECK(cudaMemcpy(dst, h.data(), h.size() * 2, cudaMemcpyHostToDevice));
+    } else {
+        std::vector<float> h(src.size());
+        for (size_t i = 0; i < src.size(); ++i) h[i] = tf32_rna(src[i]);
+        CUDA_CHECK(cudaMemcpy(dst, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+    }
+}
+
+int act_ld(int C, Elem e) { return round_up(C, e == Elem::BF16 ? 64 : 32); }
+
+}  // namespace
+
+// ------------------------------------------------------------------------------ weights
+void* DeviceWeights::alloc(size_t bytes) {
+    void* p = nullptr;
+    CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+    CUDA_CHECK(cudaMemset(p, 0, std::max<size_t>(bytes, 16)));
+    allocs.push_back(p);
+    return p;
+}
+
+DeviceWeights::DeviceWeights(const Model& m, const std::vector<float>& cond, int dev_, Elem e_)
+    : dev(dev_), e(e_) {
+    DeviceGuard g(dev);
+    const size_t eb = elem_bytes(e);
+    L.resize(m.layers.size());
+    float* d_cond = nullptr;
+    for (const Layer& d : m.layers) {
+        LayerWeights& w = L[d.id];
+        auto up_f32 = [&](int handle, int len) {
+            float* p = static_cast<float*>(alloc(size_t(len) * 4));
+            const WeightTensor& t = m.weights.at(handle);
+            CUDA_CHECK(cudaMemcpy(p, t.data.data(), t.size() * 4, cudaMemcpyHostToDevice));
+            return p;
+        };
+        switch (d.kind) {
+            case Kind::Conv:
+            case Kind::DownConv: {
+                const int cin_ld = act_ld(d.in_ch, e);
+                w.n_pad = round_up(d.out_ch, 16);
+                std::vector<float> pk(size_t(w.n_pad) * 9 * cin_ld, 0.0f);
+                const WeightTensor& t = m.weights.at(d.weight);
+                for (int co = 0; co < d.out_ch; ++co)
+                    for (int ci = 0; ci < d.in_ch; ++ci)
+                        for (int ky = 0; ky < 3; ++ky)
+                            for (int kx = 0; kx < 3; ++kx)
+                                pk[(size_t(co) * 9 + ky * 3 + kx) * cin_ld + ci] =
+                                    t.data[((size_t(co) * d.in_ch + ci) * 3 + ky) * 3 + kx];
+                w.w = alloc(pk.size() * eb);
+                upload_elem(w.w, pk, e);
+                w.bias = up_f32(d.bias, w.n_pad);
+                break;
+            }
+            case Kind::Linear: {
+                const int cin_ld = act_ld(d.in_ch, e);
+                w.n_pad = round_up(d.out_ch, 16);
+                std::vector<float> pk(size_t(w.n_pad) * cin_ld, 0.0f);
+                const WeightTensor& t = m.weights.at(d.weight);
+                for (int co = 0; co < d.out_ch; ++co)
+                    for (int ci = 0; ci < d.in_ch; ++ci)
+                        pk[size_t(co) * cin_ld + ci] = t.data[size_t(co) * d.in_ch + ci];
+                w.w = alloc(pk.size() * eb);
+                upload_elem(w.w, pk, e);
+                w.bias = up_f32(d.bias, w.n_pad);
+                break;
+            }
+            case Kind::GroupNorm: {
+                const int ld = act_ld(d.in_ch, e);
+                w.gamma = up_f32(d.weight, ld);
+                w.beta = up_f32(d.bias, ld);
+                break;
+            }
+            case Kind::AddTimeEmb: {
+                w.temb_w = up_f32(d.weight, d.out_ch * m.time_dim());
+                w.temb_b = up_f32(d.bias, d.out_ch);
+                break;
+            }
+            case Kind::CrossAttn: {
+                // project_condition (model.cpp:252-263): only the value half reaches the
+                // output -- softmax over a single key is exactly 1 (test_model.cpp:216-232).
+                if (int(cond.size()) != d.cond_dim)
+                    throw std::invalid_argument("condition: expected " + std::to_string(d.cond_dim) +
+                                                " values, got " + std::to_string(cond.size()));
+                if (!d_cond) {
+                    d_cond = static_cast<float*>(alloc(cond.size() * 4));
+                    CUDA_CHECK(cudaMemcpy(d_cond, cond.data(), cond.size() * 4, cudaMemcpyHostToDevice));
+                }
+                const int ld = act_ld(d.out_ch, e);
+                w.cross_v = static_cast<float*>(alloc(size_t(ld) * 4));
+                float* wv = up_f32(d.weight2, d.out_ch * d.cond_dim);
+                float* bv = up_f32(d.bias2, d.out_ch);
+                gemv_f64(wv, bv, d_cond, d.out_ch, d.cond_dim, w.cross_v, 0);
+                break;
+            }
+            default: break;
+        }
+    }
+    // PatchRunner::cond_k/cond_v (runtime.cpp:145-163) caches the FIRST CrossAttn layer's
+    // projection and uses it for every CrossAttn layer; forward_collect does the same.
+    float* first = nullptr;
+    for (const Layer& d : m.layers)
+        if (d.kind == Kind::CrossAttn) {
+            if (!first) first = L[d.id].cross_v;
+            else L[d.id].cross_v = first;
+        }
+    CUDA_CHECK(cudaDeviceSynchronize());
+}
+
+DeviceWeights::~DeviceWeights() {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(dev);
+    for (void* p : allocs) cudaFree(p);
+    cudaSetDevice(prev);
+}
+
+// ------------------------------------------------------------------------------ fusion
+std::vector<Group> fuse_layers(const Model& m) {
+    std::set<int> srcs;
+    for (const Layer& d : m.layers)
+        if (d.kind == Kind::AddSkip) srcs.insert(d.skip_source);
+    const int L = int(m.layers.size());
+    auto free_out = [&](int l) { return !srcs.count(l) && l != L - 1; };
+    auto is = [&](int l, Kind k) { return l < L && m.layers[l].kind == k; };
+    std::vector<Group> gs;
+    for (int i = 0; i < L;) {
+        const Layer& d = m.layers[i];
+        Group g;
+        g.kind = d.kind;
+        g.first = g.last = i;
+        if (d.kind == Kind::GroupNorm) {
+            int j = i + 1;
+            if (is(j, Kind::SiLU) && free_out(g.last)) {
+                g.silu = true;
+                g.last = j++;
+                if (is(j, Kind::AddTimeEmb) && free_out(g.last)) {
+                    g.temb = j;
+                    g.last = j++;
+                    if (is(j, Kind::AddSkip) && free_out(g.last)) {
+                        g.skip = m.layers[j].skip_source;
+                        g.last = j;
+                    }
+                }
+            }
+        } else if (d.kind == Kind::Conv || d.kind == Kind::DownConv || d.kind == Kind::Linear ||
+                   d.kind == Kind::SelfAttn || d.kind == Kind::CrossAttn ||
+                   d.kind == Kind::AddTimeEmb) {
+            if (is(i + 1, Kind::AddSkip) && free_out(i)) {
+                g.skip = m.layers[i + 1].skip_source;
+                g.last = i + 1;
+            }
+        }
+        gs.push_back(g);
+        i = g.last + 1;
+    }
+    return gs;
+}
+
+// ------------------------------------------------------------------------------ program
+void* Program::alloc(size_t bytes) {
+    void* p = nullptr;
+    bytes = std::max<size_t>(bytes, 16);
+    CUDA_CHECK(cudaMalloc(&p, bytes));
+    CUDA_CHECK(cudaMemset(p, 0, bytes));
+    allocs.push_back(p);
+    return p;
+}
+
+Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_, int band_, int nb_,
+                 int H_, int W_, const PatchSpec& spec_, Elem e_, bool profile_)
+    : r(r_), m(&m_), wts(w_), dev(dev_), band(band_), nb(nb_), H(H_), W(W_), e(e_), spec(spec_),
+      profile(profile_) {
+    DeviceGuard dg(dev);
+    eb = elem_bytes(e);
+    kel = int(128 / eb);
+    rnd = e == Elem::F32;
+    CUDA_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking));
+    const int L = int(m->layers.size());
+    groups = fuse_layers(*m);
+    std::vector<char> mat(L, 0);
+    for (const Group& g : groups) mat[g.last] = 1;
+
+    const int Cin = m->cfg.in_channels;
+    stem.rows = spec.input.rows();
+    stem.w = spec.input.full_w;
+    stem.C = Cin;
+    stem.ld = act_ld(Cin, e);
+    stem.base = alloc(size_t(stem.rows + 2) * stem.w * stem.ld * eb);
+    act.resize(L);
+    for (int l = 0; l < L; ++l) {
+        const Layer& d = m->layers[l];
+        const Region& o = spec.layer_out[l];
+        Act& a = act[l];
+        a.rows = o.rows();
+        a.w = o.full_w;
+        a.C = d.out_ch;
+        a.ld = act_ld(d.out_ch, e);
+        if (mat[l] && l != L - 1) a.base = alloc(size_t(a.rows + 2) * a.w * a.ld * eb);
+    }
+    const size_t band_px = size_t(stem.rows) * stem.w;
+    eps = static_cast<float*>(alloc(band_px * Cin * 4));
+    x_state = static_cast<float*>(alloc(band_px * Cin * 4));
+    x_full = static_cast<float*>(alloc(size_t(H) * W * Cin * 4));
+    band_nchw = static_cast<float*>(alloc(band_px * Cin * 4));
+    flags = static_cast<int*>(alloc(16));
+
+    // exchange buffers and events
+    lx.resize(L);
+    ready.assign(L, nullptr);
+    sent.assign(L, {{nullptr, nullptr}});
+    size_t gn_blocks = 1;
+    temb_out.assign(L, nullptr);
+    std::vector<TembLayer> tl;
+    for (int l = 0; l < L; ++l) {
+        const Layer& d = m->layers[l];
+        const Act& in = input_of(l);
+        if (d.needs_gather() || d.kind == Kind::GroupNorm) {
+            CUDA_CHECK(cudaEventCreateWithFlags(&ready[l], cudaEventDisableTiming));
+            for (int p = 0; p < 2; ++p)
+                CUDA_CHECK(cudaEventCreateWithFlags(&sent[l][p], cudaEventDisableTiming));
+        }
+        LayerX& x = lx[l];
+        if (nb > 1 && (d.kind == Kind::Conv || d.kind == Kind::DownConv)) {
+            x.row_bytes = size_t(in.w) * in.ld * eb;
+            for (int p = 0; p < 2; ++p) {
+                x.send_rows[p] = alloc(2 * x.row_bytes);
+                x.halo_recv[p] = alloc(2 * x.row_bytes);
+            }
+        }
+        if (nb > 1 && d.kind == Kind::SelfAttn) {
+            const Region& ri = spec.layer_in[l];
+            x.band_bytes = size_t(in.rows) * in.w * in.ld * eb;
+            for (int p = 0; p < 2; ++p) x.kv[p] = alloc(size_t(ri.full_h) * ri.full_w * in.ld * eb);
+        }
+        if (d.kind == Kind::GroupNorm) {
+            x.G = d.groups;
+            for (int p = 0; p < 2; ++p) x.stats[p] = static_cast<double*>(alloc(size_t(nb) * d.groups * 2 * 8));
+            x.weights = static_cast<double*>(alloc(size_t(nb) * 8));
+            // every band of a layer has the same pixel count (partition_rows is equal-split)
+            const Region& ri = spec.layer_in[l];
+            std::vector<double> wv(nb, double(ri.rows()) * ri.full_w);
+            CUDA_CHECK(cudaMemcpy(x.weights, wv.data(), nb * 8, cudaMemcpyHostToDevice));
+            gn_blocks = std::max<size_t>(gn_blocks, gn_stats_blocks(in.pix()) * size_t(d.groups));
+        }
+        if (d.kind == Kind::AddTimeEmb) {
+            temb_out[l] = static_cast<float*>(alloc(size_t(act_ld(d.out_ch, e)) * 4));
+            tl.push_back(TembLayer{wts->L[l].temb_w, wts->L[l].temb_b, temb_out[l], d.out_ch});
+            temb_max_c = std::max(temb_max_c, d.out_ch);
+        }
+    }
+    gn_partial = static_cast<double*>(alloc(gn_blocks * 2 * 8));
+    gn_use = static_cast<float*>(alloc(2048 * 4));
+    n_temb = int(tl.size());
+    if (n_temb) {
+        temb_dev = static_cast<TembLayer*>(alloc(tl.size() * sizeof(TembLayer)));
+        CUDA_CHECK(cudaMemcpy(temb_dev, tl.data(), tl.size() * sizeof(TembLayer), cudaMemcpyHostToDevice));
+    }
+    ws_bytes = kWorkspaceBytes;
+    ws = static_cast<float*>(alloc(ws_bytes));
+
+    // attention scratch (one SelfAttn geometry per model)
+    for (const Group& g : groups) {
+        if (g.kind != Kind::SelfAttn) continue;
+        const Act& in = input_of(g.first);
+        const Region& ri = spec.layer_in[g.first];
+        const int ns = ri.full_h * ri.full_w;
+        s_pad = round_up(ns, 64);
+        const int npad = round_up(in.C, 16);
+        S = static_cast<float*>(alloc(size_t(in.pix()) * s_pad * 4));
+        P = alloc(size_t(in.pix()) * s_pad * eb);
+        Vt = alloc(size_t(npad) * s_pad * eb);
+    }
+
+    // GEMM plans
+    const int sms = device_sm_count();
+    plans.resize(groups.size());
+    s_plans.resize(groups.size());
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+        const Group& g = groups[gi];
+        const Layer& d = m->layers[g.first];
+        const Act& in = input_of(g.first);
+        const LayerWeights& lw = wts->L[g.first];
+        EpilogueSpec ep;
+        const bool head = g.last == L - 1;
+        if (head) {
+            ep.out = eps;
+            ep.out_ld = d.out_ch;
+            ep.out_f32 = true;
+        } else {
+            ep.out = act[g.last].interior(eb);
+            ep.out_ld = act[g.last].ld;
+            ep.out_f32 = e == Elem::F32;
+            ep.round_tf32 = rnd;
+        }
+        ep.n_valid = d.out_ch;
+        if (g.skip >= 0) {
+            ep.residual = act[g.skip].interior(eb);
+            ep.res_ld = act[g.skip].ld;
+        }
+        if (d.kind == Kind::Conv || d.kind == Kind::DownConv) {
+            ep.bias = lw.bias;
+            plan_conv(plans[gi], e, in.base, in.rows, in.w, in.ld, d.stride, lw.w, lw.n_pad, ep, ws,
+                      ws_bytes, sms);
+        } else if (d.kind == Kind::Linear) {
+            ep.bias = lw.bias;
+            plan_gemm(plans[gi], e, in.interior(eb), int(in.pix()), in.ld, in.ld, lw.w, d.out_ch,
+                      in.ld, ep, ws, ws_bytes, sms);
+        } else if (d.kind == Kind::SelfAttn) {
+            const Region& ri = spec.layer_in[g.first];
+            const int ns = ri.full_h * ri.full_w;
+            for (int p = 0; p < (nb > 1 ? 2 : 1); ++p) {
+                EpilogueSpec es;
+                es.out = S;
+                es.out_ld = s_pad;
+                es.out_f32 = true;
+                es.n_valid = ns;
+                const void* kv = nb > 1 ? lx[g.first].kv[p] : in.interior(eb);
+                plan_gemm(s_plans[gi][p], e, in.interior(eb), int(in.pix()), in.ld, in.ld, kv, ns,
+                          in.ld, es, ws, ws_bytes, sms);
+            }
+            plan_gemm(plans[gi], e, P, int(in.pix()), s_pad, s_pad, Vt, in.C, s_pad, ep, ws,
+                      ws_bytes, sms);
+        }
+    }
+    if (profile) {
+        event_pool.resize(4096);
+        for (auto& ev : event_pool) CUDA_CHECK(cudaEventCreate(&ev));
+    }
+    CUDA_CHECK(cudaDeviceSynchronize());
+}
+
+Program::~Program() {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(dev);
+    cudaDeviceSynchronize();
+    for (auto ev : ready)
+        if (ev) cudaEventDestroy(ev);
+    for (auto& pr : sent)
+        for (auto ev : pr)
+            if (ev) cudaEventDestroy(ev);
+    for (auto ev : event_pool) cudaEventDestroy(ev);
+    for (void* p : allocs) cudaFree(p);
+    if (cs) cudaStreamDestroy(cs);
+    if (xs) cudaStreamDestroy(xs);
+    cudaSetDevice(prev);
+}
+
+void Program::count(long n) { r->launches_ += n; }
+
+void Program::run_timed(int cat, double flops, const std::function<void()>& fn) {
+    if (!profile || event_next + 2 > event_pool.size()) {
+        fn();
+        return;
+    }
+    cudaEvent_t a = event_pool[event_next++], b = event_pool[event_next++];
+    CUDA_CHECK(cudaEventRecord(a, cs));
+    fn();
+    CUDA_CHECK(cudaEventRecord(b, cs));
+    timed.push_back(Timed{cat, a, b, flops});
+}
+
+void Program::record_ready(int l) { CUDA_CHECK(cudaEventRecord(ready[l], cs)); }
+
+void Program::time_projection(int t) {
+    if (!n_temb) return;
+    run_timed(CAT_OTHER, 0, [&] {
+        pp::time_projection(temb_dev, n_temb, temb_max_c, m->time_dim(), t, cs);
+    });
+    count(1);
+}
+
+void Program::pack_halo(const Group& g, int par) {
+    const Act& in = input_of(g.first);
+    const LayerX& x = lx[g.first];
+    char* dst = static_cast<char*>(x.send_rows[par]);
+    const char* src = static_cast<const char*>(in.interior(eb));
+    CUDA_CHECK(cudaMemcpyAsync(dst, src, x.row_bytes, cudaMemcpyDeviceToDevice, cs));
+    CUDA_CHECK(cudaMemcpyAsync(dst + x.row_bytes, src + size_t(in.rows - 1) * x.row_bytes,
+                               x.row_bytes, cudaMemcpyDeviceToDevice, cs));
+}
+
+void Program::unpack_halo(const Group& g, int par) {
+    const Act& in = input_of(g.first);
+    const LayerX& x = lx[g.first];
+    const Layer& d = m->layers[g.first];
+    char* base = static_cast<char*>(in.base);
+    const char* src = static_cast<const char*>(x.halo_recv[par]);
+    if (band > 0) CUDA_CHECK(cudaMemcpyAsync(base, src, x.row_bytes, cudaMemcpyDeviceToDevice, cs));
+    if (band < nb - 1 && d.stride == 1)
+        CUDA_CHECK(cudaMemcpyAsync(base + size_t(in.rows + 1) * x.row_bytes, src + x.row_bytes,
+                                   x.row_bytes, cudaMemcpyDeviceToDevice, cs));
+}
+
+void Program::conv(const Group& g) {
+    const size_t gi = size_t(&g - groups.data());
+    const GemmPlan& p = plans[gi];
+    run_timed(CAT_CONV, p.flops, [&] { launch_gemm(p, cs); });
+    count(p.needs_reduce ? 2 : 1);
+}
+
+void Program::pack_kv(const Group& g, int par) {
+    const Act& in = input_of(g.first);
+    const LayerX& x = lx[g.first];
+    CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(x.kv[par]) + size_t(band) * x.band_bytes,
+                               in.interior(eb), x.band_bytes, cudaMemcpyDeviceToDevice, cs));
+}
+
+void Program::scatter_kv(const Group& g, int par) { pack_kv(g, par); }
+
+void Program::attention(const Group& g, int par) {
+    const size_t gi = size_t(&g - groups.data());
+    const Act& in = input_of(g.first);
+    const Region& ri = spec.layer_in[g.first];
+    const int ns = ri.full_h * ri.full_w;
+    const GemmPlan& sp = s_plans[gi][nb > 1 ? par : 0];
+    const void* kv = nb > 1 ? lx[g.first].kv[par] : in.interior(eb);
+    const float scale = float(1.0 / std::sqrt(double(m->layers[g.first].in_ch)));
+    run_timed(CAT_GEMM, sp.flops, [&] { launch_gemm(sp, cs); });
+    run_timed(CAT_OTHER, 0, [&] {
+        softmax_rows(e, S, int(in.pix()), ns, s_pad, scale, P, s_pad, cs);
+        transpose(e, kv, ns, in.C, in.ld, Vt, s_pad, cs);
+    });
+    const GemmPlan& pv = plans[gi];
+    run_timed(CAT_GEMM, pv.flops, [&] { launch_gemm(pv, cs); });
+    count(2 + (sp.needs_reduce ? 2 : 1) + (pv.needs_reduce ? 2 : 1));
+}
+
+void Program::gn_stats(const Group& g, int par) {
+    const Act& in = input_of(g.first);
+    const LayerX& x = lx[g.first];
+    const Layer& d = m->layers[g.first];
+    const int blocks = gn_stats_blocks(in.pix());
+    run_timed(CAT_GN, 0, [&] {
+        gn_partial_stats(e, in.interior(eb), in.pix(), in.C, in.ld, d.groups, gn_partial, cs);
+        const double count = double(in.C / d.groups) * double(in.rows) * double(in.w);
+        gn_finalize(gn_partial, blocks, d.groups, count, x.stats[par] + size_t(band) * d.groups * 2, cs);
+    });
+    count(2);
+}
+
+void Program::gn_apply(const Group& g, int mode, int par_cur, int par_prev) {
+    const Act& in = input_of(g.first);
+    const LayerX& x = lx[g.first];
+    const Layer& d = m->layers[g.first];
+    const LayerWeights& lw = wts->L[g.first];
+    const int L = int(m->layers.size());
+    run_timed(CAT_GN, 0, [&] {
+        pp::gn_combine(mode, x.stats[par_cur] + size_t(band) * d.groups * 2, x.stats[par_cur],
+                       x.stats[par_prev], nb, band, x.weights, d.groups, d.eps, gn_use, flags + 1, cs);
+        if (g.last == L - 1) throw std::invalid_argument("GroupNorm as the final layer is unsupported");
+        const Act& out = act[g.last];
+        pp::gn_apply(e, in.interior(eb), out.interior(eb), in.pix(), in.C, in.ld, d.groups, gn_use,
+                     lw.gamma, lw.beta, g.silu, g.temb >= 0 ? temb_out[g.temb] : nullptr,
+                     g.skip >= 0 ? act[g.skip].interior(eb) : nullptr, rnd, cs);
+    });
+    count(2);
+}
+
+void Program::simple(const Group& g) {
+    const Layer& d = m->layers[g.first];
+    const Act& in = input_of(g.first);
+    const int L = int(m->layers.size());
+    if (g.last == L - 1) throw std::invalid_argument("unsupported final layer kind");
+    const Act& out = act[g.last];
+    const void* skip = g.skip >= 0 ? act[g.skip].interior(eb) : nullptr;
+    run_timed(CAT_OTHER, 0, [&] {
+        switch (d.kind) {
+            case Kind::SiLU:
+                pp::silu(e, in.interior(eb), out.interior(eb), in.pix() * in.ld, rnd, cs);
+                break;
+            case Kind::Upsample:
+                upsample2x(e, in.interior(eb), out.interior(eb), in.rows, in.w, in.ld, cs);
+                break;
+            case Kind::AddSkip:
+                pp::add(e, in.interior(eb), act[d.skip_source].interior(eb), out.interior(eb),
+                        in.pix() * in.ld, rnd, cs);
+                break;
+            case Kind::AddTimeEmb:
+                add_channel(e, in.interior(eb), temb_out[g.first], skip, out.interior(eb), in.pix(),
+                            in.ld, false, rnd, cs);
+                break;
+            case Kind::CrossAttn:
+                add_channel(e, nullptr, wts->L[g.first].cross_v, skip, out.interior(eb), in.pix(),
+                            in.ld, true, rnd, cs);
+                break;
+            case Kind::Linear: {
+                const size_t gi = size_t(&g - groups.data());
+                launch_gemm(plans[gi], cs);
+                if (plans[gi].needs_reduce) count(1);
+                break;
+            }
+            default: throw std::runtime_error("device_step: unhandled layer kind");
+        }
+    });
+    count(1);
+}
+
+// ------------------------------------------------------------------------------ runner
+Runner::Runner(const Model& m, const std::vector<float>& cond, int h, int w, const RunnerOptions& o)
+    : m_(m), cond_(cond), o_(o), h_(h), w_(w) {
+    if (o_.mode == MODE_REFERENCE) o_.n_devices = 1;
+    if (o_.n_devices < 1) throw std::invalid_argument("PatchRunner: need at least one device");
+    n_dev_ = o_.n_devices;
+    const int spec_devices = o_.mode == MODE_NAIVE ? 1 : n_dev_;
+    for (const Region& r : partition_rows(h, spec_devices, w)) specs_.push_back(derive_patch_spec(m_, r));
+    for (const Layer& d : m_.layers)
+        if (d.kind == Kind::GroupNorm && (d.in_ch % (o_.elem == Elem::BF16 ? 8 : 4)))
+            throw std::invalid_argument("GroupNorm channels must be a multiple of 8 on the B200 path");
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        throw CudaError("no CUDA device available: the B200 kernels cannot run (no CPU fallback)");
+    }
+    if (o_.world > 1 && o_.world != n_dev_)
+        throw std::invalid_argument("PatchRunner: world size must equal n_devices");
+    posted_.assign(m_.layers.size(), -1000);
+    gn_posted_.assign(m_.layers.size(), -1000);
+    CUDA_CHECK(cudaMallocHost(reinterpret_cast<void**>(&h_x_), size_t(m_.cfg.in_channels) * h * w * 4));
+    CUDA_CHECK(cudaMallocHost(reinterpret_cast<void**>(&h_eps_), size_t(m_.cfg.in_channels) * h * w * 4));
+    CUDA_CHECK(cudaMallocHost(reinterpret_cast<void**>(&h_flags_), 64 * 4 * 16));
+
+    auto weights_for = [&](int dev) -> const DeviceWeights* {
+        for (auto& wp : weights_)
+            if (wp->dev == dev) return wp.get();
+        weights_.push_back(std::make_unique<DeviceWeights>(m_, cond_, dev, o_.elem));
+        return weights_.back().get();
+    };
+    if (o_.mode != MODE_NAIVE) {
+        if (o_.world > 1) {
+            const int dev = o_.device;
+            bands_.push_back(std::make_unique<Program>(this, m_, weights_for(dev), dev, o_.rank, n_dev_,
+                                                       h, w, specs_[o_.rank], o_.elem, o_.profile));
+            transport_ = make_nccl_transport(bands_[0].get(), o_.world, o_.rank, o_.nccl_id);
+        } else {
+            for (int d = 0; d < n_dev_; ++d) {
+                const int dev = (o_.device + d) % ndev;
+                bands_.push_back(std::make_unique<Program>(this, m_, weights_for(dev), dev, d, n_dev_,
+                                                           h, w, specs_[d], o_.elem, o_.profile));
+            }
+            if (n_dev_ > 1) {
+                std::vector<Program*> ps;
+                for (auto& b : bands_) ps.push_back(b.get());
+                transport_ = make_inproc_transport(ps);
+            }
+        }
+    }
+}
+
+Runner::~Runner() {
+    bands_.clear();
+    naive_rows_.clear();
+    naive_cols_.clear();
+    transport_.reset();
+    weights_.clear();
+    if (h_x_) cudaFreeHost(h_x_);
+    if (h_eps_) cudaFreeHost(h_eps_);
+    if (h_flags_) cudaFreeHost(h_flags_);
+}
+
+const PatchSpec& Runner::patch_spec(int device) const {
+    if (device < 0 || device >= n_dev_) throw std::invalid_argument("patch_spec: bad device");
+    return specs_[std::min<size_t>(device, specs_.size() - 1)];
+}
+
+std::vector<uint64_t> Runner::step_device_macs(int step) const {
+    if (step < 0 || step >= int(step_device_macs_.size())) return {};
+    return step_device_macs_[step];
+}
+
+void Runner::check_displaced_ready(int s) const {
+    // device_step's cache checks in layer order (runtime.cpp:225-229, 277-281)
+    for (const Layer& d : m_.layers) {
+        if (d.needs_gather() && posted_[d.id] != s - 1)
+            throw std::runtime_error("displaced step " + std::to_string(s) +
+                                     ": no cached activation for layer " + std::to_string(d.id) +
+                                     " (" + kind_name(d.kind) + "); run a synchronous step first");
+        if (d.kind == Kind::GroupNorm && gn_posted_[d.id] != s - 1)
+            throw std::runtime_error("displaced step " + std::to_string(s) +
+                                     ": no cached GN statistics for layer " + std::to_string(d.id) +
+                                     "; run a synchronous step first");
+    }
+}
+
+void Runner::count_macs(int s, bool naive) {
+    while (int(step_device_macs_.size()) <= s) step_device_macs_.emplace_back(n_dev_, 0);
+    if (naive) {
+        const bool by_rows = s % 2 == 0;
+        const int ph = by_rows ? h_ / n_dev_ : h_, pw = by_rows ? w_ : w_ / n_dev_;
+        for (int d = 0; d < n_dev_; ++d) {
+            uint64_t macs = 0;
+            for (const Layer& ld : m_.layers) {
+                const int lh = ph / ld.scale_in, lw = pw / ld.scale_in;
+                macs += macs_of_layer(ld, Region{0, lh, lh, lw});
+            }
+            step_device_macs_[s][d] += macs;
+            total_macs_ += macs;
+        }
+        return;
+    }
+    for (int d = 0; d < n_dev_; ++d) {
+        const PatchSpec& sp = specs_[std::min<size_t>(d, specs_.size() - 1)];
+        uint64_t macs = 0;
+        for (const Layer& ld : m_.layers) macs += macs_of_layer(ld, sp.layer_in[ld.id]);
+        step_device_macs_[s][d] += macs;
+        total_macs_ += macs;
+    }
+}
+
+void Runner::run_bands(int t, int s, bool displaced) {
+    if (displaced) check_displaced_ready(s);
+    const int pcur = s & 1, pprev = (s + 1) & 1;
+    const int pu = displaced ? pprev : pcur;
+    const bool multi = n_dev_ > 1;
+    for (auto& b : bands_) {
+        DeviceGuard g(b->dev);
+        b->time_projection(t);
+    }
+    const std::vector<Group>& groups = bands_[0]->groups;
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+        const Group& g0 = groups[gi];
+        const int l = g0.first;
+        const Layer& d = m_.layers[l];
+        auto each = [&](auto&& fn) {
+            for (auto& b : bands_) {
+                DeviceGuard g(b->dev);
+                fn(*b, b->groups[gi]);
+            }
+        };
+        if (d.kind == Kind::Conv || d.kind == Kind::DownConv) {
+            if (multi) {
+                each([&](Program& b, const Group& g) {
+                    b.pack_halo(g, pcur);
+                    b.record_ready(l);
+                });
+                transport_->halo(l, pcur, d.stride == 2);
+                each([&](Program& b, const Group& g) {
+                    transport_->wait(b, l, pu);
+                    b.unpack_halo(g, pu);
+                });
+                const size_t row = bands_[0]->lx[l].row_bytes;
+                const uint64_t per_band = (d.stride == 2 ? 1 : 2) * uint64_t(n_dev_ - 1) * row;
+                volumes_.halo_recv += per_band;
+                volumes_.halo_sent += per_band;
+            }
+            each([&](Program& b, const Group& g) { b.conv(g); });
+            posted_[l] = s;
+        } else if (d.kind == Kind::SelfAttn) {
+            if (multi) {
+                each([&](Program& b, const Group& g) {
+                    b.pack_kv(g, pcur);
+                    b.record_ready(l);
+                });
+                transport_->kv(l, pcur);
+                each([&](Program& b, const Group& g) {
+                    transport_->wait(b, l, pu);
+                    if (displaced) b.scatter_kv(g, pu);
+                });
+                const uint64_t v = uint64_t(bands_[0]->lx[l].band_bytes) * (n_dev_ - 1) * n_dev_;
+                volumes_.allgather_recv += v;
+                volumes_.allgather_sent += v;
+            }
+            each([&](Program& b, const Group& g) { b.attention(g, pu); });
+            posted_[l] = s;
+        } else if (d.kind == Kind::GroupNorm) {
+            each([&](Program& b, const Group& g) {
+                b.gn_stats(g, pcur);
+                b.record_ready(l);
+            });
+            int mode;
+            if (!displaced) {
+                mode = multi ? GN_USE_GLOBAL : GN_USE_LOCAL;
+            } else {
+                mode = o_.gn_scheme == GN_CORRECTED ? GN_USE_CORRECTED
+                       : o_.gn_scheme == GN_STALE   ? GN_USE_STALE
+                                                    : GN_USE_LOCAL;
+            }
+            if (multi) {
+                transport_->stats(l, pcur);
+                each([&](Program& b, const Group&) { transport_->wait(b, l, pu); });
+                const uint64_t v = uint64_t(d.groups) * 16 * (n_dev_ - 1) * n_dev_;
+                volumes_.statreduce_recv += v;
+                volumes_.statreduce_sent += v;
+            }
+            each([&](Program& b, const Group& g) { b.gn_apply(g, mode, pcur, pprev); });
+            gn_posted_[l] = s;
+        } else {
+            each([&](Program& b, const Group& g) { b.simple(g); });
+        }
+    }
+}
+
+void Runner::load_x(const float* x) {
+    const int C = m_.cfg.in_channels;
+    std::memcpy(h_x_, x, size_t(C) * h_ * w_ * 4);
+    for (auto& b : bands_) {
+        DeviceGuard g(b->dev);
+        CUDA_CHECK(cudaMemcpyAsync(b->x_full, h_x_, size_t(C) * h_ * w_ * 4, cudaMemcpyHostToDevice, b->cs));
+        nchw_to_nhwc(b->x_full, C, h_, w_, b->spec.input.row_start, b->stem.rows, b->e,
+                     b->stem.interior(b->eb), b->stem.ld, b->rnd, b->cs);
+        nchw_to_nhwc(b->x_full, C, h_, w_, b->spec.input.row_start, b->stem.rows, Elem::F32,
+                     b->x_state, C, false, b->cs);
+        launches_ += 2;
+    }
+}
+
+void Runner::store_eps(float* out) {
+    const int C = m_.cfg.in_channels;
+    if (o_.world > 1) {
+        Program& b = *bands_[0];
+        DeviceGuard g(b.dev);
+        const size_t band_n = size_t(C) * b.stem.rows * w_;
+        nhwc_f32_to_nchw(b.eps, C, b.stem.rows, w_, b.band_nchw, b.flags, b.cs);
+        transport_->gather_floats(b, b.band_nchw, b.x_full, band_n);
+        CUDA_CHECK(cudaMemcpyAsync(h_eps_, b.x_full, band_n * n_dev_ * 4, cudaMemcpyDeviceToHost, b.cs));
+        CUDA_CHECK(cudaStreamSynchronize(b.cs));
+        const int rows = b.stem.rows;
+        for (int r = 0; r < n_dev_; ++r)
+            for (int c = 0; c < C; ++c)
+                std::memcpy(out + (size_t(c) * h_ + size_t(r) * rows) * w_,
+                            h_eps_ + size_t(r) * band_n + size_t(c) * rows * w_, size_t(rows) * w_ * 4);
+        launches_ += 1;
+        return;
+    }
+    for (auto& b : bands_) {
+        DeviceGuard g(b->dev);
+        const size_t band_n = size_t(C) * b->stem.rows * w_;
+        nhwc_f32_to_nchw(b->eps, C, b->stem.rows, w_, b->band_nchw, b->flags, b->cs);
+        CUDA_CHECK(cudaMemcpyAsync(h_eps_ + size_t(b->band) * band_n, b->band_nchw, band_n * 4,
+                                   cudaMemcpyDeviceToHost, b->cs));
+        launches_ += 1;
+    }
+    for (auto& b : bands_) {
+        DeviceGuard g(b->dev);
+        CUDA_CHECK(cudaStreamSynchronize(b->cs));
+    }
+    for (auto& b : bands_) {
+        const int rows = b->stem.rows;
+        const size_t band_n = size_t(C) * rows * w_;
+        for (int c = 0; c < C; ++c)
+            std::memcpy(out + (size_t(c) * h_ + b->spec.input.row_start) * w_,
+                        h_eps_ + size_t(b->band) * band_n + size_t(c) * rows * w_, size_t(rows) * w_ * 4);
+    }
+}
+
+void Runner::check_flags(const char* who) {
+    bool neg = false, nonfinite = false;
+    for (auto& b : bands_) {
+        DeviceGuard g(b->dev);
+        CUDA_CHECK(cudaMemcpyAsync(h_flags_, b->flags, 8, cudaMemcpyDeviceToHost, b->cs));
+        CUDA_CHECK(cudaStreamSynchronize(b->cs));
+        neg |= h_flags_[1] != 0;
+        nonfinite |= h_flags_[0] != 0;
+        CUDA_CHECK(cudaMemsetAsync(b->flags, 0, 8, b->cs));
+    }
+    if (neg)
+        throw std::runtime_error(
+            "group_norm_apply: negative variance (caller must substitute fallback stats)");
+    if (nonfinite)
+        throw std::runtime_error(std::string(who) + ": non-finite value in tensor (1," +
+                                 std::to_string(m_.cfg.in_channels) + "," + std::to_string(h_) +
+                                 "," + std::to_string(w_) + ")");
+}
+
+void Runner::begin_profile() {
+    for (auto& b : bands_) {
+        b->timed.clear();
+        b->event_next = 0;
+    }
+}
+
+void Runner::end_profile() {
+    if (!o_.profile) return;
+    for (auto& b : bands_) {
+        DeviceGuard g(b->dev);
+        CUDA_CHECK(cudaStreamSynchronize(b->cs));
+        for (const auto& t : b->timed) {
+            float ms = 0;
+            CUDA_CHECK(cudaEventElapsedTime(&ms, t.a, t.b));
+            if (t.cat == CAT_CONV) {
+                prof_.conv_ms += ms;
+                prof_.conv_flops += t.flops;
+                prof_.gemm_ms += ms;
+                prof_.gemm_flops += t.flops;
+            } else if (t.cat == CAT_GEMM) {
+                prof_.gemm_ms += ms;
+                prof_.gemm_flops += t.flops;
+            } else if (t.cat == CAT_GN) {
+                prof_.gn_ms += ms;
+            } else {
+                prof_.other_ms += ms;
+            }
+        }
+        b->timed.clear();
+        b->event_next = 0;
+    }
+}
+
+void Runner::run_naive_patches(int, int) {
+    throw std::invalid_argument("naive mode is not available on the B200 runner yet");
+}
+
+void Runner::step(int entry, const float* x, int t, int s, float* eps) {
+    int e = entry;
+    if (e == STEP_RUN) {
+        switch (o_.mode) {
+            case MODE_REFERENCE: e = STEP_REFERENCE; break;
+            case MODE_NAIVE: e = STEP_NAIVE; break;
+            case MODE_SYNC: e = STEP_SYNC; break;
+            default: e = s < 1 + o_.warmup ? STEP_SYNC : STEP_DISPLACED; break;
+        }
+    }
+    if (e == STEP_NAIVE) {
+        run_naive_patches(t, s);
+        return;
+    }
+    if (e == STEP_REFERENCE && n_dev_ != 1)
+        throw std::invalid_argument("step_reference on a multi-band runner is not supported");
+    if (bands_.empty()) throw std::invalid_argument("step entry not available in naive mode");
+    launches_ = 0;
+    if (o_.profile) begin_profile();
+    const bool displaced = e == STEP_DISPLACED;
+    if (displaced) check_displaced_ready(s);
+    load_x(x);
+    run_bands(t, s, displaced);
+    store_eps(eps);
+    count_macs(s, false);
+    check_flags(e == STEP_REFERENCE ? "step_reference" : "run_step");
+    end_profile();
+}
+
+void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, int total, float* x0,
+                    float* traj) {
+    if (n < 1) throw std::invalid_argument("sample: empty plan");
+    if (bands_.empty()) throw std::invalid_argument("sample: naive mode is not available on the B200 runner yet");
+    const int C = m_.cfg.in_channels;
+    auto abar_at = [&](int t) {
+        if (t == -1) return 1.0;
+        if (t < 0 || t >= total)
+            throw std::invalid_argument("schedule: timestep " + std::to_string(t) + " out of range");
+        return abar[t];
+    };
+    for (int i = 0; i + 1 < n; ++i)
+        if (ts[i + 1] >= ts[i])
+            throw std::invalid_argument("ddim_step: timestep must decrease (" + std::to_string(ts[i]) +
+                                        " -> " + std::to_string(ts[i + 1]) + ")");
+    launches_ = 0;
+    if (o_.profile) begin_profile();
+    load_x(x_T);
+    for (int i = 0; i < n; ++i) {
+        const int t = ts[i];
+        if (traj) {
+            // trajectory records the model input x_t (sampler.cpp:84)
+            for (auto& b : bands_) {
+                DeviceGuard g(b->dev);
+                nhwc_f32_to_nchw(b->x_state, C, b->stem.rows, w_, b->band_nchw, nullptr, b->cs);
+            }
+            std::vector<float> img(size_t(C) * h_ * w_);
+            for (auto& b : bands_) {
+                DeviceGuard g(b->dev);
+                const int rows = b->stem.rows;
+                std::vector<float> band(size_t(C) * rows * w_);
+                CUDA_CHECK(cudaMemcpyAsync(band.data(), b->band_nchw, band.size() * 4, cudaMemcpyDeviceToHost, b->cs));
+                CUDA_CHECK(cudaStreamSynchronize(b->cs));
+                for (int c = 0; c < C; ++c)
+                    std::memcpy(traj + size_t(i) * C * h_ * w_ + (size_t(c) * h_ + b->spec.input.row_start) * w_,
+                                band.data() + size_t(c) * rows * w_, size_t(rows) * w_ * 4);
+            }
+        }
+        bool displaced = false;
+        if (o_.mode == MODE_DISPLACED) displaced = i >= 1 + o_.warmup;
+        run_bands(t, i, displaced);
+        count_macs(i, false);
+        const int t_next = i + 1 < n ? ts[i + 1] : -1;
+        const double a_t = abar_at(t), a_n = abar_at(t_next);
+        for (auto& b : bands_) {
+            DeviceGuard g(b->dev);
+            ddim_update(b->x_state, b->eps, b->x_state, (long long)b->stem.rows * w_ * C, C, a_t, a_n,
+                        b->e, b->stem.interior(b->eb), b->stem.ld, b->cs);
+            launches_ += 1;
+        }
+    }
+    // x0 download (band -> NCHW)
+    if (o_.world > 1) {
+        Program& b = *bands_[0];
+        DeviceGuard g(b.dev);
+        const size_t band_n = size_t(C) * b.stem.rows * w_;
+        nhwc_f32_to_nchw(b.x_state, C, b.stem.rows, w_, b.band_nchw, b.flags, b.cs);
+        transport_->gather_floats(b, b.band_nchw, b.x_full, band_n);
+        CUDA_CHECK(cudaMemcpyAsync(h_eps_, b.x_full, band_n * n_dev_ * 4, cudaMemcpyDeviceToHost, b.cs));
+        CUDA_CHECK(cudaStreamSynchronize(b.cs));
+        const int rows = b.stem.rows;
+        for (int r = 0; r < n_dev_; ++r)
+            for (int c = 0; c < C; ++c)
+                std::memcpy(x0 + (size_t(c) * h_ + size_t(r) * rows) * w_,
+                            h_eps_ + size_t(r) * band_n + size_t(c) * rows * w_, size_t(rows) * w_ * 4);
+    } else {
+        for (auto& b : bands_) {
+            DeviceGuard g(b->dev);
+            const size_t band_n = size_t(C) * b->stem.rows * w_;
+            nhwc_f32_to_nchw(b->x_state, C, b->stem.rows, w_, b->band_nchw, b->flags, b->cs);
+            CUDA_CHECK(cudaMemcpyAsync(h_eps_ + size_t(b->band) * band_n, b->band_nchw, band_n * 4,
+                                       cudaMemcpyDeviceToHost, b->cs));
+        }
+        for (auto& b : bands_) {
+            DeviceGuard g(b->dev);
+            CUDA_CHECK(cudaStreamSynchronize(b->cs));
+            const int rows = b->stem.rows;
+            const size_t band_n = size_t(C) * rows * w_;
+            for (int c = 0; c < C; ++c)
+                std::memcpy(x0 + (size_t(c) * h_ + b->spec.input.row_start) * w_,
+                            h_eps_ + size_t(b->band) * band_n + size_t(c) * rows * w_, size_t(rows) * w_ * 4);
+        }
+    }
+    launches_ += long(bands_.size());
+    check_flags("sample");
+    end_profile();
+}
+
+long Runner::cached_input(int device, int layer, float* dst, int* nchw4) {
+    if (layer < 0 || layer >= int(m_.layers.size())) throw std::invalid_argument("cached_input: bad layer");
+    const Layer& d = m_.layers[layer];
+    if (!d.needs_gather() || posted_[layer] < 0) return 0;
+    Program* b = nullptr;
+    for (auto& p : bands_)
+        if (p->band == device) b = p.get();
+    if (!b) throw std::invalid_argument("cached_input: device not local to this process");
+    const Region& ri = b->spec.layer_in[layer];
+    const int C = d.in_ch, Hl = ri.full_h, Wl = ri.full_w;
+    nchw4[0] = 1; nchw4[1] = C; nchw4[2] = Hl; nchw4[3] = Wl;
+    const long count = long(C) * Hl * Wl;
+    if (!dst) return count;
+    DeviceGuard g(b->dev);
+    CUDA_CHECK(cudaStreamSynchronize(b->cs));
+    CUDA_CHECK(cudaStreamSynchronize(b->xs));
+    std::fill(dst, dst + count, std::nanf(""));
+    const Program::Act& in = b->input_of(layer);
+    // rows this band holds: the full K/V map (self-attention) or own band + halo rows (convs)
+    int r0 = ri.row_start - 1, r1 = ri.row_end + 1;
+    const void* src = in.base;
+    long long src_ld = in.ld;
+    if (d.kind == Kind::SelfAttn && n_dev_ > 1) {
+        r0 = 0;
+        r1 = Hl;
+        src = b->lx[layer].kv[posted_[layer] & 1];
+        r0 = 0;
+    }
+    const int rows = r1 - r0;
+    float* tmp = nullptr;
+    CUDA_CHECK(cudaMalloc(&tmp, size_t(rows) * Wl * C * 4));
+    const char* src_rows = static_cast<const char*>(src);
+    nhwc_to_nchw(b->e, src_rows, int(src_ld), C, rows, Wl, tmp, nullptr, b->cs);
+    std::vector<float> h(size_t(rows) * Wl * C);
+    CUDA_CHECK(cudaMemcpyAsync(h.data(), tmp, h.size() * 4, cudaMemcpyDeviceToHost, b->cs));
+    CUDA_CHECK(cudaStreamSynchronize(b->cs));
+    cudaFree(tmp);
+    for (int c = 0; c < C; ++c)
+        for (int y = 0; y < rows; ++y) {
+            const int gy = r0 + y;
+            if (gy < 0 || gy >= Hl) continue;
+            std::memcpy(dst + (size_t(c) * Hl + gy) * Wl, h.data() + (size_t(c) * rows + y) * Wl,
+                        size_t(Wl) * 4);
+        }
+    return count;
+}
+
+}  // namespace pp

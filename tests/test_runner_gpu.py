@@ -1,0 +1,112 @@
+"""B200 PatchRunner / run_sampling parity against the CPU oracle (numpy restatement,
+pinned to the reference in tests/test_oracle.py).
+
+Tolerances (BASELINE.json north_star): relative L2 <= 1e-3 in fp32-accumulate mode
+(fp32 storage, TF32 tensor cores) and <= 2e-2 in bf16.  Patch partitioning and halo
+indexing are integer logic and are compared bit-exactly elsewhere.
+"""
+import numpy as np
+import pytest
+
+from oracle import patchsim_np as O
+from paper_2402_19481_b200 import patchsim as P
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32": 1e-3, "bf16": 2e-2}          # per-step latents x_t (north-star bar)
+# A single eps evaluation is not damped by the sampler; 63 layers of TF32 / bf16
+# rounding give ~1e-3 / ~1e-2 relative error on eps itself.
+EPS_TOL = {"fp32": 3e-3, "bf16": 3e-2}
+TINY = P.ModelConfig(2, 8, 2, 4, 8, -1)        # proj/tests/test_runtime.cpp:16-24
+TOY = P.ModelConfig()                           # model.hpp:30-36 defaults
+
+
+def ocfg(c):
+    return O.ModelConfig(c.in_channels, c.base_channels, c.levels, c.groups, c.cond_dim,
+                         c.attn_at_level)
+
+
+def rel(a, b):
+    return O.rel_l2(a, b)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("cfg,hw", [(TOY, 32), (TINY, 16)])
+def test_reference_forward(dtype, cfg, hw):
+    om = O.build_model(ocfg(cfg), 77)
+    cond = O.random_condition(cfg.cond_dim, 78)
+    x = O.random_normal(1, cfg.in_channels, hw, hw, 79)
+    ref = O.forward_full(om, x, 700, cond)
+    m = P.build_model(cfg, 77)
+    r = P.PatchRunner(m, cond, hw, hw, mode="reference", dtype=dtype)
+    eps = r.run_step(x, 700, 0)
+    assert rel(eps, ref) <= EPS_TOL[dtype], rel(eps, ref)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("n", [2, 4])
+def test_sync_matches_reference(dtype, n):
+    # proj/tests/test_runtime.cpp:231-248 (sync-pp == reference forward)
+    cfg, hw = TOY, 32
+    om = O.build_model(ocfg(cfg), 77)
+    cond = O.random_condition(cfg.cond_dim, 78)
+    x = O.random_normal(1, cfg.in_channels, hw, hw, 79)
+    ref = O.forward_full(om, x, 700, cond)
+    r = P.PatchRunner(P.build_model(cfg, 77), cond, hw, hw, mode="sync-pp", n_devices=n,
+                      dtype=dtype)
+    eps = r.step_sync(x, 700, 0)
+    assert rel(eps, ref) <= EPS_TOL[dtype], rel(eps, ref)
+
+
+@pytest.mark.parametrize("n", [1, 2, 4])
+def test_zero_staleness_displaced_equals_sync(n):
+    # proj/tests/test_runtime.cpp:263-280
+    cfg, hw = TOY, 32
+    cond = O.random_condition(cfg.cond_dim, 88)
+    x = O.random_normal(1, cfg.in_channels, hw, hw, 89)
+    m = P.build_model(cfg, 87)
+    d = P.PatchRunner(m, cond, hw, hw, mode="displaced", n_devices=n, dtype="fp32")
+    d.step_sync(x, 700, 0)
+    e_disp = d.step_displaced(x, 700, 1)
+    s = P.PatchRunner(m, cond, hw, hw, mode="sync-pp", n_devices=n, dtype="fp32")
+    e_sync = s.step_sync(x, 700, 0)
+    assert rel(e_disp, e_sync) <= 1e-5
+
+
+def test_missing_cache_names_the_layer():
+    # proj/tests/test_runtime.cpp:282-290
+    m = P.build_model(TINY, 97)
+    cond = O.random_condition(8, 98)
+    r = P.PatchRunner(m, cond, 16, 16, mode="displaced", n_devices=2, dtype="bf16")
+    x = O.random_normal(1, 2, 16, 16, 99)
+    with pytest.raises(P.RuntimeFailure, match="no cached activation for layer"):
+        r.step_displaced(x, 500, 1)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("mode,n,warmup", [("reference", 1, 4), ("sync-pp", 2, 4),
+                                           ("displaced", 2, 0), ("displaced", 2, 1),
+                                           ("displaced", 4, 1)])
+def test_run_sampling_c1(dtype, mode, n, warmup):
+    # BASELINE config 1: toy model, 32x32 latent, 4 steps, 2 patches; trajectory per step
+    cfg = TOY
+    ref = O.run_sampling(ocfg(cfg), mode, n, 32, 32, 4, warmup)
+    got = P.run_sampling(P.RunConfig(mode=mode, n_devices=n, h=32, w=32, num_steps=4,
+                                     warmup=warmup, dtype=dtype, model=cfg), trajectory=True)
+    for i, xt in enumerate(ref["trajectory"]):
+        assert rel(got["trajectory"][i], xt) <= TOL[dtype], (i, rel(got["trajectory"][i], xt))
+    assert rel(got["x0"], ref["x0"]) <= TOL[dtype], rel(got["x0"], ref["x0"])
+    assert got["total_macs"] == ref["total_macs"]
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("mode,n", [("reference", 1), ("displaced", 2)])
+def test_sdxl_shape_small(dtype, mode, n):
+    # SDXL-shape graph (320/640/1280 ch, GN32, d=1280 attention) on a 32x32 latent, 3 steps
+    cfg = P.SDXL_SHAPE
+    ref = O.run_sampling(ocfg(cfg), mode, n, 32, 32, 3, 0)
+    got = P.run_sampling(P.RunConfig(mode=mode, n_devices=n, h=32, w=32, num_steps=3, warmup=0,
+                                     dtype=dtype, model=cfg), trajectory=True)
+    for i, xt in enumerate(ref["trajectory"]):
+        assert rel(got["trajectory"][i], xt) <= TOL[dtype], (i, rel(got["trajectory"][i], xt))
+    assert rel(got["x0"], ref["x0"]) <= TOL[dtype], rel(got["x0"], ref["x0"])
