@@ -171,6 +171,13 @@ PP_API int pp_runner_sample(pp_runner* r, const float* x_T, const int* timesteps
 PP_API int pp_runner_profile(pp_runner* r, double* out7);
 /* kernels launched by the last step / sample call */
 PP_API long pp_runner_launches(const pp_runner* r);
+/* device time (CUDA events on the band compute streams, max over local bands) of the
+ * last pp_runner_sample denoising loop, excluding the x_T upload and x0 download */
+PP_API double pp_runner_last_device_ms(const pp_runner* r);
+/* switch per-kernel CUDA-event timing on/off (resets the pp_runner_profile totals) */
+PP_API int pp_runner_set_profile(pp_runner* r, int on);
+/* ncclGetUniqueId for the multi-process (one rank per GPU) layout */
+PP_API int pp_nccl_unique_id(void* out128);
 
 /* ---- run_sampling (proj/src/runtime.cpp:494-526) ------------------------------------------ */
 PP_API int pp_run_sampling(const pp_run_config* cfg, float* x0, float* trajectory,

@@ -43,9 +43,15 @@ PP_API int pp_dev_gemm(int dtype, const void* A, int M, int K, long long lda, co
         ep.bias = bias;
         pp::GemmPlan plan;
         const size_t ws_bytes = size_t(16) * M * ((N + 15) / 16 * 16) * sizeof(float);
-        pp::DeviceScratch ws(ws_bytes);
-        pp::plan_gemm(plan, e, A, M, K, lda, B, N, ldb, ep, static_cast<float*>(ws.ptr), ws_bytes,
-                      pp::device_sm_count(), force_splits, force_block_n);
+        pp::DeviceScratch ws(ws_bytes), tk(size_t(1) << 20);
+        CUDA_CHECK(cudaMemset(tk.ptr, 0, size_t(1) << 20));
+        pp::GemmScratch sc;
+        sc.ws = static_cast<float*>(ws.ptr);
+        sc.ws_bytes = ws_bytes;
+        sc.tickets = static_cast<unsigned int*>(tk.ptr);
+        sc.n_tickets = (size_t(1) << 20) / 4;
+        pp::plan_gemm(plan, e, A, M, K, lda, B, N, ldb, ep, sc, pp::device_sm_count(), force_splits,
+                      force_block_n);
         pp::launch_gemm(plan, static_cast<cudaStream_t>(stream));
         CUDA_CHECK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
     });
@@ -69,10 +75,15 @@ PP_API int pp_dev_conv(int dtype, const void* in, int rows, int W, int C_in_pad,
         pp::GemmPlan plan;
         const long long m_pix = (long long)(stride == 1 ? rows : rows / 2) * (stride == 1 ? W : W / 2);
         const size_t ws_bytes = size_t(16) * m_pix * n_pad * sizeof(float);
-        pp::DeviceScratch ws(ws_bytes);
-        pp::plan_conv(plan, e, in, rows, W, C_in_pad, stride, weights, n_pad, ep,
-                      static_cast<float*>(ws.ptr), ws_bytes, pp::device_sm_count(), force_splits,
-                      force_block_n);
+        pp::DeviceScratch ws(ws_bytes), tk(size_t(1) << 20);
+        CUDA_CHECK(cudaMemset(tk.ptr, 0, size_t(1) << 20));
+        pp::GemmScratch sc;
+        sc.ws = static_cast<float*>(ws.ptr);
+        sc.ws_bytes = ws_bytes;
+        sc.tickets = static_cast<unsigned int*>(tk.ptr);
+        sc.n_tickets = (size_t(1) << 20) / 4;
+        pp::plan_conv(plan, e, in, rows, W, C_in_pad, stride, weights, n_pad, ep, sc,
+                      pp::device_sm_count(), force_splits, force_block_n);
         pp::launch_gemm(plan, static_cast<cudaStream_t>(stream));
         CUDA_CHECK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
     });

@@ -3,6 +3,8 @@
 #include "model.hpp"
 #include "runtime.hpp"
 
+#include <nccl.h>
+
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -384,6 +386,25 @@ PP_API int pp_runner_profile(pp_runner* r, double* o) {
 }
 
 PP_API long pp_runner_launches(const pp_runner* r) { return r ? r->r->launches() : 0; }
+
+PP_API double pp_runner_last_device_ms(const pp_runner* r) { return r ? r->r->last_device_ms() : 0.0; }
+
+PP_API int pp_runner_set_profile(pp_runner* r, int on) {
+    return pp::guard([&] {
+        need(r, "pp_runner_set_profile");
+        r->r->set_profile(on != 0);
+    });
+}
+
+PP_API int pp_nccl_unique_id(void* out128) {
+    return pp::guard([&] {
+        need(out128, "pp_nccl_unique_id");
+        ncclUniqueId id;
+        const ncclResult_t rc = ncclGetUniqueId(&id);
+        if (rc != ncclSuccess) throw pp::NcclError(std::string("ncclGetUniqueId: ") + ncclGetErrorString(rc));
+        std::memcpy(out128, &id, sizeof(id));
+    });
+}
 
 PP_API int pp_run_sampling(const pp_run_config* c, float* x0, float* traj, uint64_t* total_macs) {
     // run_sampling (proj/src/runtime.cpp:494-526)

@@ -10,7 +10,11 @@
 // Operands are staged by TMA into 128B-swizzled shared memory, multiplied by
 // tcgen05.mma (kind::f16 for bf16, kind::tf32 for the fp32 mode) into a
 // double-buffered TMEM accumulator, and drained by four epilogue warps that
-// add bias / residual and store NHWC rows (or fp32 split-K partials).
+// add bias / residual, store NHWC rows and (optionally) fold the stored values
+// into GroupNorm statistics of the next layer (group_stats, tensor.cpp:203-235).
+// Split-K is reduced inside the kernel: every split writes an fp32 partial tile,
+// the last split to arrive (per-tile ticket) sums all partials in split order --
+// deterministic, no second launch.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -44,9 +48,17 @@ struct GemmArgs {
     const float* bias;        // [n] or null
     const void* residual;     // same element type/layout as out (ld = res_ld) or null
     long long res_ld;
-    float* partial;           // split-K workspace: [splits][m_pix][n_pad] fp32
-    int m_pix, n_pad;
     float scale;              // multiplier applied to the accumulator before bias (1 = none)
+    // split-K workspace
+    float* partial;           // [splits][m_pix][n_pad] fp32
+    unsigned int* tile_ticket;// [m_tiles * n_tiles], zero, reset by the last split
+    int m_pix, n_pad;
+    // fused GroupNorm statistics of the stored output (gn_groups == 0: off)
+    int gn_groups, gn_cpg;
+    double gn_count;          // elements per group (cpg * pixels)
+    double* gn_part;          // [m_tiles][groups][2]
+    unsigned int* gn_ticket;  // zero, reset by the last tile
+    double* gn_out;           // [groups][2] = (mean, mean_sq)
 };
 
 struct GemmPlan {
@@ -56,8 +68,6 @@ struct GemmPlan {
     int grid = 0;
     size_t smem = 0;
     Elem elem = Elem::BF16;
-    // split-K reduce epilogue
-    bool needs_reduce = false;
     double flops = 0;         // algorithmic 2*M*N*K of the layer (for rooflines)
 };
 
@@ -71,23 +81,35 @@ struct EpilogueSpec {
     const void* residual = nullptr;
     long long res_ld = 0;
     float scale = 1.0f;
+    // GroupNorm statistics of the output (groups == 0: off)
+    int gn_groups = 0;
+    double* gn_out = nullptr;
+};
+
+// Scratch shared by all GEMMs issued on one stream (they run one after another).
+struct GemmScratch {
+    float* ws = nullptr;
+    size_t ws_bytes = 0;
+    unsigned int* tickets = nullptr;   // >= max tiles, zeroed
+    size_t n_tickets = 0;
+    double* gn_part = nullptr;         // >= max m_tiles * groups * 2
+    size_t gn_part_len = 0;
+    unsigned int* gn_ticket = nullptr; // one zeroed counter
 };
 
 // Conv over a halo-padded NHWC band: in = [rows_in + 2][W][C_in_pad] (row 0 = the halo
 // row above the band, row rows_in + 1 = the halo row below). weights = [n_pad][9][C_in_pad]
 // (K-major). Output pixel (oy, ox) of the band is stored at out + (oy*out_w + ox)*out_ld.
 void plan_conv(GemmPlan& p, Elem e, const void* in, int rows_in, int W, int C_in_pad, int stride,
-               const void* weights, int n_pad, const EpilogueSpec& ep, float* workspace,
-               size_t workspace_bytes, int num_sms, int force_splits = 0, int force_block_n = 0);
+               const void* weights, int n_pad, const EpilogueSpec& ep, const GemmScratch& sc,
+               int num_sms, int force_splits = 0, int force_block_n = 0);
 
 // Plain GEMM: D[M][N] = A[M][K] * B[N][K]^T (both K-major, leading dims in elements).
 void plan_gemm(GemmPlan& p, Elem e, const void* A, int M, int K, long long lda, const void* B,
-               int N, long long ldb, const EpilogueSpec& ep, float* workspace,
-               size_t workspace_bytes, int num_sms, int force_splits = 0, int force_block_n = 0);
+               int N, long long ldb, const EpilogueSpec& ep, const GemmScratch& sc, int num_sms,
+               int force_splits = 0, int force_block_n = 0);
 
 void launch_gemm(const GemmPlan& p, cudaStream_t s);
-
-size_t gemm_workspace_bytes(const GemmPlan& p);
 
 int device_sm_count();
 

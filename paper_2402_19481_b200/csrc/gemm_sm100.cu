@@ -3,7 +3,7 @@
 // Warp roles (192 threads, 1 CTA per SM, persistent over output tiles):
 //   warp 0      TMA producer (one lane): A box + B box per 128-byte K block
 //   warp 1      TMEM owner + MMA issuer (one lane): 4 x tcgen05.mma per K block
-//   warps 2..5  epilogue: tcgen05.ld -> bias/residual -> NHWC stores
+//   warps 2..5  epilogue: tcgen05.ld -> bias/residual -> NHWC stores (+ GN statistics)
 // Pipelines: smem ring (full/empty mbarriers, TMA <-> MMA) and a 2-deep TMEM
 // accumulator ring (tmem_full/tmem_empty, MMA <-> epilogue), so the epilogue of
 // tile i overlaps the main loop of tile i+1.
@@ -29,13 +29,15 @@ constexpr int kThreads = 192;
 constexpr int kTileM = 128;
 constexpr int kBlockBytes = 128;   // K block = 128 bytes of each operand row
 constexpr int kTmemCols = 512;     // 2 accumulators x 256 columns
-constexpr int kSmemBudget = 232448 - 1024;
+constexpr int kSmemMax = 232448;
 
 __device__ __forceinline__ float round_tf32(float x) {
     uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
     return __uint_as_float(r);
 }
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 struct TileCoord {
     int ty, tx, nt, split;
@@ -52,24 +54,147 @@ __device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int t) {
     return c;
 }
 
+// Smem layout after the operand stages (all offsets from the 1024-aligned base).
+struct SmemTail {
+    uint64_t* full_bar;
+    uint64_t* empty_bar;
+    uint64_t* tfull_bar;
+    uint64_t* tempty_bar;
+    uint32_t* tmem_slot;
+    int* flags;        // [4]
+    float* bias;       // [2][256]
+    float* gn;         // [4 warps][256 cols][2]
+};
+
+__host__ __device__ inline size_t tail_bytes(int stages, bool gn) {
+    return size_t(2 * stages + 4) * 8 + 16 + 16 + 2 * 256 * 4 + (gn ? 4 * 256 * 2 * 4 : 0);
+}
+
+// Final values of one 16-column chunk of one row: bias, residual, store, GN sums.
+template <bool kTF32>
+__device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const float* sbias,
+                                             int c0, int n0, long long p, bool valid,
+                                             float* sgn_warp, int lane) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = v[j] * a.scale + sbias[c0 + j];
+    const bool full = n0 + 16 <= a.n_valid;
+    if (valid) {
+        if (kTF32 || a.out_f32) {
+            float* dst = reinterpret_cast<float*>(a.out) + p * a.out_ld + n0;
+            const float* res =
+                a.residual ? reinterpret_cast<const float*>(a.residual) + p * a.res_ld + n0 : nullptr;
+            if (full && (a.out_ld % 4) == 0 && (!res || (a.res_ld % 4) == 0)) {
+#pragma unroll
+                for (int j = 0; j < 16; j += 4) {
+                    if (res) {
+                        const float4 q = *reinterpret_cast<const float4*>(res + j);
+                        v[j] += q.x; v[j + 1] += q.y; v[j + 2] += q.z; v[j + 3] += q.w;
+                    }
+                    if (a.round_tf32) {
+                        v[j] = round_tf32(v[j]); v[j + 1] = round_tf32(v[j + 1]);
+                        v[j + 2] = round_tf32(v[j + 2]); v[j + 3] = round_tf32(v[j + 3]);
+                    }
+                    *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    if (n0 + j < a.n_valid) {
+                        float o = v[j] + (res ? res[j] : 0.0f);
+                        o = a.round_tf32 ? round_tf32(o) : o;
+                        dst[j] = o;
+                        v[j] = o;
+                    } else {
+                        v[j] = 0.0f;
+                    }
+                }
+            }
+        } else {
+            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(a.out) + p * a.out_ld + n0;
+            const __nv_bfloat16* res =
+                a.residual ? reinterpret_cast<const __nv_bfloat16*>(a.residual) + p * a.res_ld + n0
+                           : nullptr;
+            if (full && (a.out_ld % 8) == 0 && (!res || (a.res_ld % 8) == 0)) {
+#pragma unroll
+                for (int j = 0; j < 16; j += 8) {
+                    if (res) {
+                        const uint4 q = *reinterpret_cast<const uint4*>(res + j);
+                        const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const float2 f = __bfloat1622float2(q2[i]);
+                            v[j + 2 * i] += f.x;
+                            v[j + 2 * i + 1] += f.y;
+                        }
+                    }
+                    uint4 o;
+                    __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        o2[i] = __floats2bfloat162_rn(v[j + 2 * i], v[j + 2 * i + 1]);
+                        const float2 back = __bfloat1622float2(o2[i]);   // stats see stored values
+                        v[j + 2 * i] = back.x;
+                        v[j + 2 * i + 1] = back.y;
+                    }
+                    *reinterpret_cast<uint4*>(dst + j) = o;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    if (n0 + j < a.n_valid) {
+                        float o = v[j] + (res ? __bfloat162float(res[j]) : 0.0f);
+                        const __nv_bfloat16 b = __float2bfloat16(o);
+                        dst[j] = b;
+                        v[j] = __bfloat162float(b);
+                    } else {
+                        v[j] = 0.0f;
+                    }
+                }
+            }
+        }
+    }
+    if (a.gn_groups) {
+        // column sums over the warp's 32 rows (invalid rows contribute 0)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            float s = valid ? v[j] : 0.0f;
+            float q = s * s;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                s += __shfl_xor_sync(0xffffffffu, s, o);
+                q += __shfl_xor_sync(0xffffffffu, q, o);
+            }
+            if (lane == 0) {
+                sgn_warp[(c0 + j) * 2] = s;
+                sgn_warp[(c0 + j) * 2 + 1] = q;
+            }
+        }
+    }
+}
+
 template <bool kTF32>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const GemmArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    // 1024-align the dynamic smem base (SWIZZLE_128B atoms are 1024 B).
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int stages = a.stages;
     const uint32_t a_stage_bytes = kTileM * kBlockBytes;
     const uint32_t b_stage_bytes = uint32_t(a.block_n) * kBlockBytes;
     const uint32_t stage_bytes = a_stage_bytes + b_stage_bytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(stages) * stage_bytes);
-    uint64_t* full_bar = bars;
-    uint64_t* empty_bar = bars + stages;
-    uint64_t* tfull_bar = bars + 2 * stages;
-    uint64_t* tempty_bar = bars + 2 * stages + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 4);
+    SmemTail st;
+    {
+        uint8_t* p = smem + size_t(stages) * stage_bytes;
+        st.full_bar = reinterpret_cast<uint64_t*>(p);
+        st.empty_bar = st.full_bar + stages;
+        st.tfull_bar = st.empty_bar + stages;
+        st.tempty_bar = st.tfull_bar + 2;
+        st.tmem_slot = reinterpret_cast<uint32_t*>(st.tempty_bar + 2);
+        st.flags = reinterpret_cast<int*>(st.tmem_slot + 4);
+        st.bias = reinterpret_cast<float*>(st.flags + 4);
+        st.gn = st.bias + 512;
+    }
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -78,21 +203,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
         for (int s = 0; s < stages; ++s) {
-            ptx::mbar_init(&full_bar[s], 1);
-            ptx::mbar_init(&empty_bar[s], 1);
+            ptx::mbar_init(&st.full_bar[s], 1);
+            ptx::mbar_init(&st.empty_bar[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
-            ptx::mbar_init(&tfull_bar[s], 1);
-            ptx::mbar_init(&tempty_bar[s], 4);
+            ptx::mbar_init(&st.tfull_bar[s], 1);
+            ptx::mbar_init(&st.tempty_bar[s], 4);
         }
         ptx::fence_barrier_init();
         ptx::fence_proxy_async();
     }
-    if (warp == 1) ptx::tmem_alloc(tmem_slot, kTmemCols);
+    if (warp == 1) ptx::tmem_alloc(st.tmem_slot, kTmemCols);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t tmem_base = *st.tmem_slot;
 
     const int total_tiles = a.tiles_y * a.tiles_x * a.n_tiles * a.splits;
     const int conv = a.mode != 0;
@@ -103,33 +228,37 @@ __global__ void __launch_bounds__(kThreads, 1)
             // ===== TMA producer =====
             int stage = 0;
             uint32_t phase = 0;
+            const int kel = kTF32 ? 32 : 64;  // elements per 128-byte K block
             for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
                 const TileCoord tc = decode_tile(a, t);
                 const int kb0 = tc.split * a.kb_per_split;
                 const int kb1 = min(kb0 + a.kb_per_split, a.k_blocks);
+                const int oy0 = tc.ty * a.rows_box, ox0 = tc.tx * a.w_box;
+                int tap = kb0 / a.cin_chunks;
+                int chunk = kb0 - tap * a.cin_chunks;
                 for (int kb = kb0; kb < kb1; ++kb) {
-                    ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+                    ptx::mbar_wait(&st.empty_bar[stage], phase ^ 1);
                     uint8_t* sa = smem + size_t(stage) * stage_bytes;
                     uint8_t* sb = sa + a_stage_bytes;
-                    ptx::mbar_arrive_expect_tx(&full_bar[stage], a_box_bytes + b_stage_bytes);
-                    const int kel = kTF32 ? 32 : 64;  // elements per 128-byte K block
+                    ptx::mbar_arrive_expect_tx(&st.full_bar[stage], a_box_bytes + b_stage_bytes);
                     if (!conv) {
-                        ptx::tma_load_2d(sa, &tmA, &full_bar[stage], kb * kel, tc.ty * kTileM);
+                        ptx::tma_load_2d(sa, &tmA, &st.full_bar[stage], kb * kel, tc.ty * kTileM);
                     } else {
-                        const int tap = kb / a.cin_chunks;
-                        const int chunk = kb - tap * a.cin_chunks;
                         const int ky = tap / 3, kx = tap - 3 * (tap / 3);
-                        const int oy0 = tc.ty * a.rows_box, ox0 = tc.tx * a.w_box;
                         if (a.mode == 1) {
-                            ptx::tma_load_5d(sa, &tmA, &full_bar[stage], chunk * kel, 0,
+                            ptx::tma_load_5d(sa, &tmA, &st.full_bar[stage], chunk * kel, 0,
                                              ox0 + kx - 1, 0, oy0 + ky);
                         } else {
-                            ptx::tma_load_5d(sa, &tmA, &full_bar[stage], chunk * kel,
+                            ptx::tma_load_5d(sa, &tmA, &st.full_bar[stage], chunk * kel,
                                              kx == 1 ? 0 : 1, ox0 + (kx == 0 ? -1 : 0),
                                              ky == 1 ? 1 : 0, oy0 + (ky == 2 ? 1 : 0));
                         }
+                        if (++chunk == a.cin_chunks) {
+                            chunk = 0;
+                            ++tap;
+                        }
                     }
-                    ptx::tma_load_2d(sb, &tmB, &full_bar[stage], kb * kel, tc.nt * a.block_n);
+                    ptx::tma_load_2d(sb, &tmB, &st.full_bar[stage], kb * kel, tc.nt * a.block_n);
                     if (++stage == stages) {
                         stage = 0;
                         phase ^= 1;
@@ -148,11 +277,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const TileCoord tc = decode_tile(a, t);
                 const int kb0 = tc.split * a.kb_per_split;
                 const int kb1 = min(kb0 + a.kb_per_split, a.k_blocks);
-                ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+                ptx::mbar_wait(&st.tempty_bar[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + uint32_t(acc * 256);
                 for (int kb = kb0; kb < kb1; ++kb) {
-                    ptx::mbar_wait(&full_bar[stage], phase);
+                    ptx::mbar_wait(&st.full_bar[stage], phase);
                     ptx::tc_fence_after();
                     const uint32_t sa = ptx::smem_u32(smem + size_t(stage) * stage_bytes);
                     const uint32_t sb = sa + a_stage_bytes;
@@ -166,13 +295,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                         else
                             ptx::mma_bf16(d_tmem, da, db, a.idesc, accum);
                     }
-                    ptx::mma_commit(&empty_bar[stage]);
+                    ptx::mma_commit(&st.empty_bar[stage]);
                     if (++stage == stages) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                ptx::mma_commit(&tfull_bar[acc]);
+                ptx::mma_commit(&st.tfull_bar[acc]);
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
@@ -184,10 +313,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ===== epilogue (warps 2..5; TMEM lane quarter = warp % 4) =====
         const int quarter = warp & 3;
         const int r = quarter * 32 + lane;  // tile row owned by this thread
+        const int et = threadIdx.x - 64;    // 0..127
+        float* sgn_warp = st.gn + quarter * 512;
+        const int final_tiles = a.tiles_y * a.tiles_x * a.n_tiles;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+            const int cur = acc;
+            const uint32_t cur_phase = acc_phase;
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
             const TileCoord tc = decode_tile(a, t);
+            const int m_tile = tc.ty * a.tiles_x + tc.tx;
+            const int tile_id = m_tile * a.n_tiles + tc.nt;
             long long p;
             bool valid;
             if (conv) {
@@ -199,99 +339,94 @@ __global__ void __launch_bounds__(kThreads, 1)
                 p = (long long)tc.ty * kTileM + r;
                 valid = p < a.out_rows;
             }
-            ptx::mbar_wait(&tfull_bar[acc], acc_phase);
-            ptx::tc_fence_after();
-            const uint32_t t_row = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * 256);
             const int nbase = tc.nt * a.block_n;
-            for (int c0 = 0; c0 < a.block_n; c0 += 16) {
-                float v[16];
-                ptx::tmem_ld16(t_row + c0, v);
-                const int n0 = nbase + c0;
-                if (!valid) continue;
-                if (a.splits > 1) {
-                    float* dst = a.partial + ((size_t)tc.split * a.m_pix + p) * a.n_pad + n0;
+            float* sbias = st.bias + cur * 256;
+            for (int c = et; c < a.block_n; c += 128)
+                sbias[c] = (a.bias && nbase + c < a.n_valid) ? a.bias[nbase + c] : 0.0f;
+            ptx::mbar_wait(&st.tfull_bar[cur], cur_phase);
+            ptx::tc_fence_after();
+            epi_bar();
+            const uint32_t t_row = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(cur * 256);
+            if (a.splits > 1) {
+                for (int c0 = 0; c0 < a.block_n; c0 += 16) {
+                    float v[16];
+                    ptx::tmem_ld16(t_row + c0, v);
+                    if (valid) {
+                        float* dst = a.partial + ((size_t)tc.split * a.m_pix + p) * a.n_pad + nbase + c0;
 #pragma unroll
-                    for (int j = 0; j < 16; j += 4)
-                        *reinterpret_cast<float4*>(dst + j) =
-                            make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                    continue;
-                }
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    float x = v[j] * a.scale;
-                    if (a.bias && n0 + j < a.n_valid) x += a.bias[n0 + j];
-                    v[j] = x;
-                }
-                const bool full = n0 + 16 <= a.n_valid;
-                if (kTF32 || a.out_f32) {
-                    float* dst = reinterpret_cast<float*>(a.out) + p * a.out_ld + n0;
-                    const float* res = a.residual
-                                           ? reinterpret_cast<const float*>(a.residual) + p * a.res_ld + n0
-                                           : nullptr;
-                    if (full && (a.out_ld % 4) == 0 && (!res || (a.res_ld % 4) == 0)) {
-#pragma unroll
-                        for (int j = 0; j < 16; j += 4) {
-                            float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                            if (res) {
-                                const float4 q = *reinterpret_cast<const float4*>(res + j);
-                                o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
-                            }
-                            if (a.round_tf32) {
-                                o.x = round_tf32(o.x); o.y = round_tf32(o.y);
-                                o.z = round_tf32(o.z); o.w = round_tf32(o.w);
-                            }
-                            *reinterpret_cast<float4*>(dst + j) = o;
-                        }
-                    } else {
-                        for (int j = 0; j < 16 && n0 + j < a.n_valid; ++j) {
-                            float o = v[j] + (res ? res[j] : 0.0f);
-                            dst[j] = a.round_tf32 ? round_tf32(o) : o;
-                        }
-                    }
-                } else {
-                    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(a.out) + p * a.out_ld + n0;
-                    const __nv_bfloat16* res =
-                        a.residual ? reinterpret_cast<const __nv_bfloat16*>(a.residual) + p * a.res_ld + n0
-                                   : nullptr;
-                    if (full && (a.out_ld % 8) == 0 && (!res || (a.res_ld % 8) == 0)) {
-#pragma unroll
-                        for (int j = 0; j < 16; j += 8) {
-                            float w8[8];
-#pragma unroll
-                            for (int i = 0; i < 8; ++i) w8[i] = v[j + i];
-                            if (res) {
-                                const uint4 q = *reinterpret_cast<const uint4*>(res + j);
-                                const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&q);
-#pragma unroll
-                                for (int i = 0; i < 4; ++i) {
-                                    const float2 f = __bfloat1622float2(q2[i]);
-                                    // the pre-add value is rounded like the reference's
-                                    // separate layer output (bf16 storage here)
-                                    w8[2 * i] = __bfloat162float(__float2bfloat16(w8[2 * i])) + f.x;
-                                    w8[2 * i + 1] = __bfloat162float(__float2bfloat16(w8[2 * i + 1])) + f.y;
-                                }
-                            }
-                            uint4 o;
-                            __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) o2[i] = __floats2bfloat162_rn(w8[2 * i], w8[2 * i + 1]);
-                            *reinterpret_cast<uint4*>(dst + j) = o;
-                        }
-                    } else {
-                        for (int j = 0; j < 16 && n0 + j < a.n_valid; ++j) {
-                            float o = v[j];
-                            if (res) o = __bfloat162float(__float2bfloat16(o)) + __bfloat162float(res[j]);
-                            dst[j] = __float2bfloat16(o);
-                        }
+                        for (int j = 0; j < 16; j += 4)
+                            __stcg(reinterpret_cast<float4*>(dst + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
                     }
                 }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&st.tempty_bar[cur]);
+                __threadfence();
+                epi_bar();
+                if (et == 0) st.flags[cur] = atomicAdd(&a.tile_ticket[tile_id], 1u) == unsigned(a.splits - 1);
+                epi_bar();
+                if (!st.flags[cur]) continue;
+                __threadfence();
+                for (int c0 = 0; c0 < a.block_n; c0 += 16) {
+                    float v[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] = 0.0f;
+                    if (valid) {
+                        for (int k = 0; k < a.splits; ++k) {
+                            const float* src = a.partial + ((size_t)k * a.m_pix + p) * a.n_pad + nbase + c0;
+#pragma unroll
+                            for (int j = 0; j < 16; j += 4) {
+                                const float4 q = __ldcg(reinterpret_cast<const float4*>(src + j));
+                                v[j] += q.x; v[j + 1] += q.y; v[j + 2] += q.z; v[j + 3] += q.w;
+                            }
+                        }
+                    }
+                    finish_chunk<kTF32>(a, v, sbias, c0, nbase + c0, p, valid, sgn_warp, lane);
+                }
+                if (et == 0) a.tile_ticket[tile_id] = 0u;
+            } else {
+                for (int c0 = 0; c0 < a.block_n; c0 += 16) {
+                    float v[16];
+                    ptx::tmem_ld16(t_row + c0, v);
+                    finish_chunk<kTF32>(a, v, sbias, c0, nbase + c0, p, valid, sgn_warp, lane);
+                }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&st.tempty_bar[cur]);
             }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
-            if (++acc == 2) {
-                acc = 0;
-                acc_phase ^= 1;
+            if (a.gn_groups) {
+                epi_bar();
+                const int cpg = a.gn_cpg;
+                const int g0 = nbase / cpg;
+                const int gn_here = min(a.block_n, a.n_valid - nbase) / cpg;
+                for (int gl = et; gl < gn_here; gl += 128) {
+                    double s = 0.0, q = 0.0;
+                    for (int w = 0; w < 4; ++w)
+                        for (int c = gl * cpg; c < (gl + 1) * cpg; ++c) {
+                            s += double(st.gn[w * 512 + c * 2]);
+                            q += double(st.gn[w * 512 + c * 2 + 1]);
+                        }
+                    a.gn_part[((size_t)m_tile * a.gn_groups + g0 + gl) * 2] = s;
+                    a.gn_part[((size_t)m_tile * a.gn_groups + g0 + gl) * 2 + 1] = q;
+                }
+                __threadfence();
+                epi_bar();
+                if (et == 0) st.flags[2] = atomicAdd(a.gn_ticket, 1u) == unsigned(final_tiles - 1);
+                epi_bar();
+                if (st.flags[2]) {
+                    __threadfence();
+                    const int m_tiles = a.tiles_y * a.tiles_x;
+                    for (int g = et; g < a.gn_groups; g += 128) {
+                        double s = 0.0, q = 0.0;
+                        for (int m = 0; m < m_tiles; ++m) {
+                            s += __ldcg(a.gn_part + ((size_t)m * a.gn_groups + g) * 2);
+                            q += __ldcg(a.gn_part + ((size_t)m * a.gn_groups + g) * 2 + 1);
+                        }
+                        a.gn_out[g * 2] = s / a.gn_count;
+                        a.gn_out[g * 2 + 1] = q / a.gn_count;
+                    }
+                    if (et == 0) *a.gn_ticket = 0u;
+                }
             }
         }
     }
@@ -301,33 +436,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, kTmemCols);
-    }
-}
-
-// Deterministic split-K reduction: sum partials in split order, then scale, bias,
-// residual, store.  Same pixel mapping as the main epilogue.
-template <bool kTF32>
-__global__ void splitk_reduce_kernel(const GemmArgs a) {
-    const long long total = (long long)a.m_pix * a.n_valid;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long p = i / a.n_valid;
-        const int n = int(i - p * a.n_valid);
-        float s = 0.0f;
-        for (int k = 0; k < a.splits; ++k) s += a.partial[((size_t)k * a.m_pix + p) * a.n_pad + n];
-        float x = s * a.scale;
-        if (a.bias) x += a.bias[n];
-        if (kTF32 || a.out_f32) {
-            float* dst = reinterpret_cast<float*>(a.out) + p * a.out_ld + n;
-            if (a.residual) x += reinterpret_cast<const float*>(a.residual)[p * a.res_ld + n];
-            *dst = a.round_tf32 ? round_tf32(x) : x;
-        } else {
-            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(a.out) + p * a.out_ld + n;
-            if (a.residual)
-                x = __bfloat162float(__float2bfloat16(x)) +
-                    __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(a.residual)[p * a.res_ld + n]);
-            *dst = __float2bfloat16(x);
-        }
     }
 }
 
@@ -361,29 +469,31 @@ void encode(CUtensorMap* m, Elem e, int rank, const void* base, const uint64_t* 
 
 uint32_t make_idesc(Elem e, int n) {
     uint32_t d = 0;
-    d |= 1u << 4;                               // D format f32
+    d |= 1u << 4;                                    // D format f32
     const uint32_t fmt = e == Elem::BF16 ? 1u : 2u;  // BF16 / TF32
-    d |= fmt << 7;                              // A format
-    d |= fmt << 10;                             // B format
-    d |= uint32_t(n >> 3) << 17;                // N
-    d |= uint32_t(kTileM >> 4) << 24;           // M = 128
+    d |= fmt << 7;                                   // A format
+    d |= fmt << 10;                                  // B format
+    d |= uint32_t(n >> 3) << 17;                     // N
+    d |= uint32_t(kTileM >> 4) << 24;                // M = 128
     return d;
 }
 
-int stages_for(int block_n) {
-    const int stage = kTileM * kBlockBytes + block_n * kBlockBytes;
-    const int barriers = 1024;  // align slack + barriers + tmem slot
-    return std::max(2, std::min(8, (kSmemBudget - barriers) / stage));
-}
-
-size_t smem_for(int block_n, int stages) {
+size_t smem_for(int block_n, int stages, bool gn) {
     return size_t(stages) * (kTileM * kBlockBytes + block_n * kBlockBytes) + 1024 +
-           size_t(2 * stages + 4) * 8 + 16;
+           tail_bytes(stages, gn);
 }
 
-// Pick block_n and split-K from a simple cost model: per 128-byte K block a tile costs
-// max(MMA cycles, L2 feed cycles); waves are quantised over the SM count.
-void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int force_splits,
+int stages_for(int block_n, bool gn) {
+    int s = 8;
+    while (s > 2 && smem_for(block_n, s, gn) > size_t(kSmemMax)) --s;
+    return s;
+}
+
+// Pick block_n and split-K.  Cost model (cycles per SM): a 128-byte K block costs
+// max(MMA = 2*bn, L2 feed = (16 KB + 128*bn) / 33 B/clk) -- 33 B/clk/SM is the feed
+// rate measured with ncu on B200 (tensor pipe ~40% busy at bn=160); tiles are
+// quantised into waves over the SMs; split-K pays a partial write + read.
+void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int gn_cpg, int force_splits,
                    int force_block_n, int& block_n, int& splits) {
     double best = 1e300;
     block_n = 16;
@@ -391,18 +501,19 @@ void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int force_
     for (int bn = 256; bn >= 16; bn -= 16) {
         if (force_block_n && bn != force_block_n) continue;
         if (n_pad % bn) continue;
+        if (gn_cpg && bn % gn_cpg) continue;
         const int nt = n_pad / bn;
-        for (int s : {1, 2, 3, 4, 6, 8, 12, 16}) {
+        for (int s : {1, 2, 3, 4, 6, 8}) {
             if (force_splits && s != force_splits) continue;
-            if (s > 1 && k_blocks / s < 4 && !force_splits) continue;
+            if (s > 1 && k_blocks / s < 6 && !force_splits) continue;
             if (s > k_blocks) continue;
             const long long tiles = (long long)m_tiles * nt * s;
             const double waves = std::ceil(double(tiles) / num_sms);
-            const double per_kb = std::max(2.0 * bn, (16384.0 + 128.0 * bn) / 42.0);
+            const double per_kb = std::max(2.0 * bn, (16384.0 + 128.0 * bn) / 33.0);
             const double kbs = std::ceil(double(k_blocks) / s);
-            double cost = waves * (kbs * per_kb + 600.0);
-            if (s > 1) cost += 0.02 * m_tiles * 128.0 * n_pad * s / num_sms;  // reduce pass
-            if (cost < best * 0.999) {
+            double cost = waves * (kbs * per_kb + 1500.0);
+            if (s > 1) cost += (s + 1) * 128.0 * bn * 4.0 / 33.0;
+            if (cost < best * 0.98) {
                 best = cost;
                 block_n = bn;
                 splits = s;
@@ -413,21 +524,31 @@ void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int force_
 }
 
 void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const EpilogueSpec& ep,
-                 float* ws, size_t ws_bytes, int num_sms, int force_splits, int force_block_n) {
-    int bn, splits;
-    choose_tiling(m_tiles, n_pad, k_blocks, num_sms, force_splits, force_block_n, bn, splits);
+                 const GemmScratch& sc, int num_sms, int force_splits, int force_block_n) {
     GemmArgs& a = p.a;
+    const bool gn = ep.gn_groups > 0;
+    int cpg = 0;
+    if (gn) {
+        if (ep.n_valid % ep.gn_groups)
+            throw std::invalid_argument("GroupNorm statistics: channels not divisible by groups");
+        cpg = ep.n_valid / ep.gn_groups;
+        if (n_pad != ep.n_valid)
+            throw std::invalid_argument("GroupNorm statistics need unpadded output channels");
+    }
+    int bn, splits;
+    choose_tiling(m_tiles, n_pad, k_blocks, num_sms, cpg, force_splits, force_block_n, bn, splits);
+    if (gn && bn % cpg) throw std::invalid_argument("GroupNorm statistics: block_n not group aligned");
     a.block_n = bn;
     a.n_tiles = n_pad / bn;
     a.k_blocks = k_blocks;
     a.n_pad = n_pad;
-    while (splits > 1 &&
-           (size_t)splits * a.m_pix * n_pad * sizeof(float) > ws_bytes)
+    while (splits > 1 && ((size_t)splits * a.m_pix * n_pad * sizeof(float) > sc.ws_bytes ||
+                          size_t(m_tiles) * a.n_tiles > sc.n_tickets))
         --splits;
     a.splits = splits;
     a.kb_per_split = (k_blocks + splits - 1) / splits;
     a.splits = (k_blocks + a.kb_per_split - 1) / a.kb_per_split;
-    a.stages = stages_for(bn);
+    a.stages = stages_for(bn, gn);
     a.idesc = make_idesc(p.elem, bn);
     a.out = ep.out;
     a.out_ld = ep.out_ld;
@@ -438,11 +559,21 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
     a.residual = ep.residual;
     a.res_ld = ep.res_ld;
     a.scale = ep.scale;
-    a.partial = a.splits > 1 ? ws : nullptr;
-    p.needs_reduce = a.splits > 1;
+    a.partial = a.splits > 1 ? sc.ws : nullptr;
+    a.tile_ticket = sc.tickets;
+    if (gn) {
+        if (size_t(m_tiles) * ep.gn_groups * 2 > sc.gn_part_len || !sc.gn_ticket)
+            throw std::invalid_argument("GroupNorm statistics scratch too small");
+        a.gn_groups = ep.gn_groups;
+        a.gn_cpg = cpg;
+        a.gn_count = double(cpg) * double(a.m_pix);
+        a.gn_part = sc.gn_part;
+        a.gn_ticket = sc.gn_ticket;
+        a.gn_out = ep.gn_out;
+    }
     const int tiles = m_tiles * a.n_tiles * a.splits;
     p.grid = std::min(tiles, num_sms);
-    p.smem = smem_for(bn, a.stages);
+    p.smem = smem_for(bn, a.stages, gn);
 }
 
 }  // namespace
@@ -455,8 +586,8 @@ int device_sm_count() {
 }
 
 void plan_conv(GemmPlan& p, Elem e, const void* in, int rows_in, int W, int C_in_pad, int stride,
-               const void* weights, int n_pad, const EpilogueSpec& ep, float* workspace,
-               size_t workspace_bytes, int num_sms, int force_splits, int force_block_n) {
+               const void* weights, int n_pad, const EpilogueSpec& ep, const GemmScratch& sc,
+               int num_sms, int force_splits, int force_block_n) {
     std::memset(&p, 0, sizeof(p));
     p.elem = e;
     const size_t eb = elem_bytes(e);
@@ -500,8 +631,8 @@ void plan_conv(GemmPlan& p, Elem e, const void* in, int rows_in, int W, int C_in
     }
     box[0] = kel; box[1] = 1; box[2] = wb; box[3] = 1; box[4] = a.rows_box;
     encode(&p.tmA, e, 5, in, dims, strides, box);
-    finish_plan(p, a.tiles_y * a.tiles_x, n_pad, k_blocks, ep, workspace, workspace_bytes, num_sms,
-                force_splits, force_block_n);
+    finish_plan(p, a.tiles_y * a.tiles_x, n_pad, k_blocks, ep, sc, num_sms, force_splits,
+                force_block_n);
     // B: weights [n_pad][9*C_in_pad]
     uint64_t bd[2] = {uint64_t(9) * C_in_pad, uint64_t(n_pad)};
     uint64_t bs[1] = {uint64_t(9) * C_in_pad * eb};
@@ -511,8 +642,8 @@ void plan_conv(GemmPlan& p, Elem e, const void* in, int rows_in, int W, int C_in
 }
 
 void plan_gemm(GemmPlan& p, Elem e, const void* A, int M, int K, long long lda, const void* B,
-               int N, long long ldb, const EpilogueSpec& ep, float* workspace,
-               size_t workspace_bytes, int num_sms, int force_splits, int force_block_n) {
+               int N, long long ldb, const EpilogueSpec& ep, const GemmScratch& sc, int num_sms,
+               int force_splits, int force_block_n) {
     std::memset(&p, 0, sizeof(p));
     p.elem = e;
     const size_t eb = elem_bytes(e);
@@ -533,8 +664,7 @@ void plan_gemm(GemmPlan& p, Elem e, const void* A, int M, int K, long long lda, 
     uint64_t as[1] = {uint64_t(lda) * eb};
     uint32_t ab[2] = {uint32_t(kel), uint32_t(kTileM)};
     encode(&p.tmA, e, 2, A, ad, as, ab);
-    finish_plan(p, a.tiles_y, n_pad, K / kel, ep, workspace, workspace_bytes, num_sms,
-                force_splits, force_block_n);
+    finish_plan(p, a.tiles_y, n_pad, K / kel, ep, sc, num_sms, force_splits, force_block_n);
     uint64_t bd[2] = {uint64_t(K), uint64_t(N)};
     uint64_t bs[1] = {uint64_t(ldb) * eb};
     uint32_t bb[2] = {uint32_t(kel), uint32_t(a.block_n)};
@@ -542,16 +672,12 @@ void plan_gemm(GemmPlan& p, Elem e, const void* A, int M, int K, long long lda, 
     p.flops = 2.0 * double(M) * N * K;
 }
 
-size_t gemm_workspace_bytes(const GemmPlan& p) {
-    return p.needs_reduce ? size_t(p.a.splits) * p.a.m_pix * p.a.n_pad * sizeof(float) : 0;
-}
-
 void launch_gemm(const GemmPlan& p, cudaStream_t s) {
     if (p.elem == Elem::BF16) {
         static bool attr = false;
         if (!attr) {
             CUDA_CHECK(cudaFuncSetAttribute(gemm_kernel<false>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
             attr = true;
         }
         gemm_kernel<false><<<p.grid, kThreads, p.smem, s>>>(p.tmA, p.tmB, p.a);
@@ -559,21 +685,12 @@ void launch_gemm(const GemmPlan& p, cudaStream_t s) {
         static bool attr = false;
         if (!attr) {
             CUDA_CHECK(cudaFuncSetAttribute(gemm_kernel<true>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
             attr = true;
         }
         gemm_kernel<true><<<p.grid, kThreads, p.smem, s>>>(p.tmA, p.tmB, p.a);
     }
     CUDA_CHECK(cudaGetLastError());
-    if (p.needs_reduce) {
-        const long long total = (long long)p.a.m_pix * p.a.n_valid;
-        const int blocks = int(std::min<long long>((total + 255) / 256, 148 * 8));
-        if (p.elem == Elem::BF16)
-            splitk_reduce_kernel<false><<<blocks, 256, 0, s>>>(p.a);
-        else
-            splitk_reduce_kernel<true><<<blocks, 256, 0, s>>>(p.a);
-        CUDA_CHECK(cudaGetLastError());
-    }
 }
 
 }  // namespace pp

@@ -77,18 +77,24 @@ int grid_for(long long n, int threads) {
 
 // ---------------------------------------------------------------- GroupNorm stats
 constexpr int kGnThreads = 256;
-constexpr int kGnPixels = 64;
+constexpr int kGnPixels = 32;
 
+// One launch: every block reduces kGnPixels pixels to per-group fp64 partials; the last
+// block to finish (ticket) folds all partials in a fixed order into out[G][2] =
+// (mean, mean_sq) -- group_stats (tensor.cpp:203-235) with fp32 per-thread sums over
+// <= 64 values and fp64 everywhere above that.  Deterministic for a given grid.
 template <class T>
-__global__ void gn_partial_kernel(const T* __restrict__ x, long long pix, int C, int ld, int G,
-                                  double* __restrict__ partial) {
+__global__ void gn_stats_kernel(const T* __restrict__ x, long long pix, int C, int ld, int G,
+                                double count, double* __restrict__ partial,
+                                unsigned int* __restrict__ ticket, double* __restrict__ out) {
     constexpr int VEC = Vec<T>::N;
     extern __shared__ unsigned char sm_raw[];
+    __shared__ bool is_last;
     const int nvec = C / VEC;
     const int L = max(1, kGnThreads / nvec);
     float* s_sum = reinterpret_cast<float*>(sm_raw);
     float* s_sq = s_sum + L * C;
-    double* c_sum = reinterpret_cast<double*>(s_sq + L * C + (((L * C) & 1) ? 1 : 0));
+    double* c_sum = reinterpret_cast<double*>(s_sq + L * C);
     double* c_sq = c_sum + C;
     const long long p0 = (long long)blockIdx.x * kGnPixels;
     const long long p1 = min(p0 + kGnPixels, pix);
@@ -97,14 +103,24 @@ __global__ void gn_partial_kernel(const T* __restrict__ x, long long pix, int C,
         float a[VEC], b[VEC];
 #pragma unroll
         for (int i = 0; i < VEC; ++i) a[i] = b[i] = 0.0f;
-        for (long long p = p0 + pl; p < p1; p += L) {
-            float f[VEC];
-            load_vec<T>(x + p * ld + v * VEC, f);
+        for (long long p = p0 + pl; p < p1; p += 4 * L) {
+            float f[4][VEC];
 #pragma unroll
-            for (int i = 0; i < VEC; ++i) {
-                a[i] += f[i];
-                b[i] = fmaf(f[i], f[i], b[i]);
+            for (int u = 0; u < 4; ++u) {
+                if (p + u * L < p1) {
+                    load_vec<T>(x + (p + u * L) * ld + v * VEC, f[u]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) f[u][i] = 0.0f;
+                }
             }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) {
+                    a[i] += f[u][i];
+                    b[i] = fmaf(f[u][i], f[u][i], b[i]);
+                }
         }
 #pragma unroll
         for (int i = 0; i < VEC; ++i) {
@@ -133,19 +149,30 @@ __global__ void gn_partial_kernel(const T* __restrict__ x, long long pix, int C,
         partial[((long long)blockIdx.x * G + g) * 2] = a;
         partial[((long long)blockIdx.x * G + g) * 2 + 1] = b;
     }
-}
-
-__global__ void gn_finalize_kernel(const double* __restrict__ partial, int blocks, int G,
-                                   double count, double* __restrict__ out) {
-    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+    const int blocks = gridDim.x;
+    for (int g = warp; g < G; g += nw) {
         double a = 0.0, b = 0.0;
-        for (int k = 0; k < blocks; ++k) {
-            a += partial[((long long)k * G + g) * 2];
-            b += partial[((long long)k * G + g) * 2 + 1];
+        for (int k = lane; k < blocks; k += 32) {
+            a += __ldcg(partial + ((long long)k * G + g) * 2);
+            b += __ldcg(partial + ((long long)k * G + g) * 2 + 1);
         }
-        out[g * 2] = a / count;
-        out[g * 2 + 1] = b / count;
+        for (int o = 16; o; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+        }
+        if (lane == 0) {
+            out[g * 2] = a / count;
+            out[g * 2 + 1] = b / count;
+        }
     }
+    if (threadIdx.x == 0) *ticket = 0u;
 }
 
 // Device-order weighted mean (collectives.cpp:150-172), no FMA contraction.
@@ -167,76 +194,95 @@ __device__ void weighted_mean(const double* all, int n, const double* w, int G, 
     q = __ddiv_rn(b, tw);
 }
 
-__global__ void gn_combine_kernel(int mode, const double* __restrict__ fresh,
-                                  const double* __restrict__ all_cur,
-                                  const double* __restrict__ all_prev, int n, int rank,
-                                  const double* __restrict__ w, int G, float eps,
-                                  float* __restrict__ use, int* err) {
-    for (int g = threadIdx.x; g < G; g += blockDim.x) {
-        double m = fresh[g * 2], q = fresh[g * 2 + 1];
-        if (mode == GN_USE_GLOBAL) {
-            weighted_mean(all_cur, n, w, G, g, m, q);
-        } else if (mode == GN_USE_STALE) {
-            weighted_mean(all_prev, n, w, G, g, m, q);
-        } else if (mode == GN_USE_CORRECTED) {
-            // corrected_gn_stats (runtime.cpp:85-106)
-            const double lm = all_prev[((long long)rank * G + g) * 2];
-            const double lq = all_prev[((long long)rank * G + g) * 2 + 1];
-            double gm, gq;
-            weighted_mean(all_prev, n, w, G, g, gm, gq);
-            if (!(gm == lm && gq == lq)) {
-                const double cm = __dadd_rn(gm, __dsub_rn(m, lm));
-                const double cq = __dadd_rn(gq, __dsub_rn(q, lq));
-                if (!(__dsub_rn(cq, __dmul_rn(cm, cm)) < 0.0)) {
-                    m = cm;
-                    q = cq;
-                }
+// The statistics a band normalises with (runtime.cpp:242-300 + corrected_gn_stats,
+// runtime.cpp:85-106); returns (mean, 1/sqrt(var + eps)).
+__device__ void gn_use_of(const GnCombine& cb, int G, int g, float& mu, float& inv, bool& neg) {
+    double m = cb.fresh[g * 2], q = cb.fresh[g * 2 + 1];
+    if (cb.mode == GN_USE_GLOBAL) {
+        weighted_mean(cb.all_cur, cb.n, cb.weights, G, g, m, q);
+    } else if (cb.mode == GN_USE_STALE) {
+        weighted_mean(cb.all_prev, cb.n, cb.weights, G, g, m, q);
+    } else if (cb.mode == GN_USE_CORRECTED) {
+        const double lm = cb.all_prev[((long long)cb.rank * G + g) * 2];
+        const double lq = cb.all_prev[((long long)cb.rank * G + g) * 2 + 1];
+        double gm, gq;
+        weighted_mean(cb.all_prev, cb.n, cb.weights, G, g, gm, gq);
+        if (!(gm == lm && gq == lq)) {
+            const double cm = __dadd_rn(gm, __dsub_rn(m, lm));
+            const double cq = __dadd_rn(gq, __dsub_rn(q, lq));
+            if (!(__dsub_rn(cq, __dmul_rn(cm, cm)) < 0.0)) {
+                m = cm;
+                q = cq;
             }
         }
-        const double var = __dsub_rn(q, __dmul_rn(m, m));
-        if (var < 0.0) atomicExch(err, 1);  // group_norm_apply contract (tensor.cpp:256-259)
-        const double inv = 1.0 / sqrt(__dadd_rn(fmax(var, 0.0), double(eps)));
-        use[g * 2] = float(m);
-        use[g * 2 + 1] = float(inv);
     }
+    const double var = __dsub_rn(q, __dmul_rn(m, m));
+    neg = var < 0.0;
+    mu = float(m);
+    inv = float(1.0 / sqrt(__dadd_rn(fmax(var, 0.0), double(cb.eps))));
 }
 
 template <class T>
-__global__ void gn_apply_kernel(const T* __restrict__ x, T* __restrict__ y, long long pix, int C,
-                                int ld, int G, const float* __restrict__ use,
-                                const float* __restrict__ gamma, const float* __restrict__ beta,
-                                int do_silu, const float* __restrict__ temb,
-                                const T* __restrict__ skip, int round_tf32) {
+__global__ void gn_apply_kernel(const T* __restrict__ x, T* __restrict__ y, int pix, int C, int ld,
+                                int G, const GnCombine cb, const float* __restrict__ gamma,
+                                const float* __restrict__ beta, int do_silu,
+                                const float* __restrict__ temb, const T* __restrict__ skip,
+                                int round_tf32) {
     constexpr int VEC = Vec<T>::N;
+    extern __shared__ float s_tab[];   // [4][ld]: mean, inv_std*gamma, beta, temb
     __shared__ float s_use[2 * 1024];
-    for (int i = threadIdx.x; i < 2 * G; i += blockDim.x) s_use[i] = use[i];
+    float* s_mu = s_tab;
+    float* s_sc = s_tab + ld;
+    float* s_be = s_tab + 2 * ld;
+    float* s_te = s_tab + 3 * ld;
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+        float mu, inv;
+        bool neg;
+        gn_use_of(cb, G, g, mu, inv, neg);
+        s_use[2 * g] = mu;
+        s_use[2 * g + 1] = inv;
+        // group_norm_apply contract (tensor.cpp:256-259), reported once per launch
+        if (neg && blockIdx.x == 0 && cb.err) atomicExch(cb.err, 1);
+    }
     __syncthreads();
-    const int nvec = ld / VEC;
     const int cpg = C / G;
-    const long long total = pix * nvec;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const long long p = idx / nvec;
+    for (int c = threadIdx.x; c < ld; c += blockDim.x) {
+        if (c < C) {
+            const int g = c / cpg;
+            s_mu[c] = s_use[2 * g];
+            s_sc[c] = s_use[2 * g + 1] * gamma[c];
+            s_be[c] = beta[c];
+            s_te[c] = temb ? temb[c] : 0.0f;
+        } else {
+            s_mu[c] = s_sc[c] = s_be[c] = s_te[c] = 0.0f;
+        }
+    }
+    __syncthreads();
+    const unsigned nvec = unsigned(ld / VEC);
+    const unsigned total = unsigned(pix) * nvec;
+    for (unsigned idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += gridDim.x * blockDim.x) {
+        const unsigned p = idx / nvec;
         const int c0 = int(idx - p * nvec) * VEC;
         float f[VEC];
-        load_vec<T>(x + p * ld + c0, f);
+        load_vec<T>(x + size_t(idx) * VEC, f);
         float sk[VEC];
-        if (skip) load_vec<T>(skip + p * ld + c0, sk);
+        if (skip) load_vec<T>(skip + size_t(idx) * VEC, sk);
 #pragma unroll
         for (int i = 0; i < VEC; ++i) {
             const int c = c0 + i;
-            if (c < C) {
-                const int g = c / cpg;
-                float v = (f[i] - s_use[2 * g]) * s_use[2 * g + 1] * gamma[c] + beta[c];
-                if (do_silu) v = v / (1.0f + expf(-v));
-                if (temb) v = v + temb[c];
-                if (skip) v = v + sk[i];
-                f[i] = v;
-            } else {
-                f[i] = 0.0f;
+            float v = (f[i] - s_mu[c]) * s_sc[c] + s_be[c];
+            if (do_silu) {
+                if constexpr (sizeof(T) == 2)
+                    v = v / (1.0f + __expf(-v));
+                else
+                    v = v / (1.0f + expf(-v));
             }
+            v = v + s_te[c];
+            if (skip) v = v + sk[i];
+            f[i] = c < C ? v : 0.0f;
         }
-        store_vec<T>(y + p * ld + c0, f, round_tf32 != 0);
+        store_vec<T>(y + size_t(idx) * VEC, f, round_tf32 != 0);
     }
 }
 
@@ -373,14 +419,11 @@ __global__ void transpose_kernel(const T* __restrict__ V, int ns, int C, long lo
 }
 
 // ---------------------------------------------------------------- embeddings / projections
-__global__ void time_projection_kernel(const TembLayer* __restrict__ layers, int dim, int t) {
+__global__ void time_projection_kernel(const TembLayer* __restrict__ layers,
+                                       const __grid_constant__ EmbArg emb_arg) {
     extern __shared__ float emb[];
-    const int half = dim / 2;
-    for (int i = threadIdx.x; i < half; i += blockDim.x) {
-        const double freq = pow(10000.0, -2.0 * i / double(dim));
-        emb[i] = float(sin(t * freq));
-        emb[half + i] = float(cos(t * freq));
-    }
+    const int dim = emb_arg.dim;
+    for (int i = threadIdx.x; i < dim; i += blockDim.x) emb[i] = emb_arg.v[i];
     __syncthreads();
     const TembLayer L = layers[blockIdx.y];
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -480,41 +523,27 @@ __global__ void elem_to_f32_kernel(const T* __restrict__ s, float* __restrict__ 
 
 int gn_stats_blocks(long long pix) { return int((pix + kGnPixels - 1) / kGnPixels); }
 
-void gn_partial_stats(Elem e, const void* x, long long pix, int C, int ld, int groups,
-                      double* partial, cudaStream_t s) {
+void gn_stats(Elem e, const void* x, long long pix, int C, int ld, int groups, double count,
+              double* partial, unsigned int* ticket, double* out, cudaStream_t s) {
     const int VEC = e == Elem::BF16 ? 8 : 4;
     if (C % VEC || ld % VEC || C % groups)
         throw std::invalid_argument("group_stats: channels must be a multiple of the vector width");
     const int nvec = C / VEC;
     const int L = std::max(1, kGnThreads / nvec);
-    const size_t smem = size_t(2) * L * C * 4 + 8 + size_t(2) * C * 8;
-    DISPATCH(e, gn_partial_kernel<T><<<gn_stats_blocks(pix), kGnThreads, smem, s>>>(
-                    static_cast<const T*>(x), pix, C, ld, groups, partial));
-    CUDA_CHECK(cudaGetLastError());
-}
-
-void gn_finalize(const double* partial, int blocks, int groups, double count, double* out,
-                 cudaStream_t s) {
-    gn_finalize_kernel<<<1, std::min(1024, std::max(32, groups)), 0, s>>>(partial, blocks, groups,
-                                                                         count, out);
-    CUDA_CHECK(cudaGetLastError());
-}
-
-void gn_combine(int mode, const double* fresh, const double* all_cur, const double* all_prev,
-                int n_dev, int rank, const double* weights, int groups, float eps, float* use,
-                int* err, cudaStream_t s) {
-    gn_combine_kernel<<<1, std::min(1024, std::max(32, groups)), 0, s>>>(
-        mode, fresh, all_cur, all_prev, n_dev, rank, weights, groups, eps, use, err);
+    const size_t smem = size_t(2) * L * C * 4 + size_t(2) * C * 8;
+    DISPATCH(e, gn_stats_kernel<T><<<gn_stats_blocks(pix), kGnThreads, smem, s>>>(
+                    static_cast<const T*>(x), pix, C, ld, groups, count, partial, ticket, out));
     CUDA_CHECK(cudaGetLastError());
 }
 
 void gn_apply(Elem e, const void* x, void* y, long long pix, int C, int ld, int groups,
-              const float* use, const float* gamma, const float* beta, bool do_silu,
+              const GnCombine& cb, const float* gamma, const float* beta, bool do_silu,
               const float* temb, const void* skip, bool round_tf32, cudaStream_t s) {
     if (groups > 1024) throw std::invalid_argument("group_norm_apply: too many groups");
     const int VEC = e == Elem::BF16 ? 8 : 4;
-    DISPATCH(e, gn_apply_kernel<T><<<grid_for(pix * (ld / VEC), 256), 256, 0, s>>>(
-                    static_cast<const T*>(x), static_cast<T*>(y), pix, C, ld, groups, use, gamma,
+    if (pix * (ld / VEC) >= (1LL << 31)) throw std::invalid_argument("group_norm_apply: band too large");
+    DISPATCH(e, gn_apply_kernel<T><<<grid_for(pix * (ld / VEC), 256), 256, size_t(4) * ld * 4, s>>>(
+                    static_cast<const T*>(x), static_cast<T*>(y), int(pix), C, ld, groups, cb, gamma,
                     beta, do_silu ? 1 : 0, temb, static_cast<const T*>(skip), round_tf32 ? 1 : 0));
     CUDA_CHECK(cudaGetLastError());
 }
@@ -564,11 +593,15 @@ void transpose(Elem e, const void* V, int ns, int C, long long ldv, void* Vt, lo
     CUDA_CHECK(cudaGetLastError());
 }
 
-void time_projection(const TembLayer* layers_dev, int n_layers, int max_c, int dim, int t,
-                     cudaStream_t s) {
+void time_projection(const TembLayer* layers_dev, int n_layers, int max_c, const float* emb,
+                     int dim, cudaStream_t s) {
     if (n_layers == 0) return;
-    dim3 grid(std::max(1, std::min(64, (max_c + 7) / 8)), n_layers);
-    time_projection_kernel<<<grid, 256, dim * sizeof(float), s>>>(layers_dev, dim, t);
+    if (dim > kMaxEmb) throw std::invalid_argument("timestep_embedding: dim too large for the B200 path");
+    EmbArg arg;
+    arg.dim = dim;
+    for (int i = 0; i < dim; ++i) arg.v[i] = emb[i];
+    dim3 grid(std::max(1, (max_c + 7) / 8), n_layers);
+    time_projection_kernel<<<grid, 256, dim * sizeof(float), s>>>(layers_dev, arg);
     CUDA_CHECK(cudaGetLastError());
 }
 

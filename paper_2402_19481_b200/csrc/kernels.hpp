@@ -11,30 +11,34 @@
 namespace pp {
 
 // ---- GroupNorm (proj/src/tensor.cpp:203-277, proj/src/runtime.cpp:85-106) ----------------
-// Stage 1: per-block fp32 partial sums -> per-group fp64 partials [blocks][G][2].
+// One launch: per-block fp32/fp64 partial sums, folded by the last block (fixed order)
+// into stats_out[groups][2] = (mean, mean_sq); `ticket` is a zeroed device counter.
 int gn_stats_blocks(long long pix);
-void gn_partial_stats(Elem e, const void* x, long long pix, int C, int ld, int groups,
-                      double* partial, cudaStream_t s);
-// Stage 2: fixed-order fp64 reduction of the partials into the local (mean, mean_sq),
-// written to stats_out[groups][2].
-void gn_finalize(const double* partial, int blocks, int groups, double count, double* stats_out,
-                 cudaStream_t s);
+void gn_stats(Elem e, const void* x, long long pix, int C, int ld, int groups, double count,
+              double* partial, unsigned int* ticket, double* stats_out, cudaStream_t s);
 
-// Combine rule applied on the device (one thread per group):
-//   GN_USE_LOCAL      use = fresh local                (N == 1 sync, or scheme Separate)
-//   GN_USE_GLOBAL     use = weighted device-order mean of all ranks' locals (sync, N > 1)
-//   GN_USE_CORRECTED  use = corrected_gn_stats(fresh, prev_local, prev_global)
-//   GN_USE_STALE      use = prev_global
-// `all_cur` / `all_prev` are [n_dev][groups][2] (mean, mean_sq) tables; weights are the
-// per-device pixel counts (collectives.cpp:150-172 weighting).
+// Which statistics a band normalises with (evaluated in the apply kernel's prologue):
+//   GN_USE_LOCAL      fresh local                      (N == 1 sync, or scheme Separate)
+//   GN_USE_GLOBAL     weighted device-order mean of all ranks' locals (sync, N > 1)
+//   GN_USE_CORRECTED  corrected_gn_stats(fresh, prev_local, prev_global)
+//   GN_USE_STALE      prev_global
+// all_cur / all_prev are [n][groups][2] tables (rank order); weights = band pixel counts
+// (collectives.cpp:150-172 weighting).
 enum GnUse : int { GN_USE_LOCAL = 0, GN_USE_GLOBAL = 1, GN_USE_CORRECTED = 2, GN_USE_STALE = 3 };
-void gn_combine(int mode, const double* fresh_local, const double* all_cur, const double* all_prev,
-                int n_dev, int rank, const double* weights, int groups, float eps,
-                float* use_out /*[groups][2] = (mean, inv_std)*/, int* err_flag, cudaStream_t s);
+struct GnCombine {
+    int mode;
+    const double* fresh;
+    const double* all_cur;
+    const double* all_prev;
+    int n, rank;
+    const double* weights;
+    float eps;
+    int* err;   // set to 1 when a group's variance is negative
+};
 
 // y = GN(x) [-> SiLU] [+ temb[c]] [+ skip]  (fused GroupNorm / SiLU / AddTimeEmb / AddSkip)
 void gn_apply(Elem e, const void* x, void* y, long long pix, int C, int ld, int groups,
-              const float* use, const float* gamma, const float* beta, bool silu,
+              const GnCombine& cb, const float* gamma, const float* beta, bool silu,
               const float* temb, const void* skip, bool round_tf32, cudaStream_t s);
 
 // ---- pointwise (proj/src/tensor.cpp:297-334, model.cpp:278-298) ---------------------------
@@ -55,16 +59,22 @@ void transpose(Elem e, const void* V, int ns, int C, long long ldv, void* Vt, lo
                cudaStream_t s);
 
 // ---- time embedding / condition projection ----------------------------------------------
-// emb = timestep_embedding(t, dim) (model.cpp:220-231); proj[l][c] for every AddTimeEmb
-// layer in one launch: proj = W_l emb + b_l (fp64 accumulate, fp32 result).
+// proj[l][c] for every AddTimeEmb layer in one launch: proj = W_l emb + b_l (fp64
+// accumulate, fp32 result; layer_time_emb, model.cpp:278-289).  `emb` is the host
+// timestep_embedding(t, dim) (model.cpp:220-231), passed by value as a kernel argument.
 struct TembLayer {
     const float* W;   // [C][dim] fp32 (reference layout)
     const float* b;   // [C]
     float* out;       // [ld] fp32 (padding stays 0)
     int C;
 };
-void time_projection(const TembLayer* layers_dev, int n_layers, int max_c, int dim, int t,
-                     cudaStream_t s);
+constexpr int kMaxEmb = 960;
+struct EmbArg {
+    int dim;
+    float v[kMaxEmb];
+};
+void time_projection(const TembLayer* layers_dev, int n_layers, int max_c, const float* emb,
+                     int dim, cudaStream_t s);
 // v[c] = W[c][:] . cond + b[c] in fp64 (project_condition value half, model.cpp:252-263)
 void gemv_f64(const float* W, const float* b, const float* x, int rows, int cols, float* out,
               cudaStream_t s);

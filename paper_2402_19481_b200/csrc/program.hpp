@@ -94,17 +94,17 @@ struct Program {
     };
     std::vector<LayerX> lx;
     std::vector<Group> groups;
-    std::vector<GemmPlan> plans;         // per group: conv / linear / attention PV
-    std::vector<std::array<GemmPlan, 2>> s_plans;  // attention S = Q K^T per parity
+    std::vector<std::array<GemmPlan, 2>> plans;    // per group, per step parity: conv / linear / PV
+    std::vector<std::array<GemmPlan, 2>> s_plans;  // attention S = Q K^T per K/V parity
+    std::vector<char> fused_stats;                 // per GN layer: stats come from the conv epilogue
+    GemmScratch sc;
     // scratch
     double* gn_partial = nullptr;
-    float* gn_use = nullptr;
+    unsigned int* gn_ticket = nullptr;
     float* S = nullptr;
     void* P = nullptr;
     void* Vt = nullptr;
     int s_pad = 0;
-    float* ws = nullptr;
-    size_t ws_bytes = 0;
     // time embedding
     std::vector<float*> temb_out;   // per layer (nullptr unless AddTimeEmb)
     TembLayer* temb_dev = nullptr;
@@ -131,6 +131,7 @@ struct Program {
     Program& operator=(const Program&) = delete;
 
     void* alloc(size_t bytes);
+    void set_profile(bool on);
     const Act& input_of(int l) const { return l == 0 ? stem : act[l - 1]; }
     void count(long n);
     void run_timed(int cat, double flops, const std::function<void()>& fn);
@@ -139,13 +140,13 @@ struct Program {
     void time_projection(int t);
     void pack_halo(const Group& g, int par);
     void unpack_halo(const Group& g, int par);
-    void conv(const Group& g);
+    void conv(const Group& g, int par);
     void pack_kv(const Group& g, int par);
     void scatter_kv(const Group& g, int par);
-    void attention(const Group& g, int par);
+    void attention(const Group& g, int par, int par_out);
     void gn_stats(const Group& g, int par);
     void gn_apply(const Group& g, int combine_mode, int par_cur, int par_prev);
-    void simple(const Group& g);
+    void simple(const Group& g, int par);
     void record_ready(int l);
 };
 

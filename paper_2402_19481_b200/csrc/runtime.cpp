@@ -302,14 +302,27 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
         }
     }
     gn_partial = static_cast<double*>(alloc(gn_blocks * 2 * 8));
-    gn_use = static_cast<float*>(alloc(2048 * 4));
+    gn_ticket = static_cast<unsigned int*>(alloc(16));
     n_temb = int(tl.size());
     if (n_temb) {
         temb_dev = static_cast<TembLayer*>(alloc(tl.size() * sizeof(TembLayer)));
         CUDA_CHECK(cudaMemcpy(temb_dev, tl.data(), tl.size() * sizeof(TembLayer), cudaMemcpyHostToDevice));
     }
-    ws_bytes = kWorkspaceBytes;
-    ws = static_cast<float*>(alloc(ws_bytes));
+    // GEMM scratch shared by every GEMM of this band (they run in stream order)
+    long long max_pix = stem.pix();
+    int max_groups = 1;
+    for (int l = 0; l < L; ++l) {
+        max_pix = std::max(max_pix, act[l].pix());
+        if (m->layers[l].kind == Kind::GroupNorm) max_groups = std::max(max_groups, m->layers[l].groups);
+    }
+    sc.ws_bytes = kWorkspaceBytes;
+    sc.ws = static_cast<float*>(alloc(sc.ws_bytes));
+    sc.n_tickets = size_t(max_pix / 16 + 1024);
+    sc.tickets = static_cast<unsigned int*>(alloc(sc.n_tickets * 4));
+    sc.gn_part_len = size_t(max_pix / 32 + 64) * max_groups * 2;
+    sc.gn_part = static_cast<double*>(alloc(sc.gn_part_len * 8));
+    sc.gn_ticket = static_cast<unsigned int*>(alloc(16));
+    fused_stats.assign(L, 0);
 
     // attention scratch (one SelfAttn geometry per model)
     for (const Group& g : groups) {
@@ -324,7 +337,7 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
         Vt = alloc(size_t(npad) * s_pad * eb);
     }
 
-    // GEMM plans
+    // GEMM plans (per parity: the fused GroupNorm statistics land in that parity's table)
     const int sms = device_sm_count();
     plans.resize(groups.size());
     s_plans.resize(groups.size());
@@ -350,18 +363,35 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
             ep.residual = act[g.skip].interior(eb);
             ep.res_ld = act[g.skip].ld;
         }
-        if (d.kind == Kind::Conv || d.kind == Kind::DownConv) {
-            ep.bias = lw.bias;
-            plan_conv(plans[gi], e, in.base, in.rows, in.w, in.ld, d.stride, lw.w, lw.n_pad, ep, ws,
-                      ws_bytes, sms);
-        } else if (d.kind == Kind::Linear) {
-            ep.bias = lw.bias;
-            plan_gemm(plans[gi], e, in.interior(eb), int(in.pix()), in.ld, in.ld, lw.w, d.out_ch,
-                      in.ld, ep, ws, ws_bytes, sms);
-        } else if (d.kind == Kind::SelfAttn) {
-            const Region& ri = spec.layer_in[g.first];
-            const int ns = ri.full_h * ri.full_w;
-            for (int p = 0; p < (nb > 1 ? 2 : 1); ++p) {
+        // GroupNorm right after this group: fold its statistics into the epilogue
+        const int next = g.last + 1;
+        bool fuse_gn = false;
+        if ((d.kind == Kind::Conv || d.kind == Kind::DownConv) && next < L && !head &&
+            m->layers[next].kind == Kind::GroupNorm && d.out_ch % 16 == 0 &&
+            d.out_ch % m->layers[next].groups == 0) {
+            // a tile must hold whole groups: block_n a multiple of lcm(16, channels/group)
+            const int cpg = d.out_ch / m->layers[next].groups;
+            int l = 16;
+            while (l % cpg) l += 16;
+            fuse_gn = l <= 256 && d.out_ch % l == 0;
+        }
+        for (int p = 0; p < 2; ++p) {
+            EpilogueSpec e2 = ep;
+            if (fuse_gn) {
+                e2.gn_groups = m->layers[next].groups;
+                e2.gn_out = lx[next].stats[p] + size_t(band) * e2.gn_groups * 2;
+            }
+            if (d.kind == Kind::Conv || d.kind == Kind::DownConv) {
+                e2.bias = lw.bias;
+                plan_conv(plans[gi][p], e, in.base, in.rows, in.w, in.ld, d.stride, lw.w, lw.n_pad,
+                          e2, sc, sms);
+            } else if (d.kind == Kind::Linear) {
+                e2.bias = lw.bias;
+                plan_gemm(plans[gi][p], e, in.interior(eb), int(in.pix()), in.ld, in.ld, lw.w,
+                          d.out_ch, in.ld, e2, sc, sms);
+            } else if (d.kind == Kind::SelfAttn) {
+                const Region& ri = spec.layer_in[g.first];
+                const int ns = ri.full_h * ri.full_w;
                 EpilogueSpec es;
                 es.out = S;
                 es.out_ld = s_pad;
@@ -369,17 +399,24 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
                 es.n_valid = ns;
                 const void* kv = nb > 1 ? lx[g.first].kv[p] : in.interior(eb);
                 plan_gemm(s_plans[gi][p], e, in.interior(eb), int(in.pix()), in.ld, in.ld, kv, ns,
-                          in.ld, es, ws, ws_bytes, sms);
+                          in.ld, es, sc, sms);
+                plan_gemm(plans[gi][p], e, P, int(in.pix()), s_pad, s_pad, Vt, in.C, s_pad, e2, sc,
+                          sms);
             }
-            plan_gemm(plans[gi], e, P, int(in.pix()), s_pad, s_pad, Vt, in.C, s_pad, ep, ws,
-                      ws_bytes, sms);
         }
+        if (fuse_gn) fused_stats[next] = 1;
     }
-    if (profile) {
-        event_pool.resize(4096);
+    set_profile(profile);
+    CUDA_CHECK(cudaDeviceSynchronize());
+}
+
+void Program::set_profile(bool on) {
+    profile = on;
+    if (on && event_pool.empty()) {
+        DeviceGuard dg(dev);
+        event_pool.resize(16384);
         for (auto& ev : event_pool) CUDA_CHECK(cudaEventCreate(&ev));
     }
-    CUDA_CHECK(cudaDeviceSynchronize());
 }
 
 Program::~Program() {
@@ -418,7 +455,8 @@ void Program::record_ready(int l) { CUDA_CHECK(cudaEventRecord(ready[l], cs)); }
 void Program::time_projection(int t) {
     if (!n_temb) return;
     run_timed(CAT_OTHER, 0, [&] {
-        pp::time_projection(temb_dev, n_temb, temb_max_c, m->time_dim(), t, cs);
+        const std::vector<float> emb = timestep_embedding(t, m->time_dim());
+        pp::time_projection(temb_dev, n_temb, temb_max_c, emb.data(), m->time_dim(), cs);
     });
     count(1);
 }
@@ -445,11 +483,11 @@ void Program::unpack_halo(const Group& g, int par) {
                                    x.row_bytes, cudaMemcpyDeviceToDevice, cs));
 }
 
-void Program::conv(const Group& g) {
+void Program::conv(const Group& g, int par) {
     const size_t gi = size_t(&g - groups.data());
-    const GemmPlan& p = plans[gi];
+    const GemmPlan& p = plans[gi][par];
     run_timed(CAT_CONV, p.flops, [&] { launch_gemm(p, cs); });
-    count(p.needs_reduce ? 2 : 1);
+    count(1);
 }
 
 void Program::pack_kv(const Group& g, int par) {
@@ -461,12 +499,12 @@ void Program::pack_kv(const Group& g, int par) {
 
 void Program::scatter_kv(const Group& g, int par) { pack_kv(g, par); }
 
-void Program::attention(const Group& g, int par) {
+void Program::attention(const Group& g, int par, int par_out) {
     const size_t gi = size_t(&g - groups.data());
     const Act& in = input_of(g.first);
     const Region& ri = spec.layer_in[g.first];
     const int ns = ri.full_h * ri.full_w;
-    const GemmPlan& sp = s_plans[gi][nb > 1 ? par : 0];
+    const GemmPlan& sp = s_plans[gi][par];
     const void* kv = nb > 1 ? lx[g.first].kv[par] : in.interior(eb);
     const float scale = float(1.0 / std::sqrt(double(m->layers[g.first].in_ch)));
     run_timed(CAT_GEMM, sp.flops, [&] { launch_gemm(sp, cs); });
@@ -474,22 +512,21 @@ void Program::attention(const Group& g, int par) {
         softmax_rows(e, S, int(in.pix()), ns, s_pad, scale, P, s_pad, cs);
         transpose(e, kv, ns, in.C, in.ld, Vt, s_pad, cs);
     });
-    const GemmPlan& pv = plans[gi];
+    const GemmPlan& pv = plans[gi][par_out];
     run_timed(CAT_GEMM, pv.flops, [&] { launch_gemm(pv, cs); });
-    count(2 + (sp.needs_reduce ? 2 : 1) + (pv.needs_reduce ? 2 : 1));
+    count(4);
 }
 
 void Program::gn_stats(const Group& g, int par) {
     const Act& in = input_of(g.first);
     const LayerX& x = lx[g.first];
     const Layer& d = m->layers[g.first];
-    const int blocks = gn_stats_blocks(in.pix());
     run_timed(CAT_GN, 0, [&] {
-        gn_partial_stats(e, in.interior(eb), in.pix(), in.C, in.ld, d.groups, gn_partial, cs);
         const double count = double(in.C / d.groups) * double(in.rows) * double(in.w);
-        gn_finalize(gn_partial, blocks, d.groups, count, x.stats[par] + size_t(band) * d.groups * 2, cs);
+        pp::gn_stats(e, in.interior(eb), in.pix(), in.C, in.ld, d.groups, count, gn_partial,
+                     gn_ticket, x.stats[par] + size_t(band) * d.groups * 2, cs);
     });
-    count(2);
+    count(1);
 }
 
 void Program::gn_apply(const Group& g, int mode, int par_cur, int par_prev) {
@@ -498,19 +535,27 @@ void Program::gn_apply(const Group& g, int mode, int par_cur, int par_prev) {
     const Layer& d = m->layers[g.first];
     const LayerWeights& lw = wts->L[g.first];
     const int L = int(m->layers.size());
+    if (g.last == L - 1) throw std::invalid_argument("GroupNorm as the final layer is unsupported");
+    GnCombine cb;
+    cb.mode = mode;
+    cb.fresh = x.stats[par_cur] + size_t(band) * d.groups * 2;
+    cb.all_cur = x.stats[par_cur];
+    cb.all_prev = x.stats[par_prev];
+    cb.n = nb;
+    cb.rank = band;
+    cb.weights = x.weights;
+    cb.eps = d.eps;
+    cb.err = flags + 1;
     run_timed(CAT_GN, 0, [&] {
-        pp::gn_combine(mode, x.stats[par_cur] + size_t(band) * d.groups * 2, x.stats[par_cur],
-                       x.stats[par_prev], nb, band, x.weights, d.groups, d.eps, gn_use, flags + 1, cs);
-        if (g.last == L - 1) throw std::invalid_argument("GroupNorm as the final layer is unsupported");
         const Act& out = act[g.last];
-        pp::gn_apply(e, in.interior(eb), out.interior(eb), in.pix(), in.C, in.ld, d.groups, gn_use,
+        pp::gn_apply(e, in.interior(eb), out.interior(eb), in.pix(), in.C, in.ld, d.groups, cb,
                      lw.gamma, lw.beta, g.silu, g.temb >= 0 ? temb_out[g.temb] : nullptr,
                      g.skip >= 0 ? act[g.skip].interior(eb) : nullptr, rnd, cs);
     });
-    count(2);
+    count(1);
 }
 
-void Program::simple(const Group& g) {
+void Program::simple(const Group& g, int par) {
     const Layer& d = m->layers[g.first];
     const Act& in = input_of(g.first);
     const int L = int(m->layers.size());
@@ -539,8 +584,7 @@ void Program::simple(const Group& g) {
                 break;
             case Kind::Linear: {
                 const size_t gi = size_t(&g - groups.data());
-                launch_gemm(plans[gi], cs);
-                if (plans[gi].needs_reduce) count(1);
+                launch_gemm(plans[gi][par], cs);
                 break;
             }
             default: throw std::runtime_error("device_step: unhandled layer kind");
@@ -665,6 +709,7 @@ void Runner::run_bands(int t, int s, bool displaced) {
     if (displaced) check_displaced_ready(s);
     const int pcur = s & 1, pprev = (s + 1) & 1;
     const int pu = displaced ? pprev : pcur;
+    const int nb_pu = n_dev_ > 1 ? pu : pcur;
     const bool multi = n_dev_ > 1;
     for (auto& b : bands_) {
         DeviceGuard g(b->dev);
@@ -697,7 +742,7 @@ void Runner::run_bands(int t, int s, bool displaced) {
                 volumes_.halo_recv += per_band;
                 volumes_.halo_sent += per_band;
             }
-            each([&](Program& b, const Group& g) { b.conv(g); });
+            each([&](Program& b, const Group& g) { b.conv(g, pcur); });
             posted_[l] = s;
         } else if (d.kind == Kind::SelfAttn) {
             if (multi) {
@@ -714,11 +759,11 @@ void Runner::run_bands(int t, int s, bool displaced) {
                 volumes_.allgather_recv += v;
                 volumes_.allgather_sent += v;
             }
-            each([&](Program& b, const Group& g) { b.attention(g, pu); });
+            each([&](Program& b, const Group& g) { b.attention(g, nb_pu, pcur); });
             posted_[l] = s;
         } else if (d.kind == Kind::GroupNorm) {
             each([&](Program& b, const Group& g) {
-                b.gn_stats(g, pcur);
+                if (!b.fused_stats[l]) b.gn_stats(g, pcur);
                 b.record_ready(l);
             });
             int mode;
@@ -739,7 +784,7 @@ void Runner::run_bands(int t, int s, bool displaced) {
             each([&](Program& b, const Group& g) { b.gn_apply(g, mode, pcur, pprev); });
             gn_posted_[l] = s;
         } else {
-            each([&](Program& b, const Group& g) { b.simple(g); });
+            each([&](Program& b, const Group& g) { b.simple(g, pcur); });
         }
     }
 }
@@ -814,6 +859,12 @@ void Runner::check_flags(const char* who) {
         throw std::runtime_error(std::string(who) + ": non-finite value in tensor (1," +
                                  std::to_string(m_.cfg.in_channels) + "," + std::to_string(h_) +
                                  "," + std::to_string(w_) + ")");
+}
+
+void Runner::set_profile(bool on) {
+    o_.profile = on;
+    prof_ = ProfileTotals{};
+    for (auto& b : bands_) b->set_profile(on);
 }
 
 void Runner::begin_profile() {
@@ -901,6 +952,15 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
     launches_ = 0;
     if (o_.profile) begin_profile();
     load_x(x_T);
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
+    for (auto& b : bands_) {
+        DeviceGuard g(b->dev);
+        cudaEvent_t a, z;
+        CUDA_CHECK(cudaEventCreate(&a));
+        CUDA_CHECK(cudaEventCreate(&z));
+        CUDA_CHECK(cudaEventRecord(a, b->cs));
+        evs.emplace_back(a, z);
+    }
     for (int i = 0; i < n; ++i) {
         const int t = ts[i];
         if (traj) {
@@ -933,6 +993,10 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
                         b->e, b->stem.interior(b->eb), b->stem.ld, b->cs);
             launches_ += 1;
         }
+    }
+    for (size_t k = 0; k < bands_.size(); ++k) {
+        DeviceGuard g(bands_[k]->dev);
+        CUDA_CHECK(cudaEventRecord(evs[k].second, bands_[k]->cs));
     }
     // x0 download (band -> NCHW)
     if (o_.world > 1) {
@@ -967,6 +1031,16 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
         }
     }
     launches_ += long(bands_.size());
+    last_device_ms_ = 0;
+    for (size_t k = 0; k < bands_.size(); ++k) {
+        DeviceGuard g(bands_[k]->dev);
+        CUDA_CHECK(cudaEventSynchronize(evs[k].second));
+        float ms = 0;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, evs[k].first, evs[k].second));
+        last_device_ms_ = std::max(last_device_ms_, double(ms));
+        cudaEventDestroy(evs[k].first);
+        cudaEventDestroy(evs[k].second);
+    }
     check_flags("sample");
     end_profile();
 }

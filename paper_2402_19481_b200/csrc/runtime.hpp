@@ -78,7 +78,11 @@ public:
     CommVolumes volumes() const { return volumes_; }
     ProfileTotals profile() const { return prof_; }
     long launches() const { return launches_; }
+    // device time (CUDA events on the band compute streams, max over local bands) of the
+    // last sample()'s denoising loop, excluding the x_T upload and x0 download
+    double last_device_ms() const { return last_device_ms_; }
     int n_devices() const { return n_dev_; }
+    void set_profile(bool on);
 
 private:
     friend struct Program;
@@ -109,6 +113,7 @@ private:
     CommVolumes volumes_;
     ProfileTotals prof_;
     long launches_ = 0;
+    double last_device_ms_ = 0;
     // host staging (pinned)
     float* h_x_ = nullptr;      // full NCHW image
     float* h_eps_ = nullptr;    // full NCHW image

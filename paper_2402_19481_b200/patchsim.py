@@ -296,6 +296,18 @@ class PatchRunner:
     def launches(self):
         return int(N.lib().pp_runner_launches(self._r))
 
+    def last_device_ms(self):
+        return float(N.lib().pp_runner_last_device_ms(self._r))
+
+    def set_profile(self, on: bool):
+        N.check(N.lib().pp_runner_set_profile(self._r, int(on)))
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    N.check(N.lib().pp_nccl_unique_id(buf))
+    return buf.raw
+
 
 @dataclass
 class RunConfig:
