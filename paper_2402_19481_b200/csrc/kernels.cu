@@ -260,29 +260,119 @@ __global__ void gn_apply_kernel(const T* __restrict__ x, T* __restrict__ y, int 
     __syncthreads();
     const unsigned nvec = unsigned(ld / VEC);
     const unsigned total = unsigned(pix) * nvec;
-    for (unsigned idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += gridDim.x * blockDim.x) {
-        const unsigned p = idx / nvec;
-        const int c0 = int(idx - p * nvec) * VEC;
-        float f[VEC];
-        load_vec<T>(x + size_t(idx) * VEC, f);
-        float sk[VEC];
-        if (skip) load_vec<T>(skip + size_t(idx) * VEC, sk);
+    const unsigned stride = gridDim.x * blockDim.x;
+    constexpr int U = 4;   // vectors in flight per thread
+    for (unsigned idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += U * stride) {
+        float f[U][VEC], sk[U][VEC];
 #pragma unroll
-        for (int i = 0; i < VEC; ++i) {
-            const int c = c0 + i;
-            float v = (f[i] - s_mu[c]) * s_sc[c] + s_be[c];
-            if (do_silu) {
-                if constexpr (sizeof(T) == 2)
-                    v = v / (1.0f + __expf(-v));
-                else
-                    v = v / (1.0f + expf(-v));
+        for (int u = 0; u < U; ++u) {
+            const unsigned j = idx + u * stride;
+            if (j < total) {
+                load_vec<T>(x + size_t(j) * VEC, f[u]);
+                if (skip) load_vec<T>(skip + size_t(j) * VEC, sk[u]);
             }
-            v = v + s_te[c];
-            if (skip) v = v + sk[i];
-            f[i] = c < C ? v : 0.0f;
         }
-        store_vec<T>(y + size_t(idx) * VEC, f, round_tf32 != 0);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const unsigned j = idx + u * stride;
+            if (j >= total) continue;
+            const int c0 = int(j % nvec) * VEC;
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) {
+                const int c = c0 + i;
+                float v = (f[u][i] - s_mu[c]) * s_sc[c] + s_be[c];
+                if (do_silu) {
+                    if constexpr (sizeof(T) == 2)
+                        v = __fdividef(v, 1.0f + __expf(-v));
+                    else
+                        v = v / (1.0f + expf(-v));
+                }
+                v = v + s_te[c];
+                if (skip) v = v + sk[u][i];
+                f[u][i] = v;
+            }
+            if (c0 + VEC > C) {
+#pragma unroll
+                for (int i = 0; i < VEC; ++i)
+                    if (c0 + i >= C) f[u][i] = 0.0f;
+            }
+            store_vec<T>(y + size_t(j) * VEC, f[u], round_tf32 != 0);
+        }
+    }
+}
+
+// 2-D mapping: threadIdx.x / blockIdx.x select a fixed 16-byte channel vector (its GN
+// coefficients live in registers), threadIdx.y / blockIdx.y stride over pixels with four
+// vectors in flight per thread.  A warp touches 32 consecutive vectors of one pixel.
+template <class T>
+__global__ void gn_apply_2d_kernel(const T* __restrict__ x, T* __restrict__ y, int pix, int C,
+                                   int ld, int G, const GnCombine cb,
+                                   const float* __restrict__ gamma, const float* __restrict__ beta,
+                                   int do_silu, const float* __restrict__ temb,
+                                   const T* __restrict__ skip, int round_tf32) {
+    constexpr int VEC = Vec<T>::N;
+    __shared__ float s_use[2 * 1024];
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+    for (int g = tid; g < G; g += blockDim.x * blockDim.y) {
+        float mu, inv;
+        bool neg;
+        gn_use_of(cb, G, g, mu, inv, neg);
+        s_use[2 * g] = mu;
+        s_use[2 * g + 1] = inv;
+        // group_norm_apply contract (tensor.cpp:256-259), reported once per launch
+        if (neg && blockIdx.x == 0 && blockIdx.y == 0 && cb.err) atomicExch(cb.err, 1);
+    }
+    __syncthreads();
+    const int cv = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nvec = ld / VEC;
+    if (cv >= nvec) return;
+    const int c0 = cv * VEC;
+    const int cpg = C / G;
+    float mu[VEC], sc[VEC], be[VEC], te[VEC];
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+        const int c = c0 + i;
+        if (c < C) {
+            const int g = c / cpg;
+            mu[i] = s_use[2 * g];
+            sc[i] = s_use[2 * g + 1] * gamma[c];
+            be[i] = beta[c];
+            te[i] = temb ? temb[c] : 0.0f;
+        } else {
+            mu[i] = sc[i] = be[i] = te[i] = 0.0f;
+        }
+    }
+    const int pstride = blockDim.y * gridDim.y;
+    constexpr int U = 4;
+    for (int p = blockIdx.y * blockDim.y + threadIdx.y; p < pix; p += U * pstride) {
+        float f[U][VEC], sk[U][VEC];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int pp = p + u * pstride;
+            if (pp < pix) {
+                load_vec<T>(x + (size_t(pp) * nvec + cv) * VEC, f[u]);
+                if (skip) load_vec<T>(skip + (size_t(pp) * nvec + cv) * VEC, sk[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int pp = p + u * pstride;
+            if (pp >= pix) continue;
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) {
+                float v = (f[u][i] - mu[i]) * sc[i] + be[i];
+                if (do_silu) {
+                    if constexpr (sizeof(T) == 2)
+                        v = __fdividef(v, 1.0f + __expf(-v));
+                    else
+                        v = v / (1.0f + expf(-v));
+                }
+                v = v + te[i];
+                if (skip) v = v + sk[u][i];
+                f[u][i] = (c0 + i < C) ? v : 0.0f;
+            }
+            store_vec<T>(y + (size_t(pp) * nvec + cv) * VEC, f[u], round_tf32 != 0);
+        }
     }
 }
 
@@ -542,7 +632,16 @@ void gn_apply(Elem e, const void* x, void* y, long long pix, int C, int ld, int 
     if (groups > 1024) throw std::invalid_argument("group_norm_apply: too many groups");
     const int VEC = e == Elem::BF16 ? 8 : 4;
     if (pix * (ld / VEC) >= (1LL << 31)) throw std::invalid_argument("group_norm_apply: band too large");
-    DISPATCH(e, gn_apply_kernel<T><<<grid_for(pix * (ld / VEC), 256), 256, size_t(4) * ld * 4, s>>>(
+    // block = vx channel vectors x vy pixel lanes (~256 threads); grid fills ~4 waves of SMs
+    const int nvec = ld / VEC;
+    int vx = nvec;
+    while (vx > 128 && vx % 2 == 0) vx /= 2;
+    if (vx > 256) vx = 128;
+    const int gx = (nvec + vx - 1) / vx;
+    const int vy = std::max(1, 256 / vx);
+    const long long rows_needed = (pix + vy * 4 - 1) / (vy * 4);
+    const int gy = int(std::max<long long>(1, std::min<long long>(rows_needed, (148LL * 8) / gx)));
+    DISPATCH(e, gn_apply_2d_kernel<T><<<dim3(gx, gy), dim3(vx, vy), 0, s>>>(
                     static_cast<const T*>(x), static_cast<T*>(y), int(pix), C, ld, groups, cb, gamma,
                     beta, do_silu ? 1 : 0, temb, static_cast<const T*>(skip), round_tf32 ? 1 : 0));
     CUDA_CHECK(cudaGetLastError());

@@ -646,6 +646,8 @@ Runner::Runner(const Model& m, const std::vector<float>& cond, int h, int w, con
 }
 
 Runner::~Runner() {
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+    for (auto ev : graph_events_) cudaEventDestroy(ev);
     bands_.clear();
     naive_rows_.clear();
     naive_cols_.clear();
@@ -961,6 +963,73 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
         CUDA_CHECK(cudaEventRecord(a, b->cs));
         evs.emplace_back(a, z);
     }
+    // The denoising loop is captured once into a CUDA graph (per plan) and replayed:
+    // ~80 launches and ~30 exchange copies per step become one graph launch.
+    bool same_dev = true;
+    for (auto& b : bands_) same_dev &= b->dev == bands_[0]->dev;
+    const bool use_graph = !traj && !o_.profile && graphs_enabled_ && (o_.world > 1 || same_dev);
+    std::vector<double> key(ts, ts + n);
+    for (int i = 0; i < n; ++i) key.push_back(abar_at(ts[i]));
+    key.push_back(o_.mode);
+    key.push_back(o_.warmup);
+    // Graph launches are ordered on band 0's stream only: join the other bands' streams
+    // (x_T upload) before the launch and fork them again after it.
+    auto join_to_b0 = [&]() {
+        Program& b0 = *bands_[0];
+        for (auto& b : bands_) {
+            if (b.get() == &b0) continue;
+            CUDA_CHECK(cudaEventRecord(b->ready[0], b->cs));
+            CUDA_CHECK(cudaStreamWaitEvent(b0.cs, b->ready[0], 0));
+        }
+    };
+    auto fork_from_b0 = [&]() {
+        Program& b0 = *bands_[0];
+        CUDA_CHECK(cudaEventRecord(b0.ready[0], b0.cs));
+        for (auto& b : bands_)
+            if (b.get() != &b0) CUDA_CHECK(cudaStreamWaitEvent(b->cs, b0.ready[0], 0));
+    };
+    if (use_graph && graph_exec_ && key == graph_key_) {
+        Program& b0 = *bands_[0];
+        DeviceGuard g(b0.dev);
+        join_to_b0();
+        CUDA_CHECK(cudaGraphLaunch(graph_exec_, b0.cs));
+        fork_from_b0();
+        total_macs_ += graph_macs_;
+        for (size_t i = 0; i < graph_step_macs_.size(); ++i) {
+            while (step_device_macs_.size() <= i) step_device_macs_.emplace_back(n_dev_, 0);
+            for (int d = 0; d < n_dev_; ++d) step_device_macs_[i][d] += graph_step_macs_[i][d];
+        }
+        volumes_.allgather_recv += graph_vol_.allgather_recv;
+        volumes_.allgather_sent += graph_vol_.allgather_sent;
+        volumes_.halo_recv += graph_vol_.halo_recv;
+        volumes_.halo_sent += graph_vol_.halo_sent;
+        volumes_.statreduce_recv += graph_vol_.statreduce_recv;
+        volumes_.statreduce_sent += graph_vol_.statreduce_sent;
+        launches_ += graph_launches_;
+    } else {
+    const uint64_t macs0 = total_macs_;
+    const auto step_macs0 = step_device_macs_;
+    const CommVolumes vol0 = volumes_;
+    const long launches0 = launches_;
+    std::vector<cudaStream_t> others;
+    if (use_graph) {
+        Program& b0 = *bands_[0];
+        DeviceGuard g(b0.dev);
+        if (graph_exec_) {
+            cudaGraphExecDestroy(graph_exec_);
+            graph_exec_ = nullptr;
+        }
+        CUDA_CHECK(cudaStreamBeginCapture(b0.cs, cudaStreamCaptureModeThreadLocal));
+        cudaEvent_t fork;
+        CUDA_CHECK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+        CUDA_CHECK(cudaEventRecord(fork, b0.cs));
+        for (auto& b : bands_) {
+            if (b.get() != &b0) others.push_back(b->cs);
+            others.push_back(b->xs);
+        }
+        for (cudaStream_t s : others) CUDA_CHECK(cudaStreamWaitEvent(s, fork, 0));
+        graph_events_.push_back(fork);
+    }
     for (int i = 0; i < n; ++i) {
         const int t = ts[i];
         if (traj) {
@@ -993,6 +1062,47 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
                         b->e, b->stem.interior(b->eb), b->stem.ld, b->cs);
             launches_ += 1;
         }
+    }
+    if (use_graph) {
+        Program& b0 = *bands_[0];
+        DeviceGuard g(b0.dev);
+        for (cudaStream_t s : others) {
+            cudaEvent_t j;
+            CUDA_CHECK(cudaEventCreateWithFlags(&j, cudaEventDisableTiming));
+            CUDA_CHECK(cudaEventRecord(j, s));
+            CUDA_CHECK(cudaStreamWaitEvent(b0.cs, j, 0));
+            graph_events_.push_back(j);
+        }
+        cudaGraph_t graph;
+        CUDA_CHECK(cudaStreamEndCapture(b0.cs, &graph));
+        CUDA_CHECK(cudaGraphInstantiate(&graph_exec_, graph, 0));
+        CUDA_CHECK(cudaGraphDestroy(graph));
+        // events recorded inside the capture are re-armed as ordinary (completed) events
+        for (auto& b : bands_) {
+            DeviceGuard gb(b->dev);
+            for (auto ev : b->ready)
+                if (ev) CUDA_CHECK(cudaEventRecord(ev, b->cs));
+            for (auto& pr : b->sent)
+                for (auto ev : pr)
+                    if (ev) CUDA_CHECK(cudaEventRecord(ev, b->xs));
+        }
+        graph_key_ = key;
+        graph_macs_ = total_macs_ - macs0;
+        graph_step_macs_.assign(n, std::vector<uint64_t>(n_dev_, 0));
+        for (int i = 0; i < n; ++i)
+            for (int d = 0; d < n_dev_; ++d)
+                graph_step_macs_[i][d] = step_device_macs_[i][d] - (size_t(i) < step_macs0.size() ? step_macs0[i][d] : 0);
+        graph_vol_.allgather_recv = volumes_.allgather_recv - vol0.allgather_recv;
+        graph_vol_.allgather_sent = volumes_.allgather_sent - vol0.allgather_sent;
+        graph_vol_.halo_recv = volumes_.halo_recv - vol0.halo_recv;
+        graph_vol_.halo_sent = volumes_.halo_sent - vol0.halo_sent;
+        graph_vol_.statreduce_recv = volumes_.statreduce_recv - vol0.statreduce_recv;
+        graph_vol_.statreduce_sent = volumes_.statreduce_sent - vol0.statreduce_sent;
+        graph_launches_ = launches_ - launches0;
+        join_to_b0();
+        CUDA_CHECK(cudaGraphLaunch(graph_exec_, b0.cs));
+        fork_from_b0();
+    }
     }
     for (size_t k = 0; k < bands_.size(); ++k) {
         DeviceGuard g(bands_[k]->dev);

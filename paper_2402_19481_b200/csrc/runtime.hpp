@@ -114,6 +114,15 @@ private:
     ProfileTotals prof_;
     long launches_ = 0;
     double last_device_ms_ = 0;
+    // CUDA graph of the whole denoising loop (sample()), keyed by plan and mode
+    bool graphs_enabled_ = true;
+    cudaGraphExec_t graph_exec_ = nullptr;
+    std::vector<double> graph_key_;
+    std::vector<cudaEvent_t> graph_events_;
+    uint64_t graph_macs_ = 0;
+    std::vector<std::vector<uint64_t>> graph_step_macs_;
+    CommVolumes graph_vol_;
+    long graph_launches_ = 0;
     // host staging (pinned)
     float* h_x_ = nullptr;      // full NCHW image
     float* h_eps_ = nullptr;    // full NCHW image

@@ -110,3 +110,24 @@ def test_sdxl_shape_small(dtype, mode, n):
     for i, xt in enumerate(ref["trajectory"]):
         assert rel(got["trajectory"][i], xt) <= TOL[dtype], (i, rel(got["trajectory"][i], xt))
     assert rel(got["x0"], ref["x0"]) <= TOL[dtype], rel(got["x0"], ref["x0"])
+
+
+@pytest.mark.parametrize("mode,n", [("displaced", 1), ("displaced", 2), ("sync-pp", 4)])
+def test_graph_replay_is_bit_identical(mode, n):
+    # The denoising loop is captured into a CUDA graph on the first sample() and replayed
+    # afterwards; the eager path (trajectory=True disables the graph) must agree bitwise,
+    # and so must repeated replays (no float atomics anywhere: run-to-run determinism).
+    cfg = TOY
+    m = P.build_model(cfg, 42)
+    cond = O.random_condition(cfg.cond_dim, 7)
+    x = O.random_normal(1, cfg.in_channels, 32, 32, 1234)
+    abar = O.make_schedule()
+    plan = O.make_plan(1000, 6)
+    r = P.PatchRunner(m, cond, 32, 32, mode=mode, n_devices=n, warmup_steps=1, dtype="bf16")
+    eager, _ = r.sample(x, plan, abar, trajectory=True)
+    g1, _ = r.sample(x, plan, abar)
+    g2, _ = r.sample(x, plan, abar)
+    assert np.array_equal(g1, eager)
+    assert np.array_equal(g2, g1)
+    ref = O.run_sampling(ocfg(cfg), mode, n, 32, 32, 6, 1)["x0"]
+    assert rel(g2, ref) <= TOL["bf16"]
