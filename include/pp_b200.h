@@ -178,6 +178,10 @@ PP_API double pp_runner_last_device_ms(const pp_runner* r);
 PP_API int pp_runner_set_profile(pp_runner* r, int on);
 /* ncclGetUniqueId for the multi-process (one rank per GPU) layout */
 PP_API int pp_nccl_unique_id(void* out128);
+/* host stitching of a rank-ordered band all-gather [n][c][rows][w] into NCHW (c, n*rows, w),
+ * as run_workers stitches eps rows (proj/src/runtime.cpp:368-377) */
+PP_API int pp_assemble_bands(const float* gathered, int n_bands, int c, int rows, int w,
+                             float* out);
 
 /* ---- run_sampling (proj/src/runtime.cpp:494-526) ------------------------------------------ */
 PP_API int pp_run_sampling(const pp_run_config* cfg, float* x0, float* trajectory,

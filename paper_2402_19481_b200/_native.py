@@ -121,6 +121,7 @@ SIGNATURES = {
     "pp_runner_last_device_ms": (_D, [_V]),
     "pp_runner_set_profile": (_I, [_V, _I]),
     "pp_nccl_unique_id": (_I, [_V]),
+    "pp_assemble_bands": (_I, [_V, _I, _I, _I, _I, _V]),
     "pp_run_sampling": (_I, [_V, _V, _V, _V]),
     "pp_conv2d_region": (_I, [_I, _V, _I, _I, _I, _I, _I, _I, _V, _I, _I, _V, _I, _I, _V]),
     "pp_linear": (_I, [_I, _V, _I, _I, _I, _V, _I, _V, _V]),

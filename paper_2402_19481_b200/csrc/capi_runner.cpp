@@ -396,6 +396,16 @@ PP_API int pp_runner_set_profile(pp_runner* r, int on) {
     });
 }
 
+PP_API int pp_assemble_bands(const float* gathered, int n_bands, int c, int rows, int w,
+                             float* out) {
+    return pp::guard([&] {
+        need(gathered, "pp_assemble_bands");
+        need(out, "pp_assemble_bands");
+        if (n_bands < 1 || c < 1 || rows < 1 || w < 1) throw std::invalid_argument("pp_assemble_bands: bad shape");
+        pp::assemble_bands(gathered, n_bands, c, rows, w, out);
+    });
+}
+
 PP_API int pp_nccl_unique_id(void* out128) {
     return pp::guard([&] {
         need(out128, "pp_nccl_unique_id");

@@ -343,7 +343,7 @@ __global__ void gn_apply_2d_kernel(const T* __restrict__ x, T* __restrict__ y, i
         }
     }
     const int pstride = blockDim.y * gridDim.y;
-    constexpr int U = 4;
+    constexpr int U = 2;
     for (int p = blockIdx.y * blockDim.y + threadIdx.y; p < pix; p += U * pstride) {
         float f[U][VEC], sk[U][VEC];
 #pragma unroll
@@ -639,7 +639,7 @@ void gn_apply(Elem e, const void* x, void* y, long long pix, int C, int ld, int 
     if (vx > 256) vx = 128;
     const int gx = (nvec + vx - 1) / vx;
     const int vy = std::max(1, 256 / vx);
-    const long long rows_needed = (pix + vy * 4 - 1) / (vy * 4);
+    const long long rows_needed = (pix + vy - 1) / vy;
     const int gy = int(std::max<long long>(1, std::min<long long>(rows_needed, (148LL * 8) / gx)));
     DISPATCH(e, gn_apply_2d_kernel<T><<<dim3(gx, gy), dim3(vx, vy), 0, s>>>(
                     static_cast<const T*>(x), static_cast<T*>(y), int(pix), C, ld, groups, cb, gamma,

@@ -2,6 +2,7 @@
 #include "model.hpp"
 
 #include <cmath>
+#include <cstring>
 #include <stdexcept>
 
 namespace pp {
@@ -287,6 +288,15 @@ std::vector<float> timestep_embedding(int t, int dim) {
         e[half + i] = float(std::cos(t * f));
     }
     return e;
+}
+
+void assemble_bands(const float* g, int n, int C, int rows, int W, float* out) {
+    const size_t band = size_t(C) * rows * W;
+    const size_t H = size_t(n) * rows;
+    for (int r = 0; r < n; ++r)
+        for (int c = 0; c < C; ++c)
+            std::memcpy(out + (size_t(c) * H + size_t(r) * rows) * W, g + r * band + size_t(c) * rows * W,
+                        size_t(rows) * W * sizeof(float));
 }
 
 std::vector<double> make_schedule(int total, double b0, double b1) {

@@ -105,6 +105,10 @@ uint64_t model_total_macs(const Model& m, int h, int w);     // costmodel.cpp:64
 
 std::vector<float> timestep_embedding(int t, int dim);      // model.cpp:220-231
 
+// Rank-ordered all-gather result [N][C][rows][W] (each band NCHW) -> full NCHW image
+// (C, N*rows, W); the assembly run_workers does when stitching eps (runtime.cpp:368-377).
+void assemble_bands(const float* gathered, int n_bands, int C, int rows, int W, float* out);
+
 // ---- sampler schedule (proj/src/sampler.cpp:17-44) ---------------------------------------
 std::vector<double> make_schedule(int total, double beta_start, double beta_end);
 std::vector<int> make_plan(int total, int num_steps);

@@ -815,11 +815,7 @@ void Runner::store_eps(float* out) {
         transport_->gather_floats(b, b.band_nchw, b.x_full, band_n);
         CUDA_CHECK(cudaMemcpyAsync(h_eps_, b.x_full, band_n * n_dev_ * 4, cudaMemcpyDeviceToHost, b.cs));
         CUDA_CHECK(cudaStreamSynchronize(b.cs));
-        const int rows = b.stem.rows;
-        for (int r = 0; r < n_dev_; ++r)
-            for (int c = 0; c < C; ++c)
-                std::memcpy(out + (size_t(c) * h_ + size_t(r) * rows) * w_,
-                            h_eps_ + size_t(r) * band_n + size_t(c) * rows * w_, size_t(rows) * w_ * 4);
+        assemble_bands(h_eps_, n_dev_, C, b.stem.rows, w_, out);
         launches_ += 1;
         return;
     }
@@ -1117,11 +1113,7 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
         transport_->gather_floats(b, b.band_nchw, b.x_full, band_n);
         CUDA_CHECK(cudaMemcpyAsync(h_eps_, b.x_full, band_n * n_dev_ * 4, cudaMemcpyDeviceToHost, b.cs));
         CUDA_CHECK(cudaStreamSynchronize(b.cs));
-        const int rows = b.stem.rows;
-        for (int r = 0; r < n_dev_; ++r)
-            for (int c = 0; c < C; ++c)
-                std::memcpy(x0 + (size_t(c) * h_ + size_t(r) * rows) * w_,
-                            h_eps_ + size_t(r) * band_n + size_t(c) * rows * w_, size_t(rows) * w_ * 4);
+        assemble_bands(h_eps_, n_dev_, C, b.stem.rows, w_, x0);
     } else {
         for (auto& b : bands_) {
             DeviceGuard g(b->dev);

@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
-from ._native import InvalidArgument, RuntimeFailure  # noqa: F401
+from ._native import CudaError, InvalidArgument, NcclError, RuntimeFailure  # noqa: F401
 
 KINDS = ["Conv", "GroupNorm", "SiLU", "DownConv", "Upsample", "SelfAttn", "CrossAttn", "Linear",
          "AddSkip", "AddTimeEmb"]
