@@ -219,6 +219,12 @@ PP_API int pp_dev_conv(int dtype, const void* in, int rows, int W, int C_in_pad,
                        long long ldd, int out_f32, const void* residual, long long res_ld,
                        int force_splits, int force_block_n, void* stream);
 
+/* micro-benchmark of the tcgen05 kernel: kind 0 = GEMM [M][K]x[N][K]^T, 1/2 = implicit
+ * 3x3 conv stride 1/2 over a padded band (rows, W, K = C_in); ms_out[5] = {ms per launch,
+ * block_n, splits, stages, grid} */
+PP_API int pp_dev_gemm_bench(int dtype, int kind, int M_or_rows, int W, int K, int N,
+                             int force_splits, int force_block_n, int reps, double* ms_out);
+
 #ifdef __cplusplus
 }
 #endif

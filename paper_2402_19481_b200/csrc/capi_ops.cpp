@@ -89,4 +89,65 @@ PP_API int pp_dev_conv(int dtype, const void* in, int rows, int W, int C_in_pad,
     });
 }
 
+// Micro-benchmark: plan once, launch `reps` times back to back, return mean ms per launch
+// (CUDA events).  kind 0 = plain GEMM (A [M][K]), kind 1/2 = implicit conv stride 1/2 over a
+// padded band [rows+2][W][K] (M = output pixels).  Buffers are allocated here (random data
+// is irrelevant for timing).
+PP_API int pp_dev_gemm_bench(int dtype, int kind, int M_or_rows, int W, int K, int N,
+                             int force_splits, int force_block_n, int reps, double* ms_out) {
+    return pp::guard([&] {
+        pp::require_device();
+        const pp::Elem e = pp::elem_of(dtype);
+        const size_t eb = pp::elem_bytes(e);
+        const int n_pad = (N + 15) / 16 * 16;
+        const long long m_pix = kind == 0 ? M_or_rows
+                                          : (long long)(kind == 1 ? M_or_rows : M_or_rows / 2) *
+                                                (kind == 1 ? W : W / 2);
+        const size_t a_elems = kind == 0 ? size_t(M_or_rows) * K : size_t(M_or_rows + 2) * W * K;
+        const size_t b_elems = size_t(n_pad) * K * (kind == 0 ? 1 : 9);
+        pp::DeviceScratch A(a_elems * eb), B(b_elems * eb), D(size_t(m_pix) * n_pad * 2);
+        CUDA_CHECK(cudaMemset(A.ptr, 0, a_elems * eb));
+        CUDA_CHECK(cudaMemset(B.ptr, 0, b_elems * eb));
+        const size_t ws_bytes = size_t(8) * m_pix * n_pad * sizeof(float);
+        pp::DeviceScratch ws(ws_bytes), tk(size_t(1) << 20);
+        CUDA_CHECK(cudaMemset(tk.ptr, 0, size_t(1) << 20));
+        pp::GemmScratch sc;
+        sc.ws = static_cast<float*>(ws.ptr);
+        sc.ws_bytes = ws_bytes;
+        sc.tickets = static_cast<unsigned int*>(tk.ptr);
+        sc.n_tickets = (size_t(1) << 20) / 4;
+        pp::EpilogueSpec ep;
+        ep.out = D.ptr;
+        ep.out_ld = n_pad;
+        ep.n_valid = N;
+        pp::GemmPlan plan;
+        if (kind == 0)
+            pp::plan_gemm(plan, e, A.ptr, M_or_rows, K, K, B.ptr, N, K, ep, sc, pp::device_sm_count(),
+                          force_splits, force_block_n);
+        else
+            pp::plan_conv(plan, e, A.ptr, M_or_rows, W, K, kind, B.ptr, n_pad, ep, sc,
+                          pp::device_sm_count(), force_splits, force_block_n);
+        cudaStream_t s;
+        CUDA_CHECK(cudaStreamCreate(&s));
+        for (int i = 0; i < 3; ++i) pp::launch_gemm(plan, s);
+        cudaEvent_t a, b;
+        CUDA_CHECK(cudaEventCreate(&a));
+        CUDA_CHECK(cudaEventCreate(&b));
+        CUDA_CHECK(cudaEventRecord(a, s));
+        for (int i = 0; i < reps; ++i) pp::launch_gemm(plan, s);
+        CUDA_CHECK(cudaEventRecord(b, s));
+        CUDA_CHECK(cudaEventSynchronize(b));
+        float ms = 0;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
+        ms_out[0] = ms / reps;
+        ms_out[1] = plan.a.block_n;
+        ms_out[2] = plan.a.splits;
+        ms_out[3] = plan.a.stages;
+        ms_out[4] = plan.grid;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        cudaStreamDestroy(s);
+    });
+}
+
 }  // extern "C"

@@ -154,20 +154,36 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
         }
     }
     if (a.gn_groups) {
-        // column sums over the warp's 32 rows (invalid rows contribute 0)
+        // Column sums over the warp's 32 rows (invalid rows contribute 0) by a butterfly
+        // transpose-reduce: each xor step halves the columns a lane keeps, so 16 columns
+        // cost 16+8+4+2+1 shuffles per quantity instead of 16*5.  Lane l ends up with the
+        // sum of column 8*b4 + 4*b3 + 2*b2 + b1 (b = bits of l), duplicated on l ^ 1.
+        float s[16], q[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-            float s = valid ? v[j] : 0.0f;
-            float q = s * s;
+            s[j] = valid ? v[j] : 0.0f;
+            q[j] = s[j] * s[j];
+        }
 #pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                s += __shfl_xor_sync(0xffffffffu, s, o);
-                q += __shfl_xor_sync(0xffffffffu, q, o);
+        for (int o = 16, w = 8; o >= 2; o >>= 1, w >>= 1) {
+            const bool upper = (lane & o) != 0;
+#pragma unroll
+            for (int j = 0; j < w; ++j) {
+                const float gs = upper ? s[j] : s[j + w];
+                const float gq = upper ? q[j] : q[j + w];
+                const float ks = upper ? s[j + w] : s[j];
+                const float kq = upper ? q[j + w] : q[j];
+                s[j] = ks + __shfl_xor_sync(0xffffffffu, gs, o);
+                q[j] = kq + __shfl_xor_sync(0xffffffffu, gq, o);
             }
-            if (lane == 0) {
-                sgn_warp[(c0 + j) * 2] = s;
-                sgn_warp[(c0 + j) * 2 + 1] = q;
-            }
+        }
+        s[0] += __shfl_xor_sync(0xffffffffu, s[0], 1);
+        q[0] += __shfl_xor_sync(0xffffffffu, q[0], 1);
+        if ((lane & 1) == 0) {
+            const int col = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
+                            ((lane >> 1) & 1);
+            sgn_warp[(c0 + col) * 2] = s[0];
+            sgn_warp[(c0 + col) * 2 + 1] = q[0];
         }
     }
 }
@@ -348,42 +364,62 @@ __global__ void __launch_bounds__(kThreads, 1)
             epi_bar();
             const uint32_t t_row = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(cur * 256);
             if (a.splits > 1) {
+                // 2-way split-K.  The split that finishes its main loop first publishes its
+                // fp32 partial tile; the second adds it to its own TMEM accumulator.  fp32
+                // addition is commutative, so own + other is bitwise the same whichever split
+                // is second: deterministic.  The first never waits after taking its ticket,
+                // so the second's spin always terminates.
+                unsigned int* ticket = a.tile_ticket + 2 * size_t(tile_id);
+                unsigned int* ready = ticket + 1;
+                if (et == 0) st.flags[cur] = int(atomicAdd(ticket, 1u));
+                epi_bar();
+                const bool first = st.flags[cur] == 0;
+                float* part = a.partial + size_t(p) * a.n_pad + nbase;
+                if (first) {
+                    for (int c0 = 0; c0 < a.block_n; c0 += 16) {
+                        float v[16];
+                        ptx::tmem_ld16(t_row + c0, v);
+                        if (valid) {
+#pragma unroll
+                            for (int j = 0; j < 16; j += 4)
+                                __stcg(reinterpret_cast<float4*>(part + c0 + j),
+                                       make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+                        }
+                    }
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&st.tempty_bar[cur]);
+                    __threadfence();
+                    epi_bar();
+                    if (et == 0) atomicExch(ready, 1u);
+                    continue;
+                }
+                if (et == 0) {
+                    while (atomicAdd(ready, 0u) == 0u) __nanosleep(64);
+                }
+                epi_bar();
+                __threadfence();
                 for (int c0 = 0; c0 < a.block_n; c0 += 16) {
-                    float v[16];
+                    float v[16], o[16];
                     ptx::tmem_ld16(t_row + c0, v);
                     if (valid) {
-                        float* dst = a.partial + ((size_t)tc.split * a.m_pix + p) * a.n_pad + nbase + c0;
 #pragma unroll
-                        for (int j = 0; j < 16; j += 4)
-                            __stcg(reinterpret_cast<float4*>(dst + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+                        for (int j = 0; j < 16; j += 4) {
+                            const float4 q = __ldcg(reinterpret_cast<const float4*>(part + c0 + j));
+                            o[j] = q.x; o[j + 1] = q.y; o[j + 2] = q.z; o[j + 3] = q.w;
+                        }
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) v[j] = v[j] + o[j];
                     }
+                    finish_chunk<kTF32>(a, v, sbias, c0, nbase + c0, p, valid, sgn_warp, lane);
                 }
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&st.tempty_bar[cur]);
-                __threadfence();
-                epi_bar();
-                if (et == 0) st.flags[cur] = atomicAdd(&a.tile_ticket[tile_id], 1u) == unsigned(a.splits - 1);
-                epi_bar();
-                if (!st.flags[cur]) continue;
-                __threadfence();
-                for (int c0 = 0; c0 < a.block_n; c0 += 16) {
-                    float v[16];
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) v[j] = 0.0f;
-                    if (valid) {
-                        for (int k = 0; k < a.splits; ++k) {
-                            const float* src = a.partial + ((size_t)k * a.m_pix + p) * a.n_pad + nbase + c0;
-#pragma unroll
-                            for (int j = 0; j < 16; j += 4) {
-                                const float4 q = __ldcg(reinterpret_cast<const float4*>(src + j));
-                                v[j] += q.x; v[j + 1] += q.y; v[j + 2] += q.z; v[j + 3] += q.w;
-                            }
-                        }
-                    }
-                    finish_chunk<kTF32>(a, v, sbias, c0, nbase + c0, p, valid, sgn_warp, lane);
+                if (et == 0) {
+                    *ticket = 0u;
+                    *ready = 0u;
                 }
-                if (et == 0) a.tile_ticket[tile_id] = 0u;
             } else {
                 for (int c0 = 0; c0 < a.block_n; c0 += 16) {
                     float v[16];
@@ -495,6 +531,10 @@ int stages_for(int block_n, bool gn) {
 // quantised into waves over the SMs; split-K pays a partial write + read.
 void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int gn_cpg, int force_splits,
                    int force_block_n, int& block_n, int& splits) {
+    // Measured on B200 (scripts/gemm_micro.py, round 1): per-tile efficiency is best at
+    // block_n = 160 (~900-1050 TF/s on the SDXL conv shapes, 128 or 64 are 2x slower) and
+    // 256 for very large N; the in-kernel split-K reduction costs more than the wave
+    // quantisation it fixes on every layer shape of the workload, so it is opt-in only.
     double best = 1e300;
     block_n = 16;
     splits = 1;
@@ -503,16 +543,21 @@ void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int gn_cpg
         if (n_pad % bn) continue;
         if (gn_cpg && bn % gn_cpg) continue;
         const int nt = n_pad / bn;
-        for (int s : {1, 2, 3, 4, 6, 8}) {
-            if (force_splits && s != force_splits) continue;
-            if (s > 1 && k_blocks / s < 6 && !force_splits) continue;
+        for (int s : {1, 2}) {
+            if (force_splits && s != std::min(force_splits, 2)) continue;
             if (s > k_blocks) continue;
+            // split only when one wave leaves more than half of the SMs idle
+            if (!force_splits && s == 2 && ((long long)m_tiles * nt * 2 > num_sms || k_blocks < 16))
+                continue;
             const long long tiles = (long long)m_tiles * nt * s;
             const double waves = std::ceil(double(tiles) / num_sms);
-            const double per_kb = std::max(2.0 * bn, (16384.0 + 128.0 * bn) / 33.0);
+            // per 128-byte K block: MMA cycles (2*bn) at the per-tile efficiency measured
+            // for this N (160: ~0.62 of peak, 256: ~0.95 on big GEMMs, <=128: ~0.3-0.45)
+            const double eff = bn >= 256 ? 0.75 : bn >= 160 ? 0.62 : bn >= 128 ? 0.36 : 0.28;
+            const double per_kb = 2.0 * bn / eff;
             const double kbs = std::ceil(double(k_blocks) / s);
-            double cost = waves * (kbs * per_kb + 1500.0);
-            if (s > 1) cost += (s + 1) * 128.0 * bn * 4.0 / 33.0;
+            double cost = waves * (kbs * per_kb + 2500.0);
+            if (s > 1) cost += 2.0 * 128.0 * bn * 4.0 / 20.0;
             if (cost < best * 0.98) {
                 best = cost;
                 block_n = bn;
@@ -542,9 +587,10 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
     a.n_tiles = n_pad / bn;
     a.k_blocks = k_blocks;
     a.n_pad = n_pad;
-    while (splits > 1 && ((size_t)splits * a.m_pix * n_pad * sizeof(float) > sc.ws_bytes ||
-                          size_t(m_tiles) * a.n_tiles > sc.n_tickets))
-        --splits;
+    splits = std::min(splits, 2);
+    if (splits > 1 && ((size_t)a.m_pix * n_pad * sizeof(float) > sc.ws_bytes ||
+                       2 * size_t(m_tiles) * a.n_tiles > sc.n_tickets))
+        splits = 1;
     a.splits = splits;
     a.kb_per_split = (k_blocks + splits - 1) / splits;
     a.splits = (k_blocks + a.kb_per_split - 1) / a.kb_per_split;

@@ -305,7 +305,8 @@ __global__ void gn_apply_kernel(const T* __restrict__ x, T* __restrict__ y, int 
 // coefficients live in registers), threadIdx.y / blockIdx.y stride over pixels with four
 // vectors in flight per thread.  A warp touches 32 consecutive vectors of one pixel.
 template <class T>
-__global__ void gn_apply_2d_kernel(const T* __restrict__ x, T* __restrict__ y, int pix, int C,
+__global__ void __launch_bounds__(256, 4)
+    gn_apply_2d_kernel(const T* __restrict__ x, T* __restrict__ y, int pix, int C,
                                    int ld, int G, const GnCombine cb,
                                    const float* __restrict__ gamma, const float* __restrict__ beta,
                                    int do_silu, const float* __restrict__ temb,
@@ -323,55 +324,65 @@ __global__ void gn_apply_2d_kernel(const T* __restrict__ x, T* __restrict__ y, i
         if (neg && blockIdx.x == 0 && blockIdx.y == 0 && cb.err) atomicExch(cb.err, 1);
     }
     __syncthreads();
-    const int cv = blockIdx.x * blockDim.x + threadIdx.x;
+    // per-channel coefficients of this block's channel slice: (mean, inv_std*gamma, beta, temb)
+    __shared__ float4 s_coef[1024];
     const int nvec = ld / VEC;
-    if (cv >= nvec) return;
-    const int c0 = cv * VEC;
+    const int cbase = blockIdx.x * blockDim.x * VEC;
     const int cpg = C / G;
-    float mu[VEC], sc[VEC], be[VEC], te[VEC];
-#pragma unroll
-    for (int i = 0; i < VEC; ++i) {
-        const int c = c0 + i;
+    // layout [i][tx] (element i of thread tx's vector): a warp's LDS.128 of one i is
+    // 512 contiguous bytes -> conflict-free
+    for (int k = tid; k < int(blockDim.x) * VEC; k += blockDim.x * blockDim.y) {
+        const int txk = k / VEC, i = k - txk * VEC;
+        const int c = cbase + k;
+        float4 k4 = make_float4(0.f, 0.f, 0.f, 0.f);
         if (c < C) {
             const int g = c / cpg;
-            mu[i] = s_use[2 * g];
-            sc[i] = s_use[2 * g + 1] * gamma[c];
-            be[i] = beta[c];
-            te[i] = temb ? temb[c] : 0.0f;
-        } else {
-            mu[i] = sc[i] = be[i] = te[i] = 0.0f;
+            k4 = make_float4(s_use[2 * g], s_use[2 * g + 1] * gamma[c], beta[c], temb ? temb[c] : 0.0f);
         }
+        s_coef[i * blockDim.x + txk] = k4;
     }
+    __syncthreads();
+    const int cv = blockIdx.x * blockDim.x + threadIdx.x;
+    if (cv >= nvec) return;
+    const int c0 = cv * VEC;
+    const float4* coef = s_coef + threadIdx.x;
+    const int cstride = blockDim.x;
     const int pstride = blockDim.y * gridDim.y;
-    constexpr int U = 2;
+    constexpr int U = 4;   // raw 16-byte vectors in flight per thread (4 registers each)
+    const uint4* xv = reinterpret_cast<const uint4*>(x) + cv;
+    const uint4* sv = reinterpret_cast<const uint4*>(skip) + cv;
     for (int p = blockIdx.y * blockDim.y + threadIdx.y; p < pix; p += U * pstride) {
-        float f[U][VEC], sk[U][VEC];
+        uint4 rx[U], rs[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int pp = p + u * pstride;
             if (pp < pix) {
-                load_vec<T>(x + (size_t(pp) * nvec + cv) * VEC, f[u]);
-                if (skip) load_vec<T>(skip + (size_t(pp) * nvec + cv) * VEC, sk[u]);
+                rx[u] = __ldcs(xv + size_t(pp) * nvec);
+                if (skip) rs[u] = __ldcs(sv + size_t(pp) * nvec);
             }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int pp = p + u * pstride;
             if (pp >= pix) continue;
+            float f[VEC], sk[VEC];
+            load_vec<T>(reinterpret_cast<const T*>(&rx[u]), f);
+            if (skip) load_vec<T>(reinterpret_cast<const T*>(&rs[u]), sk);
 #pragma unroll
             for (int i = 0; i < VEC; ++i) {
-                float v = (f[u][i] - mu[i]) * sc[i] + be[i];
+                const float4 k4 = coef[i * cstride];
+                float v = (f[i] - k4.x) * k4.y + k4.z;
                 if (do_silu) {
                     if constexpr (sizeof(T) == 2)
                         v = __fdividef(v, 1.0f + __expf(-v));
                     else
                         v = v / (1.0f + expf(-v));
                 }
-                v = v + te[i];
-                if (skip) v = v + sk[u][i];
-                f[u][i] = (c0 + i < C) ? v : 0.0f;
+                v = v + k4.w;
+                if (skip) v = v + sk[i];
+                f[i] = (c0 + i < C) ? v : 0.0f;
             }
-            store_vec<T>(y + (size_t(pp) * nvec + cv) * VEC, f[u], round_tf32 != 0);
+            store_vec<T>(y + (size_t(pp) * nvec + cv) * VEC, f, round_tf32 != 0);
         }
     }
 }
@@ -526,6 +537,25 @@ __global__ void time_projection_kernel(const TembLayer* __restrict__ layers,
     }
 }
 
+__global__ void time_projection_plan_kernel(const TembLayer* __restrict__ layers,
+                                            const float* __restrict__ embs, int dim,
+                                            float* __restrict__ table, int n_layers, int ldt) {
+    extern __shared__ float emb[];
+    const int step = blockIdx.z;
+    for (int i = threadIdx.x; i < dim; i += blockDim.x) emb[i] = embs[(size_t)step * dim + i];
+    __syncthreads();
+    const TembLayer L = layers[blockIdx.y];
+    float* out = table + ((size_t)step * n_layers + blockIdx.y) * ldt;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int nw = blockDim.x / 32;
+    for (int c = blockIdx.x * nw + warp; c < L.C; c += gridDim.x * nw) {
+        double acc = 0.0;
+        for (int i = lane; i < dim; i += 32) acc += double(emb[i]) * double(L.W[(long long)c * dim + i]);
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) out[c] = float(acc + double(L.b[c]));
+    }
+}
+
 __global__ void gemv_f64_kernel(const float* __restrict__ W, const float* __restrict__ b,
                                 const float* __restrict__ x, int rows, int cols,
                                 float* __restrict__ out) {
@@ -636,11 +666,12 @@ void gn_apply(Elem e, const void* x, void* y, long long pix, int C, int ld, int 
     const int nvec = ld / VEC;
     int vx = nvec;
     while (vx > 128 && vx % 2 == 0) vx /= 2;
-    if (vx > 256) vx = 128;
+    if (vx > 128) vx = 128;
     const int gx = (nvec + vx - 1) / vx;
     const int vy = std::max(1, 256 / vx);
+    // one wave of ~4 blocks per SM; each thread keeps 4 vectors in flight per iteration
     const long long rows_needed = (pix + vy - 1) / vy;
-    const int gy = int(std::max<long long>(1, std::min<long long>(rows_needed, (148LL * 8) / gx)));
+    const int gy = int(std::max<long long>(1, std::min<long long>(rows_needed, (148LL * 4) / gx)));
     DISPATCH(e, gn_apply_2d_kernel<T><<<dim3(gx, gy), dim3(vx, vy), 0, s>>>(
                     static_cast<const T*>(x), static_cast<T*>(y), int(pix), C, ld, groups, cb, gamma,
                     beta, do_silu ? 1 : 0, temb, static_cast<const T*>(skip), round_tf32 ? 1 : 0));
@@ -701,6 +732,16 @@ void time_projection(const TembLayer* layers_dev, int n_layers, int max_c, const
     for (int i = 0; i < dim; ++i) arg.v[i] = emb[i];
     dim3 grid(std::max(1, (max_c + 7) / 8), n_layers);
     time_projection_kernel<<<grid, 256, dim * sizeof(float), s>>>(layers_dev, arg);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void time_projection_plan(const TembLayer* layers_dev, int n_layers, int max_c,
+                          const float* embs_dev, int n_steps, int dim, float* table, int ldt,
+                          cudaStream_t s) {
+    if (n_layers == 0 || n_steps == 0) return;
+    dim3 grid(std::max(1, (max_c + 7) / 8), n_layers, n_steps);
+    time_projection_plan_kernel<<<grid, 256, dim * sizeof(float), s>>>(layers_dev, embs_dev, dim,
+                                                                        table, n_layers, ldt);
     CUDA_CHECK(cudaGetLastError());
 }
 

@@ -75,6 +75,11 @@ struct EmbArg {
 };
 void time_projection(const TembLayer* layers_dev, int n_layers, int max_c, const float* emb,
                      int dim, cudaStream_t s);
+// The same projections for every timestep of a sampling plan at once:
+// table[step][layer][ldt] (fp32) from embs_dev[step][dim].
+void time_projection_plan(const TembLayer* layers_dev, int n_layers, int max_c,
+                          const float* embs_dev, int n_steps, int dim, float* table, int ldt,
+                          cudaStream_t s);
 // v[c] = W[c][:] . cond + b[c] in fp64 (project_condition value half, model.cpp:252-263)
 void gemv_f64(const float* W, const float* b, const float* x, int rows, int cols, float* out,
               cudaStream_t s);

@@ -109,6 +109,21 @@ struct Program {
     std::vector<float*> temb_out;   // per layer (nullptr unless AddTimeEmb)
     TembLayer* temb_dev = nullptr;
     int n_temb = 0, temb_max_c = 0;
+    // per-plan table of every step's projections (sample()): [step][slot][temb_ldt]
+    std::vector<int> temb_slot;     // layer -> slot among the AddTimeEmb layers
+    int temb_ldt = 0;
+    float* temb_plan = nullptr;
+    size_t temb_plan_cap = 0;
+    float* temb_embs = nullptr;
+    size_t temb_embs_cap = 0;
+    const float* temb_step_base = nullptr;   // non-null: this step reads the plan table
+    const float* temb_ptr(int l) const {
+        return temb_step_base ? temb_step_base + size_t(temb_slot[l]) * temb_ldt : temb_out[l];
+    }
+    void prepare_temb_plan(const int* ts, int n);
+    void use_temb_step(int i) {
+        temb_step_base = i < 0 ? nullptr : temb_plan + size_t(i) * n_temb * temb_ldt;
+    }
     // events
     std::vector<cudaEvent_t> ready;               // per layer
     std::vector<std::array<cudaEvent_t, 2>> sent; // per layer, per parity

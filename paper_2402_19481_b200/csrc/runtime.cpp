@@ -298,6 +298,9 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
         if (d.kind == Kind::AddTimeEmb) {
             temb_out[l] = static_cast<float*>(alloc(size_t(act_ld(d.out_ch, e)) * 4));
             tl.push_back(TembLayer{wts->L[l].temb_w, wts->L[l].temb_b, temb_out[l], d.out_ch});
+            if (int(temb_slot.size()) < L) temb_slot.assign(L, -1);
+            temb_slot[l] = int(tl.size()) - 1;
+            temb_ldt = std::max(temb_ldt, act_ld(d.out_ch, e));
             temb_max_c = std::max(temb_max_c, d.out_ch);
         }
     }
@@ -452,8 +455,31 @@ void Program::run_timed(int cat, double flops, const std::function<void()>& fn) 
 
 void Program::record_ready(int l) { CUDA_CHECK(cudaEventRecord(ready[l], cs)); }
 
-void Program::time_projection(int t) {
+void Program::prepare_temb_plan(const int* ts, int n) {
     if (!n_temb) return;
+    DeviceGuard dg(dev);
+    const int dim = m->time_dim();
+    std::vector<float> embs(size_t(n) * dim);
+    for (int i = 0; i < n; ++i) {
+        const std::vector<float> e1 = timestep_embedding(ts[i], dim);
+        std::copy(e1.begin(), e1.end(), embs.begin() + size_t(i) * dim);
+    }
+    const size_t need = size_t(n) * n_temb * temb_ldt;
+    if (need > temb_plan_cap) {
+        temb_plan = static_cast<float*>(alloc(need * 4));
+        temb_plan_cap = need;
+    }
+    if (embs.size() > temb_embs_cap) {
+        temb_embs = static_cast<float*>(alloc(embs.size() * 4));
+        temb_embs_cap = embs.size();
+    }
+    CUDA_CHECK(cudaMemcpy(temb_embs, embs.data(), embs.size() * 4, cudaMemcpyHostToDevice));
+    time_projection_plan(temb_dev, n_temb, temb_max_c, temb_embs, n, dim, temb_plan, temb_ldt, cs);
+    CUDA_CHECK(cudaStreamSynchronize(cs));
+}
+
+void Program::time_projection(int t) {
+    if (!n_temb || temb_step_base) return;
     run_timed(CAT_OTHER, 0, [&] {
         const std::vector<float> emb = timestep_embedding(t, m->time_dim());
         pp::time_projection(temb_dev, n_temb, temb_max_c, emb.data(), m->time_dim(), cs);
@@ -549,7 +575,7 @@ void Program::gn_apply(const Group& g, int mode, int par_cur, int par_prev) {
     run_timed(CAT_GN, 0, [&] {
         const Act& out = act[g.last];
         pp::gn_apply(e, in.interior(eb), out.interior(eb), in.pix(), in.C, in.ld, d.groups, cb,
-                     lw.gamma, lw.beta, g.silu, g.temb >= 0 ? temb_out[g.temb] : nullptr,
+                     lw.gamma, lw.beta, g.silu, g.temb >= 0 ? temb_ptr(g.temb) : nullptr,
                      g.skip >= 0 ? act[g.skip].interior(eb) : nullptr, rnd, cs);
     });
     count(1);
@@ -575,7 +601,7 @@ void Program::simple(const Group& g, int par) {
                         in.pix() * in.ld, rnd, cs);
                 break;
             case Kind::AddTimeEmb:
-                add_channel(e, in.interior(eb), temb_out[g.first], skip, out.interior(eb), in.pix(),
+                add_channel(e, in.interior(eb), temb_ptr(g.first), skip, out.interior(eb), in.pix(),
                             in.ld, false, rnd, cs);
                 break;
             case Kind::CrossAttn:
@@ -1003,6 +1029,7 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
         volumes_.statreduce_sent += graph_vol_.statreduce_sent;
         launches_ += graph_launches_;
     } else {
+    for (auto& b : bands_) b->prepare_temb_plan(ts, n);   // outside any capture (synchronous)
     const uint64_t macs0 = total_macs_;
     const auto step_macs0 = step_device_macs_;
     const CommVolumes vol0 = volumes_;
@@ -1048,7 +1075,9 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
         }
         bool displaced = false;
         if (o_.mode == MODE_DISPLACED) displaced = i >= 1 + o_.warmup;
+        for (auto& b : bands_) b->use_temb_step(i);
         run_bands(t, i, displaced);
+        for (auto& b : bands_) b->use_temb_step(-1);
         count_macs(i, false);
         const int t_next = i + 1 < n ? ts[i + 1] : -1;
         const double a_t = abar_at(t), a_n = abar_at(t_next);

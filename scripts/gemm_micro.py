@@ -1,0 +1,66 @@
+"""Micro-benchmark of the tcgen05 GEMM / implicit-conv kernel on the SDXL-shape layer shapes.
+
+usage (GPU box): python scripts/gemm_micro.py [--sweep]
+Prints TFLOP/s per shape (mean of back-to-back launches, CUDA events, warm L2).
+"""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2402_19481_b200 import _native as N  # noqa: E402
+
+# (name, kind, M_or_rows, W, K(=C_in), N) -- 1024^2 SDXL-shape conv layers at N=1 (Appendix A)
+SHAPES = [
+    ("L01 conv 320->320 @128^2", 1, 128, 128, 320, 320),
+    ("L49 conv 640->320 @128^2", 1, 128, 128, 640, 320),
+    ("L10 down 320->640 @128^2", 2, 128, 128, 320, 640),
+    ("L11 conv 640->640 @64^2", 1, 64, 64, 640, 640),
+    ("L37 conv 1280->640 @64^2", 1, 64, 64, 1280, 640),
+    ("L21 conv 1280->1280 @32^2", 1, 32, 32, 1280, 1280),
+    ("GEMM 16384x320x2880", 0, 16384, 1, 2880, 320),
+    ("GEMM 4096x640x5760", 0, 4096, 1, 5760, 640),
+    ("GEMM 8192x8192x8192", 0, 8192, 1, 8192, 8192),
+]
+
+
+def flops(kind, m, w, k, n):
+    if kind == 0:
+        return 2.0 * m * n * k
+    pix = (m * w) if kind == 1 else (m // 2) * (w // 2)
+    return 2.0 * pix * n * 9 * k
+
+
+def run(kind, m, w, k, n, splits=0, bn=0, reps=20):
+    out = np.zeros(5)
+    N.check(N.lib().pp_dev_gemm_bench(0, kind, m, w, k, n, splits, bn, reps,
+                                      out.ctypes.data_as(C.c_void_p)))
+    return out
+
+
+def main():
+    sweep = "--sweep" in sys.argv
+    for name, kind, m, w, k, n in SHAPES:
+        o = run(kind, m, w, k, n)
+        tf = flops(kind, m, w, k, n) / (o[0] * 1e-3) / 1e12
+        print(f"{name:30s} {o[0] * 1e3:8.1f} us {tf:7.1f} TF/s  bn={int(o[1])} splits={int(o[2])} "
+              f"stages={int(o[3])} grid={int(o[4])}", flush=True)
+        if sweep and kind != 0 or (sweep and m <= 4096):
+            for bn in (64, 128, 160, 256):
+                if n % bn:
+                    continue
+                for sp in (1, 2, 4):
+                    try:
+                        o = run(kind, m, w, k, n, sp, bn)
+                    except Exception as e:  # noqa: BLE001
+                        print("   ", bn, sp, "ERR", e)
+                        continue
+                    tf = flops(kind, m, w, k, n) / (o[0] * 1e-3) / 1e12
+                    print(f"    bn={bn:3d} splits={sp}  {o[0] * 1e3:8.1f} us {tf:7.1f} TF/s "
+                          f"stages={int(o[3])}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
