@@ -95,6 +95,14 @@ PP_API int pp_dev_conv(int dtype, const void* in, int rows, int W, int C_in_pad,
 // is irrelevant for timing).
 PP_API int pp_dev_gemm_bench(int dtype, int kind, int M_or_rows, int W, int K, int N,
                              int force_splits, int force_block_n, int reps, double* ms_out) {
+    // reps < 0: flags in the high bits -- bit 20 = fused GroupNorm statistics (32 groups),
+    // bit 21 = flush L2 (256 MiB memset) before every timed launch
+    const bool gn = reps > 0 && (reps & (1 << 20));
+    const bool flush = reps > 0 && (reps & (1 << 21));
+    // bit 22 = no MMA, bit 23 = no TMA, bit 24 = no epilogue work
+    const int debug = reps > 0 ? (reps >> 22) & 63 : 0;
+    const int cgroup = reps > 0 ? (reps >> 28) & 7 : 0;   // bits 28-30: commit group
+    reps &= 0xFFFFF;
     return pp::guard([&] {
         pp::require_device();
         const pp::Elem e = pp::elem_of(dtype);
@@ -120,6 +128,16 @@ PP_API int pp_dev_gemm_bench(int dtype, int kind, int M_or_rows, int W, int K, i
         ep.out = D.ptr;
         ep.out_ld = n_pad;
         ep.n_valid = N;
+        pp::DeviceScratch gp(size_t(1) << 22), gt(64), go(32 * 16);
+        if (gn) {
+            CUDA_CHECK(cudaMemset(gt.ptr, 0, 64));
+            sc.gn_part = static_cast<double*>(gp.ptr);
+            sc.gn_part_len = (size_t(1) << 22) / 8;
+            sc.gn_ticket = static_cast<unsigned int*>(gt.ptr);
+            ep.gn_groups = 32;
+            ep.gn_out = static_cast<double*>(go.ptr);
+        }
+        pp::DeviceScratch fl(flush ? size_t(256) << 20 : 16);
         pp::GemmPlan plan;
         if (kind == 0)
             pp::plan_gemm(plan, e, A.ptr, M_or_rows, K, K, B.ptr, N, K, ep, sc, pp::device_sm_count(),
@@ -127,18 +145,33 @@ PP_API int pp_dev_gemm_bench(int dtype, int kind, int M_or_rows, int W, int K, i
         else
             pp::plan_conv(plan, e, A.ptr, M_or_rows, W, K, kind, B.ptr, n_pad, ep, sc,
                           pp::device_sm_count(), force_splits, force_block_n);
+        plan.a.debug = debug;
+        if (cgroup) plan.a.commit_group = std::min(cgroup, plan.a.stages / 2);
         cudaStream_t s;
         CUDA_CHECK(cudaStreamCreate(&s));
         for (int i = 0; i < 3; ++i) pp::launch_gemm(plan, s);
         cudaEvent_t a, b;
         CUDA_CHECK(cudaEventCreate(&a));
         CUDA_CHECK(cudaEventCreate(&b));
-        CUDA_CHECK(cudaEventRecord(a, s));
-        for (int i = 0; i < reps; ++i) pp::launch_gemm(plan, s);
-        CUDA_CHECK(cudaEventRecord(b, s));
-        CUDA_CHECK(cudaEventSynchronize(b));
         float ms = 0;
-        CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
+        if (!flush) {
+            CUDA_CHECK(cudaEventRecord(a, s));
+            for (int i = 0; i < reps; ++i) pp::launch_gemm(plan, s);
+            CUDA_CHECK(cudaEventRecord(b, s));
+            CUDA_CHECK(cudaEventSynchronize(b));
+            CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
+        } else {
+            for (int i = 0; i < reps; ++i) {
+                CUDA_CHECK(cudaMemsetAsync(fl.ptr, i & 0xff, size_t(256) << 20, s));
+                CUDA_CHECK(cudaEventRecord(a, s));
+                pp::launch_gemm(plan, s);
+                CUDA_CHECK(cudaEventRecord(b, s));
+                CUDA_CHECK(cudaEventSynchronize(b));
+                float one = 0;
+                CUDA_CHECK(cudaEventElapsedTime(&one, a, b));
+                ms += one;
+            }
+        }
         ms_out[0] = ms / reps;
         ms_out[1] = plan.a.block_n;
         ms_out[2] = plan.a.splits;

@@ -59,6 +59,8 @@ struct GemmArgs {
     double* gn_part;          // [m_tiles][groups][2]
     unsigned int* gn_ticket;  // zero, reset by the last tile
     double* gn_out;           // [groups][2] = (mean, mean_sq)
+    int debug;                // micro-benchmarks only: bit0 = no MMA, bit1 = no TMA loads
+    int commit_group;         // K blocks per smem-release commit (<= stages / 2)
 };
 
 struct GemmPlan {

@@ -240,91 +240,102 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int a_box_bytes = conv ? a.rows_box * a.w_box * kBlockBytes : a_stage_bytes;
 
     if (warp == 0) {
-        if (lane == 0) {
-            // ===== TMA producer =====
-            int stage = 0;
-            uint32_t phase = 0;
-            const int kel = kTF32 ? 32 : 64;  // elements per 128-byte K block
-            for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-                const TileCoord tc = decode_tile(a, t);
-                const int kb0 = tc.split * a.kb_per_split;
-                const int kb1 = min(kb0 + a.kb_per_split, a.k_blocks);
-                const int oy0 = tc.ty * a.rows_box, ox0 = tc.tx * a.w_box;
-                int tap = kb0 / a.cin_chunks;
-                int chunk = kb0 - tap * a.cin_chunks;
-                for (int kb = kb0; kb < kb1; ++kb) {
-                    ptx::mbar_wait(&st.empty_bar[stage], phase ^ 1);
-                    uint8_t* sa = smem + size_t(stage) * stage_bytes;
-                    uint8_t* sb = sa + a_stage_bytes;
-                    ptx::mbar_arrive_expect_tx(&st.full_bar[stage], a_box_bytes + b_stage_bytes);
-                    if (!conv) {
-                        ptx::tma_load_2d(sa, &tmA, &st.full_bar[stage], kb * kel, tc.ty * kTileM);
+        // ===== TMA producer (warp-uniform loop, one elected lane issues) =====
+        int stage = 0;
+        uint32_t phase = 0;
+        const int kel = kTF32 ? 32 : 64;  // elements per 128-byte K block
+        for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+            const TileCoord tc = decode_tile(a, t);
+            const int kb0 = tc.split * a.kb_per_split;
+            const int kb1 = min(kb0 + a.kb_per_split, a.k_blocks);
+            const int oy0 = tc.ty * a.rows_box, ox0 = tc.tx * a.w_box;
+            const int bcoord = tc.nt * a.block_n;
+            int tap = kb0 / a.cin_chunks;
+            int chunk = kb0 - tap * a.cin_chunks;
+            for (int kb = kb0; kb < kb1; ++kb) {
+                ptx::mbar_wait(&st.empty_bar[stage], phase ^ 1);
+                uint8_t* sa = smem + size_t(stage) * stage_bytes;
+                uint8_t* sb = sa + a_stage_bytes;
+                if (ptx::elect_one()) {
+                    if (a.debug & 2) {   // micro-benchmark: barriers only, no data movement
+                        ptx::mbar_arrive(&st.full_bar[stage]);
                     } else {
-                        const int ky = tap / 3, kx = tap - 3 * (tap / 3);
-                        if (a.mode == 1) {
-                            ptx::tma_load_5d(sa, &tmA, &st.full_bar[stage], chunk * kel, 0,
-                                             ox0 + kx - 1, 0, oy0 + ky);
+                        ptx::mbar_arrive_expect_tx(&st.full_bar[stage], a_box_bytes + b_stage_bytes);
+                        if (!conv) {
+                            ptx::tma_load_2d(sa, &tmA, &st.full_bar[stage], kb * kel, tc.ty * kTileM);
                         } else {
-                            ptx::tma_load_5d(sa, &tmA, &st.full_bar[stage], chunk * kel,
-                                             kx == 1 ? 0 : 1, ox0 + (kx == 0 ? -1 : 0),
-                                             ky == 1 ? 1 : 0, oy0 + (ky == 2 ? 1 : 0));
+                            const int ky = tap / 3, kx = tap - 3 * ky;
+                            if (a.mode == 1) {
+                                ptx::tma_load_5d(sa, &tmA, &st.full_bar[stage], chunk * kel, 0,
+                                                 ox0 + kx - 1, 0, oy0 + ky);
+                            } else {
+                                ptx::tma_load_5d(sa, &tmA, &st.full_bar[stage], chunk * kel,
+                                                 kx == 1 ? 0 : 1, ox0 + (kx == 0 ? -1 : 0),
+                                                 ky == 1 ? 1 : 0, oy0 + (ky == 2 ? 1 : 0));
+                            }
                         }
-                        if (++chunk == a.cin_chunks) {
-                            chunk = 0;
-                            ++tap;
-                        }
+                        ptx::tma_load_2d(sb, &tmB, &st.full_bar[stage], kb * kel, bcoord);
                     }
-                    ptx::tma_load_2d(sb, &tmB, &st.full_bar[stage], kb * kel, tc.nt * a.block_n);
-                    if (++stage == stages) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+                }
+                __syncwarp();
+                if (conv && ++chunk == a.cin_chunks) {
+                    chunk = 0;
+                    ++tap;
+                }
+                if (++stage == stages) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // ===== MMA issuer =====
-            int stage = 0;
-            uint32_t phase = 0;
-            int acc = 0;
-            uint32_t acc_phase = 0;
-            for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-                const TileCoord tc = decode_tile(a, t);
-                const int kb0 = tc.split * a.kb_per_split;
-                const int kb1 = min(kb0 + a.kb_per_split, a.k_blocks);
-                ptx::mbar_wait(&st.tempty_bar[acc], acc_phase ^ 1);
-                ptx::tc_fence_after();
-                const uint32_t d_tmem = tmem_base + uint32_t(acc * 256);
-                for (int kb = kb0; kb < kb1; ++kb) {
+        // ===== MMA issuer (warp-uniform loop, one elected lane issues) =====
+        // Descriptors: stage s, K step k = base + s * (stage_bytes >> 4) + 2 * k (the start
+        // address field is addr >> 4; +32 bytes per 16-element bf16 / 8-element tf32 step).
+        const uint32_t smem0 = ptx::smem_u32(smem);
+        const uint64_t desc_a0 = ptx::smem_desc_sw128(smem0);
+        const uint64_t desc_b0 = ptx::smem_desc_sw128(smem0 + a_stage_bytes);
+        const uint64_t desc_stride = stage_bytes >> 4;
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+            const TileCoord tc = decode_tile(a, t);
+            const int kb0 = tc.split * a.kb_per_split;
+            const int kb1 = min(kb0 + a.kb_per_split, a.k_blocks);
+            ptx::mbar_wait(&st.tempty_bar[acc], acc_phase ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t d_tmem = tmem_base + uint32_t(acc * 256);
+            for (int kb = kb0; kb < kb1; ++kb) {
+                if (!(a.debug & 16)) {   // debug bit 16: no wait (micro-benchmark only)
                     ptx::mbar_wait(&st.full_bar[stage], phase);
                     ptx::tc_fence_after();
-                    const uint32_t sa = ptx::smem_u32(smem + size_t(stage) * stage_bytes);
-                    const uint32_t sb = sa + a_stage_bytes;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const uint64_t da = ptx::smem_desc_sw128(sa + k * 32);
-                        const uint64_t db = ptx::smem_desc_sw128(sb + k * 32);
-                        const uint32_t accum = (kb > kb0 || k > 0) ? 1u : 0u;
+                }
+                const uint64_t da = desc_a0 + uint64_t(stage) * desc_stride;
+                const uint64_t db = desc_b0 + uint64_t(stage) * desc_stride;
+                if (ptx::elect_one()) {
+                    if (!(a.debug & 1)) {
                         if (kTF32)
-                            ptx::mma_tf32(d_tmem, da, db, a.idesc, accum);
+                            ptx::mma4_tf32(d_tmem, da, db, a.idesc, kb > kb0 ? 1u : 0u);
                         else
-                            ptx::mma_bf16(d_tmem, da, db, a.idesc, accum);
+                            ptx::mma4_bf16(d_tmem, da, db, a.idesc, kb > kb0 ? 1u : 0u);
                     }
                     ptx::mma_commit(&st.empty_bar[stage]);
-                    if (++stage == stages) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
                 }
-                ptx::mma_commit(&st.tfull_bar[acc]);
-                if (++acc == 2) {
-                    acc = 0;
-                    acc_phase ^= 1;
+                __syncwarp();
+                if (++stage == stages) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
+            if (ptx::elect_one()) ptx::mma_commit(&st.tfull_bar[acc]);
+            __syncwarp();
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
         }
-        __syncwarp();
     } else {
         // ===== epilogue (warps 2..5; TMEM lane quarter = warp % 4) =====
         const int quarter = warp & 3;
@@ -361,6 +372,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 sbias[c] = (a.bias && nbase + c < a.n_valid) ? a.bias[nbase + c] : 0.0f;
             ptx::mbar_wait(&st.tfull_bar[cur], cur_phase);
             ptx::tc_fence_after();
+            if (a.debug & 4) {   // micro-benchmark: release the accumulator, no epilogue work
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&st.tempty_bar[cur]);
+                continue;
+            }
             epi_bar();
             const uint32_t t_row = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(cur * 256);
             if (a.splits > 1) {
@@ -450,18 +467,53 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (et == 0) st.flags[2] = atomicAdd(a.gn_ticket, 1u) == unsigned(final_tiles - 1);
                 epi_bar();
                 if (st.flags[2]) {
+                    // last tile of the GEMM: fold the per-m-tile partials.  P threads per
+                    // group each sum a fixed residue class of m-tiles (8 loads in flight),
+                    // then one thread adds the P partials in order -> deterministic.
                     __threadfence();
                     const int m_tiles = a.tiles_y * a.tiles_x;
-                    for (int g = et; g < a.gn_groups; g += 128) {
+                    const int G = a.gn_groups;
+                    const int P = G >= 128 ? 1 : 128 / G;
+                    double* sfold = reinterpret_cast<double*>(st.gn);   // [P][G][2] (<= 256 x 2)
+                    for (int w = et; w < G * P; w += 128) {
+                        const int g = w % G, part = w / G;
                         double s = 0.0, q = 0.0;
-                        for (int m = 0; m < m_tiles; ++m) {
-                            s += __ldcg(a.gn_part + ((size_t)m * a.gn_groups + g) * 2);
-                            q += __ldcg(a.gn_part + ((size_t)m * a.gn_groups + g) * 2 + 1);
+                        for (int m0 = part; m0 < m_tiles; m0 += 8 * P) {
+                            double ls[8], lq[8];
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                const int m = m0 + u * P;
+                                ls[u] = m < m_tiles ? __ldcg(a.gn_part + ((size_t)m * G + g) * 2) : 0.0;
+                                lq[u] = m < m_tiles ? __ldcg(a.gn_part + ((size_t)m * G + g) * 2 + 1) : 0.0;
+                            }
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                s += ls[u];
+                                q += lq[u];
+                            }
                         }
-                        a.gn_out[g * 2] = s / a.gn_count;
-                        a.gn_out[g * 2 + 1] = q / a.gn_count;
+                        if (G * P <= 512) {
+                            sfold[(part * G + g) * 2] = s;
+                            sfold[(part * G + g) * 2 + 1] = q;
+                        } else {
+                            a.gn_out[g * 2] = s / a.gn_count;   // P == 1
+                            a.gn_out[g * 2 + 1] = q / a.gn_count;
+                        }
+                    }
+                    epi_bar();
+                    if (G * P <= 512) {
+                        for (int g = et; g < G; g += 128) {
+                            double s = 0.0, q = 0.0;
+                            for (int part = 0; part < P; ++part) {
+                                s += sfold[(part * G + g) * 2];
+                                q += sfold[(part * G + g) * 2 + 1];
+                            }
+                            a.gn_out[g * 2] = s / a.gn_count;
+                            a.gn_out[g * 2 + 1] = q / a.gn_count;
+                        }
                     }
                     if (et == 0) *a.gn_ticket = 0u;
+                    epi_bar();
                 }
             }
         }
@@ -595,6 +647,7 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
     a.kb_per_split = (k_blocks + splits - 1) / splits;
     a.splits = (k_blocks + a.kb_per_split - 1) / a.kb_per_split;
     a.stages = stages_for(bn, gn);
+    a.commit_group = 1;
     a.idesc = make_idesc(p.elem, bn);
     a.out = ep.out;
     a.out_ld = ep.out_ld;

@@ -11,6 +11,19 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// One lane of the (converged) warp: elect.sync.  Lets the whole warp run a warp-uniform
+// loop while a single lane issues tcgen05 / TMA instructions, so the compiler keeps the
+// loop state in uniform registers (no per-instruction ELECT loop).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 // ---- mbarrier ------------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
@@ -106,6 +119,31 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint6
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// The four K=16 (bf16) / K=8 (tf32) steps of one 128-byte K block in a single asm block:
+// descriptor k = base + 2*k (32 bytes further in the swizzled row), accumulate = acc0 for
+// the first step and 1 for the rest.  One asm statement keeps the issue path short.
+#define PP_MMA4(KIND)                                                                      \
+    asm volatile(                                                                          \
+        "{\n\t.reg .pred p;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"                      \
+        "setp.ne.b32 p, %4, 0;\n\t"                                                         \
+        "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"               \
+        "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"               \
+        "tcgen05.mma.cta_group::1.kind::" KIND " [%0], %1, %2, %3, p;\n\t"                 \
+        "tcgen05.mma.cta_group::1.kind::" KIND " [%0], a1, b1, %3, 1;\n\t"                 \
+        "tcgen05.mma.cta_group::1.kind::" KIND " [%0], a2, b2, %3, 1;\n\t"                 \
+        "tcgen05.mma.cta_group::1.kind::" KIND " [%0], a3, b3, %3, 1;\n\t}" ::"r"(d_tmem), \
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(acc0)                                    \
+        : "memory")
+__device__ __forceinline__ void mma4_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t acc0) {
+    PP_MMA4("f16");
+}
+__device__ __forceinline__ void mma4_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t acc0) {
+    PP_MMA4("tf32");
+}
+#undef PP_MMA4
+
 // Arrive on an mbarrier when all previously issued tcgen05 ops of this thread finish.
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile(

@@ -1,7 +1,8 @@
 """Micro-benchmark of the tcgen05 GEMM / implicit-conv kernel on the SDXL-shape layer shapes.
 
-usage (GPU box): python scripts/gemm_micro.py [--sweep]
-Prints TFLOP/s per shape (mean of back-to-back launches, CUDA events, warm L2).
+usage (GPU box): python scripts/gemm_micro.py [--sweep] [--variants]
+Prints TFLOP/s per shape (mean of launches, CUDA events).  --variants adds the fused
+GroupNorm-statistics epilogue and a cold L2 (256 MiB flush before each launch).
 """
 import ctypes as C
 import os
@@ -20,10 +21,13 @@ SHAPES = [
     ("L11 conv 640->640 @64^2", 1, 64, 64, 640, 640),
     ("L37 conv 1280->640 @64^2", 1, 64, 64, 1280, 640),
     ("L21 conv 1280->1280 @32^2", 1, 32, 32, 1280, 1280),
+    ("L01/8 band 320->320 16x128", 1, 16, 128, 320, 320),
+    ("L11/8 band 640->640 8x64", 1, 8, 64, 640, 640),
+    ("L21/8 band 1280 4x32", 1, 4, 32, 1280, 1280),
     ("GEMM 16384x320x2880", 0, 16384, 1, 2880, 320),
-    ("GEMM 4096x640x5760", 0, 4096, 1, 5760, 640),
     ("GEMM 8192x8192x8192", 0, 8192, 1, 8192, 8192),
 ]
+GN, FLUSH = 1 << 20, 1 << 21
 
 
 def flops(kind, m, w, k, n):
@@ -42,16 +46,28 @@ def run(kind, m, w, k, n, splits=0, bn=0, reps=20):
 
 def main():
     sweep = "--sweep" in sys.argv
+    variants = "--variants" in sys.argv
     for name, kind, m, w, k, n in SHAPES:
         o = run(kind, m, w, k, n)
         tf = flops(kind, m, w, k, n) / (o[0] * 1e-3) / 1e12
-        print(f"{name:30s} {o[0] * 1e3:8.1f} us {tf:7.1f} TF/s  bn={int(o[1])} splits={int(o[2])} "
-              f"stages={int(o[3])} grid={int(o[4])}", flush=True)
-        if sweep and kind != 0 or (sweep and m <= 4096):
+        line = (f"{name:30s} {o[0] * 1e3:8.1f} us {tf:7.1f} TF/s  bn={int(o[1])} "
+                f"splits={int(o[2])} stages={int(o[3])} grid={int(o[4])}")
+        if variants and kind != 0:
+            g = run(kind, m, w, k, n, reps=20 | GN)
+            c = run(kind, m, w, k, n, reps=10 | GN | FLUSH)
+            nm = run(kind, m, w, k, n, reps=20 | (1 << 22))
+            nt = run(kind, m, w, k, n, reps=20 | (2 << 22))
+            ne = run(kind, m, w, k, n, reps=20 | (4 << 22))
+            nb = run(kind, m, w, k, n, reps=20 | (6 << 22))
+            line += (f" | +gn {g[0] * 1e3:7.1f} us | +gn+coldL2 {c[0] * 1e3:7.1f} us"
+                     f" | noMMA {nm[0] * 1e3:7.1f} us | noTMA {nt[0] * 1e3:7.1f} us"
+                     f" | noEpi {ne[0] * 1e3:7.1f} us | mmaOnly {nb[0] * 1e3:7.1f} us")
+        print(line, flush=True)
+        if sweep and kind != 0:
             for bn in (64, 128, 160, 256):
                 if n % bn:
                     continue
-                for sp in (1, 2, 4):
+                for sp in (1, 2):
                     try:
                         o = run(kind, m, w, k, n, sp, bn)
                     except Exception as e:  # noqa: BLE001
