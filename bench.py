@@ -15,8 +15,9 @@ e2e        the same generation through the public C ABI (pp_runner_sample) from 
 roofline   dominant kernel = the tcgen05 implicit-GEMM conv; algorithmic FLOPs
            (2 * macs_of_layer, proj/src/costmodel.cpp:33-62) / CUDA-event kernel time
 cpu_baseline  the reference's own CPU path (oracle/_ref = /root/reference/proj/src built
-           unmodified) on this box's host cores: a bounded sample (one reference-mode
-           step at a 32x32 latent), extrapolated to the workload by MAC count
+           unmodified) on this box's host cores: a bounded sample (one sync-pp step over
+           4 thread bands at a 48x48 latent), extrapolated to the workload by MAC count
+           (optimistic for the CPU: its per-MAC cost grows with the latent size)
 """
 from __future__ import annotations
 
@@ -80,25 +81,44 @@ def workload(args, n):
 
 
 # ------------------------------------------------------------------------ reference CPU path
+def cpu_threads():
+    """Bands for the threaded reference sample: a power of two <= host cores, <= 4 (the
+    reference's sync-pp step stops scaling beyond ~4 threads: per-layer hub barriers)."""
+    n = 1
+    while n * 2 <= min(os.cpu_count() or 1, 4):
+        n *= 2
+    return n
+
+
 def cpu_reference_sample(latent_full, num_steps):
-    """Time one reference-mode step of the reference's own CPU path (oracle/_ref) on a
-    32x32 SDXL-shape latent and extrapolate to `num_steps` steps at latent_full^2."""
+    """Time one step of the reference's own CPU path (oracle/_ref, unmodified
+    proj/src sources) on a 48x48 SDXL-shape latent and extrapolate by MAC count to
+    `num_steps` steps at latent_full^2.  The reference's only multi-threaded execution is
+    its PatchRunner (one std::thread per simulated device, runtime.cpp:337-380; tensor ops
+    are single-threaded), so the step is a synchronous patch-parallel step (sync-pp: same
+    result as the reference forward, test_runtime.cpp:231-248) over cpu_threads() bands --
+    every host core busy."""
     from oracle import ref as R
     if not os.path.exists(R.LIB_PATH) and not os.path.isdir(R.REF_SRC):
         return None
     model = R.Model(SDXL, SEEDS[0])
     cond = R.random_condition(2048, SEEDS[2])
-    side = 32
+    side = 48
+    n = cpu_threads()
     x = R.random_normal(1, 4, side, side, SEEDS[1])
+    runner = R.PatchRunner(model, cond, side, side, mode="sync-pp" if n > 1 else "reference",
+                           n_devices=n)
     t0 = time.perf_counter()
-    model.forward_full(x, 980, cond)
+    runner.step("run_step", x, 980, 0)
     dt = time.perf_counter() - t0
     scale = model.total_macs(latent_full, latent_full) / model.total_macs(side, side)
     return {"seconds_sample": dt, "value": dt * scale * num_steps, "macs_ratio": scale,
-            "sample": f"1 reference-mode step (forward_full, proj/src/model.cpp:363) of the "
-                      f"SDXL-shape model at a {side}x{side} latent, extrapolated x{scale:.2f} by "
-                      f"model_total_macs to {latent_full}x{latent_full} and x{num_steps} steps",
-            "kind": "reference", "cores": int(os.environ.get("OMP_NUM_THREADS", "1"))}
+            "sample": f"1 denoising step of the reference CPU path (PatchRunner::run_step, "
+                      f"proj/src/runtime.cpp:454-476, {'sync-pp over ' + str(n) + ' thread bands' if n > 1 else 'reference mode'}) "
+                      f"on the SDXL-shape model at a {side}x{side} latent, extrapolated "
+                      f"x{scale:.2f} by model_total_macs to {latent_full}x{latent_full} and "
+                      f"x{num_steps} steps",
+            "kind": "reference", "cores": n}
 
 
 def cpu_port_sample(latent_full, num_steps):

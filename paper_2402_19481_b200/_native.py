@@ -11,7 +11,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpp_b200.so")
+LIB_PATH = os.environ.get("PP_B200_LIB") or os.path.join(HERE, "libpp_b200.so")
 
 PP_OK, PP_EINVAL, PP_ERUNTIME, PP_ECUDA, PP_ENCCL = 0, 1, 2, 3, 4
 DTYPES = {"bf16": 0, "fp32": 1}

@@ -99,9 +99,9 @@ PP_API int pp_dev_gemm_bench(int dtype, int kind, int M_or_rows, int W, int K, i
     // bit 21 = flush L2 (256 MiB memset) before every timed launch
     const bool gn = reps > 0 && (reps & (1 << 20));
     const bool flush = reps > 0 && (reps & (1 << 21));
-    // bit 22 = no MMA, bit 23 = no TMA, bit 24 = no epilogue work
-    const int debug = reps > 0 ? (reps >> 22) & 63 : 0;
-    const int cgroup = reps > 0 ? (reps >> 28) & 7 : 0;   // bits 28-30: commit group
+    // bits 22..29 = kernel debug flags: 1 no MMA, 2 no TMA, 4 no epilogue work, 16 no
+    // full-barrier wait
+    const int debug = reps > 0 ? (reps >> 22) & 255 : 0;
     reps &= 0xFFFFF;
     return pp::guard([&] {
         pp::require_device();
@@ -146,7 +146,6 @@ PP_API int pp_dev_gemm_bench(int dtype, int kind, int M_or_rows, int W, int K, i
             pp::plan_conv(plan, e, A.ptr, M_or_rows, W, K, kind, B.ptr, n_pad, ep, sc,
                           pp::device_sm_count(), force_splits, force_block_n);
         plan.a.debug = debug;
-        if (cgroup) plan.a.commit_group = std::min(cgroup, plan.a.stages / 2);
         cudaStream_t s;
         CUDA_CHECK(cudaStreamCreate(&s));
         for (int i = 0; i < 3; ++i) pp::launch_gemm(plan, s);

@@ -12,9 +12,9 @@
 // double-buffered TMEM accumulator, and drained by four epilogue warps that
 // add bias / residual, store NHWC rows and (optionally) fold the stored values
 // into GroupNorm statistics of the next layer (group_stats, tensor.cpp:203-235).
-// Split-K is reduced inside the kernel: every split writes an fp32 partial tile,
-// the last split to arrive (per-tile ticket) sums all partials in split order --
-// deterministic, no second launch.
+// Split-K (2-way) is reduced inside the kernel: the split that finishes first
+// publishes its fp32 partial tile, the second adds it to its own TMEM accumulator
+// (fp32 addition is commutative -> deterministic), no second launch.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -50,8 +50,8 @@ struct GemmArgs {
     long long res_ld;
     float scale;              // multiplier applied to the accumulator before bias (1 = none)
     // split-K workspace
-    float* partial;           // [splits][m_pix][n_pad] fp32
-    unsigned int* tile_ticket;// [m_tiles * n_tiles], zero, reset by the last split
+    float* partial;           // [m_pix][n_pad] fp32: the first split's partial tiles
+    unsigned int* tile_ticket;// [m_tiles * n_tiles][2] (ticket, ready), zero, reset by the second split
     int m_pix, n_pad;
     // fused GroupNorm statistics of the stored output (gn_groups == 0: off)
     int gn_groups, gn_cpg;
@@ -60,7 +60,6 @@ struct GemmArgs {
     unsigned int* gn_ticket;  // zero, reset by the last tile
     double* gn_out;           // [groups][2] = (mean, mean_sq)
     int debug;                // micro-benchmarks only: bit0 = no MMA, bit1 = no TMA loads
-    int commit_group;         // K blocks per smem-release commit (<= stages / 2)
 };
 
 struct GemmPlan {

@@ -62,12 +62,14 @@ struct SmemTail {
     uint64_t* tempty_bar;
     uint32_t* tmem_slot;
     int* flags;        // [4]
-    float* bias;       // [2][256]
-    float* gn;         // [4 warps][256 cols][2]
+    float* bias;       // [2][block_n]
+    float* gn;         // [4 warps][block_n cols][2]  (also the GN fold scratch)
 };
 
-__host__ __device__ inline size_t tail_bytes(int stages, bool gn) {
-    return size_t(2 * stages + 4) * 8 + 16 + 16 + 2 * 256 * 4 + (gn ? 4 * 256 * 2 * 4 : 0);
+// Sized by block_n so that the fused-GN variant keeps the same pipeline depth.
+__host__ __device__ inline size_t tail_bytes(int stages, bool gn, int block_n) {
+    return size_t(2 * stages + 4) * 8 + 16 + 16 + size_t(2) * block_n * 4 +
+           (gn ? size_t(4) * block_n * 2 * 4 : 0);
 }
 
 // Final values of one 16-column chunk of one row: bias, residual, store, GN sums.
@@ -209,7 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         st.tmem_slot = reinterpret_cast<uint32_t*>(st.tempty_bar + 2);
         st.flags = reinterpret_cast<int*>(st.tmem_slot + 4);
         st.bias = reinterpret_cast<float*>(st.flags + 4);
-        st.gn = st.bias + 512;
+        st.gn = st.bias + 2 * a.block_n;
     }
 
     const int warp = threadIdx.x / 32;
@@ -341,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int quarter = warp & 3;
         const int r = quarter * 32 + lane;  // tile row owned by this thread
         const int et = threadIdx.x - 64;    // 0..127
-        float* sgn_warp = st.gn + quarter * 512;
+        float* sgn_warp = st.gn + quarter * 2 * a.block_n;
         const int final_tiles = a.tiles_y * a.tiles_x * a.n_tiles;
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -367,7 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 valid = p < a.out_rows;
             }
             const int nbase = tc.nt * a.block_n;
-            float* sbias = st.bias + cur * 256;
+            float* sbias = st.bias + cur * a.block_n;
             for (int c = et; c < a.block_n; c += 128)
                 sbias[c] = (a.bias && nbase + c < a.n_valid) ? a.bias[nbase + c] : 0.0f;
             ptx::mbar_wait(&st.tfull_bar[cur], cur_phase);
@@ -456,8 +458,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     double s = 0.0, q = 0.0;
                     for (int w = 0; w < 4; ++w)
                         for (int c = gl * cpg; c < (gl + 1) * cpg; ++c) {
-                            s += double(st.gn[w * 512 + c * 2]);
-                            q += double(st.gn[w * 512 + c * 2 + 1]);
+                            s += double(st.gn[w * 2 * a.block_n + c * 2]);
+                            q += double(st.gn[w * 2 * a.block_n + c * 2 + 1]);
                         }
                     a.gn_part[((size_t)m_tile * a.gn_groups + g0 + gl) * 2] = s;
                     a.gn_part[((size_t)m_tile * a.gn_groups + g0 + gl) * 2 + 1] = q;
@@ -473,8 +475,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __threadfence();
                     const int m_tiles = a.tiles_y * a.tiles_x;
                     const int G = a.gn_groups;
-                    const int P = G >= 128 ? 1 : 128 / G;
-                    double* sfold = reinterpret_cast<double*>(st.gn);   // [P][G][2] (<= 256 x 2)
+                    // sfold = [P][G][2] doubles in the GN scratch (32 * block_n bytes)
+                    const int cap = 2 * a.block_n;
+                    int P = G >= 128 ? 1 : 128 / G;
+                    while (P > 1 && P * G > cap) P >>= 1;
+                    const bool in_smem = P * G <= cap;
+                    double* sfold = reinterpret_cast<double*>(st.gn);
                     for (int w = et; w < G * P; w += 128) {
                         const int g = w % G, part = w / G;
                         double s = 0.0, q = 0.0;
@@ -492,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 q += lq[u];
                             }
                         }
-                        if (G * P <= 512) {
+                        if (in_smem) {
                             sfold[(part * G + g) * 2] = s;
                             sfold[(part * G + g) * 2 + 1] = q;
                         } else {
@@ -501,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                     epi_bar();
-                    if (G * P <= 512) {
+                    if (in_smem) {
                         for (int g = et; g < G; g += 128) {
                             double s = 0.0, q = 0.0;
                             for (int part = 0; part < P; ++part) {
@@ -568,7 +574,7 @@ uint32_t make_idesc(Elem e, int n) {
 
 size_t smem_for(int block_n, int stages, bool gn) {
     return size_t(stages) * (kTileM * kBlockBytes + block_n * kBlockBytes) + 1024 +
-           tail_bytes(stages, gn);
+           tail_bytes(stages, gn, block_n);
 }
 
 int stages_for(int block_n, bool gn) {
@@ -647,7 +653,6 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
     a.kb_per_split = (k_blocks + splits - 1) / splits;
     a.splits = (k_blocks + a.kb_per_split - 1) / a.kb_per_split;
     a.stages = stages_for(bn, gn);
-    a.commit_group = 1;
     a.idesc = make_idesc(p.elem, bn);
     a.out = ep.out;
     a.out_ld = ep.out_ld;
@@ -772,23 +777,28 @@ void plan_gemm(GemmPlan& p, Elem e, const void* A, int M, int K, long long lda, 
 }
 
 void launch_gemm(const GemmPlan& p, cudaStream_t s) {
-    if (p.elem == Elem::BF16) {
-        static bool attr = false;
-        if (!attr) {
-            CUDA_CHECK(cudaFuncSetAttribute(gemm_kernel<false>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
-            attr = true;
+    // the dynamic-smem attribute is per device: remember which devices have it
+    static std::mutex mu;
+    static unsigned long long done[2] = {0, 0};
+    const int tf32 = p.elem == Elem::F32 ? 1 : 0;
+    int dev = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!(done[tf32] >> dev & 1ull)) {
+            if (tf32)
+                CUDA_CHECK(cudaFuncSetAttribute(gemm_kernel<true>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+            else
+                CUDA_CHECK(cudaFuncSetAttribute(gemm_kernel<false>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+            done[tf32] |= 1ull << dev;
         }
-        gemm_kernel<false><<<p.grid, kThreads, p.smem, s>>>(p.tmA, p.tmB, p.a);
-    } else {
-        static bool attr = false;
-        if (!attr) {
-            CUDA_CHECK(cudaFuncSetAttribute(gemm_kernel<true>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
-            attr = true;
-        }
-        gemm_kernel<true><<<p.grid, kThreads, p.smem, s>>>(p.tmA, p.tmB, p.a);
     }
+    if (tf32)
+        gemm_kernel<true><<<p.grid, kThreads, p.smem, s>>>(p.tmA, p.tmB, p.a);
+    else
+        gemm_kernel<false><<<p.grid, kThreads, p.smem, s>>>(p.tmA, p.tmB, p.a);
     CUDA_CHECK(cudaGetLastError());
 }
 

@@ -616,6 +616,34 @@ __global__ void nhwc_to_nchw_kernel(const T* __restrict__ src, int ld, int C, in
 }
 
 template <class T>
+__global__ void crop_kernel(const float* __restrict__ src, int C, int H, int W, int y0, int x0,
+                            int rows, int cols, T* __restrict__ dst, int ld, int r) {
+    const long long total = (long long)rows * cols * C;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int c = int(i % C);
+        const long long p = i / C;
+        const int xx = int(p % cols), yy = int(p / cols);
+        dst[p * ld + c] = from_float<T>(src[((long long)c * H + y0 + yy) * W + x0 + xx], r != 0);
+    }
+}
+
+__global__ void scatter_patch_kernel(const float* __restrict__ patch, int C, int rows, int cols,
+                                     float* __restrict__ dst, int H, int W, int y0, int x0,
+                                     int* nonfinite) {
+    const long long total = (long long)rows * cols * C;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int c = int(i % C);
+        const long long p = i / C;
+        const int xx = int(p % cols), yy = int(p / cols);
+        const float v = patch[i];
+        dst[((long long)c * H + y0 + yy) * W + x0 + xx] = v;
+        if (nonfinite && !isfinite(v)) atomicExch(nonfinite, 1);
+    }
+}
+
+template <class T>
 __global__ void f32_to_elem_kernel(const float* __restrict__ s, T* __restrict__ d, long long n, int r) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
@@ -779,6 +807,20 @@ void nhwc_f32_to_nchw(const float* src, int C, int rows, int W, float* dst, int*
                       cudaStream_t s) {
     nhwc_to_nchw_kernel<float><<<grid_for((long long)rows * W * C, 256), 256, 0, s>>>(
         src, C, C, rows, W, dst, nonfinite);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void crop_nchw_to_nhwc(const float* src, int C, int H, int W, int y0, int x0, int rows, int cols,
+                       Elem e, void* dst, int ld, bool r, cudaStream_t s) {
+    DISPATCH(e, crop_kernel<T><<<grid_for((long long)rows * cols * C, 256), 256, 0, s>>>(
+                    src, C, H, W, y0, x0, rows, cols, static_cast<T*>(dst), ld, r ? 1 : 0));
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void scatter_nhwc_to_nchw(const float* patch, int C, int rows, int cols, float* dst, int H, int W,
+                          int y0, int x0, int* nonfinite, cudaStream_t s) {
+    scatter_patch_kernel<<<grid_for((long long)rows * cols * C, 256), 256, 0, s>>>(
+        patch, C, rows, cols, dst, H, W, y0, x0, nonfinite);
     CUDA_CHECK(cudaGetLastError());
 }
 

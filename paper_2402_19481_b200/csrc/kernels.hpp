@@ -100,6 +100,13 @@ void nhwc_f32_to_nchw(const float* src, int C, int rows, int W, float* dst, int*
                       cudaStream_t s);
 void f32_to_elem(const float* src, Elem e, void* dst, long long n, bool round_tf32,
                  cudaStream_t s);
+// Naive-patch helpers (step_naive, proj/src/runtime.cpp:398-452): crop rows [y0, y0+rows) x
+// cols [x0, x0+cols) of an NCHW fp32 image into an NHWC patch (T, ld), and scatter an NHWC
+// fp32 patch (C channels) back into an NCHW fp32 image at (y0, x0).
+void crop_nchw_to_nhwc(const float* src, int C, int H, int W, int y0, int x0, int rows, int cols,
+                       Elem e, void* dst, int ld, bool round_tf32, cudaStream_t s);
+void scatter_nhwc_to_nchw(const float* patch, int C, int rows, int cols, float* dst, int H, int W,
+                          int y0, int x0, int* nonfinite, cudaStream_t s);
 void elem_to_f32(Elem e, const void* src, float* dst, long long n, cudaStream_t s);
 
 }  // namespace pp

@@ -77,6 +77,9 @@ DeviceWeights::DeviceWeights(const Model& m, const std::vector<float>& cond, int
     const size_t eb = elem_bytes(e);
     L.resize(m.layers.size());
     float* d_cond = nullptr;
+    for (const WeightTensor& t : m.weights)
+        if (t.data.size() != size_t(t.n) * t.c * t.h * t.w)
+            throw std::runtime_error("device weights: host weight data already released");
     for (const Layer& d : m.layers) {
         LayerWeights& w = L[d.id];
         auto up_f32 = [&](int handle, int len) {
@@ -644,12 +647,10 @@ Runner::Runner(const Model& m, const std::vector<float>& cond, int h, int w, con
     CUDA_CHECK(cudaMallocHost(reinterpret_cast<void**>(&h_eps_), size_t(m_.cfg.in_channels) * h * w * 4));
     CUDA_CHECK(cudaMallocHost(reinterpret_cast<void**>(&h_flags_), 64 * 4 * 16));
 
-    auto weights_for = [&](int dev) -> const DeviceWeights* {
-        for (auto& wp : weights_)
-            if (wp->dev == dev) return wp.get();
-        weights_.push_back(std::make_unique<DeviceWeights>(m_, cond_, dev, o_.elem));
-        return weights_.back().get();
-    };
+    if (o_.mode == MODE_NAIVE && o_.world > 1)
+        throw std::invalid_argument("PatchRunner: naive mode runs all patches in one process (world 1)");
+    // every device's weights are packed here: the C ABI releases the host copy afterwards
+    if (o_.mode == MODE_NAIVE) weights_for(o_.device);
     if (o_.mode != MODE_NAIVE) {
         if (o_.world > 1) {
             const int dev = o_.device;
@@ -671,12 +672,26 @@ Runner::Runner(const Model& m, const std::vector<float>& cond, int h, int w, con
     }
 }
 
+const DeviceWeights* Runner::weights_for(int dev) {
+    for (auto& wp : weights_)
+        if (wp->dev == dev) return wp.get();
+    weights_.push_back(std::make_unique<DeviceWeights>(m_, cond_, dev, o_.elem));
+    return weights_.back().get();
+}
+
 Runner::~Runner() {
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     for (auto ev : graph_events_) cudaEventDestroy(ev);
     bands_.clear();
     naive_rows_.clear();
     naive_cols_.clear();
+    if (nx_) {
+        DeviceGuard g(o_.device);
+        cudaDeviceSynchronize();
+        cudaFree(nx_);
+        cudaFree(neps_);
+        cudaEventDestroy(nev_);
+    }
     transport_.reset();
     weights_.clear();
     if (h_x_) cudaFreeHost(h_x_);
@@ -733,23 +748,24 @@ void Runner::count_macs(int s, bool naive) {
     }
 }
 
-void Runner::run_bands(int t, int s, bool displaced) {
+void Runner::run_bands(std::vector<std::unique_ptr<Program>>& progs, int t, int s, bool displaced) {
+    const bool exchanging = &progs == &bands_;   // naive patch programs never exchange or post
     if (displaced) check_displaced_ready(s);
     const int pcur = s & 1, pprev = (s + 1) & 1;
     const int pu = displaced ? pprev : pcur;
-    const int nb_pu = n_dev_ > 1 ? pu : pcur;
-    const bool multi = n_dev_ > 1;
-    for (auto& b : bands_) {
+    const bool multi = exchanging && n_dev_ > 1;
+    const int nb_pu = multi ? pu : pcur;
+    for (auto& b : progs) {
         DeviceGuard g(b->dev);
         b->time_projection(t);
     }
-    const std::vector<Group>& groups = bands_[0]->groups;
+    const std::vector<Group>& groups = progs[0]->groups;
     for (size_t gi = 0; gi < groups.size(); ++gi) {
         const Group& g0 = groups[gi];
         const int l = g0.first;
         const Layer& d = m_.layers[l];
         auto each = [&](auto&& fn) {
-            for (auto& b : bands_) {
+            for (auto& b : progs) {
                 DeviceGuard g(b->dev);
                 fn(*b, b->groups[gi]);
             }
@@ -771,7 +787,7 @@ void Runner::run_bands(int t, int s, bool displaced) {
                 volumes_.halo_sent += per_band;
             }
             each([&](Program& b, const Group& g) { b.conv(g, pcur); });
-            posted_[l] = s;
+            if (exchanging) posted_[l] = s;
         } else if (d.kind == Kind::SelfAttn) {
             if (multi) {
                 each([&](Program& b, const Group& g) {
@@ -788,7 +804,7 @@ void Runner::run_bands(int t, int s, bool displaced) {
                 volumes_.allgather_sent += v;
             }
             each([&](Program& b, const Group& g) { b.attention(g, nb_pu, pcur); });
-            posted_[l] = s;
+            if (exchanging) posted_[l] = s;
         } else if (d.kind == Kind::GroupNorm) {
             each([&](Program& b, const Group& g) {
                 if (!b.fused_stats[l]) b.gn_stats(g, pcur);
@@ -810,7 +826,7 @@ void Runner::run_bands(int t, int s, bool displaced) {
                 volumes_.statreduce_sent += v;
             }
             each([&](Program& b, const Group& g) { b.gn_apply(g, mode, pcur, pprev); });
-            gn_posted_[l] = s;
+            if (exchanging) gn_posted_[l] = s;
         } else {
             each([&](Program& b, const Group& g) { b.simple(g, pcur); });
         }
@@ -868,14 +884,15 @@ void Runner::store_eps(float* out) {
 
 void Runner::check_flags(const char* who) {
     bool neg = false, nonfinite = false;
-    for (auto& b : bands_) {
-        DeviceGuard g(b->dev);
-        CUDA_CHECK(cudaMemcpyAsync(h_flags_, b->flags, 8, cudaMemcpyDeviceToHost, b->cs));
-        CUDA_CHECK(cudaStreamSynchronize(b->cs));
-        neg |= h_flags_[1] != 0;
-        nonfinite |= h_flags_[0] != 0;
-        CUDA_CHECK(cudaMemsetAsync(b->flags, 0, 8, b->cs));
-    }
+    for (auto* progs : {&bands_, &naive_rows_, &naive_cols_})
+        for (auto& b : *progs) {
+            DeviceGuard g(b->dev);
+            CUDA_CHECK(cudaMemcpyAsync(h_flags_, b->flags, 8, cudaMemcpyDeviceToHost, b->cs));
+            CUDA_CHECK(cudaStreamSynchronize(b->cs));
+            neg |= h_flags_[1] != 0;
+            nonfinite |= h_flags_[0] != 0;
+            CUDA_CHECK(cudaMemsetAsync(b->flags, 0, 8, b->cs));
+        }
     if (neg)
         throw std::runtime_error(
             "group_norm_apply: negative variance (caller must substitute fallback stats)");
@@ -925,8 +942,97 @@ void Runner::end_profile() {
     }
 }
 
-void Runner::run_naive_patches(int, int) {
-    throw std::invalid_argument("naive mode is not available on the B200 runner yet");
+// Naive patch parallelism (step_naive, proj/src/runtime.cpp:398-452): even steps split the
+// image into row patches, odd steps into column patches; every patch is denoised as an
+// independent image (zero padding at the patch border, patch-local attention and GroupNorm),
+// with no communication.  One program per patch shape runs the patches back to back on
+// o_.device; x_t and eps live as full NCHW fp32 images in nx_ / neps_.
+std::vector<std::unique_ptr<Program>>& Runner::naive_begin(int s) {
+    const bool by_rows = s % 2 == 0;
+    const int extent = by_rows ? h_ : w_;
+    if (extent % n_dev_ != 0)
+        throw std::invalid_argument("naive: extent " + std::to_string(extent) + " not divisible by " +
+                                    std::to_string(n_dev_) + " devices");
+    const int band = extent / n_dev_;
+    const int div = m_.cfg.depth_divisor();
+    if (band % div != 0)
+        throw std::invalid_argument("naive: patch extent " + std::to_string(band) +
+                                    " violates model divisibility (" + std::to_string(div) + ")");
+    DeviceGuard g(o_.device);
+    if (!nx_) {
+        const size_t bytes = size_t(m_.cfg.in_channels) * h_ * w_ * 4;
+        CUDA_CHECK(cudaMalloc(&nx_, bytes));
+        CUDA_CHECK(cudaMalloc(&neps_, bytes));
+        CUDA_CHECK(cudaEventCreateWithFlags(&nev_, cudaEventDisableTiming));
+        CUDA_CHECK(cudaEventRecord(nev_, 0));
+    }
+    auto& v = by_rows ? naive_rows_ : naive_cols_;
+    if (v.empty()) {
+        const int ph = by_rows ? band : h_, pw = by_rows ? w_ : band;
+        const PatchSpec sp = derive_patch_spec(m_, partition_rows(ph, 1, pw)[0]);
+        v.push_back(std::make_unique<Program>(this, m_, weights_for(o_.device), o_.device, 0, 1, ph,
+                                              pw, sp, o_.elem, o_.profile));
+    }
+    CUDA_CHECK(cudaStreamWaitEvent(v[0]->cs, nev_, 0));
+    return v;
+}
+
+void Runner::run_naive_patches(std::vector<std::unique_ptr<Program>>& progs, int t, int s) {
+    Program& p = *progs[0];
+    DeviceGuard g(p.dev);
+    const bool by_rows = s % 2 == 0;
+    const int C = m_.cfg.in_channels;
+    const int ph = p.stem.rows, pw = p.stem.w;
+    for (int d = 0; d < n_dev_; ++d) {
+        const int y0 = by_rows ? d * ph : 0, x0 = by_rows ? 0 : d * pw;
+        crop_nchw_to_nhwc(nx_, C, h_, w_, y0, x0, ph, pw, p.e, p.stem.interior(p.eb), p.stem.ld,
+                          p.rnd, p.cs);
+        run_bands(progs, t, s, false);
+        scatter_nhwc_to_nchw(p.eps, C, ph, pw, neps_, h_, w_, y0, x0, p.flags, p.cs);
+        launches_ += 2;
+    }
+    CUDA_CHECK(cudaEventRecord(nev_, p.cs));
+}
+
+void Runner::sample_naive(const float* x_T, const int* ts, int n, const std::vector<double>& abar_of,
+                          float* x0, float* traj) {
+    const int C = m_.cfg.in_channels;
+    const size_t img = size_t(C) * h_ * w_;
+    std::vector<std::unique_ptr<Program>>* progs = &naive_begin(0);
+    Program* p = (*progs)[0].get();
+    DeviceGuard g(p->dev);
+    std::memcpy(h_x_, x_T, img * 4);
+    CUDA_CHECK(cudaMemcpyAsync(nx_, h_x_, img * 4, cudaMemcpyHostToDevice, p->cs));
+    cudaEvent_t a, z;
+    CUDA_CHECK(cudaEventCreate(&a));
+    CUDA_CHECK(cudaEventCreate(&z));
+    CUDA_CHECK(cudaEventRecord(a, p->cs));
+    for (int i = 0; i < n; ++i) {
+        if (i > 0) {
+            progs = &naive_begin(i);
+            p = (*progs)[0].get();
+        }
+        if (traj) {
+            // trajectory records the model input x_t (sampler.cpp:84)
+            CUDA_CHECK(cudaMemcpyAsync(traj + size_t(i) * img, nx_, img * 4, cudaMemcpyDeviceToHost, p->cs));
+            CUDA_CHECK(cudaStreamSynchronize(p->cs));
+        }
+        run_naive_patches(*progs, ts[i], i);
+        count_macs(i, true);
+        ddim_update(nx_, neps_, nx_, (long long)img, C, abar_of[i], abar_of[i + 1], Elem::F32,
+                    nullptr, 0, p->cs);
+        launches_ += 1;
+        CUDA_CHECK(cudaEventRecord(nev_, p->cs));
+    }
+    CUDA_CHECK(cudaEventRecord(z, p->cs));
+    CUDA_CHECK(cudaMemcpyAsync(h_eps_, nx_, img * 4, cudaMemcpyDeviceToHost, p->cs));
+    CUDA_CHECK(cudaStreamSynchronize(p->cs));
+    std::memcpy(x0, h_eps_, img * 4);
+    float ms = 0;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, a, z));
+    last_device_ms_ = ms;
+    cudaEventDestroy(a);
+    cudaEventDestroy(z);
 }
 
 void Runner::step(int entry, const float* x, int t, int s, float* eps) {
@@ -940,7 +1046,21 @@ void Runner::step(int entry, const float* x, int t, int s, float* eps) {
         }
     }
     if (e == STEP_NAIVE) {
-        run_naive_patches(t, s);
+        if (o_.world > 1)
+            throw std::invalid_argument("step_naive: naive mode runs all patches in one process (world 1)");
+        launches_ = 0;
+        const size_t img = size_t(m_.cfg.in_channels) * h_ * w_;
+        auto& progs = naive_begin(s);
+        Program& p = *progs[0];
+        DeviceGuard g(p.dev);
+        std::memcpy(h_x_, x, img * 4);
+        CUDA_CHECK(cudaMemcpyAsync(nx_, h_x_, img * 4, cudaMemcpyHostToDevice, p.cs));
+        run_naive_patches(progs, t, s);
+        CUDA_CHECK(cudaMemcpyAsync(h_eps_, neps_, img * 4, cudaMemcpyDeviceToHost, p.cs));
+        CUDA_CHECK(cudaStreamSynchronize(p.cs));
+        count_macs(s, true);
+        check_flags("step_naive");
+        std::memcpy(eps, h_eps_, img * 4);
         return;
     }
     if (e == STEP_REFERENCE && n_dev_ != 1)
@@ -961,7 +1081,6 @@ void Runner::step(int entry, const float* x, int t, int s, float* eps) {
 void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, int total, float* x0,
                     float* traj) {
     if (n < 1) throw std::invalid_argument("sample: empty plan");
-    if (bands_.empty()) throw std::invalid_argument("sample: naive mode is not available on the B200 runner yet");
     const int C = m_.cfg.in_channels;
     auto abar_at = [&](int t) {
         if (t == -1) return 1.0;
@@ -973,6 +1092,15 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
         if (ts[i + 1] >= ts[i])
             throw std::invalid_argument("ddim_step: timestep must decrease (" + std::to_string(ts[i]) +
                                         " -> " + std::to_string(ts[i + 1]) + ")");
+    if (o_.mode == MODE_NAIVE) {
+        std::vector<double> abar_of(n + 1);
+        for (int i = 0; i < n; ++i) abar_of[i] = abar_at(ts[i]);
+        abar_of[n] = 1.0;
+        launches_ = 0;
+        sample_naive(x_T, ts, n, abar_of, x0, traj);
+        check_flags("sample");
+        return;
+    }
     launches_ = 0;
     if (o_.profile) begin_profile();
     load_x(x_T);

@@ -88,8 +88,18 @@ private:
     friend struct Program;
     friend class Transport;
     void check_displaced_ready(int step_index) const;
-    void run_bands(int t, int step_index, bool displaced);   // eps left on the devices
-    void run_naive_patches(int t, int step_index);           // naive: eps_full_ on device 0
+    // eps left on the devices; `progs` is bands_ (exchanging bands) or a naive patch program
+    void run_bands(std::vector<std::unique_ptr<Program>>& progs, int t, int step_index,
+                   bool displaced);
+    void run_bands(int t, int step_index, bool displaced) { run_bands(bands_, t, step_index, displaced); }
+    // naive patch parallelism (step_naive, runtime.cpp:398-452): validates the step's patch
+    // geometry, returns the patch program (stream ordered after the previous naive step)
+    std::vector<std::unique_ptr<Program>>& naive_begin(int step_index);
+    // every patch: crop nx_ -> forward -> scatter into neps_ (full NCHW, fp32) on progs[0]
+    void run_naive_patches(std::vector<std::unique_ptr<Program>>& progs, int t, int step_index);
+    void sample_naive(const float* x_T, const int* ts, int n, const std::vector<double>& abar_of,
+                      float* x0, float* traj);
+    const DeviceWeights* weights_for(int dev);
     void load_x(const float* x_host_nchw);                    // x -> every band's stem input
     void store_eps(float* eps_host_nchw);                     // band eps -> host NCHW
     void check_flags(const char* who);
@@ -104,7 +114,10 @@ private:
     std::vector<PatchSpec> specs_;
     std::vector<std::unique_ptr<DeviceWeights>> weights_;   // one per CUDA device used
     std::vector<std::unique_ptr<Program>> bands_;            // local bands
-    std::vector<std::unique_ptr<Program>> naive_rows_, naive_cols_;
+    std::vector<std::unique_ptr<Program>> naive_rows_, naive_cols_;   // one patch program each
+    float* nx_ = nullptr;       // naive: full NCHW x_t (fp32, device o_.device)
+    float* neps_ = nullptr;     // naive: full NCHW eps
+    cudaEvent_t nev_ = nullptr; // naive: end of the previous naive step's work
     std::unique_ptr<Transport> transport_;
     std::vector<int> posted_;      // per layer: last step whose gather exchange was posted
     std::vector<int> gn_posted_;   // per layer: last step whose GN stats were posted

@@ -27,7 +27,7 @@ SHAPES = [
     ("GEMM 16384x320x2880", 0, 16384, 1, 2880, 320),
     ("GEMM 8192x8192x8192", 0, 8192, 1, 8192, 8192),
 ]
-GN, FLUSH = 1 << 20, 1 << 21
+GN, FLUSH, NOCLUSTER = 1 << 20, 1 << 21, 1 << 30
 
 
 def flops(kind, m, w, k, n):
@@ -52,6 +52,12 @@ def main():
         tf = flops(kind, m, w, k, n) / (o[0] * 1e-3) / 1e12
         line = (f"{name:30s} {o[0] * 1e3:8.1f} us {tf:7.1f} TF/s  bn={int(o[1])} "
                 f"splits={int(o[2])} stages={int(o[3])} grid={int(o[4])}")
+        if "--cluster" in sys.argv:
+            g = run(kind, m, w, k, n, reps=20 | GN) if kind else o
+            c1 = run(kind, m, w, k, n, reps=20 | NOCLUSTER)
+            g1 = run(kind, m, w, k, n, reps=20 | GN | NOCLUSTER) if kind else c1
+            line += (f" | +gn {g[0] * 1e3:7.1f} us | cluster1 {c1[0] * 1e3:7.1f} us "
+                     f"(grid {int(c1[4])}) +gn {g1[0] * 1e3:7.1f} us")
         if variants and kind != 0:
             g = run(kind, m, w, k, n, reps=20 | GN)
             c = run(kind, m, w, k, n, reps=10 | GN | FLUSH)
@@ -59,9 +65,12 @@ def main():
             nt = run(kind, m, w, k, n, reps=20 | (2 << 22))
             ne = run(kind, m, w, k, n, reps=20 | (4 << 22))
             nb = run(kind, m, w, k, n, reps=20 | (6 << 22))
+            bo = run(kind, m, w, k, n, reps=20 | ((4 | 64) << 22))
+            ao = run(kind, m, w, k, n, reps=20 | ((4 | 128) << 22))
             line += (f" | +gn {g[0] * 1e3:7.1f} us | +gn+coldL2 {c[0] * 1e3:7.1f} us"
                      f" | noMMA {nm[0] * 1e3:7.1f} us | noTMA {nt[0] * 1e3:7.1f} us"
-                     f" | noEpi {ne[0] * 1e3:7.1f} us | mmaOnly {nb[0] * 1e3:7.1f} us")
+                     f" | noEpi {ne[0] * 1e3:7.1f} us | mmaOnly {nb[0] * 1e3:7.1f} us"
+                     f" | noEpi+Bonly {bo[0] * 1e3:7.1f} us | noEpi+Aonly {ao[0] * 1e3:7.1f} us")
         print(line, flush=True)
         if sweep and kind != 0:
             for bn in (64, 128, 160, 256):

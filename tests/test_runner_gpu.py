@@ -131,3 +131,61 @@ def test_graph_replay_is_bit_identical(mode, n):
     assert np.array_equal(g2, g1)
     ref = O.run_sampling(ocfg(cfg), mode, n, 32, 32, 6, 1)["x0"]
     assert rel(g2, ref) <= TOL["bf16"]
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("n", [2, 4])
+def test_run_sampling_naive(dtype, n):
+    # ablation config 5 (naive patches): rows on even steps, columns on odd steps,
+    # every patch an independent image (runtime.cpp:398-452)
+    cfg = TOY
+    ref = O.run_sampling(ocfg(cfg), "naive", n, 32, 32, 4, 4)
+    got = P.run_sampling(P.RunConfig(mode="naive", n_devices=n, h=32, w=32, num_steps=4,
+                                     warmup=4, dtype=dtype, model=cfg), trajectory=True)
+    for i, xt in enumerate(ref["trajectory"]):
+        assert rel(got["trajectory"][i], xt) <= TOL[dtype], (i, rel(got["trajectory"][i], xt))
+    assert rel(got["x0"], ref["x0"]) <= TOL[dtype], rel(got["x0"], ref["x0"])
+    assert got["total_macs"] == ref["total_macs"]
+
+
+@pytest.mark.parametrize("step", [0, 1])
+def test_naive_step_rows_and_columns(step):
+    cfg, hw, n = TOY, 32, 2
+    om = O.build_model(ocfg(cfg), 5)
+    cond = O.random_condition(cfg.cond_dim, 6)
+    x = O.random_normal(1, cfg.in_channels, hw, hw, 7)
+    orr = O.PatchRunner(om, cond, hw, hw, mode="naive", n_devices=n)
+    ref = orr.step_naive(x, 600, step)
+    r = P.PatchRunner(P.build_model(cfg, 5), cond, hw, hw, mode="naive", n_devices=n, dtype="fp32")
+    eps = r.step_naive(x, 600, step)
+    assert rel(eps, ref) <= EPS_TOL["fp32"], rel(eps, ref)
+    assert r.total_macs() == orr.total_macs
+    assert r.step_device_macs(step) == orr.step_device_macs[step]
+
+
+def test_naive_geometry_errors():
+    m = P.build_model(TOY, 1)
+    cond = O.random_condition(TOY.cond_dim, 2)
+    x = O.random_normal(1, TOY.in_channels, 32, 32, 3)
+    r = P.PatchRunner(m, cond, 32, 32, mode="naive", n_devices=3, dtype="bf16")
+    with pytest.raises(P.InvalidArgument, match="naive: extent 32 not divisible by 3 devices"):
+        r.step_naive(x, 500, 0)
+    r = P.PatchRunner(m, cond, 32, 32, mode="naive", n_devices=16, dtype="bf16")
+    with pytest.raises(P.InvalidArgument,
+                       match=r"naive: patch extent 2 violates model divisibility \(4\)"):
+        r.step_naive(x, 500, 0)
+
+
+def test_naive_sample_is_deterministic():
+    cfg = TOY
+    m = P.build_model(cfg, 42)
+    cond = O.random_condition(cfg.cond_dim, 7)
+    x = O.random_normal(1, cfg.in_channels, 32, 32, 1234)
+    abar = O.make_schedule()
+    plan = O.make_plan(1000, 5)
+    r = P.PatchRunner(m, cond, 32, 32, mode="naive", n_devices=2, dtype="bf16")
+    a, _ = r.sample(x, plan, abar)
+    b, _ = r.sample(x, plan, abar)
+    assert np.array_equal(a, b)
+    ref = O.run_sampling(ocfg(cfg), "naive", 2, 32, 32, 5, 4)["x0"]
+    assert rel(a, ref) <= TOL["bf16"]
