@@ -225,6 +225,11 @@ PP_API int pp_dev_conv(int dtype, const void* in, int rows, int W, int C_in_pad,
 PP_API int pp_dev_gemm_bench(int dtype, int kind, int M_or_rows, int W, int K, int N,
                              int force_splits, int force_block_n, int reps, double* ms_out);
 
+/* micro-benchmark of the fused GroupNorm apply / statistics kernels on a [pix][C] band:
+ * out[2] = {us per gn_apply, us per gn_stats}; flags: 1 SiLU, 2 temb, 4 skip */
+PP_API int pp_dev_gn_bench(int dtype, long long pix, int C, int G, int flags, int reps,
+                           double* out);
+
 #ifdef __cplusplus
 }
 #endif

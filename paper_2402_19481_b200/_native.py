@@ -123,6 +123,7 @@ SIGNATURES = {
     "pp_nccl_unique_id": (_I, [_V]),
     "pp_assemble_bands": (_I, [_V, _I, _I, _I, _I, _V]),
     "pp_dev_gemm_bench": (_I, [_I, _I, _I, _I, _I, _I, _I, _I, _I, _V]),
+    "pp_dev_gn_bench": (_I, [_I, _LL, _I, _I, _I, _I, _V]),
     "pp_run_sampling": (_I, [_V, _V, _V, _V]),
     "pp_conv2d_region": (_I, [_I, _V, _I, _I, _I, _I, _I, _I, _V, _I, _I, _V, _I, _I, _V]),
     "pp_linear": (_I, [_I, _V, _I, _I, _I, _V, _I, _V, _V]),

@@ -183,3 +183,66 @@ PP_API int pp_dev_gemm_bench(int dtype, int kind, int M_or_rows, int W, int K, i
 }
 
 }  // extern "C"
+
+#include "kernels.hpp"
+
+#include <functional>
+
+extern "C" {
+
+// Micro-benchmark of the fused GroupNorm apply (and the standalone statistics kernel) on a
+// [pix][C] bf16/fp32 band: mean us per launch over `reps` back-to-back launches.
+// out[0] = gn_apply, out[1] = gn_stats.  flags: 1 SiLU, 2 temb, 4 skip.
+PP_API int pp_dev_gn_bench(int dtype, long long pix, int C, int G, int flags, int reps,
+                           double* out) {
+    return pp::guard([&] {
+        pp::require_device();
+        const pp::Elem e = pp::elem_of(dtype);
+        const size_t eb = pp::elem_bytes(e);
+        pp::DeviceScratch x(pix * C * eb), y(pix * C * eb), sk(pix * C * eb), st(G * 16),
+            gam(C * 4), bet(C * 4), te(C * 4), part(size_t(4) << 20), tick(64);
+        CUDA_CHECK(cudaMemset(x.ptr, 0x3c, pix * C * eb));
+        CUDA_CHECK(cudaMemset(sk.ptr, 0x3c, pix * C * eb));
+        CUDA_CHECK(cudaMemset(gam.ptr, 0, C * 4));
+        CUDA_CHECK(cudaMemset(bet.ptr, 0, C * 4));
+        CUDA_CHECK(cudaMemset(te.ptr, 0, C * 4));
+        CUDA_CHECK(cudaMemset(st.ptr, 0, G * 16));
+        CUDA_CHECK(cudaMemset(tick.ptr, 0, 64));
+        pp::GnCombine cb{};
+        cb.mode = 0;
+        cb.fresh = static_cast<const double*>(st.ptr);
+        cb.eps = 1e-5f;
+        cudaStream_t s;
+        CUDA_CHECK(cudaStreamCreate(&s));
+        cudaEvent_t a, b;
+        CUDA_CHECK(cudaEventCreate(&a));
+        CUDA_CHECK(cudaEventCreate(&b));
+        auto apply = [&] {
+            pp::gn_apply(e, x.ptr, y.ptr, pix, C, C, G, cb, static_cast<const float*>(gam.ptr),
+                         static_cast<const float*>(bet.ptr), flags & 1,
+                         (flags & 2) ? static_cast<const float*>(te.ptr) : nullptr,
+                         (flags & 4) ? sk.ptr : nullptr, false, s);
+        };
+        auto stats = [&] {
+            pp::gn_stats(e, x.ptr, pix, C, C, G, double(C / G) * double(pix),
+                         static_cast<double*>(part.ptr), static_cast<unsigned int*>(tick.ptr),
+                         static_cast<double*>(st.ptr), s);
+        };
+        for (int k = 0; k < 2; ++k) {
+            auto fn = k == 0 ? std::function<void()>(apply) : std::function<void()>(stats);
+            for (int i = 0; i < 3; ++i) fn();
+            CUDA_CHECK(cudaEventRecord(a, s));
+            for (int i = 0; i < reps; ++i) fn();
+            CUDA_CHECK(cudaEventRecord(b, s));
+            CUDA_CHECK(cudaEventSynchronize(b));
+            float ms = 0;
+            CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
+            out[k] = ms * 1e3 / reps;
+        }
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        cudaStreamDestroy(s);
+    });
+}
+
+}  // extern "C"

@@ -38,6 +38,7 @@ struct GemmArgs {
     int k_blocks;             // total 128-byte K blocks
     int splits, kb_per_split; // split-K
     int stages;               // smem pipeline depth
+    int kps;                  // 128-byte K blocks per pipeline stage (1 or 2)
     uint32_t idesc;           // tcgen05 instruction descriptor
     // epilogue
     void* out;                // output base (already offset to pixel 0 of the band)
@@ -59,6 +60,10 @@ struct GemmArgs {
     double* gn_part;          // [m_tiles][groups][2]
     unsigned int* gn_ticket;  // zero, reset by the last tile
     double* gn_out;           // [groups][2] = (mean, mean_sq)
+    const void* b_base;       // B tensor (weights) and its size: with b_static, every CTA
+    long long b_bytes;        // prefetches its 1/grid slice into L2 at kernel start
+    int b_static;             // 1: B is weights (not written by an earlier kernel on the stream):
+                              //    its first boxes are prefetched before griddepcontrol.wait
     int debug;                // micro-benchmarks only: bit0 = no MMA, bit1 = no TMA loads
 };
 
@@ -69,6 +74,7 @@ struct GemmPlan {
     int grid = 0;
     size_t smem = 0;
     Elem elem = Elem::BF16;
+    int pair = 0;             // 1: CTA-pair (cta_group::2, M = 256) kernel, clusters of 2
     double flops = 0;         // algorithmic 2*M*N*K of the layer (for rooflines)
 };
 
@@ -106,9 +112,10 @@ void plan_conv(GemmPlan& p, Elem e, const void* in, int rows_in, int W, int C_in
                int num_sms, int force_splits = 0, int force_block_n = 0);
 
 // Plain GEMM: D[M][N] = A[M][K] * B[N][K]^T (both K-major, leading dims in elements).
+// b_static: B holds weights that no kernel on the stream writes (prefetched under PDL).
 void plan_gemm(GemmPlan& p, Elem e, const void* A, int M, int K, long long lda, const void* B,
                int N, long long ldb, const EpilogueSpec& ep, const GemmScratch& sc, int num_sms,
-               int force_splits = 0, int force_block_n = 0);
+               int force_splits = 0, int force_block_n = 0, bool b_static = false);
 
 void launch_gemm(const GemmPlan& p, cudaStream_t s);
 

@@ -8,6 +8,7 @@
 // accumulator ring (tmem_full/tmem_empty, MMA <-> epilogue), so the epilogue of
 // tile i overlaps the main loop of tile i+1.
 #include "gemm.hpp"
+#include "pdl.cuh"
 #include "ptx.cuh"
 #include "util.hpp"
 
@@ -16,6 +17,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -25,7 +27,7 @@ namespace pp {
 
 namespace {
 
-constexpr int kThreads = 192;
+constexpr int kThreads = 224;   // warp 0: TMA, 1: MMA, 2-5: epilogue, 6: TMA
 constexpr int kTileM = 128;
 constexpr int kBlockBytes = 128;   // K block = 128 bytes of each operand row
 constexpr int kTmemCols = 512;     // 2 accumulators x 256 columns
@@ -40,17 +42,20 @@ __device__ __forceinline__ float round_tf32(float x) {
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 struct TileCoord {
-    int ty, tx, nt, split;
+    int m, ty, tx, nt, split;
 };
 
-__device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int t) {
+// Work unit t -> (split, N tile, M unit); the CTA's M tile is unit * P + rank (P = CTAs
+// per cluster).  m >= tiles_y * tiles_x only for the peer of an odd last unit.
+template <int P>
+__device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int t, int rank) {
     TileCoord c;
     c.split = t % a.splits;
     int rest = t / a.splits;
     c.nt = rest % a.n_tiles;
-    int m = rest / a.n_tiles;
-    c.tx = m % a.tiles_x;
-    c.ty = m / a.tiles_x;
+    c.m = (rest / a.n_tiles) * P + rank;
+    c.tx = c.m % a.tiles_x;
+    c.ty = c.m / a.tiles_x;
     return c;
 }
 
@@ -190,16 +195,25 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
     }
 }
 
-template <bool kTF32>
+// kPair: CTA-pair (cta_group::2) variant, launched as clusters of 2.  The pair computes a
+// 256 x block_n tile: each CTA stages its own 128 A rows and half of the B rows, the leader
+// (rank 0) issues M=256 MMAs that read both CTAs' smem, and each CTA's TMEM receives its
+// own 128 rows, so the epilogue is unchanged.  Per SM this halves the B bytes staged and
+// read per MMA (the single-CTA kernel is shared-memory-bandwidth bound at block_n <= 256).
+template <bool kTF32, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const GemmArgs a) {
+    constexpr int P = kPair ? 2 : 1;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int stages = a.stages;
-    const uint32_t a_stage_bytes = kTileM * kBlockBytes;
-    const uint32_t b_stage_bytes = uint32_t(a.block_n) * kBlockBytes;
+    const int kps = a.kps;                                      // K blocks per stage (1 or 2)
+    const uint32_t a_slot = kTileM * kBlockBytes;               // one A box slot
+    const uint32_t b_slot = uint32_t(a.block_n / P) * kBlockBytes;
+    const uint32_t a_stage_bytes = kps * a_slot;
+    const uint32_t b_stage_bytes = kps * b_slot;
     const uint32_t stage_bytes = a_stage_bytes + b_stage_bytes;
     SmemTail st;
     {
@@ -216,6 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
+    const int rank = kPair ? int(ptx::cluster_ctarank()) : 0;
 
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmA);
@@ -226,63 +241,162 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int s = 0; s < 2; ++s) {
             ptx::mbar_init(&st.tfull_bar[s], 1);
-            ptx::mbar_init(&st.tempty_bar[s], 4);
+            ptx::mbar_init(&st.tempty_bar[s], 4 * P);
         }
         ptx::fence_barrier_init();
         ptx::fence_proxy_async();
     }
-    if (warp == 1) ptx::tmem_alloc(st.tmem_slot, kTmemCols);
+    if (warp == 1) {
+        if (kPair)
+            ptx::tmem_alloc_pair(st.tmem_slot, kTmemCols);
+        else
+            ptx::tmem_alloc(st.tmem_slot, kTmemCols);
+    }
     ptx::tc_fence_before();
-    __syncthreads();
+    if (kPair)
+        ptx::cluster_sync();   // peer barriers initialised before any multicast commit
+    else
+        __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *st.tmem_slot;
+    pdl_trigger();   // the next kernel on the stream may start its own prologue now
 
-    const int total_tiles = a.tiles_y * a.tiles_x * a.n_tiles * a.splits;
+    const int m_tiles = a.tiles_y * a.tiles_x;
+    const int total_tiles = (m_tiles + P - 1) / P * a.n_tiles * a.splits;
+    const int tile0 = blockIdx.x / P, tile_step = gridDim.x / P;
     const int conv = a.mode != 0;
-    const int a_box_bytes = conv ? a.rows_box * a.w_box * kBlockBytes : a_stage_bytes;
+    const int a_box_bytes = conv ? a.rows_box * a.w_box * kBlockBytes : int(a_slot);
 
-    if (warp == 0) {
-        // ===== TMA producer (warp-uniform loop, one elected lane issues) =====
+    if (warp == 0 || warp == kThreads / 32 - 1) {
+        // ===== TMA producers: two warps, stage-interleaved (warp-uniform loops, one elected
+        // lane issues).  One stage = kps consecutive 128-byte K blocks: kps A boxes and one
+        // 3-D B box, completing on one full barrier.  Both warps walk the same (tile, K)
+        // sequence; warp pw only waits/issues on the stages with iteration index % 2 == pw,
+        // which halves the serial control work (mbarrier wait, expect_tx, TMA issue) each
+        // warp does per stage.
+        const int pw = warp == 0 ? 0 : 1;
         int stage = 0;
         uint32_t phase = 0;
         const int kel = kTF32 ? 32 : 64;  // elements per 128-byte K block
-        for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-            const TileCoord tc = decode_tile(a, t);
+        // pair: every box completes on the leader's full barrier
+        const uint32_t full_leader = kPair ? ptx::mapa(ptx::smem_u32(st.full_bar), 0) : 0u;
+        // PDL: the weights (B) do not depend on the previous kernel, so the first tile's
+        // first `pre` stages get their B boxes (and are armed for A + B) before waiting for
+        // it; only the A boxes (activations) wait.
+        int pre = 0;
+        if (a.b_static && tile0 < total_tiles && !(a.debug & 2)) {
+            const TileCoord tc = decode_tile<P>(a, tile0, rank);
+            const int kb0 = tc.split * a.kb_per_split;
+            const int kb1 = min(kb0 + a.kb_per_split, a.k_blocks);
+            pre = min(stages, (kb1 - kb0 + kps - 1) / kps);
+            const int bcoord = tc.nt * a.block_n + rank * (a.block_n / P);
+            for (int i = pw; i < pre; i += 2) {
+                if (ptx::elect_one()) {
+                    uint8_t* sb = smem + size_t(i) * stage_bytes + a_stage_bytes;
+                    const int nk = min(kps, kb1 - (kb0 + i * kps));
+                    if (rank == 0)
+                        ptx::mbar_arrive_expect_tx(&st.full_bar[i],
+                                                   P * (nk * a_box_bytes + b_stage_bytes));
+                    if (kPair)
+                        ptx::tma_load_3d_pair(sb, &tmB, full_leader + uint32_t(i) * 8u, 0, bcoord,
+                                              kb0 + i * kps);
+                    else
+                        ptx::tma_load_3d(sb, &tmB, &st.full_bar[i], 0, bcoord, kb0 + i * kps);
+                }
+                __syncwarp();
+            }
+        }
+        if (a.b_static && pw == 0 && a.b_bytes > 0 && !(a.debug & 2)) {
+            // The weights are streamed from HBM once per layer (155 MB per UNet step do not
+            // stay in L2): pull this CTA's 1/grid slice of the whole B tensor into L2 now,
+            // so the B boxes of later K blocks hit L2 instead of paying HBM latency in the
+            // K loop.  Issued before pdl_wait: overlaps the previous kernel's tail.
+            const long long per = ((a.b_bytes + gridDim.x - 1) / gridDim.x + 15) / 16 * 16;
+            const long long lo = per * blockIdx.x;
+            const long long hi = min(a.b_bytes, lo + per);
+            if (ptx::elect_one()) {
+                const char* base = static_cast<const char*>(a.b_base);
+                for (long long off = lo; off < hi; off += 32768)
+                    ptx::prefetch_l2_bulk(base + off, uint32_t(min(32768LL, hi - off)));
+            }
+            __syncwarp();
+        }
+        pdl_wait();
+        int it = 0;
+        for (int t = tile0; t < total_tiles; t += tile_step) {
+            const TileCoord tc = decode_tile<P>(a, t, rank);
             const int kb0 = tc.split * a.kb_per_split;
             const int kb1 = min(kb0 + a.kb_per_split, a.k_blocks);
             const int oy0 = tc.ty * a.rows_box, ox0 = tc.tx * a.w_box;
-            const int bcoord = tc.nt * a.block_n;
-            int tap = kb0 / a.cin_chunks;
-            int chunk = kb0 - tap * a.cin_chunks;
-            for (int kb = kb0; kb < kb1; ++kb) {
-                ptx::mbar_wait(&st.empty_bar[stage], phase ^ 1);
-                uint8_t* sa = smem + size_t(stage) * stage_bytes;
-                uint8_t* sb = sa + a_stage_bytes;
-                if (ptx::elect_one()) {
-                    if (a.debug & 2) {   // micro-benchmark: barriers only, no data movement
-                        ptx::mbar_arrive(&st.full_bar[stage]);
-                    } else {
-                        ptx::mbar_arrive_expect_tx(&st.full_bar[stage], a_box_bytes + b_stage_bytes);
-                        if (!conv) {
-                            ptx::tma_load_2d(sa, &tmA, &st.full_bar[stage], kb * kel, tc.ty * kTileM);
+            const int bcoord = tc.nt * a.block_n + rank * (a.block_n / P);
+            const int arow = tc.ty * kTileM;
+            // conv K position of block kb0: tap (ky, kx), channel chunk cj
+            int cj = kb0 % a.cin_chunks;
+            const int tap0 = kb0 / a.cin_chunks;
+            int ky = tap0 / 3, kx = tap0 - 3 * (tap0 / 3);
+            for (int kb = kb0; kb < kb1; kb += kps) {
+                const int nk = min(kps, kb1 - kb);
+                if ((it & 1) == pw) {
+                    ptx::mbar_wait(&st.empty_bar[stage], phase ^ 1);
+                    uint8_t* sa = smem + size_t(stage) * stage_bytes;
+                    uint8_t* sb = sa + a_stage_bytes;
+                    if (ptx::elect_one()) {
+                        if (a.debug & 2) {   // micro-benchmark: barriers only, no data movement
+                            ptx::mbar_arrive(&st.full_bar[stage]);
                         } else {
-                            const int ky = tap / 3, kx = tap - 3 * ky;
-                            if (a.mode == 1) {
-                                ptx::tma_load_5d(sa, &tmA, &st.full_bar[stage], chunk * kel, 0,
-                                                 ox0 + kx - 1, 0, oy0 + ky);
-                            } else {
-                                ptx::tma_load_5d(sa, &tmA, &st.full_bar[stage], chunk * kel,
-                                                 kx == 1 ? 0 : 1, ox0 + (kx == 0 ? -1 : 0),
-                                                 ky == 1 ? 1 : 0, oy0 + (ky == 2 ? 1 : 0));
+                            const bool b_done = it < pre;   // armed + B issued before pdl_wait
+                            if (rank == 0 && !b_done)
+                                ptx::mbar_arrive_expect_tx(&st.full_bar[stage],
+                                                           P * (nk * a_box_bytes + b_stage_bytes));
+                            const uint32_t fb = kPair ? full_leader + uint32_t(stage) * 8u : 0u;
+                            int c_j = cj, c_x = kx, c_y = ky;
+                            for (int j = 0; j < nk; ++j) {
+                                uint8_t* dst = sa + j * a_slot;
+                                if (!conv) {
+                                    if (kPair)
+                                        ptx::tma_load_2d_pair(dst, &tmA, fb, (kb + j) * kel, arow);
+                                    else
+                                        ptx::tma_load_2d(dst, &tmA, &st.full_bar[stage],
+                                                         (kb + j) * kel, arow);
+                                } else {
+                                    int c1 = 0, c2 = ox0 + c_x - 1, c3 = 0, c4 = oy0 + c_y;
+                                    if (a.mode == 2) {
+                                        c1 = c_x == 1 ? 0 : 1; c2 = ox0 + (c_x == 0 ? -1 : 0);
+                                        c3 = c_y == 1 ? 1 : 0; c4 = oy0 + (c_y == 2 ? 1 : 0);
+                                    }
+                                    if (kPair)
+                                        ptx::tma_load_5d_pair(dst, &tmA, fb, c_j * kel, c1, c2, c3, c4);
+                                    else
+                                        ptx::tma_load_5d(dst, &tmA, &st.full_bar[stage], c_j * kel,
+                                                         c1, c2, c3, c4);
+                                    if (++c_j == a.cin_chunks) {
+                                        c_j = 0;
+                                        if (++c_x == 3) {
+                                            c_x = 0;
+                                            ++c_y;
+                                        }
+                                    }
+                                }
+                            }
+                            if (!b_done) {
+                                if (kPair)
+                                    ptx::tma_load_3d_pair(sb, &tmB, fb, 0, bcoord, kb);
+                                else
+                                    ptx::tma_load_3d(sb, &tmB, &st.full_bar[stage], 0, bcoord, kb);
                             }
                         }
-                        ptx::tma_load_2d(sb, &tmB, &st.full_bar[stage], kb * kel, bcoord);
                     }
+                    __syncwarp();
                 }
-                __syncwarp();
-                if (conv && ++chunk == a.cin_chunks) {
-                    chunk = 0;
-                    ++tap;
+                ++it;
+                for (int j = 0; j < nk; ++j) {
+                    if (++cj == a.cin_chunks) {
+                        cj = 0;
+                        if (++kx == 3) {
+                            kx = 0;
+                            ++ky;
+                        }
+                    }
                 }
                 if (++stage == stages) {
                     stage = 0;
@@ -290,40 +404,58 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == 1 && rank == 0) {
         // ===== MMA issuer (warp-uniform loop, one elected lane issues) =====
-        // Descriptors: stage s, K step k = base + s * (stage_bytes >> 4) + 2 * k (the start
-        // address field is addr >> 4; +32 bytes per 16-element bf16 / 8-element tf32 step).
+        // Descriptors: stage s, block j, K step k = base + s * (stage_bytes >> 4) +
+        // j * (slot >> 4) + 2 * k (the start address field is addr >> 4; +32 bytes per
+        // 16-element bf16 / 8-element tf32 step).
         const uint32_t smem0 = ptx::smem_u32(smem);
         const uint64_t desc_a0 = ptx::smem_desc_sw128(smem0);
         const uint64_t desc_b0 = ptx::smem_desc_sw128(smem0 + a_stage_bytes);
         const uint64_t desc_stride = stage_bytes >> 4;
+        const uint64_t a_next = a_slot >> 4, b_next = b_slot >> 4;
         int stage = 0;
         uint32_t phase = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-            const TileCoord tc = decode_tile(a, t);
+        for (int t = tile0; t < total_tiles; t += tile_step) {
+            const TileCoord tc = decode_tile<P>(a, t, 0);
             const int kb0 = tc.split * a.kb_per_split;
             const int kb1 = min(kb0 + a.kb_per_split, a.k_blocks);
             ptx::mbar_wait(&st.tempty_bar[acc], acc_phase ^ 1);
             ptx::tc_fence_after();
             const uint32_t d_tmem = tmem_base + uint32_t(acc * 256);
-            for (int kb = kb0; kb < kb1; ++kb) {
-                if (!(a.debug & 16)) {   // debug bit 16: no wait (micro-benchmark only)
-                    ptx::mbar_wait(&st.full_bar[stage], phase);
-                    ptx::tc_fence_after();
-                }
+            for (int kb = kb0; kb < kb1; kb += kps) {
+                const bool two = kb + 1 < kb1 && kps == 2;
+                ptx::mbar_wait(&st.full_bar[stage], phase);
+                ptx::tc_fence_after();
                 const uint64_t da = desc_a0 + uint64_t(stage) * desc_stride;
                 const uint64_t db = desc_b0 + uint64_t(stage) * desc_stride;
                 if (ptx::elect_one()) {
                     if (!(a.debug & 1)) {
-                        if (kTF32)
-                            ptx::mma4_tf32(d_tmem, da, db, a.idesc, kb > kb0 ? 1u : 0u);
-                        else
-                            ptx::mma4_bf16(d_tmem, da, db, a.idesc, kb > kb0 ? 1u : 0u);
+                        const uint32_t acc0 = kb > kb0 ? 1u : 0u;
+                        if (kPair) {
+                            if (kTF32) {
+                                ptx::mma4_tf32_pair(d_tmem, da, db, a.idesc, acc0);
+                                if (two) ptx::mma4_tf32_pair(d_tmem, da + a_next, db + b_next, a.idesc, 1u);
+                            } else {
+                                ptx::mma4_bf16_pair(d_tmem, da, db, a.idesc, acc0);
+                                if (two) ptx::mma4_bf16_pair(d_tmem, da + a_next, db + b_next, a.idesc, 1u);
+                            }
+                        } else {
+                            if (kTF32) {
+                                ptx::mma4_tf32(d_tmem, da, db, a.idesc, acc0);
+                                if (two) ptx::mma4_tf32(d_tmem, da + a_next, db + b_next, a.idesc, 1u);
+                            } else {
+                                ptx::mma4_bf16(d_tmem, da, db, a.idesc, acc0);
+                                if (two) ptx::mma4_bf16(d_tmem, da + a_next, db + b_next, a.idesc, 1u);
+                            }
+                        }
                     }
-                    ptx::mma_commit(&st.empty_bar[stage]);
+                    if (kPair)
+                        ptx::mma_commit_pair(&st.empty_bar[stage], 3);
+                    else
+                        ptx::mma_commit(&st.empty_bar[stage]);
                 }
                 __syncwarp();
                 if (++stage == stages) {
@@ -331,31 +463,48 @@ __global__ void __launch_bounds__(kThreads, 1)
                     phase ^= 1;
                 }
             }
-            if (ptx::elect_one()) ptx::mma_commit(&st.tfull_bar[acc]);
+            if (ptx::elect_one()) {
+                if (kPair)
+                    ptx::mma_commit_pair(&st.tfull_bar[acc], 3);
+                else
+                    ptx::mma_commit(&st.tfull_bar[acc]);
+            }
             __syncwarp();
             if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
             }
         }
-    } else {
+    } else if (warp >= 2 && warp <= 5) {
         // ===== epilogue (warps 2..5; TMEM lane quarter = warp % 4) =====
         const int quarter = warp & 3;
         const int r = quarter * 32 + lane;  // tile row owned by this thread
         const int et = threadIdx.x - 64;    // 0..127
         float* sgn_warp = st.gn + quarter * 2 * a.block_n;
-        const int final_tiles = a.tiles_y * a.tiles_x * a.n_tiles;
+        const int final_tiles = m_tiles * a.n_tiles;
+        // accumulator release: the MMA issuer (the leader's, for a pair) waits for 4*P warps
+        const uint32_t tempty_leader = kPair ? ptx::mapa(ptx::smem_u32(st.tempty_bar), 0) : 0u;
+        auto release = [&](int which) {
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (kPair)
+                    ptx::mbar_arrive_cluster(tempty_leader + uint32_t(which) * 8u);
+                else
+                    ptx::mbar_arrive(&st.tempty_bar[which]);
+            }
+        };
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        for (int t = tile0; t < total_tiles; t += tile_step) {
             const int cur = acc;
             const uint32_t cur_phase = acc_phase;
             if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
             }
-            const TileCoord tc = decode_tile(a, t);
-            const int m_tile = tc.ty * a.tiles_x + tc.tx;
+            const TileCoord tc = decode_tile<P>(a, t, rank);
+            const int m_tile = tc.m;
             const int tile_id = m_tile * a.n_tiles + tc.nt;
             long long p;
             bool valid;
@@ -374,10 +523,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 sbias[c] = (a.bias && nbase + c < a.n_valid) ? a.bias[nbase + c] : 0.0f;
             ptx::mbar_wait(&st.tfull_bar[cur], cur_phase);
             ptx::tc_fence_after();
-            if (a.debug & 4) {   // micro-benchmark: release the accumulator, no epilogue work
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&st.tempty_bar[cur]);
+            if ((a.debug & 4) || (kPair && m_tile >= m_tiles)) {
+                // micro-benchmark (no epilogue work) / the empty half of an odd last pair unit
+                release(cur);
                 continue;
             }
             epi_bar();
@@ -405,36 +553,49 @@ __global__ void __launch_bounds__(kThreads, 1)
                                        make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
                         }
                     }
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&st.tempty_bar[cur]);
-                    __threadfence();
+                    release(cur);
+                    // publish: CTA barrier, then one gpu-scope fence + flag (the fence is
+                    // cumulative over the other threads' stores ordered before the barrier)
                     epi_bar();
-                    if (et == 0) atomicExch(ready, 1u);
+                    if (et == 0) {
+                        __threadfence();
+                        atomicExch(ready, 1u);
+                    }
                     continue;
                 }
                 if (et == 0) {
                     while (atomicAdd(ready, 0u) == 0u) __nanosleep(64);
+                    __threadfence();
                 }
                 epi_bar();
-                __threadfence();
-                for (int c0 = 0; c0 < a.block_n; c0 += 16) {
-                    float v[16], o[16];
-                    ptx::tmem_ld16(t_row + c0, v);
+                // 64 partial columns (16 loads) in flight per round trip
+                for (int cb = 0; cb < a.block_n; cb += 64) {
+                    const int nc = min(64, a.block_n - cb);
+                    float o[64];
                     if (valid) {
 #pragma unroll
-                        for (int j = 0; j < 16; j += 4) {
-                            const float4 q = __ldcg(reinterpret_cast<const float4*>(part + c0 + j));
-                            o[j] = q.x; o[j + 1] = q.y; o[j + 2] = q.z; o[j + 3] = q.w;
+                        for (int j = 0; j < 64; j += 4) {
+                            if (j < nc) {
+                                const float4 q = __ldcg(reinterpret_cast<const float4*>(part + cb + j));
+                                o[j] = q.x; o[j + 1] = q.y; o[j + 2] = q.z; o[j + 3] = q.w;
+                            }
                         }
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) v[j] = v[j] + o[j];
                     }
-                    finish_chunk<kTF32>(a, v, sbias, c0, nbase + c0, p, valid, sgn_warp, lane);
+#pragma unroll
+                    for (int c1 = 0; c1 < 64; c1 += 16) {
+                        if (c1 < nc) {
+                            float v[16];
+                            ptx::tmem_ld16(t_row + cb + c1, v);
+                            if (valid) {
+#pragma unroll
+                                for (int j = 0; j < 16; ++j) v[j] = v[j] + o[c1 + j];
+                            }
+                            finish_chunk<kTF32>(a, v, sbias, cb + c1, nbase + cb + c1, p, valid,
+                                                sgn_warp, lane);
+                        }
+                    }
                 }
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&st.tempty_bar[cur]);
+                release(cur);
                 if (et == 0) {
                     *ticket = 0u;
                     *ready = 0u;
@@ -445,34 +606,50 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::tmem_ld16(t_row + c0, v);
                     finish_chunk<kTF32>(a, v, sbias, c0, nbase + c0, p, valid, sgn_warp, lane);
                 }
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&st.tempty_bar[cur]);
+                release(cur);
             }
             if (a.gn_groups) {
                 epi_bar();
                 const int cpg = a.gn_cpg;
                 const int g0 = nbase / cpg;
                 const int gn_here = min(a.block_n, a.n_valid - nbase) / cpg;
-                for (int gl = et; gl < gn_here; gl += 128) {
+                // 8 threads per group: lane sub of the 8 sums the (warp, column) entries
+                // e = sub, sub + 8, ... of the group's 4 * cpg column sums, then a fixed
+                // xor-tree over the 8 lanes -> deterministic, short dependency chains.
+                const int sub = et & 7;
+                const unsigned gmask = 0xFFu << (lane & 24);
+                const int n_e = 4 * cpg;
+                for (int gl = et >> 3; gl < gn_here; gl += 16) {
                     double s = 0.0, q = 0.0;
-                    for (int w = 0; w < 4; ++w)
-                        for (int c = gl * cpg; c < (gl + 1) * cpg; ++c) {
-                            s += double(st.gn[w * 2 * a.block_n + c * 2]);
-                            q += double(st.gn[w * 2 * a.block_n + c * 2 + 1]);
-                        }
-                    a.gn_part[((size_t)m_tile * a.gn_groups + g0 + gl) * 2] = s;
-                    a.gn_part[((size_t)m_tile * a.gn_groups + g0 + gl) * 2 + 1] = q;
+                    for (int e = sub; e < n_e; e += 8) {
+                        const int w = e / cpg;
+                        const int c = gl * cpg + (e - w * cpg);
+                        const float2 v = *reinterpret_cast<const float2*>(st.gn + (w * a.block_n + c) * 2);
+                        s += double(v.x);
+                        q += double(v.y);
+                    }
+#pragma unroll
+                    for (int o = 4; o; o >>= 1) {
+                        s += __shfl_xor_sync(gmask, s, o);
+                        q += __shfl_xor_sync(gmask, q, o);
+                    }
+                    if (sub == 0) {
+                        double2* dst = reinterpret_cast<double2*>(a.gn_part) + (size_t)m_tile * a.gn_groups + g0 + gl;
+                        *dst = make_double2(s, q);
+                    }
                 }
-                __threadfence();
                 epi_bar();
-                if (et == 0) st.flags[2] = atomicAdd(a.gn_ticket, 1u) == unsigned(final_tiles - 1);
+                if (et == 0) {
+                    __threadfence();   // cumulative over the partials stored before the barrier
+                    const bool last = atomicAdd(a.gn_ticket, 1u) == unsigned(final_tiles - 1);
+                    if (last) __threadfence();
+                    st.flags[2] = last;
+                }
                 epi_bar();
                 if (st.flags[2]) {
                     // last tile of the GEMM: fold the per-m-tile partials.  P threads per
-                    // group each sum a fixed residue class of m-tiles (8 loads in flight),
+                    // group each sum a fixed residue class of m-tiles (16 loads in flight),
                     // then one thread adds the P partials in order -> deterministic.
-                    __threadfence();
                     const int m_tiles = a.tiles_y * a.tiles_x;
                     const int G = a.gn_groups;
                     // sfold = [P][G][2] doubles in the GN scratch (32 * block_n bytes)
@@ -484,16 +661,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int w = et; w < G * P; w += 128) {
                         const int g = w % G, part = w / G;
                         double s = 0.0, q = 0.0;
-                        for (int m0 = part; m0 < m_tiles; m0 += 8 * P) {
-                            double ls[8], lq[8];
+                        for (int m0 = part; m0 < m_tiles; m0 += 16 * P) {
+                            double ls[16], lq[16];
 #pragma unroll
-                            for (int u = 0; u < 8; ++u) {
+                            for (int u = 0; u < 16; ++u) {
                                 const int m = m0 + u * P;
                                 ls[u] = m < m_tiles ? __ldcg(a.gn_part + ((size_t)m * G + g) * 2) : 0.0;
                                 lq[u] = m < m_tiles ? __ldcg(a.gn_part + ((size_t)m * G + g) * 2 + 1) : 0.0;
                             }
 #pragma unroll
-                            for (int u = 0; u < 8; ++u) {
+                            for (int u = 0; u < 16; ++u) {
                                 s += ls[u];
                                 q += lq[u];
                             }
@@ -526,10 +703,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     ptx::tc_fence_before();
-    __syncthreads();
+    if (kPair)
+        ptx::cluster_sync();   // the leader's last MMAs wrote the peer's TMEM
+    else
+        __syncthreads();
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, kTmemCols);
+        if (kPair)
+            ptx::tmem_dealloc_pair(tmem_base, kTmemCols);
+        else
+            ptx::tmem_dealloc(tmem_base, kTmemCols);
     }
 }
 
@@ -561,65 +744,102 @@ void encode(CUtensorMap* m, Elem e, int rank, const void* base, const uint64_t* 
         throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
 }
 
-uint32_t make_idesc(Elem e, int n) {
+// B operand [rows][K] (K-major, leading dim ld elements) as a 3-D map {kel, rows, K/kel}
+// (dim 2 = 128-byte K block, stride 128 B): a {kel, box_rows, kps} box lands as kps
+// consecutive [box_rows][128 B] swizzled slots.
+void encode_b(CUtensorMap* m, Elem e, const void* base, int rows, int K, long long ld, int box_rows,
+              int kps) {
+    const uint64_t eb = elem_bytes(e);
+    const int kel = int(kBlockBytes / eb);
+    uint64_t d[3] = {uint64_t(kel), uint64_t(rows), uint64_t(K / kel)};
+    uint64_t st[2] = {uint64_t(ld) * eb, uint64_t(kBlockBytes)};
+    uint32_t b[3] = {uint32_t(kel), uint32_t(box_rows), uint32_t(kps)};
+    encode(m, e, 3, base, d, st, b);
+}
+
+uint32_t make_idesc(Elem e, int n, int m) {
     uint32_t d = 0;
     d |= 1u << 4;                                    // D format f32
     const uint32_t fmt = e == Elem::BF16 ? 1u : 2u;  // BF16 / TF32
     d |= fmt << 7;                                   // A format
     d |= fmt << 10;                                  // B format
     d |= uint32_t(n >> 3) << 17;                     // N
-    d |= uint32_t(kTileM >> 4) << 24;                // M = 128
+    d |= uint32_t(m >> 4) << 24;                     // M = 128 (single CTA) / 256 (pair)
     return d;
 }
 
-size_t smem_for(int block_n, int stages, bool gn) {
-    return size_t(stages) * (kTileM * kBlockBytes + block_n * kBlockBytes) + 1024 +
-           tail_bytes(stages, gn, block_n);
+size_t smem_for(int block_n, int stages, bool gn, int pair, int kps) {
+    return size_t(stages) * kps * (kTileM * kBlockBytes + block_n / (pair ? 2 : 1) * kBlockBytes) +
+           1024 + tail_bytes(stages, gn, block_n);
 }
 
-int stages_for(int block_n, bool gn) {
+int stages_for(int block_n, bool gn, int pair, int kps) {
     int s = 8;
-    while (s > 2 && smem_for(block_n, s, gn) > size_t(kSmemMax)) --s;
+    while (s > 2 && smem_for(block_n, s, gn, pair, kps) > size_t(kSmemMax)) --s;
     return s;
 }
 
-// Pick block_n and split-K.  Cost model (cycles per SM): a 128-byte K block costs
-// max(MMA = 2*bn, L2 feed = (16 KB + 128*bn) / 33 B/clk) -- 33 B/clk/SM is the feed
-// rate measured with ncu on B200 (tensor pipe ~40% busy at bn=160); tiles are
-// quantised into waves over the SMs; split-K pays a partial write + read.
+// K blocks per stage: 2 halves the per-block barrier / issue work of the single-thread TMA
+// and MMA loops (measured ~450 cycles per iteration, more than the MMAs of a block_n <= 224
+// block take), as long as at least 3 stages (6 blocks) still fit.  PP_KPS overrides.
+int choose_kps(int block_n, bool gn, int pair) {
+    static const int forced = [] {
+        const char* v = std::getenv("PP_KPS");
+        return v ? std::atoi(v) : 0;
+    }();
+    if (forced == 1 || forced == 2) return forced;
+    return stages_for(block_n, gn, pair, 2) >= 3 ? 2 : 1;
+}
+
+// Per-tile tensor-pipe efficiency by (pair, block_n): measured on B200 with
+// scripts/gemm_micro.py on the SDXL-shape conv layers.  The single-CTA kernel is bound by
+// shared-memory bandwidth (TMA writes + MMA operand reads of a 128 x block_n tile); the
+// CTA pair halves the B bytes per SM.
+double tile_eff(int pair, int bn) {
+    if (pair) return bn >= 256 ? 0.90 : bn >= 160 ? 0.60 : bn >= 128 ? 0.35 : 0.27;
+    return bn >= 256 ? 0.75 : bn >= 160 ? 0.62 : bn >= 128 ? 0.36 : 0.28;
+}
+
+// Pick (pair, block_n, split-K).  Cost model (cycles per SM): a 128-byte K block costs
+// 2 * block_n MMA cycles / tile_eff; tiles are quantised into waves over the SMs (pairs
+// over SM pairs); split-K pays a partial write + read.
+//   force_splits: bits 0-3 = splits (0 auto), bit 4 = force pair, bit 5 = force single CTA
 void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int gn_cpg, int force_splits,
-                   int force_block_n, int& block_n, int& splits) {
-    // Measured on B200 (scripts/gemm_micro.py, round 1): per-tile efficiency is best at
-    // block_n = 160 (~900-1050 TF/s on the SDXL conv shapes, 128 or 64 are 2x slower) and
-    // 256 for very large N; the in-kernel split-K reduction costs more than the wave
-    // quantisation it fixes on every layer shape of the workload, so it is opt-in only.
+                   int force_block_n, int& block_n, int& splits, int& pair) {
     double best = 1e300;
     block_n = 16;
     splits = 1;
-    for (int bn = 256; bn >= 16; bn -= 16) {
-        if (force_block_n && bn != force_block_n) continue;
-        if (n_pad % bn) continue;
-        if (gn_cpg && bn % gn_cpg) continue;
-        const int nt = n_pad / bn;
-        for (int s : {1, 2}) {
-            if (force_splits && s != std::min(force_splits, 2)) continue;
-            if (s > k_blocks) continue;
-            // split only when one wave leaves more than half of the SMs idle
-            if (!force_splits && s == 2 && ((long long)m_tiles * nt * 2 > num_sms || k_blocks < 16))
-                continue;
-            const long long tiles = (long long)m_tiles * nt * s;
-            const double waves = std::ceil(double(tiles) / num_sms);
-            // per 128-byte K block: MMA cycles (2*bn) at the per-tile efficiency measured
-            // for this N (160: ~0.62 of peak, 256: ~0.95 on big GEMMs, <=128: ~0.3-0.45)
-            const double eff = bn >= 256 ? 0.75 : bn >= 160 ? 0.62 : bn >= 128 ? 0.36 : 0.28;
-            const double per_kb = 2.0 * bn / eff;
-            const double kbs = std::ceil(double(k_blocks) / s);
-            double cost = waves * (kbs * per_kb + 2500.0);
-            if (s > 1) cost += 2.0 * 128.0 * bn * 4.0 / 20.0;
-            if (cost < best * 0.98) {
-                best = cost;
-                block_n = bn;
-                splits = s;
+    pair = 0;
+    const int fs = force_splits & 15;
+    const bool force_pair = force_splits & 16, force_single = force_splits & 32;
+    for (int pr = 0; pr <= 1; ++pr) {
+        if ((force_pair && !pr) || (force_single && pr)) continue;
+        if (pr && m_tiles < 2 && !force_pair) continue;
+        const int P = pr ? 2 : 1;
+        const int slots = num_sms / P;
+        const int units = (m_tiles + P - 1) / P;
+        for (int bn = 256; bn >= 16; bn -= 16) {
+            if (force_block_n && bn != force_block_n) continue;
+            if (n_pad % bn) continue;
+            if (gn_cpg && bn % gn_cpg) continue;
+            const int nt = n_pad / bn;
+            for (int s : {1, 2}) {
+                if (fs && s != std::min(fs, 2)) continue;
+                if (s > k_blocks) continue;
+                // split only when one wave leaves more than half of the SMs idle
+                if (!fs && s == 2 && ((long long)units * nt * 2 > slots || k_blocks < 16)) continue;
+                const long long tiles = (long long)units * nt * s;
+                const double waves = std::ceil(double(tiles) / slots);
+                const double per_kb = 2.0 * bn / tile_eff(pr, bn);
+                const double kbs = std::ceil(double(k_blocks) / s);
+                double cost = waves * (kbs * per_kb + 2500.0);
+                if (s > 1) cost += 2.0 * 128.0 * bn * 4.0 / 20.0;
+                if (cost < best * 0.98) {
+                    best = cost;
+                    block_n = bn;
+                    splits = s;
+                    pair = pr;
+                }
             }
         }
     }
@@ -638,9 +858,12 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
         if (n_pad != ep.n_valid)
             throw std::invalid_argument("GroupNorm statistics need unpadded output channels");
     }
-    int bn, splits;
-    choose_tiling(m_tiles, n_pad, k_blocks, num_sms, cpg, force_splits, force_block_n, bn, splits);
+    int bn, splits, pair;
+    choose_tiling(m_tiles, n_pad, k_blocks, num_sms, cpg, force_splits, force_block_n, bn, splits,
+                  pair);
     if (gn && bn % cpg) throw std::invalid_argument("GroupNorm statistics: block_n not group aligned");
+    if (pair && bn % 16) throw std::invalid_argument("CTA-pair GEMM: block_n % 16 != 0");
+    p.pair = pair;
     a.block_n = bn;
     a.n_tiles = n_pad / bn;
     a.k_blocks = k_blocks;
@@ -649,11 +872,13 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
     if (splits > 1 && ((size_t)a.m_pix * n_pad * sizeof(float) > sc.ws_bytes ||
                        2 * size_t(m_tiles) * a.n_tiles > sc.n_tickets))
         splits = 1;
+    a.kps = choose_kps(bn, gn, pair);
     a.splits = splits;
     a.kb_per_split = (k_blocks + splits - 1) / splits;
+    a.kb_per_split = (a.kb_per_split + a.kps - 1) / a.kps * a.kps;   // whole stages per split
     a.splits = (k_blocks + a.kb_per_split - 1) / a.kb_per_split;
-    a.stages = stages_for(bn, gn);
-    a.idesc = make_idesc(p.elem, bn);
+    a.stages = stages_for(bn, gn, pair, a.kps);
+    a.idesc = make_idesc(p.elem, bn, pair ? 2 * kTileM : kTileM);
     a.out = ep.out;
     a.out_ld = ep.out_ld;
     a.n_valid = ep.n_valid;
@@ -675,9 +900,10 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
         a.gn_ticket = sc.gn_ticket;
         a.gn_out = ep.gn_out;
     }
-    const int tiles = m_tiles * a.n_tiles * a.splits;
-    p.grid = std::min(tiles, num_sms);
-    p.smem = smem_for(bn, a.stages, gn);
+    const int P = pair ? 2 : 1;
+    const int units = (m_tiles + P - 1) / P * a.n_tiles * a.splits;
+    p.grid = P * std::min(units, num_sms / P);
+    p.smem = smem_for(bn, a.stages, gn, pair, a.kps);
 }
 
 }  // namespace
@@ -737,17 +963,18 @@ void plan_conv(GemmPlan& p, Elem e, const void* in, int rows_in, int W, int C_in
     encode(&p.tmA, e, 5, in, dims, strides, box);
     finish_plan(p, a.tiles_y * a.tiles_x, n_pad, k_blocks, ep, sc, num_sms, force_splits,
                 force_block_n);
-    // B: weights [n_pad][9*C_in_pad]
-    uint64_t bd[2] = {uint64_t(9) * C_in_pad, uint64_t(n_pad)};
-    uint64_t bs[1] = {uint64_t(9) * C_in_pad * eb};
-    uint32_t bb[2] = {uint32_t(kel), uint32_t(a.block_n)};
-    encode(&p.tmB, e, 2, weights, bd, bs, bb);
+    // B: weights [n_pad][9*C_in_pad] viewed as [K blocks][n_pad][kel]: one box = kps blocks
+    encode_b(&p.tmB, e, weights, n_pad, 9 * C_in_pad, 9LL * C_in_pad, a.block_n / (p.pair ? 2 : 1),
+             a.kps);
     p.flops = 2.0 * a.m_pix * double(ep.n_valid) * 9.0 * C_in_pad;
+    a.b_static = 1;   // conv weights
+    a.b_base = weights;
+    a.b_bytes = (long long)n_pad * 9 * C_in_pad * (long long)eb;
 }
 
 void plan_gemm(GemmPlan& p, Elem e, const void* A, int M, int K, long long lda, const void* B,
                int N, long long ldb, const EpilogueSpec& ep, const GemmScratch& sc, int num_sms,
-               int force_splits, int force_block_n) {
+               int force_splits, int force_block_n, bool b_static) {
     std::memset(&p, 0, sizeof(p));
     p.elem = e;
     const size_t eb = elem_bytes(e);
@@ -769,37 +996,38 @@ void plan_gemm(GemmPlan& p, Elem e, const void* A, int M, int K, long long lda, 
     uint32_t ab[2] = {uint32_t(kel), uint32_t(kTileM)};
     encode(&p.tmA, e, 2, A, ad, as, ab);
     finish_plan(p, a.tiles_y, n_pad, K / kel, ep, sc, num_sms, force_splits, force_block_n);
-    uint64_t bd[2] = {uint64_t(K), uint64_t(N)};
-    uint64_t bs[1] = {uint64_t(ldb) * eb};
-    uint32_t bb[2] = {uint32_t(kel), uint32_t(a.block_n)};
-    encode(&p.tmB, e, 2, B, bd, bs, bb);
+    encode_b(&p.tmB, e, B, N, K, ldb, a.block_n / (p.pair ? 2 : 1), a.kps);
     p.flops = 2.0 * double(M) * N * K;
+    a.b_static = b_static ? 1 : 0;
+    a.b_base = B;
+    a.b_bytes = b_static ? ((long long)(N - 1) * ldb + K) * (long long)eb / 16 * 16 : 0;
 }
 
-void launch_gemm(const GemmPlan& p, cudaStream_t s) {
+template <bool kTF32, bool kPair>
+void launch_variant(const GemmPlan& p, cudaStream_t s) {
     // the dynamic-smem attribute is per device: remember which devices have it
     static std::mutex mu;
-    static unsigned long long done[2] = {0, 0};
-    const int tf32 = p.elem == Elem::F32 ? 1 : 0;
+    static unsigned long long done = 0;
     int dev = 0;
     CUDA_CHECK(cudaGetDevice(&dev));
     {
         std::lock_guard<std::mutex> lk(mu);
-        if (!(done[tf32] >> dev & 1ull)) {
-            if (tf32)
-                CUDA_CHECK(cudaFuncSetAttribute(gemm_kernel<true>,
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
-            else
-                CUDA_CHECK(cudaFuncSetAttribute(gemm_kernel<false>,
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
-            done[tf32] |= 1ull << dev;
+        if (!(done >> dev & 1ull)) {
+            CUDA_CHECK(cudaFuncSetAttribute(gemm_kernel<kTF32, kPair>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+            done |= 1ull << dev;
         }
     }
+    launch_pdl(gemm_kernel<kTF32, kPair>, dim3(p.grid), dim3(kThreads), p.smem, s, kPair ? 2 : 1,
+               p.tmA, p.tmB, p.a);
+}
+
+void launch_gemm(const GemmPlan& p, cudaStream_t s) {
+    const bool tf32 = p.elem == Elem::F32;
     if (tf32)
-        gemm_kernel<true><<<p.grid, kThreads, p.smem, s>>>(p.tmA, p.tmB, p.a);
+        p.pair ? launch_variant<true, true>(p, s) : launch_variant<true, false>(p, s);
     else
-        gemm_kernel<false><<<p.grid, kThreads, p.smem, s>>>(p.tmA, p.tmB, p.a);
-    CUDA_CHECK(cudaGetLastError());
+        p.pair ? launch_variant<false, true>(p, s) : launch_variant<false, false>(p, s);
 }
 
 }  // namespace pp

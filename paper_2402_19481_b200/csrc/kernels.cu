@@ -1,9 +1,11 @@
 // HBM-bound kernels (see kernels.hpp).  128-bit vectorised NHWC access; all
 // reductions are fixed-order (no float atomics) so every run is bit-deterministic.
 #include "kernels.hpp"
+#include "pdl.cuh"
 #include "util.hpp"
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cmath>
@@ -76,105 +78,6 @@ int grid_for(long long n, int threads) {
 }
 
 // ---------------------------------------------------------------- GroupNorm stats
-constexpr int kGnThreads = 256;
-constexpr int kGnPixels = 32;
-
-// One launch: every block reduces kGnPixels pixels to per-group fp64 partials; the last
-// block to finish (ticket) folds all partials in a fixed order into out[G][2] =
-// (mean, mean_sq) -- group_stats (tensor.cpp:203-235) with fp32 per-thread sums over
-// <= 64 values and fp64 everywhere above that.  Deterministic for a given grid.
-template <class T>
-__global__ void gn_stats_kernel(const T* __restrict__ x, long long pix, int C, int ld, int G,
-                                double count, double* __restrict__ partial,
-                                unsigned int* __restrict__ ticket, double* __restrict__ out) {
-    constexpr int VEC = Vec<T>::N;
-    extern __shared__ unsigned char sm_raw[];
-    __shared__ bool is_last;
-    const int nvec = C / VEC;
-    const int L = max(1, kGnThreads / nvec);
-    float* s_sum = reinterpret_cast<float*>(sm_raw);
-    float* s_sq = s_sum + L * C;
-    double* c_sum = reinterpret_cast<double*>(s_sq + L * C);
-    double* c_sq = c_sum + C;
-    const long long p0 = (long long)blockIdx.x * kGnPixels;
-    const long long p1 = min(p0 + kGnPixels, pix);
-    for (int idx = threadIdx.x; idx < L * nvec; idx += blockDim.x) {
-        const int pl = idx / nvec, v = idx - pl * nvec;
-        float a[VEC], b[VEC];
-#pragma unroll
-        for (int i = 0; i < VEC; ++i) a[i] = b[i] = 0.0f;
-        for (long long p = p0 + pl; p < p1; p += 4 * L) {
-            float f[4][VEC];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (p + u * L < p1) {
-                    load_vec<T>(x + (p + u * L) * ld + v * VEC, f[u]);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < VEC; ++i) f[u][i] = 0.0f;
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int i = 0; i < VEC; ++i) {
-                    a[i] += f[u][i];
-                    b[i] = fmaf(f[u][i], f[u][i], b[i]);
-                }
-        }
-#pragma unroll
-        for (int i = 0; i < VEC; ++i) {
-            s_sum[pl * C + v * VEC + i] = a[i];
-            s_sq[pl * C + v * VEC + i] = b[i];
-        }
-    }
-    __syncthreads();
-    for (int c = threadIdx.x; c < C; c += blockDim.x) {
-        double a = 0.0, b = 0.0;
-        for (int pl = 0; pl < L; ++pl) {
-            a += double(s_sum[pl * C + c]);
-            b += double(s_sq[pl * C + c]);
-        }
-        c_sum[c] = a;
-        c_sq[c] = b;
-    }
-    __syncthreads();
-    const int cpg = C / G;
-    for (int g = threadIdx.x; g < G; g += blockDim.x) {
-        double a = 0.0, b = 0.0;
-        for (int c = g * cpg; c < (g + 1) * cpg; ++c) {
-            a += c_sum[c];
-            b += c_sq[c];
-        }
-        partial[((long long)blockIdx.x * G + g) * 2] = a;
-        partial[((long long)blockIdx.x * G + g) * 2 + 1] = b;
-    }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!is_last) return;
-    __threadfence();
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
-    const int blocks = gridDim.x;
-    for (int g = warp; g < G; g += nw) {
-        double a = 0.0, b = 0.0;
-        for (int k = lane; k < blocks; k += 32) {
-            a += __ldcg(partial + ((long long)k * G + g) * 2);
-            b += __ldcg(partial + ((long long)k * G + g) * 2 + 1);
-        }
-        for (int o = 16; o; o >>= 1) {
-            a += __shfl_xor_sync(0xffffffffu, a, o);
-            b += __shfl_xor_sync(0xffffffffu, b, o);
-        }
-        if (lane == 0) {
-            out[g * 2] = a / count;
-            out[g * 2 + 1] = b / count;
-        }
-    }
-    if (threadIdx.x == 0) *ticket = 0u;
-}
-
 // Device-order weighted mean (collectives.cpp:150-172), no FMA contraction.
 __device__ void weighted_mean(const double* all, int n, const double* w, int G, int g, double& m,
                               double& q) {
@@ -222,174 +125,262 @@ __device__ void gn_use_of(const GnCombine& cb, int G, int g, float& mu, float& i
     inv = float(1.0 / sqrt(__dadd_rn(fmax(var, 0.0), double(cb.eps))));
 }
 
-template <class T>
-__global__ void gn_apply_kernel(const T* __restrict__ x, T* __restrict__ y, int pix, int C, int ld,
-                                int G, const GnCombine cb, const float* __restrict__ gamma,
-                                const float* __restrict__ beta, int do_silu,
-                                const float* __restrict__ temb, const T* __restrict__ skip,
-                                int round_tf32) {
+// One pass over a band for GroupNorm: APPLY computes y = GN(x) [-> SiLU] [+ temb] [+ skip]
+// (group_norm_apply, tensor.cpp:240-277, with the fused SiLU / AddTimeEmb / AddSkip of the
+// following layers); STATS folds the group statistics of the stored values (y, or x when
+// !APPLY) into out[G][2] = (mean, mean_sq) (group_stats, tensor.cpp:203-235).
+// Thread (tx, ty) owns one 16-byte channel vector and kGnU pixels (all loads in flight at
+// once); its GN coefficients live in registers (two groups at most per vector).  Statistics:
+// fp32 per-thread sums over kGnU pixels, fp64 above, fixed-order block reduction and a
+// fixed-order fold by the last block -> deterministic.  gamma / beta are weights and are
+// loaded before griddepcontrol.wait; everything else after it.
+constexpr int kGnU = 4;         // pixels per thread (apply)
+constexpr int kGnUStats = 16;   // pixels per thread with statistics (fewer blocks to fold)
+
+template <class T, bool APPLY, bool STATS, int U>
+__global__ void __launch_bounds__(256)
+    gn_pass_kernel(const T* __restrict__ x, T* __restrict__ y, int pix, int C, int ld, int G,
+                   const GnCombine cb, const float* __restrict__ gamma,
+                   const float* __restrict__ beta, int do_silu, const float* __restrict__ temb,
+                   const T* __restrict__ skip, int round_tf32, const GnStatsOut so) {
     constexpr int VEC = Vec<T>::N;
-    extern __shared__ float s_tab[];   // [4][ld]: mean, inv_std*gamma, beta, temb
-    __shared__ float s_use[2 * 1024];
-    float* s_mu = s_tab;
-    float* s_sc = s_tab + ld;
-    float* s_be = s_tab + 2 * ld;
-    float* s_te = s_tab + 3 * ld;
-    for (int g = threadIdx.x; g < G; g += blockDim.x) {
-        float mu, inv;
-        bool neg;
-        gn_use_of(cb, G, g, mu, inv, neg);
-        s_use[2 * g] = mu;
-        s_use[2 * g + 1] = inv;
-        // group_norm_apply contract (tensor.cpp:256-259), reported once per launch
-        if (neg && blockIdx.x == 0 && cb.err) atomicExch(cb.err, 1);
-    }
-    __syncthreads();
-    const int cpg = C / G;
-    for (int c = threadIdx.x; c < ld; c += blockDim.x) {
-        if (c < C) {
-            const int g = c / cpg;
-            s_mu[c] = s_use[2 * g];
-            s_sc[c] = s_use[2 * g + 1] * gamma[c];
-            s_be[c] = beta[c];
-            s_te[c] = temb ? temb[c] : 0.0f;
-        } else {
-            s_mu[c] = s_sc[c] = s_be[c] = s_te[c] = 0.0f;
-        }
-    }
-    __syncthreads();
-    const unsigned nvec = unsigned(ld / VEC);
-    const unsigned total = unsigned(pix) * nvec;
-    const unsigned stride = gridDim.x * blockDim.x;
-    constexpr int U = 4;   // vectors in flight per thread
-    for (unsigned idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += U * stride) {
-        float f[U][VEC], sk[U][VEC];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const unsigned j = idx + u * stride;
-            if (j < total) {
-                load_vec<T>(x + size_t(j) * VEC, f[u]);
-                if (skip) load_vec<T>(skip + size_t(j) * VEC, sk[u]);
+    const int vx = blockDim.x, vy = blockDim.y;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int tid = ty * vx + tx;
+    const int nthr = vx * vy;
+    const int nvec = ld / VEC;
+    const int cv = blockIdx.x * vx + tx;
+    const bool active = cv < nvec;
+    const int c0 = cv * VEC;
+    const int cb0 = blockIdx.x * vx * VEC;    // first channel of this block
+    const int bch = vx * VEC;                 // channels of this block
+    const bool full = active && c0 + VEC <= C;
+    float sc[VEC], sh[VEC], tb[VEC], mu[VEC];
+    if (APPLY) {   // weights: safe to read before the previous kernel completes
+        if (full) {
+            load_vec<float>(gamma + c0, sc);
+            load_vec<float>(beta + c0, sh);
+            if constexpr (VEC == 8) {
+                load_vec<float>(gamma + c0 + 4, sc + 4);
+                load_vec<float>(beta + c0 + 4, sh + 4);
             }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const unsigned j = idx + u * stride;
-            if (j >= total) continue;
-            const int c0 = int(j % nvec) * VEC;
+        } else {
 #pragma unroll
             for (int i = 0; i < VEC; ++i) {
-                const int c = c0 + i;
-                float v = (f[u][i] - s_mu[c]) * s_sc[c] + s_be[c];
-                if (do_silu) {
-                    if constexpr (sizeof(T) == 2)
-                        v = __fdividef(v, 1.0f + __expf(-v));
-                    else
-                        v = v / (1.0f + expf(-v));
-                }
-                v = v + s_te[c];
-                if (skip) v = v + sk[u][i];
-                f[u][i] = v;
+                const bool ok = active && c0 + i < C;
+                sc[i] = ok ? gamma[c0 + i] : 0.0f;
+                sh[i] = ok ? beta[c0 + i] : 0.0f;
             }
-            if (c0 + VEC > C) {
-#pragma unroll
-                for (int i = 0; i < VEC; ++i)
-                    if (c0 + i >= C) f[u][i] = 0.0f;
-            }
-            store_vec<T>(y + size_t(j) * VEC, f[u], round_tf32 != 0);
         }
     }
-}
-
-// 2-D mapping: threadIdx.x / blockIdx.x select a fixed 16-byte channel vector (its GN
-// coefficients live in registers), threadIdx.y / blockIdx.y stride over pixels with four
-// vectors in flight per thread.  A warp touches 32 consecutive vectors of one pixel.
-template <class T>
-__global__ void __launch_bounds__(256, 4)
-    gn_apply_2d_kernel(const T* __restrict__ x, T* __restrict__ y, int pix, int C,
-                                   int ld, int G, const GnCombine cb,
-                                   const float* __restrict__ gamma, const float* __restrict__ beta,
-                                   int do_silu, const float* __restrict__ temb,
-                                   const T* __restrict__ skip, int round_tf32) {
-    constexpr int VEC = Vec<T>::N;
-    __shared__ float s_use[2 * 1024];
-    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-    for (int g = tid; g < G; g += blockDim.x * blockDim.y) {
-        float mu, inv;
-        bool neg;
-        gn_use_of(cb, G, g, mu, inv, neg);
-        s_use[2 * g] = mu;
-        s_use[2 * g + 1] = inv;
-        // group_norm_apply contract (tensor.cpp:256-259), reported once per launch
-        if (neg && blockIdx.x == 0 && blockIdx.y == 0 && cb.err) atomicExch(cb.err, 1);
-    }
-    __syncthreads();
-    // per-channel coefficients of this block's channel slice: (mean, inv_std*gamma, beta, temb)
-    __shared__ float4 s_coef[1024];
-    const int nvec = ld / VEC;
-    const int cbase = blockIdx.x * blockDim.x * VEC;
-    const int cpg = C / G;
-    // layout [i][tx] (element i of thread tx's vector): a warp's LDS.128 of one i is
-    // 512 contiguous bytes -> conflict-free
-    for (int k = tid; k < int(blockDim.x) * VEC; k += blockDim.x * blockDim.y) {
-        const int txk = k / VEC, i = k - txk * VEC;
-        const int c = cbase + k;
-        float4 k4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (c < C) {
-            const int g = c / cpg;
-            k4 = make_float4(s_use[2 * g], s_use[2 * g + 1] * gamma[c], beta[c], temb ? temb[c] : 0.0f);
-        }
-        s_coef[i * blockDim.x + txk] = k4;
-    }
-    __syncthreads();
-    const int cv = blockIdx.x * blockDim.x + threadIdx.x;
-    if (cv >= nvec) return;
-    const int c0 = cv * VEC;
-    const float4* coef = s_coef + threadIdx.x;
-    const int cstride = blockDim.x;
-    const int pstride = blockDim.y * gridDim.y;
-    constexpr int U = 4;   // raw 16-byte vectors in flight per thread (4 registers each)
+    pdl_wait();
+    pdl_trigger();
+    const int pstride = vy * gridDim.y;
+    const int p_first = blockIdx.y * vy + ty;
+    // first round of loads in flight before the group coefficients are computed
     const uint4* xv = reinterpret_cast<const uint4*>(x) + cv;
     const uint4* sv = reinterpret_cast<const uint4*>(skip) + cv;
-    for (int p = blockIdx.y * blockDim.y + threadIdx.y; p < pix; p += U * pstride) {
-        uint4 rx[U], rs[U];
+    uint4 rx[U], rs[U];
+    if (active) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int pp = p + u * pstride;
+            const int pp = p_first + u * pstride;
             if (pp < pix) {
                 rx[u] = __ldcs(xv + size_t(pp) * nvec);
-                if (skip) rs[u] = __ldcs(sv + size_t(pp) * nvec);
+                if (APPLY && skip) rs[u] = __ldcs(sv + size_t(pp) * nvec);
             }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int pp = p + u * pstride;
-            if (pp >= pix) continue;
-            float f[VEC], sk[VEC];
-            load_vec<T>(reinterpret_cast<const T*>(&rx[u]), f);
-            if (skip) load_vec<T>(reinterpret_cast<const T*>(&rs[u]), sk);
-#pragma unroll
-            for (int i = 0; i < VEC; ++i) {
-                const float4 k4 = coef[i * cstride];
-                float v = (f[i] - k4.x) * k4.y + k4.z;
-                if (do_silu) {
-                    if constexpr (sizeof(T) == 2)
-                        v = __fdividef(v, 1.0f + __expf(-v));
-                    else
-                        v = v / (1.0f + expf(-v));
-                }
-                v = v + k4.w;
-                if (skip) v = v + sk[i];
-                f[i] = (c0 + i < C) ? v : 0.0f;
-            }
-            store_vec<T>(y + (size_t(pp) * nvec + cv) * VEC, f, round_tf32 != 0);
         }
     }
+    if (APPLY) {
+        // (mean, 1/std) of the groups this block touches, one thread per group
+        __shared__ float s_mi[2 * 1024];
+        const int cpg = C / G;
+        const int g_first = min(cb0, C - 1) / cpg;
+        const int n_g = (min(cb0 + bch, C) - 1) / cpg - g_first + 1;
+        for (int j = tid; j < n_g; j += nthr) {
+            float m_, i_;
+            bool neg;
+            gn_use_of(cb, G, g_first + j, m_, i_, neg);
+            // group_norm_apply contract (tensor.cpp:256-259)
+            if (neg && cb.err) atomicExch(cb.err, 1);
+            s_mi[2 * j] = m_;
+            s_mi[2 * j + 1] = i_;
+        }
+        if (temb) {
+            if (full) {
+                load_vec<float>(temb + c0, tb);
+                if constexpr (VEC == 8) load_vec<float>(temb + c0 + 4, tb + 4);
+            } else {
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) tb[i] = (active && c0 + i < C) ? temb[c0 + i] : 0.0f;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) tb[i] = 0.0f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) {
+            const int j = min(c0 + i, C - 1) / cpg - g_first;
+            mu[i] = s_mi[2 * j];
+            sc[i] *= s_mi[2 * j + 1];
+        }
+    }
+    float ss[VEC], sq[VEC];
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) ss[i] = sq[i] = 0.0f;
+    if (active) {
+        for (int p = p_first; p < pix; p += U * pstride) {
+            if (p != p_first) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int pp = p + u * pstride;
+                    if (pp < pix) {
+                        rx[u] = __ldcs(xv + size_t(pp) * nvec);
+                        if (APPLY && skip) rs[u] = __ldcs(sv + size_t(pp) * nvec);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int pp = p + u * pstride;
+                if (pp >= pix) continue;
+                float f[VEC];
+                load_vec<T>(reinterpret_cast<const T*>(&rx[u]), f);
+                if (APPLY) {
+                    float sk[VEC];
+                    if (skip) load_vec<T>(reinterpret_cast<const T*>(&rs[u]), sk);
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) f[i] = (f[i] - mu[i]) * sc[i] + sh[i];
+                    if (do_silu) {
+                        if constexpr (sizeof(T) == 2) {
+                            // bf16 output: sigmoid(v) = 0.5 + 0.5 tanh(v / 2) with one packed
+                            // f16x2 tanh per two elements (the SFU is this kernel's bound:
+                            // ex2 + rcp per element was 4x the MUFU work); |err| ~ 2^-11,
+                            // below the bf16 rounding of the stored value
+#pragma unroll
+                            for (int i = 0; i < VEC; i += 2) {
+                                const __half2 hv = __floats2half2_rn(0.5f * f[i], 0.5f * f[i + 1]);
+                                uint32_t hi = *reinterpret_cast<const uint32_t*>(&hv), ho;
+                                asm("tanh.approx.f16x2 %0, %1;" : "=r"(ho) : "r"(hi));
+                                const float2 t = __half22float2(*reinterpret_cast<const __half2*>(&ho));
+                                f[i] = f[i] * fmaf(0.5f, t.x, 0.5f);
+                                f[i + 1] = f[i + 1] * fmaf(0.5f, t.y, 0.5f);
+                            }
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i) f[i] = f[i] / (1.0f + expf(-f[i]));
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) {
+                        float v = f[i] + tb[i];
+                        if (skip) v = v + sk[i];
+                        f[i] = (c0 + i < C) ? v : 0.0f;
+                    }
+                    uint4 o;
+                    store_vec<T>(reinterpret_cast<T*>(&o), f, round_tf32 != 0);
+                    *reinterpret_cast<uint4*>(y + (size_t(pp) * nvec + cv) * VEC) = o;
+                    if (STATS) load_vec<T>(reinterpret_cast<const T*>(&o), f);   // stored values
+                }
+                if (STATS) {
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) {
+                        ss[i] += f[i];
+                        sq[i] = fmaf(f[i], f[i], sq[i]);
+                    }
+                }
+            }
+        }
+    }
+    if (!STATS) return;
+    // ---- block reduction: per channel over ty (fp64, fixed order), then per group
+    __shared__ float r_s[256 * VEC], r_q[256 * VEC];
+    __shared__ double c_s[1024], c_q[1024];
+    __shared__ bool is_last;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+        r_s[(ty * vx + tx) * VEC + i] = ss[i];
+        r_q[(ty * vx + tx) * VEC + i] = sq[i];
+    }
+    __syncthreads();
+    for (int c = tid; c < bch; c += nthr) {
+        double a = 0.0, b = 0.0;
+        for (int r = 0; r < vy; ++r) {
+            a += double(r_s[r * bch + c]);
+            b += double(r_q[r * bch + c]);
+        }
+        c_s[c] = a;
+        c_q[c] = b;
+    }
+    __syncthreads();
+    const int Gs = so.G;
+    const int cpg2 = C / Gs;
+    const size_t blk = size_t(blockIdx.y) * gridDim.x + blockIdx.x;
+    for (int g = tid; g < Gs; g += nthr) {
+        double a = 0.0, b = 0.0;
+        const int lo = max(g * cpg2, cb0), hi = min((g + 1) * cpg2, min(cb0 + bch, C));
+        for (int c = lo; c < hi; ++c) {
+            a += c_s[c - cb0];
+            b += c_q[c - cb0];
+        }
+        reinterpret_cast<double2*>(so.partial)[blk * Gs + g] = make_double2(a, b);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        const unsigned nb = gridDim.x * gridDim.y;
+        is_last = atomicAdd(so.ticket, 1u) == nb - 1;
+        if (is_last) __threadfence();
+    }
+    __syncthreads();
+    if (!is_last) return;
+    // ---- last block: fold the per-block partials, P lanes per group, fixed order (full
+    // warps only, so the xor-shuffles never name a missing lane)
+    const int nblk = gridDim.x * gridDim.y;
+    const int nfull = (nthr / 32) * 32;
+    if (tid < nfull) {
+        int P = 1;
+        while (P * 2 <= 32 && P * 2 * Gs <= nfull) P *= 2;
+        for (int base = 0; base < Gs * P; base += nfull) {
+            const int w = base + tid;
+            const int g = w / P, part = w % P;
+            double a = 0.0, b = 0.0;
+            if (g < Gs) {
+                for (int k0 = part; k0 < nblk; k0 += 8 * P) {
+                    double2 v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int k = k0 + u * P;
+                        v[u] = k < nblk ? __ldcg(reinterpret_cast<const double2*>(so.partial) +
+                                                 size_t(k) * Gs + g)
+                                        : make_double2(0.0, 0.0);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        a += v[u].x;
+                        b += v[u].y;
+                    }
+                }
+            }
+            for (int o = P / 2; o; o >>= 1) {
+                a += __shfl_xor_sync(0xffffffffu, a, o);
+                b += __shfl_xor_sync(0xffffffffu, b, o);
+            }
+            if (g < Gs && part == 0) {
+                so.out[g * 2] = a / so.count;
+                so.out[g * 2 + 1] = b / so.count;
+            }
+        }
+    }
+    if (tid == 0) *so.ticket = 0u;
 }
 
 // ---------------------------------------------------------------- pointwise
 template <class T>
 __global__ void silu_kernel(const T* __restrict__ x, T* __restrict__ y, long long nv, int r) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int VEC = Vec<T>::N;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nv;
          i += (long long)gridDim.x * blockDim.x) {
@@ -404,6 +395,8 @@ __global__ void silu_kernel(const T* __restrict__ x, T* __restrict__ y, long lon
 template <class T>
 __global__ void add_kernel(const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ o,
                            long long nv, int r) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int VEC = Vec<T>::N;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nv;
          i += (long long)gridDim.x * blockDim.x) {
@@ -420,6 +413,8 @@ template <class T>
 __global__ void add_channel_kernel(const T* __restrict__ x, const float* __restrict__ vec,
                                    const T* __restrict__ skip, T* __restrict__ o, long long pix,
                                    int ld, int r) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int VEC = Vec<T>::N;
     const int nvec = ld / VEC;
     const long long total = pix * nvec;
@@ -448,6 +443,8 @@ __global__ void add_channel_kernel(const T* __restrict__ x, const float* __restr
 template <class T>
 __global__ void upsample_kernel(const T* __restrict__ x, T* __restrict__ y, int rows, int W,
                                 int ld) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int VEC = Vec<T>::N;
     const int nvec = ld / VEC;
     const long long total = (long long)rows * W * nvec;
@@ -470,6 +467,8 @@ __global__ void upsample_kernel(const T* __restrict__ x, T* __restrict__ y, int 
 template <class T>
 __global__ void softmax_kernel(const float* __restrict__ S, int ns, long long lds, float scale,
                                T* __restrict__ P, long long ldp) {
+    pdl_wait();
+    pdl_trigger();
     const int row = blockIdx.x;
     const float* s = S + (long long)row * lds;
     __shared__ float red[32];
@@ -506,6 +505,8 @@ __global__ void softmax_kernel(const float* __restrict__ S, int ns, long long ld
 template <class T>
 __global__ void transpose_kernel(const T* __restrict__ V, int ns, int C, long long ldv,
                                  T* __restrict__ Vt, long long ldt) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ T tile[32][33];
     const int j0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
     for (int k = threadIdx.y; k < 32; k += blockDim.y) {
@@ -522,6 +523,8 @@ __global__ void transpose_kernel(const T* __restrict__ V, int ns, int C, long lo
 // ---------------------------------------------------------------- embeddings / projections
 __global__ void time_projection_kernel(const TembLayer* __restrict__ layers,
                                        const __grid_constant__ EmbArg emb_arg) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ float emb[];
     const int dim = emb_arg.dim;
     for (int i = threadIdx.x; i < dim; i += blockDim.x) emb[i] = emb_arg.v[i];
@@ -540,6 +543,8 @@ __global__ void time_projection_kernel(const TembLayer* __restrict__ layers,
 __global__ void time_projection_plan_kernel(const TembLayer* __restrict__ layers,
                                             const float* __restrict__ embs, int dim,
                                             float* __restrict__ table, int n_layers, int ldt) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ float emb[];
     const int step = blockIdx.z;
     for (int i = threadIdx.x; i < dim; i += blockDim.x) emb[i] = embs[(size_t)step * dim + i];
@@ -559,6 +564,8 @@ __global__ void time_projection_plan_kernel(const TembLayer* __restrict__ layers
 __global__ void gemv_f64_kernel(const float* __restrict__ W, const float* __restrict__ b,
                                 const float* __restrict__ x, int rows, int cols,
                                 float* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int nw = blockDim.x / 32;
     for (int r = blockIdx.x * nw + warp; r < rows; r += gridDim.x * nw) {
@@ -574,6 +581,8 @@ template <class T>
 __global__ void ddim_kernel(const float* __restrict__ x, const float* __restrict__ eps,
                             float* __restrict__ xo, long long n, int C, double sa, double s1,
                             double sn, double s1n, T* __restrict__ stem, int stem_ld) {
+    pdl_wait();
+    pdl_trigger();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const double e = double(eps[i]);
@@ -590,6 +599,8 @@ __global__ void ddim_kernel(const float* __restrict__ x, const float* __restrict
 template <class T>
 __global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, int C, int H, int W, int r0,
                                     int rows, T* __restrict__ dst, int ld, int r) {
+    pdl_wait();
+    pdl_trigger();
     const long long total = (long long)rows * W * C;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
@@ -603,6 +614,8 @@ __global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, int C, int H,
 template <class T>
 __global__ void nhwc_to_nchw_kernel(const T* __restrict__ src, int ld, int C, int rows, int W,
                                     float* __restrict__ dst, int* nonfinite) {
+    pdl_wait();
+    pdl_trigger();
     const long long total = (long long)rows * W * C;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
@@ -618,6 +631,8 @@ __global__ void nhwc_to_nchw_kernel(const T* __restrict__ src, int ld, int C, in
 template <class T>
 __global__ void crop_kernel(const float* __restrict__ src, int C, int H, int W, int y0, int x0,
                             int rows, int cols, T* __restrict__ dst, int ld, int r) {
+    pdl_wait();
+    pdl_trigger();
     const long long total = (long long)rows * cols * C;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
@@ -631,6 +646,8 @@ __global__ void crop_kernel(const float* __restrict__ src, int C, int H, int W, 
 __global__ void scatter_patch_kernel(const float* __restrict__ patch, int C, int rows, int cols,
                                      float* __restrict__ dst, int H, int W, int y0, int x0,
                                      int* nonfinite) {
+    pdl_wait();
+    pdl_trigger();
     const long long total = (long long)rows * cols * C;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
@@ -645,12 +662,16 @@ __global__ void scatter_patch_kernel(const float* __restrict__ patch, int C, int
 
 template <class T>
 __global__ void f32_to_elem_kernel(const float* __restrict__ s, T* __restrict__ d, long long n, int r) {
+    pdl_wait();
+    pdl_trigger();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
         d[i] = from_float<T>(s[i], r != 0);
 }
 template <class T>
 __global__ void elem_to_f32_kernel(const T* __restrict__ s, float* __restrict__ d, long long n) {
+    pdl_wait();
+    pdl_trigger();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
         d[i] = to_float(s[i]);
@@ -669,53 +690,83 @@ __global__ void elem_to_f32_kernel(const T* __restrict__ s, float* __restrict__ 
 
 }  // namespace
 
-int gn_stats_blocks(long long pix) { return int((pix + kGnPixels - 1) / kGnPixels); }
-
-void gn_stats(Elem e, const void* x, long long pix, int C, int ld, int groups, double count,
-              double* partial, unsigned int* ticket, double* out, cudaStream_t s) {
+// Launch shape of gn_pass_kernel: block = vx channel vectors x vy pixel lanes (~256
+// threads), grid.y sized so every thread owns kGnU pixels (one round of loads in flight),
+// capped at ~8 resident blocks per SM.
+struct GnShape {
+    dim3 grid, block;
+};
+GnShape gn_shape(Elem e, long long pix, int ld, int U) {
     const int VEC = e == Elem::BF16 ? 8 : 4;
-    if (C % VEC || ld % VEC || C % groups)
-        throw std::invalid_argument("group_stats: channels must be a multiple of the vector width");
-    const int nvec = C / VEC;
-    const int L = std::max(1, kGnThreads / nvec);
-    const size_t smem = size_t(2) * L * C * 4 + size_t(2) * C * 8;
-    DISPATCH(e, gn_stats_kernel<T><<<gn_stats_blocks(pix), kGnThreads, smem, s>>>(
-                    static_cast<const T*>(x), pix, C, ld, groups, count, partial, ticket, out));
-    CUDA_CHECK(cudaGetLastError());
-}
-
-void gn_apply(Elem e, const void* x, void* y, long long pix, int C, int ld, int groups,
-              const GnCombine& cb, const float* gamma, const float* beta, bool do_silu,
-              const float* temb, const void* skip, bool round_tf32, cudaStream_t s) {
-    if (groups > 1024) throw std::invalid_argument("group_norm_apply: too many groups");
-    const int VEC = e == Elem::BF16 ? 8 : 4;
-    if (pix * (ld / VEC) >= (1LL << 31)) throw std::invalid_argument("group_norm_apply: band too large");
-    // block = vx channel vectors x vy pixel lanes (~256 threads); grid fills ~4 waves of SMs
     const int nvec = ld / VEC;
     int vx = nvec;
     while (vx > 128 && vx % 2 == 0) vx /= 2;
     if (vx > 128) vx = 128;
     const int gx = (nvec + vx - 1) / vx;
     const int vy = std::max(1, 256 / vx);
-    // one wave of ~4 blocks per SM; each thread keeps 4 vectors in flight per iteration
-    const long long rows_needed = (pix + vy - 1) / vy;
-    const int gy = int(std::max<long long>(1, std::min<long long>(rows_needed, (148LL * 4) / gx)));
-    DISPATCH(e, gn_apply_2d_kernel<T><<<dim3(gx, gy), dim3(vx, vy), 0, s>>>(
-                    static_cast<const T*>(x), static_cast<T*>(y), int(pix), C, ld, groups, cb, gamma,
-                    beta, do_silu ? 1 : 0, temb, static_cast<const T*>(skip), round_tf32 ? 1 : 0));
+    const long long want = (pix + (long long)vy * U - 1) / ((long long)vy * U);
+    const int gy = int(std::max<long long>(1, std::min<long long>(want, std::max(1, 1184 / gx))));
+    return {dim3(gx, gy), dim3(vx, vy)};
+}
+
+int gn_stats_blocks(long long) { return 1184 + 1184; }   // >= gx * gy of every gn_shape
+
+void gn_stats(Elem e, const void* x, long long pix, int C, int ld, int groups, double count,
+              double* partial, unsigned int* ticket, double* out, cudaStream_t s) {
+    const int VEC = e == Elem::BF16 ? 8 : 4;
+    if (C % VEC || ld % VEC || C % groups)
+        throw std::invalid_argument("group_stats: channels must be a multiple of the vector width");
+    if (pix * (ld / VEC) >= (1LL << 31)) throw std::invalid_argument("group_stats: band too large");
+    const GnShape sh = gn_shape(e, pix, ld, kGnUStats);
+    GnStatsOut so;
+    so.G = groups;
+    so.count = count;
+    so.partial = partial;
+    so.ticket = ticket;
+    so.out = out;
+    GnCombine cb{};
+    DISPATCH(e, launch_pdl(gn_pass_kernel<T, false, true, kGnUStats>, sh.grid, sh.block, 0, s, 1,
+                           static_cast<const T*>(x), static_cast<T*>(nullptr), int(pix), C, ld,
+                           groups, cb, static_cast<const float*>(nullptr),
+                           static_cast<const float*>(nullptr), 0, static_cast<const float*>(nullptr),
+                           static_cast<const T*>(nullptr), 0, so));
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void gn_apply(Elem e, const void* x, void* y, long long pix, int C, int ld, int groups,
+              const GnCombine& cb, const float* gamma, const float* beta, bool do_silu,
+              const float* temb, const void* skip, bool round_tf32, cudaStream_t s,
+              const GnStatsOut* out_stats) {
+    if (groups > 1024) throw std::invalid_argument("group_norm_apply: too many groups");
+    const int VEC = e == Elem::BF16 ? 8 : 4;
+    if (pix * (ld / VEC) >= (1LL << 31)) throw std::invalid_argument("group_norm_apply: band too large");
+    const bool st = out_stats && out_stats->G > 0;
+    const GnShape sh = gn_shape(e, pix, ld, st ? kGnUStats : kGnU);
+    if (st) {
+        if (C % out_stats->G) throw std::invalid_argument("group_stats: channels not divisible by groups");
+        DISPATCH(e, launch_pdl(gn_pass_kernel<T, true, true, kGnUStats>, sh.grid, sh.block, 0, s, 1,
+                               static_cast<const T*>(x), static_cast<T*>(y), int(pix), C, ld, groups,
+                               cb, gamma, beta, do_silu ? 1 : 0, temb, static_cast<const T*>(skip),
+                               round_tf32 ? 1 : 0, *out_stats));
+    } else {
+        DISPATCH(e, launch_pdl(gn_pass_kernel<T, true, false, kGnU>, sh.grid, sh.block, 0, s, 1,
+                               static_cast<const T*>(x), static_cast<T*>(y), int(pix), C, ld, groups,
+                               cb, gamma, beta, do_silu ? 1 : 0, temb, static_cast<const T*>(skip),
+                               round_tf32 ? 1 : 0, GnStatsOut{}));
+    }
     CUDA_CHECK(cudaGetLastError());
 }
 
 void silu(Elem e, const void* x, void* y, long long n, bool r, cudaStream_t s) {
     const int VEC = e == Elem::BF16 ? 8 : 4;
-    DISPATCH(e, silu_kernel<T><<<grid_for(n / VEC, 256), 256, 0, s>>>(
+    DISPATCH(e, launch_pdl(silu_kernel<T>, dim3(grid_for(n / VEC, 256)), dim3(256), 0, s, 1, 
                     static_cast<const T*>(x), static_cast<T*>(y), n / VEC, r ? 1 : 0));
     CUDA_CHECK(cudaGetLastError());
 }
 
 void add(Elem e, const void* x, const void* y, void* o, long long n, bool r, cudaStream_t s) {
     const int VEC = e == Elem::BF16 ? 8 : 4;
-    DISPATCH(e, add_kernel<T><<<grid_for(n / VEC, 256), 256, 0, s>>>(
+    DISPATCH(e, launch_pdl(add_kernel<T>, dim3(grid_for(n / VEC, 256)), dim3(256), 0, s, 1, 
                     static_cast<const T*>(x), static_cast<const T*>(y), static_cast<T*>(o),
                     n / VEC, r ? 1 : 0));
     CUDA_CHECK(cudaGetLastError());
@@ -724,7 +775,7 @@ void add(Elem e, const void* x, const void* y, void* o, long long n, bool r, cud
 void add_channel(Elem e, const void* x, const float* vec, const void* skip, void* o,
                  long long pix, int ld, bool, bool r, cudaStream_t s) {
     const int VEC = e == Elem::BF16 ? 8 : 4;
-    DISPATCH(e, add_channel_kernel<T><<<grid_for(pix * ld / VEC, 256), 256, 0, s>>>(
+    DISPATCH(e, launch_pdl(add_channel_kernel<T>, dim3(grid_for(pix * ld / VEC, 256)), dim3(256), 0, s, 1, 
                     static_cast<const T*>(x), vec, static_cast<const T*>(skip), static_cast<T*>(o),
                     pix, ld, r ? 1 : 0));
     CUDA_CHECK(cudaGetLastError());
@@ -732,21 +783,21 @@ void add_channel(Elem e, const void* x, const float* vec, const void* skip, void
 
 void upsample2x(Elem e, const void* x, void* y, int rows, int W, int ld, cudaStream_t s) {
     const int VEC = e == Elem::BF16 ? 8 : 4;
-    DISPATCH(e, upsample_kernel<T><<<grid_for((long long)rows * W * ld / VEC, 256), 256, 0, s>>>(
+    DISPATCH(e, launch_pdl(upsample_kernel<T>, dim3(grid_for((long long)rows * W * ld / VEC, 256)), dim3(256), 0, s, 1, 
                     static_cast<const T*>(x), static_cast<T*>(y), rows, W, ld));
     CUDA_CHECK(cudaGetLastError());
 }
 
 void softmax_rows(Elem e, const float* S, int m, int ns, long long lds, float scale, void* P,
                   long long ldp, cudaStream_t s) {
-    DISPATCH(e, softmax_kernel<T><<<m, 256, 0, s>>>(S, ns, lds, scale, static_cast<T*>(P), ldp));
+    DISPATCH(e, launch_pdl(softmax_kernel<T>, dim3(m), dim3(256), 0, s, 1, S, ns, lds, scale, static_cast<T*>(P), ldp));
     CUDA_CHECK(cudaGetLastError());
 }
 
 void transpose(Elem e, const void* V, int ns, int C, long long ldv, void* Vt, long long ldt,
                cudaStream_t s) {
     dim3 grid((ns + 31) / 32, (C + 31) / 32), block(32, 8);
-    DISPATCH(e, transpose_kernel<T><<<grid, block, 0, s>>>(static_cast<const T*>(V), ns, C, ldv,
+    DISPATCH(e, launch_pdl(transpose_kernel<T>, dim3(grid), dim3(block), 0, s, 1, static_cast<const T*>(V), ns, C, ldv,
                                                           static_cast<T*>(Vt), ldt));
     CUDA_CHECK(cudaGetLastError());
 }
@@ -759,7 +810,7 @@ void time_projection(const TembLayer* layers_dev, int n_layers, int max_c, const
     arg.dim = dim;
     for (int i = 0; i < dim; ++i) arg.v[i] = emb[i];
     dim3 grid(std::max(1, (max_c + 7) / 8), n_layers);
-    time_projection_kernel<<<grid, 256, dim * sizeof(float), s>>>(layers_dev, arg);
+    launch_pdl(time_projection_kernel, dim3(grid), dim3(256), dim * sizeof(float), s, 1, layers_dev, arg);
     CUDA_CHECK(cudaGetLastError());
 }
 
@@ -768,14 +819,14 @@ void time_projection_plan(const TembLayer* layers_dev, int n_layers, int max_c,
                           cudaStream_t s) {
     if (n_layers == 0 || n_steps == 0) return;
     dim3 grid(std::max(1, (max_c + 7) / 8), n_layers, n_steps);
-    time_projection_plan_kernel<<<grid, 256, dim * sizeof(float), s>>>(layers_dev, embs_dev, dim,
+    launch_pdl(time_projection_plan_kernel, dim3(grid), dim3(256), dim * sizeof(float), s, 1, layers_dev, embs_dev, dim,
                                                                         table, n_layers, ldt);
     CUDA_CHECK(cudaGetLastError());
 }
 
 void gemv_f64(const float* W, const float* b, const float* x, int rows, int cols, float* out,
               cudaStream_t s) {
-    gemv_f64_kernel<<<std::max(1, std::min(148, (rows + 7) / 8)), 256, 0, s>>>(W, b, x, rows, cols,
+    launch_pdl(gemv_f64_kernel, dim3(std::max(1, std::min(148, (rows + 7) / 8))), dim3(256), 0, s, 1, W, b, x, rows, cols,
                                                                               out);
     CUDA_CHECK(cudaGetLastError());
 }
@@ -784,54 +835,54 @@ void ddim_update(const float* x, const float* eps, float* xo, long long n, int C
                  double abar_n, Elem e, void* stem, int stem_ld, cudaStream_t s) {
     const double sa = std::sqrt(abar_t), s1 = std::sqrt(1.0 - abar_t);
     const double sn = std::sqrt(abar_n), s1n = std::sqrt(1.0 - abar_n);
-    DISPATCH(e, ddim_kernel<T><<<grid_for(n, 256), 256, 0, s>>>(x, eps, xo, n, C, sa, s1, sn, s1n,
+    DISPATCH(e, launch_pdl(ddim_kernel<T>, dim3(grid_for(n, 256)), dim3(256), 0, s, 1, x, eps, xo, n, C, sa, s1, sn, s1n,
                                                                 static_cast<T*>(stem), stem_ld));
     CUDA_CHECK(cudaGetLastError());
 }
 
 void nchw_to_nhwc(const float* src, int C, int H, int W, int r0, int rows, Elem e, void* dst,
                   int ld, bool r, cudaStream_t s) {
-    DISPATCH(e, nchw_to_nhwc_kernel<T><<<grid_for((long long)rows * W * C, 256), 256, 0, s>>>(
+    DISPATCH(e, launch_pdl(nchw_to_nhwc_kernel<T>, dim3(grid_for((long long)rows * W * C, 256)), dim3(256), 0, s, 1, 
                     src, C, H, W, r0, rows, static_cast<T*>(dst), ld, r ? 1 : 0));
     CUDA_CHECK(cudaGetLastError());
 }
 
 void nhwc_to_nchw(Elem e, const void* src, int ld, int C, int rows, int W, float* dst,
                   int* nonfinite, cudaStream_t s) {
-    DISPATCH(e, nhwc_to_nchw_kernel<T><<<grid_for((long long)rows * W * C, 256), 256, 0, s>>>(
+    DISPATCH(e, launch_pdl(nhwc_to_nchw_kernel<T>, dim3(grid_for((long long)rows * W * C, 256)), dim3(256), 0, s, 1, 
                     static_cast<const T*>(src), ld, C, rows, W, dst, nonfinite));
     CUDA_CHECK(cudaGetLastError());
 }
 
 void nhwc_f32_to_nchw(const float* src, int C, int rows, int W, float* dst, int* nonfinite,
                       cudaStream_t s) {
-    nhwc_to_nchw_kernel<float><<<grid_for((long long)rows * W * C, 256), 256, 0, s>>>(
+    launch_pdl(nhwc_to_nchw_kernel<float>, dim3(grid_for((long long)rows * W * C, 256)), dim3(256), 0, s, 1, 
         src, C, C, rows, W, dst, nonfinite);
     CUDA_CHECK(cudaGetLastError());
 }
 
 void crop_nchw_to_nhwc(const float* src, int C, int H, int W, int y0, int x0, int rows, int cols,
                        Elem e, void* dst, int ld, bool r, cudaStream_t s) {
-    DISPATCH(e, crop_kernel<T><<<grid_for((long long)rows * cols * C, 256), 256, 0, s>>>(
+    DISPATCH(e, launch_pdl(crop_kernel<T>, dim3(grid_for((long long)rows * cols * C, 256)), dim3(256), 0, s, 1, 
                     src, C, H, W, y0, x0, rows, cols, static_cast<T*>(dst), ld, r ? 1 : 0));
     CUDA_CHECK(cudaGetLastError());
 }
 
 void scatter_nhwc_to_nchw(const float* patch, int C, int rows, int cols, float* dst, int H, int W,
                           int y0, int x0, int* nonfinite, cudaStream_t s) {
-    scatter_patch_kernel<<<grid_for((long long)rows * cols * C, 256), 256, 0, s>>>(
+    launch_pdl(scatter_patch_kernel, dim3(grid_for((long long)rows * cols * C, 256)), dim3(256), 0, s, 1, 
         patch, C, rows, cols, dst, H, W, y0, x0, nonfinite);
     CUDA_CHECK(cudaGetLastError());
 }
 
 void f32_to_elem(const float* src, Elem e, void* dst, long long n, bool r, cudaStream_t s) {
-    DISPATCH(e, f32_to_elem_kernel<T><<<grid_for(n, 256), 256, 0, s>>>(src, static_cast<T*>(dst), n,
+    DISPATCH(e, launch_pdl(f32_to_elem_kernel<T>, dim3(grid_for(n, 256)), dim3(256), 0, s, 1, src, static_cast<T*>(dst), n,
                                                                        r ? 1 : 0));
     CUDA_CHECK(cudaGetLastError());
 }
 
 void elem_to_f32(Elem e, const void* src, float* dst, long long n, cudaStream_t s) {
-    DISPATCH(e, elem_to_f32_kernel<T><<<grid_for(n, 256), 256, 0, s>>>(static_cast<const T*>(src),
+    DISPATCH(e, launch_pdl(elem_to_f32_kernel<T>, dim3(grid_for(n, 256)), dim3(256), 0, s, 1, static_cast<const T*>(src),
                                                                        dst, n));
     CUDA_CHECK(cudaGetLastError());
 }

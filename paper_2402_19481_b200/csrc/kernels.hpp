@@ -36,10 +36,22 @@ struct GnCombine {
     int* err;   // set to 1 when a group's variance is negative
 };
 
-// y = GN(x) [-> SiLU] [+ temb[c]] [+ skip]  (fused GroupNorm / SiLU / AddTimeEmb / AddSkip)
+// Group statistics of a band written by a GroupNorm pass (the next layer's GroupNorm):
+// out[G][2] = (mean, mean_sq) of the stored values; partial >= gn_stats_blocks() * G * 2.
+struct GnStatsOut {
+    int G = 0;                      // 0: off
+    double count = 0;               // elements per group (channels/group * pixels)
+    double* partial = nullptr;
+    unsigned int* ticket = nullptr; // zero; reset by the last block
+    double* out = nullptr;
+};
+
+// y = GN(x) [-> SiLU] [+ temb[c]] [+ skip]  (fused GroupNorm / SiLU / AddTimeEmb / AddSkip),
+// optionally with the statistics of y for a following GroupNorm
 void gn_apply(Elem e, const void* x, void* y, long long pix, int C, int ld, int groups,
               const GnCombine& cb, const float* gamma, const float* beta, bool silu,
-              const float* temb, const void* skip, bool round_tf32, cudaStream_t s);
+              const float* temb, const void* skip, bool round_tf32, cudaStream_t s,
+              const GnStatsOut* out_stats = nullptr);
 
 // ---- pointwise (proj/src/tensor.cpp:297-334, model.cpp:278-298) ---------------------------
 void silu(Elem e, const void* x, void* y, long long n, bool round_tf32, cudaStream_t s);

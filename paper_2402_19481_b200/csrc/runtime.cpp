@@ -7,6 +7,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <set>
 #include <stdexcept>
@@ -394,7 +396,7 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
             } else if (d.kind == Kind::Linear) {
                 e2.bias = lw.bias;
                 plan_gemm(plans[gi][p], e, in.interior(eb), int(in.pix()), in.ld, in.ld, lw.w,
-                          d.out_ch, in.ld, e2, sc, sms);
+                          d.out_ch, in.ld, e2, sc, sms, 0, 0, /*b_static=*/true);
             } else if (d.kind == Kind::SelfAttn) {
                 const Region& ri = spec.layer_in[g.first];
                 const int ns = ri.full_h * ri.full_w;
@@ -917,12 +919,16 @@ void Runner::begin_profile() {
 
 void Runner::end_profile() {
     if (!o_.profile) return;
+    // PP_PROFILE_DUMP=<file>: append one line per timed launch (band, category, us, GFLOP)
+    static const char* dump_path = std::getenv("PP_PROFILE_DUMP");
+    FILE* dump = dump_path ? std::fopen(dump_path, "a") : nullptr;
     for (auto& b : bands_) {
         DeviceGuard g(b->dev);
         CUDA_CHECK(cudaStreamSynchronize(b->cs));
         for (const auto& t : b->timed) {
             float ms = 0;
             CUDA_CHECK(cudaEventElapsedTime(&ms, t.a, t.b));
+            if (dump) std::fprintf(dump, "%d %d %.3f %.4f\n", b->band, t.cat, ms * 1e3, t.flops * 1e-9);
             if (t.cat == CAT_CONV) {
                 prof_.conv_ms += ms;
                 prof_.conv_flops += t.flops;
@@ -940,6 +946,7 @@ void Runner::end_profile() {
         b->timed.clear();
         b->event_next = 0;
     }
+    if (dump) std::fclose(dump);
 }
 
 // Naive patch parallelism (step_naive, proj/src/runtime.cpp:398-452): even steps split the

@@ -28,6 +28,7 @@ SHAPES = [
     ("GEMM 8192x8192x8192", 0, 8192, 1, 8192, 8192),
 ]
 GN, FLUSH, NOCLUSTER = 1 << 20, 1 << 21, 1 << 30
+PAIR, SINGLE = 16, 32   # force_splits flag bits: CTA-pair / single-CTA kernel
 
 
 def flops(kind, m, w, k, n):
@@ -52,6 +53,9 @@ def main():
         tf = flops(kind, m, w, k, n) / (o[0] * 1e-3) / 1e12
         line = (f"{name:30s} {o[0] * 1e3:8.1f} us {tf:7.1f} TF/s  bn={int(o[1])} "
                 f"splits={int(o[2])} stages={int(o[3])} grid={int(o[4])}")
+        if kind != 0:
+            g = run(kind, m, w, k, n, reps=20 | GN)
+            line += f" | +gn {g[0] * 1e3:7.1f} us"
         if "--cluster" in sys.argv:
             g = run(kind, m, w, k, n, reps=20 | GN) if kind else o
             c1 = run(kind, m, w, k, n, reps=20 | NOCLUSTER)
@@ -72,6 +76,20 @@ def main():
                      f" | noEpi {ne[0] * 1e3:7.1f} us | mmaOnly {nb[0] * 1e3:7.1f} us"
                      f" | noEpi+Bonly {bo[0] * 1e3:7.1f} us | noEpi+Aonly {ao[0] * 1e3:7.1f} us")
         print(line, flush=True)
+        if "--cta" in sys.argv:
+            for cta, nm in ((SINGLE, "single"), (PAIR, "pair")):
+                for bn in (128, 160, 256):
+                    if n % bn:
+                        continue
+                    for sp in (1, 2):
+                        try:
+                            o = run(kind, m, w, k, n, sp | cta, bn)
+                        except Exception as e:  # noqa: BLE001
+                            print("   ", nm, bn, sp, "ERR", e)
+                            continue
+                        tf = flops(kind, m, w, k, n) / (o[0] * 1e-3) / 1e12
+                        print(f"    {nm:6s} bn={bn:3d} splits={sp}  {o[0] * 1e3:8.1f} us "
+                              f"{tf:7.1f} TF/s stages={int(o[3])} grid={int(o[4])}", flush=True)
         if sweep and kind != 0:
             for bn in (64, 128, 160, 256):
                 if n % bn:

@@ -9,6 +9,9 @@ from paper_2402_19481_b200 import _native as N  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
+# force_splits flag bits: run the CTA-pair (cta_group::2, M=256) or the single-CTA kernel
+PAIR, SINGLE = 16, 32
+
 
 def _p(t):
     return C.c_void_p(t.data_ptr()) if t is not None else None
@@ -33,23 +36,25 @@ def gemm(dtype, A, B, bias=None, splits=0, bn=0, out_f32=True):
 @pytest.mark.parametrize("M,Nn,K", [(128, 128, 64), (256, 320, 2880), (1000, 640, 576),
                                     (64, 16, 128), (1024, 1024, 1280), (128, 1280, 1024)])
 @pytest.mark.parametrize("splits", [0, 1, 3])
-def test_gemm_bf16(M, Nn, K, splits):
+@pytest.mark.parametrize("cta", [0, PAIR, SINGLE])
+def test_gemm_bf16(M, Nn, K, splits, cta):
     g = torch.Generator(device="cuda").manual_seed(M + Nn + K)
     A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
     B = torch.randn(Nn, K, device="cuda", generator=g).bfloat16()
     bias = torch.randn(Nn, device="cuda", generator=g)
-    D = gemm("bf16", A, B, bias, splits=splits)
+    D = gemm("bf16", A, B, bias, splits=splits | cta)
     ref = A.double() @ B.double().T + bias.double()
     err = (D.double() - ref).norm() / ref.norm()
     assert err < 1e-5, err
 
 
 @pytest.mark.parametrize("M,Nn,K", [(128, 128, 32), (300, 320, 288), (1024, 1024, 1280)])
-def test_gemm_tf32(M, Nn, K):
+@pytest.mark.parametrize("cta", [0, PAIR, SINGLE])
+def test_gemm_tf32(M, Nn, K, cta):
     g = torch.Generator(device="cuda").manual_seed(7)
     A = _tf32(torch.randn(M, K, device="cuda", generator=g))
     B = _tf32(torch.randn(Nn, K, device="cuda", generator=g))
-    D = gemm("fp32", A, B)
+    D = gemm("fp32", A, B, splits=cta)
     ref = A.double() @ B.double().T
     err = (D.double() - ref).norm() / ref.norm()
     assert err < 1e-5, err
@@ -87,7 +92,7 @@ def test_conv(rows, W, C, co, stride, dtype):
     orow = rows if stride == 1 else rows // 2
     ow = W if stride == 1 else W // 2
     out = torch.zeros(orow, ow, co, device="cuda", dtype=torch.float32)
-    for splits in (0, 2):
+    for splits in (0, 2, PAIR, PAIR | 2, SINGLE, SINGLE | 2):
         out.zero_()
         N.check(N.lib().pp_dev_conv(N.DTYPES[dtype], _p(inp), rows, W, C, stride, _p(wp), n_pad, co,
                                     _p(bias), _p(out), co, 1, None, 0, splits, 0, None))
