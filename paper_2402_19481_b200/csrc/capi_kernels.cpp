@@ -262,8 +262,8 @@ PP_API int pp_group_stats(int dtype, const float* x, int n, int c, int h, int w,
                         band[(size_t(yy - y0) * w + xx) * ld + ci] = x[((size_t(b) * c + ci) * h + yy) * w + xx];
             DevElems dx(band, e, false);
             const long long pix = (long long)(y1 - y0) * w;
-            pp::DeviceScratch part(size_t(pp::gn_stats_blocks(pix)) * groups * 16 + 16), tk(16), st(size_t(groups) * 16);
-            CUDA_CHECK(cudaMemset(tk.ptr, 0, 16));
+            pp::DeviceScratch part(size_t(pp::gn_stats_blocks(pix)) * groups * 16 + 16), tk(1024), st(size_t(groups) * 16);
+            CUDA_CHECK(cudaMemset(tk.ptr, 0, 1024));
             pp::gn_stats(e, dx.mem.ptr, pix, c, ld, groups, double(c / groups) * double(pix),
                          static_cast<double*>(part.ptr), static_cast<unsigned int*>(tk.ptr),
                          static_cast<double*>(st.ptr), 0);

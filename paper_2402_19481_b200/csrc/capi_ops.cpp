@@ -200,14 +200,14 @@ PP_API int pp_dev_gn_bench(int dtype, long long pix, int C, int G, int flags, in
         const pp::Elem e = pp::elem_of(dtype);
         const size_t eb = pp::elem_bytes(e);
         pp::DeviceScratch x(pix * C * eb), y(pix * C * eb), sk(pix * C * eb), st(G * 16),
-            gam(C * 4), bet(C * 4), te(C * 4), part(size_t(4) << 20), tick(64);
+            gam(C * 4), bet(C * 4), te(C * 4), part(size_t(4) << 20), tick(1024);
         CUDA_CHECK(cudaMemset(x.ptr, 0x3c, pix * C * eb));
         CUDA_CHECK(cudaMemset(sk.ptr, 0x3c, pix * C * eb));
         CUDA_CHECK(cudaMemset(gam.ptr, 0, C * 4));
         CUDA_CHECK(cudaMemset(bet.ptr, 0, C * 4));
         CUDA_CHECK(cudaMemset(te.ptr, 0, C * 4));
         CUDA_CHECK(cudaMemset(st.ptr, 0, G * 16));
-        CUDA_CHECK(cudaMemset(tick.ptr, 0, 64));
+        CUDA_CHECK(cudaMemset(tick.ptr, 0, 1024));
         pp::GnCombine cb{};
         cb.mode = 0;
         cb.fresh = static_cast<const double*>(st.ptr);
@@ -217,11 +217,21 @@ PP_API int pp_dev_gn_bench(int dtype, long long pix, int C, int G, int flags, in
         cudaEvent_t a, b;
         CUDA_CHECK(cudaEventCreate(&a));
         CUDA_CHECK(cudaEventCreate(&b));
+        pp::DeviceScratch st2(G * 16), tick2(1024);
+        CUDA_CHECK(cudaMemset(tick2.ptr, 0, 1024));
+        pp::GnStatsOut so;   // flags & 8: fused statistics of the output
+        if (flags & 8) {
+            so.G = G;
+            so.count = double(C / G) * double(pix);
+            so.partial = static_cast<double*>(part.ptr);
+            so.ticket = static_cast<unsigned int*>(tick2.ptr);
+            so.out = static_cast<double*>(st2.ptr);
+        }
         auto apply = [&] {
             pp::gn_apply(e, x.ptr, y.ptr, pix, C, C, G, cb, static_cast<const float*>(gam.ptr),
                          static_cast<const float*>(bet.ptr), flags & 1,
                          (flags & 2) ? static_cast<const float*>(te.ptr) : nullptr,
-                         (flags & 4) ? sk.ptr : nullptr, false, s);
+                         (flags & 4) ? sk.ptr : nullptr, false, s, &so);
         };
         auto stats = [&] {
             pp::gn_stats(e, x.ptr, pix, C, C, G, double(C / G) * double(pix),

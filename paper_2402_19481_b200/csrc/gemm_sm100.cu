@@ -541,17 +541,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (et == 0) st.flags[cur] = int(atomicAdd(ticket, 1u));
                 epi_bar();
                 const bool first = st.flags[cur] == 0;
-                float* part = a.partial + size_t(p) * a.n_pad + nbase;
+                // partial tile layout [block_n / 4][128 rows] of float4: for a fixed column
+                // quad the 32 lanes of a warp touch 512 contiguous bytes (coalesced)
+                float4* part = reinterpret_cast<float4*>(a.partial) +
+                               size_t(tile_id) * (kTileM / 4) * a.block_n + r;
                 if (first) {
                     for (int c0 = 0; c0 < a.block_n; c0 += 16) {
                         float v[16];
                         ptx::tmem_ld16(t_row + c0, v);
-                        if (valid) {
 #pragma unroll
-                            for (int j = 0; j < 16; j += 4)
-                                __stcg(reinterpret_cast<float4*>(part + c0 + j),
-                                       make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
-                        }
+                        for (int j = 0; j < 16; j += 4)
+                            __stcg(part + size_t((c0 + j) / 4) * kTileM,
+                                   make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
                     }
                     release(cur);
                     // publish: CTA barrier, then one gpu-scope fence + flag (the fence is
@@ -576,7 +577,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int j = 0; j < 64; j += 4) {
                             if (j < nc) {
-                                const float4 q = __ldcg(reinterpret_cast<const float4*>(part + cb + j));
+                                const float4 q = __ldcg(part + size_t((cb + j) / 4) * kTileM);
                                 o[j] = q.x; o[j + 1] = q.y; o[j + 2] = q.z; o[j + 3] = q.w;
                             }
                         }
@@ -796,7 +797,7 @@ int choose_kps(int block_n, bool gn, int pair) {
 // shared-memory bandwidth (TMA writes + MMA operand reads of a 128 x block_n tile); the
 // CTA pair halves the B bytes per SM.
 double tile_eff(int pair, int bn) {
-    if (pair) return bn >= 256 ? 0.90 : bn >= 160 ? 0.60 : bn >= 128 ? 0.35 : 0.27;
+    if (pair) return bn >= 256 ? 0.90 : bn >= 160 ? 0.64 : bn >= 128 ? 0.35 : 0.27;
     return bn >= 256 ? 0.75 : bn >= 160 ? 0.62 : bn >= 128 ? 0.36 : 0.28;
 }
 
@@ -869,7 +870,7 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
     a.k_blocks = k_blocks;
     a.n_pad = n_pad;
     splits = std::min(splits, 2);
-    if (splits > 1 && ((size_t)a.m_pix * n_pad * sizeof(float) > sc.ws_bytes ||
+    if (splits > 1 && ((size_t)m_tiles * kTileM * n_pad * sizeof(float) > sc.ws_bytes ||
                        2 * size_t(m_tiles) * a.n_tiles > sc.n_tickets))
         splits = 1;
     a.kps = choose_kps(bn, gn, pair);

@@ -99,7 +99,24 @@ __device__ void weighted_mean(const double* all, int n, const double* w, int G, 
 
 // The statistics a band normalises with (runtime.cpp:242-300 + corrected_gn_stats,
 // runtime.cpp:85-106); returns (mean, 1/sqrt(var + eps)).
-__device__ void gn_use_of(const GnCombine& cb, int G, int g, float& mu, float& inv, bool& neg) {
+__device__ __forceinline__ void gn_use_of_multi(const GnCombine& cb, int G, int g, float& mu,
+                                                float& inv, bool& neg);
+// Fast path: one band's own fresh statistics.
+__device__ __forceinline__ void gn_use_of(const GnCombine& cb, int G, int g, float& mu, float& inv,
+                                          bool& neg) {
+    if (cb.mode == GN_USE_LOCAL || (cb.mode == GN_USE_GLOBAL && cb.n == 1)) {
+        const double m = cb.fresh[g * 2], q = cb.fresh[g * 2 + 1];
+        const double var = __dsub_rn(q, __dmul_rn(m, m));
+        neg = var < 0.0;
+        mu = float(m);
+        inv = float(1.0 / sqrt(__dadd_rn(fmax(var, 0.0), double(cb.eps))));
+        return;
+    }
+    gn_use_of_multi(cb, G, g, mu, inv, neg);
+}
+
+__device__ __forceinline__ void gn_use_of_multi(const GnCombine& cb, int G, int g, float& mu,
+                                                float& inv, bool& neg) {
     double m = cb.fresh[g * 2], q = cb.fresh[g * 2 + 1];
     if (cb.mode == GN_USE_GLOBAL) {
         weighted_mean(cb.all_cur, cb.n, cb.weights, G, g, m, q);
@@ -135,10 +152,49 @@ __device__ void gn_use_of(const GnCombine& cb, int G, int g, float& mu, float& i
 // fixed-order fold by the last block -> deterministic.  gamma / beta are weights and are
 // loaded before griddepcontrol.wait; everything else after it.
 constexpr int kGnU = 4;         // pixels per thread (apply)
-constexpr int kGnUStats = 16;   // pixels per thread with statistics (fewer blocks to fold)
+constexpr int kGnUStats = 8;   // pixels per thread with statistics (fewer blocks to fold)
+
+constexpr int kGnRange = 32;   // blocks per first-level statistics fold
+
+// dst[g] = sum_{k < n} src[k * G + g] / div (double2 = (sum, sum_sq)), fixed order: thread
+// (part, g) sums k = part, part + parts, ...; the parts are added in order through smem
+// (scratch >= 2 * parts * G doubles).  Reads with ld.global.cg (partials of other blocks).
+__device__ void fold_fixed(const double2* src, int n, int G, double2* dst, double div, int tid,
+                           int nthr, double* scratch) {
+    const int parts = max(1, min(8, nthr / G));
+    if (tid < parts * G) {
+        const int g = tid % G, pt = tid / G;
+        double a = 0.0, b = 0.0;
+        for (int k0 = pt; k0 < n; k0 += 4 * parts) {
+            double2 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int k = k0 + u * parts;
+                v[u] = k < n ? __ldcg(src + size_t(k) * G + g) : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                a += v[u].x;
+                b += v[u].y;
+            }
+        }
+        scratch[(pt * G + g) * 2] = a;
+        scratch[(pt * G + g) * 2 + 1] = b;
+    }
+    __syncthreads();
+    for (int g = tid; g < G; g += nthr) {
+        double a = 0.0, b = 0.0;
+        for (int pt = 0; pt < parts; ++pt) {
+            a += scratch[(pt * G + g) * 2];
+            b += scratch[(pt * G + g) * 2 + 1];
+        }
+        dst[g] = make_double2(a / div, b / div);
+    }
+    __syncthreads();
+}
 
 template <class T, bool APPLY, bool STATS, int U>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, (STATS ? 2 : 3))
     gn_pass_kernel(const T* __restrict__ x, T* __restrict__ y, int pix, int C, int ld, int G,
                    const GnCombine cb, const float* __restrict__ gamma,
                    const float* __restrict__ beta, int do_silu, const float* __restrict__ temb,
@@ -155,7 +211,7 @@ __global__ void __launch_bounds__(256)
     const int cb0 = blockIdx.x * vx * VEC;    // first channel of this block
     const int bch = vx * VEC;                 // channels of this block
     const bool full = active && c0 + VEC <= C;
-    float sc[VEC], sh[VEC], tb[VEC], mu[VEC];
+    float sc[VEC], sh[VEC], tb[VEC];
     if (APPLY) {   // weights: safe to read before the previous kernel completes
         if (full) {
             load_vec<float>(gamma + c0, sc);
@@ -177,20 +233,6 @@ __global__ void __launch_bounds__(256)
     pdl_trigger();
     const int pstride = vy * gridDim.y;
     const int p_first = blockIdx.y * vy + ty;
-    // first round of loads in flight before the group coefficients are computed
-    const uint4* xv = reinterpret_cast<const uint4*>(x) + cv;
-    const uint4* sv = reinterpret_cast<const uint4*>(skip) + cv;
-    uint4 rx[U], rs[U];
-    if (active) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int pp = p_first + u * pstride;
-            if (pp < pix) {
-                rx[u] = __ldcs(xv + size_t(pp) * nvec);
-                if (APPLY && skip) rs[u] = __ldcs(sv + size_t(pp) * nvec);
-            }
-        }
-    }
     if (APPLY) {
         // (mean, 1/std) of the groups this block touches, one thread per group
         __shared__ float s_mi[2 * 1024];
@@ -220,10 +262,24 @@ __global__ void __launch_bounds__(256)
         }
         __syncthreads();
 #pragma unroll
-        for (int i = 0; i < VEC; ++i) {
+        for (int i = 0; i < VEC; ++i) {   // y = x * sc + sh  (sc = gamma / std, sh = beta - mean * sc)
             const int j = min(c0 + i, C - 1) / cpg - g_first;
-            mu[i] = s_mi[2 * j];
             sc[i] *= s_mi[2 * j + 1];
+            sh[i] = fmaf(-s_mi[2 * j], sc[i], sh[i]);
+        }
+    }
+    // first round of loads
+    const uint4* xv = reinterpret_cast<const uint4*>(x) + cv;
+    const uint4* sv = reinterpret_cast<const uint4*>(skip) + cv;
+    uint4 rx[U], rs[U];
+    if (active) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int pp = p_first + u * pstride;
+            if (pp < pix) {
+                rx[u] = __ldcs(xv + size_t(pp) * nvec);
+                if (APPLY && skip) rs[u] = __ldcs(sv + size_t(pp) * nvec);
+            }
         }
     }
     float ss[VEC], sq[VEC];
@@ -251,7 +307,7 @@ __global__ void __launch_bounds__(256)
                     float sk[VEC];
                     if (skip) load_vec<T>(reinterpret_cast<const T*>(&rs[u]), sk);
 #pragma unroll
-                    for (int i = 0; i < VEC; ++i) f[i] = (f[i] - mu[i]) * sc[i] + sh[i];
+                    for (int i = 0; i < VEC; ++i) f[i] = fmaf(f[i], sc[i], sh[i]);
                     if (do_silu) {
                         if constexpr (sizeof(T) == 2) {
                             // bf16 output: sigmoid(v) = 0.5 + 0.5 tanh(v / 2) with one packed
@@ -296,7 +352,9 @@ __global__ void __launch_bounds__(256)
     if (!STATS) return;
     // ---- block reduction: per channel over ty (fp64, fixed order), then per group
     __shared__ float r_s[256 * VEC], r_q[256 * VEC];
-    __shared__ double c_s[1024], c_q[1024];
+    __shared__ double c_sq2[2048];
+    double* c_s = c_sq2;
+    double* c_q = c_sq2 + 1024;
     __shared__ bool is_last;
 #pragma unroll
     for (int i = 0; i < VEC; ++i) {
@@ -326,53 +384,35 @@ __global__ void __launch_bounds__(256)
         }
         reinterpret_cast<double2*>(so.partial)[blk * Gs + g] = make_double2(a, b);
     }
+    // ---- two-level fixed-order fold: the last block of each range of kGnRange blocks (by
+    // block index) folds that range; the last range folder folds the range sums.  Counters:
+    // ticket[0] = ranges done, ticket[1 + r] = blocks of range r done (each reset by its folder).
+    const int nblk = gridDim.x * gridDim.y;
+    const int nrange = (nblk + kGnRange - 1) / kGnRange;
+    const int r = int(blk / kGnRange);
+    const int rsize = min(kGnRange, nblk - r * kGnRange);
+    double2* part1 = reinterpret_cast<double2*>(so.partial);
+    double2* part2 = part1 + size_t(nblk) * Gs;
     __syncthreads();
     if (tid == 0) {
         __threadfence();
-        const unsigned nb = gridDim.x * gridDim.y;
-        is_last = atomicAdd(so.ticket, 1u) == nb - 1;
+        is_last = atomicAdd(so.ticket + 1 + r, 1u) == unsigned(rsize - 1);
         if (is_last) __threadfence();
     }
     __syncthreads();
     if (!is_last) return;
-    // ---- last block: fold the per-block partials, P lanes per group, fixed order (full
-    // warps only, so the xor-shuffles never name a missing lane)
-    const int nblk = gridDim.x * gridDim.y;
-    const int nfull = (nthr / 32) * 32;
-    if (tid < nfull) {
-        int P = 1;
-        while (P * 2 <= 32 && P * 2 * Gs <= nfull) P *= 2;
-        for (int base = 0; base < Gs * P; base += nfull) {
-            const int w = base + tid;
-            const int g = w / P, part = w % P;
-            double a = 0.0, b = 0.0;
-            if (g < Gs) {
-                for (int k0 = part; k0 < nblk; k0 += 8 * P) {
-                    double2 v[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int k = k0 + u * P;
-                        v[u] = k < nblk ? __ldcg(reinterpret_cast<const double2*>(so.partial) +
-                                                 size_t(k) * Gs + g)
-                                        : make_double2(0.0, 0.0);
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        a += v[u].x;
-                        b += v[u].y;
-                    }
-                }
-            }
-            for (int o = P / 2; o; o >>= 1) {
-                a += __shfl_xor_sync(0xffffffffu, a, o);
-                b += __shfl_xor_sync(0xffffffffu, b, o);
-            }
-            if (g < Gs && part == 0) {
-                so.out[g * 2] = a / so.count;
-                so.out[g * 2 + 1] = b / so.count;
-            }
-        }
+    fold_fixed(part1 + size_t(r) * kGnRange * Gs, rsize, Gs, part2 + size_t(r) * Gs, 1.0, tid, nthr,
+               c_s);
+    if (tid == 0) so.ticket[1 + r] = 0u;
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        is_last = atomicAdd(so.ticket, 1u) == unsigned(nrange - 1);
+        if (is_last) __threadfence();
     }
+    __syncthreads();
+    if (!is_last) return;
+    fold_fixed(part2, nrange, Gs, reinterpret_cast<double2*>(so.out), so.count, tid, nthr, c_s);
     if (tid == 0) *so.ticket = 0u;
 }
 
@@ -709,7 +749,8 @@ GnShape gn_shape(Elem e, long long pix, int ld, int U) {
     return {dim3(gx, gy), dim3(vx, vy)};
 }
 
-int gn_stats_blocks(long long) { return 1184 + 1184; }   // >= gx * gy of every gn_shape
+// >= gx * gy of every gn_shape, plus the second-level range sums
+int gn_stats_blocks(long long) { return 1184 + 1184 + 80; }
 
 void gn_stats(Elem e, const void* x, long long pix, int C, int ld, int groups, double count,
               double* partial, unsigned int* ticket, double* out, cudaStream_t s) {

@@ -310,7 +310,7 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
         }
     }
     gn_partial = static_cast<double*>(alloc(gn_blocks * 2 * 8));
-    gn_ticket = static_cast<unsigned int*>(alloc(16));
+    gn_ticket = static_cast<unsigned int*>(alloc(1024));   // fold counters (kernels.cu)
     n_temb = int(tl.size());
     if (n_temb) {
         temb_dev = static_cast<TembLayer*>(alloc(tl.size() * sizeof(TembLayer)));
@@ -413,6 +413,14 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
             }
         }
         if (fuse_gn) fused_stats[next] = 1;
+    }
+    // a GroupNorm group whose output feeds another GroupNorm (the head GN after the last
+    // res block) computes that GroupNorm's statistics in the same pass
+    for (const Group& g : groups) {
+        const int next = g.last + 1;
+        if (g.kind == Kind::GroupNorm && next < L - 1 && m->layers[next].kind == Kind::GroupNorm &&
+            m->layers[g.first].out_ch % m->layers[next].groups == 0)
+            fused_stats[next] = 2;
     }
     set_profile(profile);
     CUDA_CHECK(cudaDeviceSynchronize());
@@ -577,11 +585,21 @@ void Program::gn_apply(const Group& g, int mode, int par_cur, int par_prev) {
     cb.weights = x.weights;
     cb.eps = d.eps;
     cb.err = flags + 1;
+    GnStatsOut so;
+    const int next = g.last + 1;
+    if (next < L && fused_stats[next] == 2) {
+        const Layer& dn = m->layers[next];
+        so.G = dn.groups;
+        so.count = double(in.C / dn.groups) * double(in.rows) * double(in.w);
+        so.partial = gn_partial;
+        so.ticket = gn_ticket;
+        so.out = lx[next].stats[par_cur] + size_t(band) * dn.groups * 2;
+    }
     run_timed(CAT_GN, 0, [&] {
         const Act& out = act[g.last];
         pp::gn_apply(e, in.interior(eb), out.interior(eb), in.pix(), in.C, in.ld, d.groups, cb,
                      lw.gamma, lw.beta, g.silu, g.temb >= 0 ? temb_ptr(g.temb) : nullptr,
-                     g.skip >= 0 ? act[g.skip].interior(eb) : nullptr, rnd, cs);
+                     g.skip >= 0 ? act[g.skip].interior(eb) : nullptr, rnd, cs, &so);
     });
     count(1);
 }
