@@ -69,9 +69,9 @@ struct Scratch {
     pp::DeviceScratch ws, tk, gp, gt;
     pp::GemmScratch sc;
     explicit Scratch(size_t ws_bytes)
-        : ws(ws_bytes), tk(size_t(1) << 20), gp(size_t(1) << 20), gt(64) {
+        : ws(ws_bytes), tk(size_t(1) << 20), gp(size_t(1) << 20), gt(1024) {
         CUDA_CHECK(cudaMemset(tk.ptr, 0, size_t(1) << 20));
-        CUDA_CHECK(cudaMemset(gt.ptr, 0, 64));
+        CUDA_CHECK(cudaMemset(gt.ptr, 0, 1024));
         sc.ws = static_cast<float*>(ws.ptr);
         sc.ws_bytes = ws_bytes;
         sc.tickets = static_cast<unsigned int*>(tk.ptr);

@@ -128,9 +128,9 @@ PP_API int pp_dev_gemm_bench(int dtype, int kind, int M_or_rows, int W, int K, i
         ep.out = D.ptr;
         ep.out_ld = n_pad;
         ep.n_valid = N;
-        pp::DeviceScratch gp(size_t(1) << 22), gt(64), go(32 * 16);
+        pp::DeviceScratch gp(size_t(1) << 22), gt(1024), go(32 * 16);
         if (gn) {
-            CUDA_CHECK(cudaMemset(gt.ptr, 0, 64));
+            CUDA_CHECK(cudaMemset(gt.ptr, 0, 1024));
             sc.gn_part = static_cast<double*>(gp.ptr);
             sc.gn_part_len = (size_t(1) << 22) / 8;
             sc.gn_ticket = static_cast<unsigned int*>(gt.ptr);

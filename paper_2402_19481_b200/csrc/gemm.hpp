@@ -58,10 +58,11 @@ struct GemmArgs {
     int gn_groups, gn_cpg;
     double gn_count;          // elements per group (cpg * pixels)
     double* gn_part;          // [m_tiles][groups][2]
-    unsigned int* gn_ticket;  // zero, reset by the last tile
+    unsigned int* gn_ticket;  // [1 + n_tiles] zeroed counters, each reset by its folder
     double* gn_out;           // [groups][2] = (mean, mean_sq)
     const void* b_base;       // B tensor (weights) and its size: with b_static, every CTA
     long long b_bytes;        // prefetches its 1/grid slice into L2 at kernel start
+    int tma_store;            // 1: the CTA's last tile is stored through tmD (smem staging)
     int b_static;             // 1: B is weights (not written by an earlier kernel on the stream):
                               //    its first boxes are prefetched before griddepcontrol.wait
     int debug;                // micro-benchmarks only: bit0 = no MMA, bit1 = no TMA loads
@@ -70,6 +71,7 @@ struct GemmArgs {
 struct GemmPlan {
     CUtensorMap tmA;
     CUtensorMap tmB;
+    CUtensorMap tmD;          // output (TMA-store epilogue)
     GemmArgs a;
     int grid = 0;
     size_t smem = 0;
@@ -101,7 +103,7 @@ struct GemmScratch {
     size_t n_tickets = 0;
     double* gn_part = nullptr;         // >= max m_tiles * groups * 2
     size_t gn_part_len = 0;
-    unsigned int* gn_ticket = nullptr; // one zeroed counter
+    unsigned int* gn_ticket = nullptr; // zeroed counters: [1 + N tiles] (>= 256)
 };
 
 // Conv over a halo-padded NHWC band: in = [rows_in + 2][W][C_in_pad] (row 0 = the halo

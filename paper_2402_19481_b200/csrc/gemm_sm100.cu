@@ -78,10 +78,12 @@ __host__ __device__ inline size_t tail_bytes(int stages, bool gn, int block_n) {
 }
 
 // Final values of one 16-column chunk of one row: bias, residual, store, GN sums.
+// srow != nullptr: the row goes to the smem staging tile (dense [row][block_n], stored later
+// by one TMA box) instead of straight to global memory.
 template <bool kTF32>
 __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const float* sbias,
                                              int c0, int n0, long long p, bool valid,
-                                             float* sgn_warp, int lane) {
+                                             float* sgn_warp, int lane, uint8_t* srow) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = v[j] * a.scale + sbias[c0 + j];
     const bool full = n0 + 16 <= a.n_valid;
@@ -101,7 +103,11 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
                         v[j] = round_tf32(v[j]); v[j + 1] = round_tf32(v[j + 1]);
                         v[j + 2] = round_tf32(v[j + 2]); v[j + 3] = round_tf32(v[j + 3]);
                     }
-                    *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                    const float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                    if (srow)
+                        *reinterpret_cast<float4*>(srow + (c0 + j) * 4) = o;
+                    else
+                        *reinterpret_cast<float4*>(dst + j) = o;
                 }
             } else {
 #pragma unroll
@@ -109,11 +115,17 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
                     if (n0 + j < a.n_valid) {
                         float o = v[j] + (res ? res[j] : 0.0f);
                         o = a.round_tf32 ? round_tf32(o) : o;
-                        dst[j] = o;
+                        if (!srow) dst[j] = o;
                         v[j] = o;
                     } else {
                         v[j] = 0.0f;
                     }
+                }
+                if (srow) {
+#pragma unroll
+                    for (int j = 0; j < 16; j += 4)
+                        *reinterpret_cast<float4*>(srow + (c0 + j) * 4) =
+                            make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                 }
             }
         } else {
@@ -143,7 +155,10 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
                         v[j + 2 * i] = back.x;
                         v[j + 2 * i + 1] = back.y;
                     }
-                    *reinterpret_cast<uint4*>(dst + j) = o;
+                    if (srow)
+                        *reinterpret_cast<uint4*>(srow + (c0 + j) * 2) = o;
+                    else
+                        *reinterpret_cast<uint4*>(dst + j) = o;
                 }
             } else {
 #pragma unroll
@@ -151,10 +166,21 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
                     if (n0 + j < a.n_valid) {
                         float o = v[j] + (res ? __bfloat162float(res[j]) : 0.0f);
                         const __nv_bfloat16 b = __float2bfloat16(o);
-                        dst[j] = b;
+                        if (!srow) dst[j] = b;
                         v[j] = __bfloat162float(b);
                     } else {
                         v[j] = 0.0f;
+                    }
+                }
+                if (srow) {
+#pragma unroll
+                    for (int j = 0; j < 16; j += 8) {
+                        uint4 o;
+                        __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            o2[i] = __floats2bfloat162_rn(v[j + 2 * i], v[j + 2 * i + 1]);
+                        *reinterpret_cast<uint4*>(srow + (c0 + j) * 2) = o;
                     }
                 }
             }
@@ -203,7 +229,7 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
 template <bool kTF32, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const GemmArgs a) {
+                const __grid_constant__ CUtensorMap tmD, const GemmArgs a) {
     constexpr int P = kPair ? 2 : 1;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -235,6 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
+        if (a.tma_store) ptx::prefetch_tmap(&tmD);
         for (int s = 0; s < stages; ++s) {
             ptx::mbar_init(&st.full_bar[s], 1);
             ptx::mbar_init(&st.empty_bar[s], 1);
@@ -480,8 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int quarter = warp & 3;
         const int r = quarter * 32 + lane;  // tile row owned by this thread
         const int et = threadIdx.x - 64;    // 0..127
-        float* sgn_warp = st.gn + quarter * 2 * a.block_n;
-        const int final_tiles = m_tiles * a.n_tiles;
+        float* sgn_warp = st.gn + quarter * 2 * a.block_n;   // [block_n / cpg][2] used
         // accumulator release: the MMA issuer (the leader's, for a pair) waits for 4*P warps
         const uint32_t tempty_leader = kPair ? ptx::mapa(ptx::smem_u32(st.tempty_bar), 0) : 0u;
         auto release = [&](int which) {
@@ -519,6 +545,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             const int nbase = tc.nt * a.block_n;
             float* sbias = st.bias + cur * a.block_n;
+            // the CTA's last tile: the smem ring is idle once its accumulator is full, so the
+            // output tile is staged there and written by one TMA box (coalesced) instead of
+            // 128 per-thread row stores
+            const bool stage_out = a.tma_store && t + tile_step >= total_tiles;
+            const int eb_out = (kTF32 || a.out_f32) ? 4 : 2;
+            uint8_t* srow = stage_out ? smem + size_t(r) * a.block_n * eb_out : nullptr;
             for (int c = et; c < a.block_n; c += 128)
                 sbias[c] = (a.bias && nbase + c < a.n_valid) ? a.bias[nbase + c] : 0.0f;
             ptx::mbar_wait(&st.tfull_bar[cur], cur_phase);
@@ -592,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 for (int j = 0; j < 16; ++j) v[j] = v[j] + o[c1 + j];
                             }
                             finish_chunk<kTF32>(a, v, sbias, cb + c1, nbase + cb + c1, p, valid,
-                                                sgn_warp, lane);
+                                                sgn_warp, lane, srow);
                         }
                     }
                 }
@@ -605,15 +637,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int c0 = 0; c0 < a.block_n; c0 += 16) {
                     float v[16];
                     ptx::tmem_ld16(t_row + c0, v);
-                    finish_chunk<kTF32>(a, v, sbias, c0, nbase + c0, p, valid, sgn_warp, lane);
+                    finish_chunk<kTF32>(a, v, sbias, c0, nbase + c0, p, valid, sgn_warp, lane, srow);
                 }
                 release(cur);
+            }
+            if (stage_out) {
+                ptx::fence_proxy_async();   // staged rows -> visible to the TMA engine
+                epi_bar();
+                if (et == 0) {
+                    if (conv)
+                        ptx::tma_store_3d(&tmD, smem, nbase, tc.tx * a.w_box, tc.ty * a.rows_box);
+                    else
+                        ptx::tma_store_2d(&tmD, smem, nbase, tc.ty * kTileM);
+                    ptx::bulk_commit();
+                    ptx::bulk_wait_all();
+                }
             }
             if (a.gn_groups) {
                 epi_bar();
                 const int cpg = a.gn_cpg;
                 const int g0 = nbase / cpg;
-                const int gn_here = min(a.block_n, a.n_valid - nbase) / cpg;
+                const int gn_here = a.block_n / cpg;
                 // 8 threads per group: lane sub of the 8 sums the (warp, column) entries
                 // e = sub, sub + 8, ... of the group's 4 * cpg column sums, then a fixed
                 // xor-tree over the 8 lanes -> deterministic, short dependency chains.
@@ -640,63 +684,53 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 epi_bar();
+                // the last M tile of this N tile folds the N tile's groups (the N tiles fold
+                // disjoint groups in parallel); counter gn_ticket[1 + nt]
                 if (et == 0) {
                     __threadfence();   // cumulative over the partials stored before the barrier
-                    const bool last = atomicAdd(a.gn_ticket, 1u) == unsigned(final_tiles - 1);
+                    const bool last = atomicAdd(a.gn_ticket + 1 + tc.nt, 1u) == unsigned(m_tiles - 1);
                     if (last) __threadfence();
                     st.flags[2] = last;
                 }
                 epi_bar();
                 if (st.flags[2]) {
-                    // last tile of the GEMM: fold the per-m-tile partials.  P threads per
-                    // group each sum a fixed residue class of m-tiles (16 loads in flight),
-                    // then one thread adds the P partials in order -> deterministic.
-                    const int m_tiles = a.tiles_y * a.tiles_x;
+                    // P threads per group each sum a fixed residue class of M tiles (16 loads
+                    // in flight), the P partials are added in order -> deterministic
                     const int G = a.gn_groups;
-                    // sfold = [P][G][2] doubles in the GN scratch (32 * block_n bytes)
-                    const int cap = 2 * a.block_n;
-                    int P = G >= 128 ? 1 : 128 / G;
-                    while (P > 1 && P * G > cap) P >>= 1;
-                    const bool in_smem = P * G <= cap;
-                    double* sfold = reinterpret_cast<double*>(st.gn);
-                    for (int w = et; w < G * P; w += 128) {
-                        const int g = w % G, part = w / G;
+                    int P = 1;
+                    while (P * 2 * gn_here <= 128 && P * 2 * gn_here <= 2 * a.block_n) P *= 2;
+                    double* sfold = reinterpret_cast<double*>(st.gn);   // [P][gn_here][2]
+                    if (et < P * gn_here) {
+                        const int gl = et % gn_here, part = et / gn_here;
+                        const double2* src = reinterpret_cast<const double2*>(a.gn_part) + g0 + gl;
                         double s = 0.0, q = 0.0;
                         for (int m0 = part; m0 < m_tiles; m0 += 16 * P) {
-                            double ls[16], lq[16];
+                            double2 v[16];
 #pragma unroll
                             for (int u = 0; u < 16; ++u) {
                                 const int m = m0 + u * P;
-                                ls[u] = m < m_tiles ? __ldcg(a.gn_part + ((size_t)m * G + g) * 2) : 0.0;
-                                lq[u] = m < m_tiles ? __ldcg(a.gn_part + ((size_t)m * G + g) * 2 + 1) : 0.0;
+                                v[u] = m < m_tiles ? __ldcg(src + (size_t)m * G) : make_double2(0.0, 0.0);
                             }
 #pragma unroll
                             for (int u = 0; u < 16; ++u) {
-                                s += ls[u];
-                                q += lq[u];
+                                s += v[u].x;
+                                q += v[u].y;
                             }
                         }
-                        if (in_smem) {
-                            sfold[(part * G + g) * 2] = s;
-                            sfold[(part * G + g) * 2 + 1] = q;
-                        } else {
-                            a.gn_out[g * 2] = s / a.gn_count;   // P == 1
-                            a.gn_out[g * 2 + 1] = q / a.gn_count;
-                        }
+                        sfold[(part * gn_here + gl) * 2] = s;
+                        sfold[(part * gn_here + gl) * 2 + 1] = q;
                     }
                     epi_bar();
-                    if (in_smem) {
-                        for (int g = et; g < G; g += 128) {
-                            double s = 0.0, q = 0.0;
-                            for (int part = 0; part < P; ++part) {
-                                s += sfold[(part * G + g) * 2];
-                                q += sfold[(part * G + g) * 2 + 1];
-                            }
-                            a.gn_out[g * 2] = s / a.gn_count;
-                            a.gn_out[g * 2 + 1] = q / a.gn_count;
+                    for (int gl = et; gl < gn_here; gl += 128) {
+                        double s = 0.0, q = 0.0;
+                        for (int part = 0; part < P; ++part) {
+                            s += sfold[(part * gn_here + gl) * 2];
+                            q += sfold[(part * gn_here + gl) * 2 + 1];
                         }
+                        a.gn_out[(g0 + gl) * 2] = s / a.gn_count;
+                        a.gn_out[(g0 + gl) * 2 + 1] = q / a.gn_count;
                     }
-                    if (et == 0) *a.gn_ticket = 0u;
+                    if (et == 0) a.gn_ticket[1 + tc.nt] = 0u;
                     epi_bar();
                 }
             }
@@ -756,6 +790,40 @@ void encode_b(CUtensorMap* m, Elem e, const void* base, int rows, int K, long lo
     uint64_t st[2] = {uint64_t(ld) * eb, uint64_t(kBlockBytes)};
     uint32_t b[3] = {uint32_t(kel), uint32_t(box_rows), uint32_t(kps)};
     encode(m, e, 3, base, d, st, b);
+}
+
+// Output map for the TMA-store epilogue (no swizzle): rank 2/3, dims/strides as given.
+void encode_plain(CUtensorMap* m, bool f32, int rank, const void* base, const uint64_t* dims,
+                  const uint64_t* strides_bytes, const uint32_t* box) {
+    uint32_t estr[5] = {1, 1, 1, 1, 1};
+    const CUresult r = get_encode()(
+        m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank,
+        const_cast<void*>(base), dims, strides_bytes, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw std::runtime_error("cuTensorMapEncodeTiled (output) failed (" + std::to_string(int(r)) + ")");
+}
+
+// Enable the TMA-store epilogue when the output rows are 16-byte aligned.
+void plan_output_map(GemmPlan& p, bool conv) {
+    GemmArgs& a = p.a;
+    const bool f32 = p.elem == Elem::F32 || a.out_f32;
+    const uint64_t eb = f32 ? 4 : 2;
+    a.tma_store = 0;
+    if (std::getenv("PP_NO_TMA_STORE")) return;
+    if ((uint64_t(a.out_ld) * eb) % 16 || (reinterpret_cast<uintptr_t>(a.out) % 16)) return;
+    if (conv) {
+        uint64_t d[3] = {uint64_t(a.n_valid), uint64_t(a.out_w), uint64_t(a.out_rows)};
+        uint64_t st[2] = {uint64_t(a.out_ld) * eb, uint64_t(a.out_w) * a.out_ld * eb};
+        uint32_t b[3] = {uint32_t(a.block_n), uint32_t(a.w_box), uint32_t(a.rows_box)};
+        encode_plain(&p.tmD, f32, 3, a.out, d, st, b);
+    } else {
+        uint64_t d[2] = {uint64_t(a.n_valid), uint64_t(a.out_rows)};
+        uint64_t st[1] = {uint64_t(a.out_ld) * eb};
+        uint32_t b[2] = {uint32_t(a.block_n), uint32_t(kTileM)};
+        encode_plain(&p.tmD, f32, 2, a.out, d, st, b);
+    }
+    a.tma_store = 1;
 }
 
 uint32_t make_idesc(Elem e, int n, int m) {
@@ -969,6 +1037,7 @@ void plan_conv(GemmPlan& p, Elem e, const void* in, int rows_in, int W, int C_in
              a.kps);
     p.flops = 2.0 * a.m_pix * double(ep.n_valid) * 9.0 * C_in_pad;
     a.b_static = 1;   // conv weights
+    plan_output_map(p, true);
     a.b_base = weights;
     a.b_bytes = (long long)n_pad * 9 * C_in_pad * (long long)eb;
 }
@@ -1000,6 +1069,7 @@ void plan_gemm(GemmPlan& p, Elem e, const void* A, int M, int K, long long lda, 
     encode_b(&p.tmB, e, B, N, K, ldb, a.block_n / (p.pair ? 2 : 1), a.kps);
     p.flops = 2.0 * double(M) * N * K;
     a.b_static = b_static ? 1 : 0;
+    plan_output_map(p, false);
     a.b_base = B;
     a.b_bytes = b_static ? ((long long)(N - 1) * ldb + K) * (long long)eb / 16 * 16 : 0;
 }
@@ -1020,7 +1090,7 @@ void launch_variant(const GemmPlan& p, cudaStream_t s) {
         }
     }
     launch_pdl(gemm_kernel<kTF32, kPair>, dim3(p.grid), dim3(kThreads), p.smem, s, kPair ? 2 : 1,
-               p.tmA, p.tmB, p.a);
+               p.tmA, p.tmB, p.tmD, p.a);
 }
 
 void launch_gemm(const GemmPlan& p, cudaStream_t s) {

@@ -329,7 +329,7 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
     sc.tickets = static_cast<unsigned int*>(alloc(sc.n_tickets * 4));
     sc.gn_part_len = size_t(max_pix / 32 + 64) * max_groups * 2;
     sc.gn_part = static_cast<double*>(alloc(sc.gn_part_len * 8));
-    sc.gn_ticket = static_cast<unsigned int*>(alloc(16));
+    sc.gn_ticket = static_cast<unsigned int*>(alloc(1024));   // 1 + N tiles counters
     fused_stats.assign(L, 0);
 
     // attention scratch (one SelfAttn geometry per model)
