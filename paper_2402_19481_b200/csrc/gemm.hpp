@@ -33,12 +33,14 @@ struct GemmArgs {
     int rows_box, w_box;      // conv: output rows / cols covered by one 128-row M tile
     int tiles_y, tiles_x;     // M-tile grid (plain: tiles_y = ceil(M/128), tiles_x = 1)
     int out_rows, out_w;      // valid output extent in pixels (plain: M, 1)
-    int n_tiles, block_n;     // N tiling (block_n % 16 == 0, <= 256)
+    int n_tiles, block_n;     // N tiling (block_n % 16 == 0, <= 256; <= 512 as two N halves)
     int cin_chunks;           // conv: channel chunks of 128 B per tap; plain: k_blocks
     int k_blocks;             // total 128-byte K blocks
     int splits, kb_per_split; // split-K
     int stages;               // smem pipeline depth
     int kps;                  // 128-byte K blocks per pipeline stage (1 or 2)
+    int n_sub;                // MMAs per K step along N (2: block_n > 256, N = block_n / 2 each)
+    int n_acc;                // TMEM accumulators in the MMA <-> epilogue ring (1 or 2)
     uint32_t idesc;           // tcgen05 instruction descriptor
     // epilogue
     void* out;                // output base (already offset to pixel 0 of the band)

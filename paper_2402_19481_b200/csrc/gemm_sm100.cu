@@ -77,6 +77,25 @@ __host__ __device__ inline size_t tail_bytes(int stages, bool gn, int block_n) {
            (gn ? size_t(4) * block_n * 2 * 4 : 0);
 }
 
+// B box(es) of one stage.  A CTA stages block_n / P / n_sub weight rows per N half: for a
+// wide tile (n_sub == 2) the halves are separate boxes (TMA box dims are <= 256) landing
+// (rows * kps) slots apart; in a CTA pair each CTA loads its share (rank) of every half.
+// bcoord = first weight row of this CTA's share of half 0.  kPair: complete_tx on the
+// leader's barrier (shared::cluster address bar_cl), else on the local barrier bar.
+template <bool kPair>
+__device__ __forceinline__ void load_b(uint8_t* sb, const CUtensorMap* tm, uint64_t* bar,
+                                       uint32_t bar_cl, int bcoord, int kb, const GemmArgs& a) {
+    const int hrow = a.block_n / a.n_sub;                 // weight rows per N half
+    const int brows = hrow / (kPair ? 2 : 1);             // rows this CTA stages per half
+    for (int h = 0; h < a.n_sub; ++h) {
+        uint8_t* dst = sb + size_t(h) * brows * kBlockBytes * a.kps;
+        if (kPair)
+            ptx::tma_load_3d_pair(dst, tm, bar_cl, 0, bcoord + h * hrow, kb);
+        else
+            ptx::tma_load_3d(dst, tm, bar, 0, bcoord + h * hrow, kb);
+    }
+}
+
 // Final values of one 16-column chunk of one row: bias, residual, store, GN sums.
 // srow != nullptr: the row goes to the smem staging tile (dense [row][block_n], stored later
 // by one TMA box) instead of straight to global memory.
@@ -316,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int kb0 = tc.split * a.kb_per_split;
             const int kb1 = min(kb0 + a.kb_per_split, a.k_blocks);
             pre = min(stages, (kb1 - kb0 + kps - 1) / kps);
-            const int bcoord = tc.nt * a.block_n + rank * (a.block_n / P);
+            const int bcoord = tc.nt * a.block_n + rank * (a.block_n / a.n_sub / P);
             for (int i = pw; i < pre; i += 2) {
                 if (ptx::elect_one()) {
                     uint8_t* sb = smem + size_t(i) * stage_bytes + a_stage_bytes;
@@ -324,11 +343,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (rank == 0)
                         ptx::mbar_arrive_expect_tx(&st.full_bar[i],
                                                    P * (nk * a_box_bytes + b_stage_bytes));
-                    if (kPair)
-                        ptx::tma_load_3d_pair(sb, &tmB, full_leader + uint32_t(i) * 8u, 0, bcoord,
-                                              kb0 + i * kps);
-                    else
-                        ptx::tma_load_3d(sb, &tmB, &st.full_bar[i], 0, bcoord, kb0 + i * kps);
+                    load_b<kPair>(sb, &tmB, &st.full_bar[i], full_leader + uint32_t(i) * 8u, bcoord,
+                                  kb0 + i * kps, a);
                 }
                 __syncwarp();
             }
@@ -355,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int kb0 = tc.split * a.kb_per_split;
             const int kb1 = min(kb0 + a.kb_per_split, a.k_blocks);
             const int oy0 = tc.ty * a.rows_box, ox0 = tc.tx * a.w_box;
-            const int bcoord = tc.nt * a.block_n + rank * (a.block_n / P);
+            const int bcoord = tc.nt * a.block_n + rank * (a.block_n / a.n_sub / P);
             const int arow = tc.ty * kTileM;
             // conv K position of block kb0: tap (ky, kx), channel chunk cj
             int cj = kb0 % a.cin_chunks;
@@ -406,10 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 }
                             }
                             if (!b_done) {
-                                if (kPair)
-                                    ptx::tma_load_3d_pair(sb, &tmB, fb, 0, bcoord, kb);
-                                else
-                                    ptx::tma_load_3d(sb, &tmB, &st.full_bar[stage], 0, bcoord, kb);
+                                load_b<kPair>(sb, &tmB, &st.full_bar[stage], fb, bcoord, kb, a);
                             }
                         }
                     }
@@ -441,6 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t desc_b0 = ptx::smem_desc_sw128(smem0 + a_stage_bytes);
         const uint64_t desc_stride = stage_bytes >> 4;
         const uint64_t a_next = a_slot >> 4, b_next = b_slot >> 4;
+        const uint32_t b_half = uint32_t(a.block_n / 2 / P) * kBlockBytes;   // n_sub == 2
         int stage = 0;
         uint32_t phase = 0;
         int acc = 0;
@@ -459,7 +473,28 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint64_t da = desc_a0 + uint64_t(stage) * desc_stride;
                 const uint64_t db = desc_b0 + uint64_t(stage) * desc_stride;
                 if (ptx::elect_one()) {
-                    if (!(a.debug & 1)) {
+                    if (!(a.debug & 1) && a.n_sub == 2) {
+                        // wide tile (block_n > 256): two N halves per K step, each an MMA of
+                        // N = block_n / 2 into its own TMEM column range, sharing the A tile
+                        const uint32_t acc0 = kb > kb0 ? 1u : 0u;
+                        const uint64_t bh = uint64_t(b_half) >> 4;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const uint32_t dh = d_tmem + uint32_t(h * (a.block_n / 2));
+                            if (kPair) {
+                                if (kTF32)
+                                    ptx::mma4_tf32_pair(dh, da, db + h * bh, a.idesc, acc0);
+                                else
+                                    ptx::mma4_bf16_pair(dh, da, db + h * bh, a.idesc, acc0);
+                            } else if (kTF32) {
+                                ptx::mma4_tf32(dh, da, db + h * bh, a.idesc, acc0);
+                                if (two) ptx::mma4_tf32(dh, da + a_next, db + b_next + h * bh, a.idesc, 1u);
+                            } else {
+                                ptx::mma4_bf16(dh, da, db + h * bh, a.idesc, acc0);
+                                if (two) ptx::mma4_bf16(dh, da + a_next, db + b_next + h * bh, a.idesc, 1u);
+                            }
+                        }
+                    } else if (!(a.debug & 1)) {
                         const uint32_t acc0 = kb > kb0 ? 1u : 0u;
                         if (kPair) {
                             if (kTF32) {
@@ -497,7 +532,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mma_commit(&st.tfull_bar[acc]);
             }
             __syncwarp();
-            if (++acc == 2) {
+            if (++acc == a.n_acc) {
                 acc = 0;
                 acc_phase ^= 1;
             }
@@ -525,7 +560,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = tile0; t < total_tiles; t += tile_step) {
             const int cur = acc;
             const uint32_t cur_phase = acc_phase;
-            if (++acc == 2) {
+            if (++acc == a.n_acc) {
                 acc = 0;
                 acc_phase ^= 1;
             }
@@ -812,6 +847,7 @@ void plan_output_map(GemmPlan& p, bool conv) {
     a.tma_store = 0;
     if (std::getenv("PP_NO_TMA_STORE")) return;
     if ((uint64_t(a.out_ld) * eb) % 16 || (reinterpret_cast<uintptr_t>(a.out) % 16)) return;
+    if (a.block_n > 256) return;   // TMA box dims are <= 256
     if (conv) {
         uint64_t d[3] = {uint64_t(a.n_valid), uint64_t(a.out_w), uint64_t(a.out_rows)};
         uint64_t st[2] = {uint64_t(a.out_ld) * eb, uint64_t(a.out_w) * a.out_ld * eb};
@@ -865,6 +901,7 @@ int choose_kps(int block_n, bool gn, int pair) {
 // shared-memory bandwidth (TMA writes + MMA operand reads of a 128 x block_n tile); the
 // CTA pair halves the B bytes per SM.
 double tile_eff(int pair, int bn) {
+    if (bn > 256) return 0.85;   // wide tile: 8+ MMAs per stage hide the issue loop
     if (pair) return bn >= 256 ? 0.90 : bn >= 160 ? 0.64 : bn >= 128 ? 0.35 : 0.27;
     return bn >= 256 ? 0.75 : bn >= 160 ? 0.62 : bn >= 128 ? 0.36 : 0.28;
 }
@@ -880,6 +917,8 @@ void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int gn_cpg
     splits = 1;
     pair = 0;
     const int fs = force_splits & 15;
+    static const bool wide_env = std::getenv("PP_WIDE") != nullptr;
+    const bool wide_ok = wide_env || force_block_n > 256;
     const bool force_pair = force_splits & 16, force_single = force_splits & 32;
     for (int pr = 0; pr <= 1; ++pr) {
         if ((force_pair && !pr) || (force_single && pr)) continue;
@@ -887,8 +926,9 @@ void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int gn_cpg
         const int P = pr ? 2 : 1;
         const int slots = num_sms / P;
         const int units = (m_tiles + P - 1) / P;
-        for (int bn = 256; bn >= 16; bn -= 16) {
+        for (int bn = 512; bn >= 16; bn -= 16) {
             if (force_block_n && bn != force_block_n) continue;
+            if (bn > 256 && (bn % 32 || !wide_ok)) continue;
             if (n_pad % bn) continue;
             if (gn_cpg && bn % gn_cpg) continue;
             const int nt = n_pad / bn;
@@ -902,6 +942,7 @@ void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int gn_cpg
                 const double per_kb = 2.0 * bn / tile_eff(pr, bn);
                 const double kbs = std::ceil(double(k_blocks) / s);
                 double cost = waves * (kbs * per_kb + 2500.0);
+                if (bn > 256) cost += (waves - 1) * 4000.0;   // one accumulator: epilogue exposed
                 if (s > 1) cost += 2.0 * 128.0 * bn * 4.0 / 20.0;
                 if (cost < best * 0.98) {
                     best = cost;
@@ -941,13 +982,15 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
     if (splits > 1 && ((size_t)m_tiles * kTileM * n_pad * sizeof(float) > sc.ws_bytes ||
                        2 * size_t(m_tiles) * a.n_tiles > sc.n_tickets))
         splits = 1;
-    a.kps = choose_kps(bn, gn, pair);
+    a.n_sub = bn > 256 ? 2 : 1;
+    a.n_acc = bn > 256 ? 1 : 2;
+    a.kps = a.n_sub == 2 ? 1 : choose_kps(bn, gn, pair);
     a.splits = splits;
     a.kb_per_split = (k_blocks + splits - 1) / splits;
     a.kb_per_split = (a.kb_per_split + a.kps - 1) / a.kps * a.kps;   // whole stages per split
     a.splits = (k_blocks + a.kb_per_split - 1) / a.kb_per_split;
     a.stages = stages_for(bn, gn, pair, a.kps);
-    a.idesc = make_idesc(p.elem, bn, pair ? 2 * kTileM : kTileM);
+    a.idesc = make_idesc(p.elem, bn / a.n_sub, pair ? 2 * kTileM : kTileM);
     a.out = ep.out;
     a.out_ld = ep.out_ld;
     a.n_valid = ep.n_valid;
@@ -1033,8 +1076,8 @@ void plan_conv(GemmPlan& p, Elem e, const void* in, int rows_in, int W, int C_in
     finish_plan(p, a.tiles_y * a.tiles_x, n_pad, k_blocks, ep, sc, num_sms, force_splits,
                 force_block_n);
     // B: weights [n_pad][9*C_in_pad] viewed as [K blocks][n_pad][kel]: one box = kps blocks
-    encode_b(&p.tmB, e, weights, n_pad, 9 * C_in_pad, 9LL * C_in_pad, a.block_n / (p.pair ? 2 : 1),
-             a.kps);
+    encode_b(&p.tmB, e, weights, n_pad, 9 * C_in_pad, 9LL * C_in_pad,
+             a.block_n / (p.pair ? 2 : 1) / a.n_sub, a.kps);
     p.flops = 2.0 * a.m_pix * double(ep.n_valid) * 9.0 * C_in_pad;
     a.b_static = 1;   // conv weights
     plan_output_map(p, true);
@@ -1066,7 +1109,7 @@ void plan_gemm(GemmPlan& p, Elem e, const void* A, int M, int K, long long lda, 
     uint32_t ab[2] = {uint32_t(kel), uint32_t(kTileM)};
     encode(&p.tmA, e, 2, A, ad, as, ab);
     finish_plan(p, a.tiles_y, n_pad, K / kel, ep, sc, num_sms, force_splits, force_block_n);
-    encode_b(&p.tmB, e, B, N, K, ldb, a.block_n / (p.pair ? 2 : 1), a.kps);
+    encode_b(&p.tmB, e, B, N, K, ldb, a.block_n / (p.pair ? 2 : 1) / a.n_sub, a.kps);
     p.flops = 2.0 * double(M) * N * K;
     a.b_static = b_static ? 1 : 0;
     plan_output_map(p, false);
