@@ -62,6 +62,18 @@ struct GemmArgs {
     double* gn_part;          // [m_tiles][groups][2]
     unsigned int* gn_ticket;  // [1 + n_tiles] zeroed counters, each reset by its folder
     double* gn_out;           // [groups][2] = (mean, mean_sq)
+    // fused GroupNorm apply (conv -> GroupNorm [-> SiLU] [-> +temb] [-> +skip] in one kernel,
+    // one tile per CTA, all CTAs resident): the raw conv tile stays in TMEM while the
+    // statistics are reduced, then is normalised from TMEM and written to `out`
+    int gn_apply;
+    const float* gn_gamma;
+    const float* gn_beta;
+    const float* gn_temb;     // [n] or null (per step: patched at launch)
+    const void* gn_skip;      // same layout as out (ld = gn_skip_ld) or null
+    long long gn_skip_ld;
+    int gn_silu;
+    float gn_eps;
+    int* gn_err;              // set to 1 when a group's variance is negative
     const void* b_base;       // B tensor (weights) and its size: with b_static, every CTA
     long long b_bytes;        // prefetches its 1/grid slice into L2 at kernel start
     int tma_store;            // 1: the CTA's last tile is stored through tmD (smem staging)
@@ -95,6 +107,17 @@ struct EpilogueSpec {
     // GroupNorm statistics of the output (groups == 0: off)
     int gn_groups = 0;
     double* gn_out = nullptr;
+    // fused GroupNorm apply (requires gn_groups): `out` receives GN(conv) [SiLU] [+temb]
+    // [+skip]; the raw conv output is never stored
+    bool gn_apply = false;
+    const float* gn_gamma = nullptr;
+    const float* gn_beta = nullptr;
+    const float* gn_temb = nullptr;
+    const void* gn_skip = nullptr;
+    long long gn_skip_ld = 0;
+    bool gn_silu = false;
+    float gn_eps = 1e-5f;
+    int* gn_err = nullptr;
 };
 
 // Scratch shared by all GEMMs issued on one stream (they run one after another).

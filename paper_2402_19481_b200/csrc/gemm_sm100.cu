@@ -13,6 +13,7 @@
 #include "util.hpp"
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -125,7 +126,7 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
                     const float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                     if (srow)
                         *reinterpret_cast<float4*>(srow + (c0 + j) * 4) = o;
-                    else
+                    else if (!a.gn_apply)
                         *reinterpret_cast<float4*>(dst + j) = o;
                 }
             } else {
@@ -134,7 +135,7 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
                     if (n0 + j < a.n_valid) {
                         float o = v[j] + (res ? res[j] : 0.0f);
                         o = a.round_tf32 ? round_tf32(o) : o;
-                        if (!srow) dst[j] = o;
+                        if (!srow && !a.gn_apply) dst[j] = o;
                         v[j] = o;
                     } else {
                         v[j] = 0.0f;
@@ -176,7 +177,7 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
                     }
                     if (srow)
                         *reinterpret_cast<uint4*>(srow + (c0 + j) * 2) = o;
-                    else
+                    else if (!a.gn_apply)
                         *reinterpret_cast<uint4*>(dst + j) = o;
                 }
             } else {
@@ -185,7 +186,7 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
                     if (n0 + j < a.n_valid) {
                         float o = v[j] + (res ? __bfloat162float(res[j]) : 0.0f);
                         const __nv_bfloat16 b = __float2bfloat16(o);
-                        if (!srow) dst[j] = b;
+                        if (!srow && !a.gn_apply) dst[j] = b;
                         v[j] = __bfloat162float(b);
                     } else {
                         v[j] = 0.0f;
@@ -251,8 +252,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const __grid_constant__ CUtensorMap tmD, const GemmArgs a) {
     constexpr int P = kPair ? 2 : 1;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte aligned base derived from smem_raw by pointer arithmetic (not an integer
+    // cast), so the compiler keeps the shared address space: LDS/STS for the tail arrays
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     const int stages = a.stages;
     const int kps = a.kps;                                      // K blocks per stage (1 or 2)
     const uint32_t a_slot = kTileM * kBlockBytes;               // one A box slot
@@ -586,6 +588,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool stage_out = a.tma_store && t + tile_step >= total_tiles;
             const int eb_out = (kTF32 || a.out_f32) ? 4 : 2;
             uint8_t* srow = stage_out ? smem + size_t(r) * a.block_n * eb_out : nullptr;
+            uint8_t* srow1 = a.gn_apply ? nullptr : srow;   // fused GN: pass 1 stores nothing
             for (int c = et; c < a.block_n; c += 128)
                 sbias[c] = (a.bias && nbase + c < a.n_valid) ? a.bias[nbase + c] : 0.0f;
             ptx::mbar_wait(&st.tfull_bar[cur], cur_phase);
@@ -632,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     continue;
                 }
                 if (et == 0) {
-                    while (atomicAdd(ready, 0u) == 0u) __nanosleep(64);
+                    while (ptx::ld_acquire_gpu(ready) == 0u) __nanosleep(64);
                     __threadfence();
                 }
                 epi_bar();
@@ -658,12 +661,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                                 for (int j = 0; j < 16; ++j) v[j] = v[j] + o[c1 + j];
                             }
+                            if (a.gn_apply) ptx::tmem_st16(t_row + cb + c1, v);   // acc + partial
                             finish_chunk<kTF32>(a, v, sbias, cb + c1, nbase + cb + c1, p, valid,
-                                                sgn_warp, lane, srow);
+                                                sgn_warp, lane, srow1);
                         }
                     }
                 }
-                release(cur);
+                if (!a.gn_apply) release(cur);
                 if (et == 0) {
                     *ticket = 0u;
                     *ready = 0u;
@@ -672,11 +676,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int c0 = 0; c0 < a.block_n; c0 += 16) {
                     float v[16];
                     ptx::tmem_ld16(t_row + c0, v);
-                    finish_chunk<kTF32>(a, v, sbias, c0, nbase + c0, p, valid, sgn_warp, lane, srow);
+                    finish_chunk<kTF32>(a, v, sbias, c0, nbase + c0, p, valid, sgn_warp, lane, srow1);
                 }
-                release(cur);
+                if (!a.gn_apply) release(cur);
             }
-            if (stage_out) {
+            if (stage_out && !a.gn_apply) {
                 ptx::fence_proxy_async();   // staged rows -> visible to the TMA engine
                 epi_bar();
                 if (et == 0) {
@@ -767,6 +771,154 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     if (et == 0) a.gn_ticket[1 + tc.nt] = 0u;
                     epi_bar();
+                }
+            }
+            if (a.gn_apply) {
+                // ===== fused GroupNorm apply, pass 2 (one tile per CTA, all CTAs resident) =====
+                // wait for this N tile's statistics (folded above by the N tile's last CTA)
+                unsigned int* nt_ready = a.gn_ticket + 1 + a.n_tiles + tc.nt;
+                unsigned int* nt_used = a.gn_ticket + 1 + 2 * a.n_tiles + tc.nt;
+                if (et == 0 && !(a.debug & 32)) {
+                    if (st.flags[2]) {
+                        __threadfence();
+                        atomicExch(nt_ready, 1u);
+                    } else {
+                        while (ptx::ld_acquire_gpu(nt_ready) == 0u) __nanosleep(64);
+                        __threadfence();
+                    }
+                }
+                epi_bar();
+                // per-column coefficients: y = x * sc + sh (sc = gamma / std, sh = beta - mean
+                // * sc; the same fp32 formulas as gn_pass_kernel), then SiLU, + temb, + skip
+                float* s_sc = st.gn;
+                float* s_sh = s_sc + a.block_n;
+                float* s_te = s_sh + a.block_n;
+                for (int c = et; c < a.block_n && !(a.debug & 64); c += 128) {
+                    const int g = (nbase + c) / a.gn_cpg;
+                    const double m = __ldcg(a.gn_out + g * 2), q = __ldcg(a.gn_out + g * 2 + 1);
+                    const double var = __dsub_rn(q, __dmul_rn(m, m));
+                    if (var < 0.0 && a.gn_err) atomicExch(a.gn_err, 1);
+                    const float mu = float(m);
+                    const float inv = float(1.0 / sqrt(__dadd_rn(fmax(var, 0.0), double(a.gn_eps))));
+                    const float sc = a.gn_gamma[nbase + c] * inv;
+                    s_sc[c] = sc;
+                    s_sh[c] = fmaf(-mu, sc, a.gn_beta[nbase + c]);
+                    s_te[c] = a.gn_temb ? a.gn_temb[nbase + c] : 0.0f;
+                }
+                epi_bar();
+                if (et == 0 && atomicAdd(nt_used, 1u) == unsigned(m_tiles - 1)) {
+                    *nt_ready = 0u;   // every CTA of this N tile has passed the wait
+                    *nt_used = 0u;
+                }
+                ptx::tmem_wait_st();
+                const bool f32out = kTF32 || a.out_f32;
+                for (int c0 = 0; c0 < a.block_n && !(a.debug & 128); c0 += 16) {
+                    float v[16], cb[16], cs[16], ch[16];
+                    ptx::tmem_ld16(t_row + c0, v);
+#pragma unroll
+                    for (int j = 0; j < 16; j += 4) {
+                        *reinterpret_cast<float4*>(cb + j) = *reinterpret_cast<const float4*>(sbias + c0 + j);
+                        *reinterpret_cast<float4*>(cs + j) = *reinterpret_cast<const float4*>(s_sc + c0 + j);
+                        *reinterpret_cast<float4*>(ch + j) = *reinterpret_cast<const float4*>(s_sh + c0 + j);
+                    }
+                    // the raw conv value exactly as the unfused path stores it
+                    if (!f32out) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            v[j] = __bfloat162float(__float2bfloat16(v[j] * a.scale + cb[j]));
+                    } else if (a.round_tf32) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) v[j] = round_tf32(v[j] * a.scale + cb[j]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) v[j] = v[j] * a.scale + cb[j];
+                    }
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] = fmaf(v[j], cs[j], ch[j]);
+                    if (a.gn_silu) {
+                        if (!f32out) {
+#pragma unroll
+                            for (int j = 0; j < 16; j += 2) {
+                                const __half2 hv = __floats2half2_rn(0.5f * v[j], 0.5f * v[j + 1]);
+                                uint32_t hi = *reinterpret_cast<const uint32_t*>(&hv), ho;
+                                asm("tanh.approx.f16x2 %0, %1;" : "=r"(ho) : "r"(hi));
+                                const float2 t2 = __half22float2(*reinterpret_cast<const __half2*>(&ho));
+                                v[j] = v[j] * fmaf(0.5f, t2.x, 0.5f);
+                                v[j + 1] = v[j + 1] * fmaf(0.5f, t2.y, 0.5f);
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) v[j] = v[j] / (1.0f + expf(-v[j]));
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < 16; j += 4) {
+                        const float4 t4 = *reinterpret_cast<const float4*>(s_te + c0 + j);
+                        v[j] += t4.x; v[j + 1] += t4.y; v[j + 2] += t4.z; v[j + 3] += t4.w;
+                    }
+                    if (valid && a.gn_skip) {
+                        if (f32out) {
+                            const float* sk = reinterpret_cast<const float*>(a.gn_skip) + p * a.gn_skip_ld + nbase + c0;
+#pragma unroll
+                            for (int j = 0; j < 16; j += 4) {
+                                const float4 q = *reinterpret_cast<const float4*>(sk + j);
+                                v[j] += q.x; v[j + 1] += q.y; v[j + 2] += q.z; v[j + 3] += q.w;
+                            }
+                        } else {
+                            const __nv_bfloat16* sk =
+                                reinterpret_cast<const __nv_bfloat16*>(a.gn_skip) + p * a.gn_skip_ld + nbase + c0;
+#pragma unroll
+                            for (int j = 0; j < 16; j += 8) {
+                                const uint4 q = *reinterpret_cast<const uint4*>(sk + j);
+                                const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    const float2 f = __bfloat1622float2(q2[i]);
+                                    v[j + 2 * i] += f.x;
+                                    v[j + 2 * i + 1] += f.y;
+                                }
+                            }
+                        }
+                    }
+                    if (valid) {
+                        uint8_t* dst = srow ? srow + size_t(c0) * (f32out ? 4 : 2)
+                                            : static_cast<uint8_t*>(a.out) +
+                                                  (size_t(p) * a.out_ld + nbase + c0) * (f32out ? 4 : 2);
+                        if (f32out) {
+#pragma unroll
+                            for (int j = 0; j < 16; j += 4) {
+                                float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                                if (a.round_tf32) {
+                                    o.x = round_tf32(o.x); o.y = round_tf32(o.y);
+                                    o.z = round_tf32(o.z); o.w = round_tf32(o.w);
+                                }
+                                *reinterpret_cast<float4*>(dst + j * 4) = o;
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 16; j += 8) {
+                                uint4 o;
+                                __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+                                for (int i = 0; i < 4; ++i)
+                                    o2[i] = __floats2bfloat162_rn(v[j + 2 * i], v[j + 2 * i + 1]);
+                                *reinterpret_cast<uint4*>(dst + j * 2) = o;
+                            }
+                        }
+                    }
+                }
+                release(cur);
+                if (stage_out) {
+                    ptx::fence_proxy_async();
+                    epi_bar();
+                    if (et == 0) {
+                        if (conv)
+                            ptx::tma_store_3d(&tmD, smem, nbase, tc.tx * a.w_box, tc.ty * a.rows_box);
+                        else
+                            ptx::tma_store_2d(&tmD, smem, nbase, tc.ty * kTileM);
+                        ptx::bulk_commit();
+                        ptx::bulk_wait_all();
+                    }
                 }
             }
         }
@@ -911,14 +1063,14 @@ double tile_eff(int pair, int bn) {
 // over SM pairs); split-K pays a partial write + read.
 //   force_splits: bits 0-3 = splits (0 auto), bit 4 = force pair, bit 5 = force single CTA
 void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int gn_cpg, int force_splits,
-                   int force_block_n, int& block_n, int& splits, int& pair) {
+                   int force_block_n, int& block_n, int& splits, int& pair, bool one_wave = false) {
     double best = 1e300;
     block_n = 16;
     splits = 1;
     pair = 0;
     const int fs = force_splits & 15;
     static const bool wide_env = std::getenv("PP_WIDE") != nullptr;
-    const bool wide_ok = wide_env || force_block_n > 256;
+    const bool wide_ok = wide_env || force_block_n > 256 || one_wave;
     const bool force_pair = force_splits & 16, force_single = force_splits & 32;
     for (int pr = 0; pr <= 1; ++pr) {
         if ((force_pair && !pr) || (force_single && pr)) continue;
@@ -938,6 +1090,7 @@ void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int gn_cpg
                 // split only when one wave leaves more than half of the SMs idle
                 if (!fs && s == 2 && ((long long)units * nt * 2 > slots || k_blocks < 16)) continue;
                 const long long tiles = (long long)units * nt * s;
+                if (one_wave && tiles > slots) continue;   // fused GroupNorm: every tile resident
                 const double waves = std::ceil(double(tiles) / slots);
                 const double per_kb = 2.0 * bn / tile_eff(pr, bn);
                 const double kbs = std::ceil(double(k_blocks) / s);
@@ -970,7 +1123,15 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
     }
     int bn, splits, pair;
     choose_tiling(m_tiles, n_pad, k_blocks, num_sms, cpg, force_splits, force_block_n, bn, splits,
-                  pair);
+                  pair, ep.gn_apply);
+    if (ep.gn_apply) {
+        if (!gn) throw std::invalid_argument("fused GroupNorm apply needs the statistics epilogue");
+        if (ep.residual) throw std::invalid_argument("fused GroupNorm apply: conv residual unsupported");
+        const int P = pair ? 2 : 1;
+        const long long tiles = (long long)(m_tiles + P - 1) / P * (n_pad / bn) * splits;
+        if (bn % cpg || tiles > num_sms / P)
+            throw std::invalid_argument("fused GroupNorm apply: no single-wave tiling");
+    }
     if (gn && bn % cpg) throw std::invalid_argument("GroupNorm statistics: block_n not group aligned");
     if (pair && bn % 16) throw std::invalid_argument("CTA-pair GEMM: block_n % 16 != 0");
     p.pair = pair;
@@ -1011,6 +1172,15 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
         a.gn_part = sc.gn_part;
         a.gn_ticket = sc.gn_ticket;
         a.gn_out = ep.gn_out;
+        a.gn_apply = ep.gn_apply ? 1 : 0;
+        a.gn_gamma = ep.gn_gamma;
+        a.gn_beta = ep.gn_beta;
+        a.gn_temb = ep.gn_temb;
+        a.gn_skip = ep.gn_skip;
+        a.gn_skip_ld = ep.gn_skip_ld;
+        a.gn_silu = ep.gn_silu ? 1 : 0;
+        a.gn_eps = ep.gn_eps;
+        a.gn_err = ep.gn_err;
     }
     const int P = pair ? 2 : 1;
     const int units = (m_tiles + P - 1) / P * a.n_tiles * a.splits;

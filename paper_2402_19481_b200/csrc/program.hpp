@@ -97,6 +97,9 @@ struct Program {
     std::vector<std::array<GemmPlan, 2>> plans;    // per group, per step parity: conv / linear / PV
     std::vector<std::array<GemmPlan, 2>> s_plans;  // attention S = Q K^T per K/V parity
     std::vector<char> fused_stats;                 // per GN layer: stats come from the conv epilogue
+    std::vector<std::array<GemmPlan, 2>> fplans;   // per conv group: conv + next GN group fused
+    std::vector<char> gn_fusable;                  // per group: fplans valid
+    std::vector<char> fused_now;                   // per GN layer: applied by this step's conv
     GemmScratch sc;
     // scratch
     double* gn_partial = nullptr;
@@ -155,7 +158,7 @@ struct Program {
     void time_projection(int t);
     void pack_halo(const Group& g, int par);
     void unpack_halo(const Group& g, int par);
-    void conv(const Group& g, int par);
+    void conv(const Group& g, int par, bool gn_fresh = false);
     void pack_kv(const Group& g, int par);
     void scatter_kv(const Group& g, int par);
     void attention(const Group& g, int par, int par_out);

@@ -422,6 +422,60 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
             m->layers[g.first].out_ch % m->layers[next].groups == 0)
             fused_stats[next] = 2;
     }
+    // Single band: conv -> GroupNorm group in ONE kernel (the raw conv tile stays in TMEM
+    // while the statistics are reduced, then is normalised and stored; the raw conv output is
+    // never written).  Needs fresh statistics (one band: no cross-band reduction), a conv
+    // output nothing else reads, and a single-wave tiling; otherwise the two-kernel path.
+    fplans.resize(groups.size());
+    gn_fusable.assign(groups.size(), 0);
+    fused_now.assign(L, 0);
+    // Measured on B200 (scripts/fused_diag.py): the second TMEM pass runs on the 4 epilogue
+    // warps only and costs more than the separate 720-thread/SM GroupNorm pass it replaces
+    // (41.8 vs 33.5 + 5.4 us at 64^2 x 640), so the fused path is opt-in (PP_GN_FUSE=1).
+    if (nb == 1 && std::getenv("PP_GN_FUSE")) {
+        std::set<int> srcs;
+        for (const Layer& d : m->layers)
+            if (d.kind == Kind::AddSkip) srcs.insert(d.skip_source);
+        for (size_t gi = 0; gi + 1 < groups.size(); ++gi) {
+            const Group& g = groups[gi];
+            const Group& gq = groups[gi + 1];
+            const Layer& d = m->layers[g.first];
+            if (!(d.kind == Kind::Conv || d.kind == Kind::DownConv) || g.skip >= 0 || g.last != g.first)
+                continue;
+            if (gq.kind != Kind::GroupNorm || !fused_stats[gq.first] || srcs.count(g.last)) continue;
+            if (gq.last + 1 < L && fused_stats[gq.last + 1] == 2) continue;   // output stats wanted
+            const Layer& dn = m->layers[gq.first];
+            const LayerWeights& lw = wts->L[g.first];
+            const LayerWeights& lg = wts->L[gq.first];
+            const Act& in = input_of(g.first);
+            try {
+                for (int p = 0; p < 2; ++p) {
+                    EpilogueSpec ep;
+                    ep.out = act[gq.last].interior(eb);
+                    ep.out_ld = act[gq.last].ld;
+                    ep.out_f32 = e == Elem::F32;
+                    ep.round_tf32 = rnd;
+                    ep.n_valid = d.out_ch;
+                    ep.bias = lw.bias;
+                    ep.gn_groups = dn.groups;
+                    ep.gn_out = lx[gq.first].stats[p] + size_t(band) * dn.groups * 2;
+                    ep.gn_apply = true;
+                    ep.gn_gamma = lg.gamma;
+                    ep.gn_beta = lg.beta;
+                    ep.gn_skip = gq.skip >= 0 ? act[gq.skip].interior(eb) : nullptr;
+                    ep.gn_skip_ld = gq.skip >= 0 ? act[gq.skip].ld : 0;
+                    ep.gn_silu = gq.silu;
+                    ep.gn_eps = dn.eps;
+                    ep.gn_err = flags + 1;
+                    plan_conv(fplans[gi][p], e, in.base, in.rows, in.w, in.ld, d.stride, lw.w,
+                              lw.n_pad, ep, sc, sms);
+                }
+                gn_fusable[gi] = 1;
+            } catch (const std::invalid_argument&) {
+                gn_fusable[gi] = 0;
+            }
+        }
+    }
     set_profile(profile);
     CUDA_CHECK(cudaDeviceSynchronize());
 }
@@ -522,8 +576,19 @@ void Program::unpack_halo(const Group& g, int par) {
                                    x.row_bytes, cudaMemcpyDeviceToDevice, cs));
 }
 
-void Program::conv(const Group& g, int par) {
+void Program::conv(const Group& g, int par, bool gn_fresh) {
     const size_t gi = size_t(&g - groups.data());
+    if (gn_fresh && gn_fusable[gi]) {
+        // conv + the following GroupNorm group in one kernel (see the Program constructor)
+        const Group& gq = groups[gi + 1];
+        GemmPlan p = fplans[gi][par];
+        p.a.gn_temb = gq.temb >= 0 ? temb_ptr(gq.temb) : nullptr;
+        fused_now[gq.first] = 1;
+        run_timed(CAT_CONV, p.flops, [&] { launch_gemm(p, cs); });
+        count(1);
+        return;
+    }
+    if (gi + 1 < groups.size()) fused_now[groups[gi + 1].first] = 0;
     const GemmPlan& p = plans[gi][par];
     run_timed(CAT_CONV, p.flops, [&] { launch_gemm(p, cs); });
     count(1);
@@ -806,7 +871,10 @@ void Runner::run_bands(std::vector<std::unique_ptr<Program>>& progs, int t, int 
                 volumes_.halo_recv += per_band;
                 volumes_.halo_sent += per_band;
             }
-            each([&](Program& b, const Group& g) { b.conv(g, pcur); });
+            // fused conv + GroupNorm needs this step's own fresh statistics: one band and not
+            // the Stale scheme of a displaced step
+            const bool gn_fresh = !multi && !(displaced && o_.gn_scheme == GN_STALE);
+            each([&](Program& b, const Group& g) { b.conv(g, pcur, gn_fresh); });
             if (exchanging) posted_[l] = s;
         } else if (d.kind == Kind::SelfAttn) {
             if (multi) {
@@ -826,6 +894,12 @@ void Runner::run_bands(std::vector<std::unique_ptr<Program>>& progs, int t, int 
             each([&](Program& b, const Group& g) { b.attention(g, nb_pu, pcur); });
             if (exchanging) posted_[l] = s;
         } else if (d.kind == Kind::GroupNorm) {
+            if (!multi && progs[0]->fused_now[l]) {
+                // already applied by the fused conv kernel (single band, fresh statistics)
+                each([&](Program& b, const Group&) { b.record_ready(l); });
+                if (exchanging) gn_posted_[l] = s;
+                continue;
+            }
             each([&](Program& b, const Group& g) {
                 if (!b.fused_stats[l]) b.gn_stats(g, pcur);
                 b.record_ready(l);

@@ -189,3 +189,17 @@ def test_naive_sample_is_deterministic():
     assert np.array_equal(a, b)
     ref = O.run_sampling(ocfg(cfg), "naive", 2, 32, 32, 5, 4)["x0"]
     assert rel(a, ref) <= TOL["bf16"]
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_fused_conv_groupnorm_forward(dtype, monkeypatch):
+    # opt-in single-kernel conv -> GroupNorm(+SiLU+temb) path (PP_GN_FUSE=1): same parity bar
+    monkeypatch.setenv("PP_GN_FUSE", "1")
+    cfg, hw = TOY, 32
+    om = O.build_model(ocfg(cfg), 77)
+    cond = O.random_condition(cfg.cond_dim, 78)
+    x = O.random_normal(1, cfg.in_channels, hw, hw, 79)
+    ref = O.forward_full(om, x, 700, cond)
+    r = P.PatchRunner(P.build_model(cfg, 77), cond, hw, hw, mode="reference", dtype=dtype)
+    eps = r.run_step(x, 700, 0)
+    assert rel(eps, ref) <= EPS_TOL[dtype], rel(eps, ref)
