@@ -838,13 +838,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (a.gn_silu) {
                         if (!f32out) {
 #pragma unroll
-                            for (int j = 0; j < 16; j += 2) {
-                                const __half2 hv = __floats2half2_rn(0.5f * v[j], 0.5f * v[j + 1]);
-                                uint32_t hi = *reinterpret_cast<const uint32_t*>(&hv), ho;
-                                asm("tanh.approx.f16x2 %0, %1;" : "=r"(ho) : "r"(hi));
-                                const float2 t2 = __half22float2(*reinterpret_cast<const __half2*>(&ho));
-                                v[j] = v[j] * fmaf(0.5f, t2.x, 0.5f);
-                                v[j + 1] = v[j + 1] * fmaf(0.5f, t2.y, 0.5f);
+                            for (int j = 0; j < 16; ++j) {   // silu = h + h tanh(h), h = v / 2
+                                const float h = 0.5f * v[j];
+                                float tt;
+                                asm("tanh.approx.f32 %0, %1;" : "=f"(tt) : "f"(h));
+                                v[j] = fmaf(h, tt, h);
                             }
                         } else {
 #pragma unroll

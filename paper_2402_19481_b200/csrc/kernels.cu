@@ -310,18 +310,15 @@ __global__ void __launch_bounds__(256, (STATS ? 2 : 3))
                     for (int i = 0; i < VEC; ++i) f[i] = fmaf(f[i], sc[i], sh[i]);
                     if (do_silu) {
                         if constexpr (sizeof(T) == 2) {
-                            // bf16 output: sigmoid(v) = 0.5 + 0.5 tanh(v / 2) with one packed
-                            // f16x2 tanh per two elements (the SFU is this kernel's bound:
-                            // ex2 + rcp per element was 4x the MUFU work); |err| ~ 2^-11,
-                            // below the bf16 rounding of the stored value
+                            // bf16 output: silu(v) = h + h tanh(h), h = v / 2, with one
+                            // tanh.approx.f32 (MUFU.TANH) per element (the SFU-bound ex2 + rcp
+                            // form was 2 MUFU ops); |err| ~ 2^-11, below the bf16 rounding
 #pragma unroll
-                            for (int i = 0; i < VEC; i += 2) {
-                                const __half2 hv = __floats2half2_rn(0.5f * f[i], 0.5f * f[i + 1]);
-                                uint32_t hi = *reinterpret_cast<const uint32_t*>(&hv), ho;
-                                asm("tanh.approx.f16x2 %0, %1;" : "=r"(ho) : "r"(hi));
-                                const float2 t = __half22float2(*reinterpret_cast<const __half2*>(&ho));
-                                f[i] = f[i] * fmaf(0.5f, t.x, 0.5f);
-                                f[i + 1] = f[i + 1] * fmaf(0.5f, t.y, 0.5f);
+                            for (int i = 0; i < VEC; ++i) {
+                                const float h = 0.5f * f[i];
+                                float t;
+                                asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(h));
+                                f[i] = fmaf(h, t, h);
                             }
                         } else {
 #pragma unroll
