@@ -100,6 +100,7 @@ struct Program {
     std::vector<std::array<GemmPlan, 2>> fplans;   // per conv group: conv + next GN group fused
     std::vector<char> gn_fusable;                  // per group: fplans valid
     std::vector<char> fused_now;                   // per GN layer: applied by this step's conv
+    std::vector<char> merged_into_prev;            // per group: computed by the previous group
     GemmScratch sc;
     // scratch
     double* gn_partial = nullptr;

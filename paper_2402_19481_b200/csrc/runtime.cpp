@@ -345,6 +345,25 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
         Vt = alloc(size_t(npad) * s_pad * eb);
     }
 
+    // SelfAttn(+AddSkip) followed by CrossAttn+AddSkip of that output: CrossAttn's output is
+    // the broadcast W_v cond + b_v (model.cpp:252-271), so the pair is one PV GEMM epilogue:
+    // out = P V^T + skip + v_cross (the cross value as the GEMM bias); the SelfAttn group's
+    // own output is not materialised.
+    merged_into_prev.assign(groups.size(), 0);
+    {
+        std::set<int> srcs_all;
+        std::multiset<int> srcs_count;
+        for (const Layer& d : m->layers)
+            if (d.kind == Kind::AddSkip) srcs_count.insert(d.skip_source);
+        for (size_t gi = 0; gi + 1 < groups.size(); ++gi) {
+            const Group& g = groups[gi];
+            const Group& gc = groups[gi + 1];
+            if (g.kind == Kind::SelfAttn && gc.kind == Kind::CrossAttn && gc.skip == g.last &&
+                srcs_count.count(g.last) == 1 && gc.last != L - 1 && !std::getenv("PP_NO_XATTN_MERGE"))
+                merged_into_prev[gi + 1] = 1;
+        }
+    }
+
     // GEMM plans (per parity: the fused GroupNorm statistics land in that parity's table)
     const int sms = device_sm_count();
     plans.resize(groups.size());
@@ -398,6 +417,12 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
                 plan_gemm(plans[gi][p], e, in.interior(eb), int(in.pix()), in.ld, in.ld, lw.w,
                           d.out_ch, in.ld, e2, sc, sms, 0, 0, /*b_static=*/true);
             } else if (d.kind == Kind::SelfAttn) {
+                if (gi + 1 < groups.size() && merged_into_prev[gi + 1]) {
+                    const Group& gc = groups[gi + 1];
+                    e2.out = act[gc.last].interior(eb);
+                    e2.out_ld = act[gc.last].ld;
+                    e2.bias = wts->L[gc.first].cross_v;
+                }
                 const Region& ri = spec.layer_in[g.first];
                 const int ns = ri.full_h * ri.full_w;
                 EpilogueSpec es;
@@ -921,6 +946,8 @@ void Runner::run_bands(std::vector<std::unique_ptr<Program>>& progs, int t, int 
             }
             each([&](Program& b, const Group& g) { b.gn_apply(g, mode, pcur, pprev); });
             if (exchanging) gn_posted_[l] = s;
+        } else if (progs[0]->merged_into_prev[gi]) {
+            // folded into the previous group's GEMM epilogue (SelfAttn -> CrossAttn)
         } else {
             each([&](Program& b, const Group& g) { b.simple(g, pcur); });
         }
