@@ -159,6 +159,11 @@ PP_API int pp_runner_step_device_macs(const pp_runner* r, int step, uint64_t* pe
 /* bytes this runtime actually moved: {allgather_recv, allgather_sent, halo_recv, halo_sent,
  * statreduce_recv, statreduce_sent} (CommVolumes, proj/include/patchsim/trace.hpp:37-52) */
 PP_API int pp_runner_volumes(const pp_runner* r, uint64_t* v6);
+/* RawTrace of one device (PatchRunner::trace(), proj/include/patchsim/runtime.hpp:71): rows
+ * of 9 uint64 {device, step, layer, kind (0 Compute/1 Post/2 Wait), prim (0 AllGather/
+ * 1 Halo/2 StatReduce), macs, bytes_recv, bytes_sent, tag}; Post bytes follow the
+ * reference hub's accounting.  Returns the event count (-1 on error); out9 may be NULL. */
+PP_API long pp_runner_trace(const pp_runner* r, int device, uint64_t* out9, long cap);
 /* sample() (proj/src/sampler.cpp:76-95) with the DDIM-eta0 update on the GPU:
  * x_T (NCHW host), plan timesteps, alpha_bar table; x0 out; trajectory optional
  * (num_steps model inputs x_t, NCHW). */

@@ -239,6 +239,22 @@ class PatchRunner:
         lib().ref_runner_volumes(C.c_void_p(self.r), _p(v))
         return [int(x) for x in v]
 
+    def trace(self, dev=0):
+        """PatchRunner::trace() (runtime.hpp:71) rows: (device, step, layer, kind, prim, macs,
+        bytes_recv, bytes_sent, tag)."""
+        f = lib().ref_runner_trace
+        f.restype = C.c_long
+        f.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_long]
+        n = f(C.c_void_p(self.r), dev, None, 0)
+        out = np.zeros((max(n, 1), 9), dtype=np.uint64)
+        f(C.c_void_p(self.r), dev, _p(out), n)
+        rows = []
+        for r in out[:n]:
+            v = [int(x) for x in r]
+            v[2] = v[2] - (1 << 64) if v[2] >= (1 << 63) else v[2]
+            rows.append(tuple(v))
+        return rows
+
 
 def run_sampling(cfg6, mode="reference", n_devices=1, h=48, w=48, num_steps=50, warmup=4,
                  gn_scheme="corrected", stress=False, seeds=(42, 1234, 7),

@@ -180,6 +180,22 @@ void ref_runner_volumes(void* rp, uint64_t* v6) {
     v6[3] = v.halo_sent; v6[4] = v.statreduce_recv; v6[5] = v.statreduce_sent;
 }
 
+// trace rows of 9 uint64 {device, step, layer, kind, prim, macs, recv, sent, tag}
+long ref_runner_trace(void* rp, int dev, uint64_t* out9, long cap) {
+    const RawTrace& t = static_cast<RunnerBox*>(rp)->runner->trace();
+    if (dev < 0 || dev >= int(t.per_device.size())) return 0;
+    const auto& v = t.per_device[size_t(dev)];
+    const long n = long(v.size());
+    for (long i = 0; out9 && i < n && i < cap; ++i) {
+        const RawEvent& e = v[size_t(i)];
+        uint64_t* o = out9 + 9 * i;
+        o[0] = uint64_t(e.device); o[1] = uint64_t(e.step); o[2] = uint64_t(int64_t(e.layer));
+        o[3] = uint64_t(e.kind); o[4] = uint64_t(e.prim); o[5] = e.macs;
+        o[6] = e.bytes_recv; o[7] = e.bytes_sent; o[8] = e.tag;
+    }
+    return n;
+}
+
 // ---- run_sampling ----------------------------------------------------------------
 // icfg = {mode, n_devices, h, w, num_steps, warmup, gn_scheme, stress, schedule_steps}
 // seeds = {model, noise, cond}; traj may be null (num_steps * 4*h*w floats).

@@ -115,6 +115,7 @@ SIGNATURES = {
     "pp_runner_total_macs": (_U64, [_V]),
     "pp_runner_step_device_macs": (_I, [_V, _I, _V]),
     "pp_runner_volumes": (_I, [_V, _V]),
+    "pp_runner_trace": (_L, [_V, _I, _V, _L]),
     "pp_runner_sample": (_I, [_V, _V, _V, _I, _V, _I, _V, _V]),
     "pp_runner_profile": (_I, [_V, _V]),
     "pp_runner_launches": (_L, [_V]),

@@ -364,6 +364,27 @@ PP_API int pp_runner_volumes(const pp_runner* r, uint64_t* v6) {
     });
 }
 
+// RawTrace of `device` (proj/include/patchsim/trace.hpp:18-35) as rows of 9 uint64:
+// {device, step, layer (int64), kind, prim, macs, bytes_recv, bytes_sent, tag}.  Returns the
+// event count (rows written: min(count, cap)); out may be null to query the count.
+PP_API long pp_runner_trace(const pp_runner* r, int device, uint64_t* out9, long cap) {
+    long n = -1;
+    const int rc = pp::guard([&] {
+        need(r, "pp_runner_trace");
+        const auto& t = r->r->trace(device);
+        n = long(t.size());
+        if (!out9) return;
+        for (long i = 0; i < n && i < cap; ++i) {
+            const pp::TraceEvent& e = t[size_t(i)];
+            uint64_t* o = out9 + 9 * i;
+            o[0] = uint64_t(e.device); o[1] = uint64_t(e.step); o[2] = uint64_t(int64_t(e.layer));
+            o[3] = uint64_t(e.kind); o[4] = uint64_t(e.prim); o[5] = e.macs;
+            o[6] = e.bytes_recv; o[7] = e.bytes_sent; o[8] = e.tag;
+        }
+    });
+    return rc == PP_OK ? n : -1;
+}
+
 PP_API int pp_runner_sample(pp_runner* r, const float* x_T, const int* ts, int n, const double* abar,
                             int total, float* x0, float* traj) {
     return pp::guard([&] {

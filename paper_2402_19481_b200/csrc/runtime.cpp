@@ -858,6 +858,103 @@ void Runner::count_macs(int s, bool naive) {
     }
 }
 
+const std::vector<TraceEvent>& Runner::trace(int device) const {
+    static const std::vector<TraceEvent> empty;
+    if (device < 0 || device >= int(trace_.size())) return empty;
+    return trace_[device];
+}
+
+// The reference's trace of one step (PatchRunner::record calls in device_step,
+// step_reference and step_naive, proj/src/runtime.cpp:185-330, 382-452): host bookkeeping that
+// follows the same rules, so the event sequence is identical for the same calls.
+void Runner::record_trace(int s, int kind) {
+    const int n = n_dev_;
+    const int L = int(m_.layers.size());
+    if (int(trace_.size()) < n) {
+        trace_.resize(n);
+        tr_act_step_.assign(n, std::vector<int>(L, -1));
+        tr_gn_step_.assign(n, std::vector<int>(L, -1));
+    }
+    auto tag = [](int step, int layer, int prim) {
+        return (uint64_t(uint32_t(step + 1)) << 24) | (uint64_t(uint32_t(layer + 1)) << 4) |
+               uint64_t(uint8_t(prim));
+    };
+    enum { COMPUTE = 0, POST = 1, WAIT = 2 };
+    enum { AG = 0, SR = 2 };
+    auto ev = [&](int d, int l, int k, int prim, uint64_t macs, uint64_t rb, uint64_t sb, uint64_t tg) {
+        TraceEvent e;
+        e.device = d; e.step = s; e.layer = l; e.kind = k; e.prim = prim;
+        e.macs = macs; e.bytes_recv = rb; e.bytes_sent = sb; e.tag = tg;
+        trace_[d].push_back(e);
+    };
+    if (kind == 0) {   // step_reference: device 0, whole image
+        for (const Layer& d : m_.layers) {
+            const int lh = h_ / d.scale_in, lw = w_ / d.scale_in;
+            ev(0, d.id, COMPUTE, AG, macs_of_layer(d, Region{0, lh, lh, lw}), 0, 0, 0);
+        }
+        return;
+    }
+    if (kind == 3) {   // step_naive: every device its own row / column patch
+        const bool by_rows = s % 2 == 0;
+        const int ph = by_rows ? h_ / n : h_, pw = by_rows ? w_ : w_ / n;
+        for (int dv = 0; dv < n; ++dv)
+            for (const Layer& d : m_.layers) {
+                const int lh = ph / d.scale_in, lw = pw / d.scale_in;
+                ev(dv, d.id, COMPUTE, AG, macs_of_layer(d, Region{0, lh, lh, lw}), 0, 0, 0);
+            }
+        return;
+    }
+    const bool displaced = kind == 2;
+    for (int dv = 0; dv < n; ++dv) {
+        const PatchSpec& sp = specs_[std::min<size_t>(dv, specs_.size() - 1)];
+        for (const Layer& d : m_.layers) {
+            const int l = d.id;
+            const Region& reg = sp.layer_in[l];
+            if (d.needs_gather()) {
+                const uint64_t own = uint64_t(d.in_ch) * reg.rows() * reg.full_w * 4;
+                const uint64_t xfer = own * uint64_t(n - 1);
+                int& cs = tr_act_step_[dv][l];
+                if (!displaced) {
+                    if (n > 1) {
+                        ev(dv, l, POST, AG, 0, xfer, xfer, tag(s, l, AG));
+                        ev(dv, l, WAIT, AG, 0, 0, 0, tag(s, l, AG));
+                    }
+                    cs = s;
+                } else {
+                    if (n > 1) {
+                        ev(dv, l, POST, AG, 0, xfer, xfer, tag(s, l, AG));
+                        if (cs >= 0 && cs == s - 2) {
+                            ev(dv, l, WAIT, AG, 0, 0, 0, tag(s - 1, l, AG));
+                            cs = s - 1;
+                        }
+                    }
+                    if (n == 1) cs = s;
+                }
+            } else if (d.kind == Kind::GroupNorm) {
+                const uint64_t sb = uint64_t(d.groups) * 2 * 8 * uint64_t(n - 1);
+                int& gs = tr_gn_step_[dv][l];
+                if (!displaced) {
+                    if (n > 1) {
+                        ev(dv, l, POST, SR, 0, sb, sb, tag(s, l, SR));
+                        ev(dv, l, WAIT, SR, 0, 0, 0, tag(s, l, SR));
+                    }
+                    gs = s;
+                } else {
+                    if (n > 1) {
+                        ev(dv, l, POST, SR, 0, sb, sb, tag(s, l, SR));
+                        if (gs >= 0 && gs == s - 2) {
+                            ev(dv, l, WAIT, SR, 0, 0, 0, tag(s - 1, l, SR));
+                            gs = s - 1;
+                        }
+                    }
+                    if (n == 1) gs = s;
+                }
+            }
+            ev(dv, l, COMPUTE, AG, macs_of_layer(d, reg), 0, 0, 0);
+        }
+    }
+}
+
 void Runner::run_bands(std::vector<std::unique_ptr<Program>>& progs, int t, int s, bool displaced) {
     const bool exchanging = &progs == &bands_;   // naive patch programs never exchange or post
     if (displaced) check_displaced_ready(s);
@@ -1145,6 +1242,7 @@ void Runner::sample_naive(const float* x_T, const int* ts, int n, const std::vec
         }
         run_naive_patches(*progs, ts[i], i);
         count_macs(i, true);
+        record_trace(i, 3);
         ddim_update(nx_, neps_, nx_, (long long)img, C, abar_of[i], abar_of[i + 1], Elem::F32,
                     nullptr, 0, p->cs);
         launches_ += 1;
@@ -1185,6 +1283,7 @@ void Runner::step(int entry, const float* x, int t, int s, float* eps) {
         CUDA_CHECK(cudaMemcpyAsync(h_eps_, neps_, img * 4, cudaMemcpyDeviceToHost, p.cs));
         CUDA_CHECK(cudaStreamSynchronize(p.cs));
         count_macs(s, true);
+        record_trace(s, 3);
         check_flags("step_naive");
         std::memcpy(eps, h_eps_, img * 4);
         return;
@@ -1200,6 +1299,7 @@ void Runner::step(int entry, const float* x, int t, int s, float* eps) {
     run_bands(t, s, displaced);
     store_eps(eps);
     count_macs(s, false);
+    record_trace(s, e == STEP_REFERENCE ? 0 : displaced ? 2 : 1);
     check_flags(e == STEP_REFERENCE ? "step_reference" : "run_step");
     end_profile();
 }
@@ -1282,6 +1382,10 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
         volumes_.statreduce_recv += graph_vol_.statreduce_recv;
         volumes_.statreduce_sent += graph_vol_.statreduce_sent;
         launches_ += graph_launches_;
+        for (int i = 0; i < n; ++i)
+            record_trace(i, o_.mode == MODE_REFERENCE                          ? 0
+                            : (o_.mode == MODE_DISPLACED && i >= 1 + o_.warmup) ? 2
+                                                                                : 1);
     } else {
     for (auto& b : bands_) b->prepare_temb_plan(ts, n);   // outside any capture (synchronous)
     const uint64_t macs0 = total_macs_;
@@ -1333,6 +1437,7 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
         run_bands(t, i, displaced);
         for (auto& b : bands_) b->use_temb_step(-1);
         count_macs(i, false);
+        record_trace(i, o_.mode == MODE_REFERENCE ? 0 : displaced ? 2 : 1);
         const int t_next = i + 1 < n ? ts[i + 1] : -1;
         const double a_t = abar_at(t), a_n = abar_at(t_next);
         for (auto& b : bands_) {

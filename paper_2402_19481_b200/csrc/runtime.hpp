@@ -49,6 +49,17 @@ struct CommVolumes {
     uint64_t statreduce_recv = 0, statreduce_sent = 0;
 };
 
+// One entry of the reference's RawTrace (proj/include/patchsim/trace.hpp:18-35): per-device
+// program order, no wall clock.  kind 0 Compute / 1 Post / 2 Wait; prim 0 AllGather / 1 Halo /
+// 2 StatReduce.  Post bytes use the reference hub's accounting (the full fp32 layer input
+// gathered to every device, collectives.cpp:70-72) so simulate_timeline sees the same
+// trace; the bytes the B200 runtime actually moves (halo rows, K/V bands, stats) are
+// reported separately by volumes().
+struct TraceEvent {
+    int device = 0, step = 0, layer = -1, kind = 0, prim = 0;
+    uint64_t macs = 0, bytes_recv = 0, bytes_sent = 0, tag = 0;
+};
+
 struct ProfileTotals {
     double conv_ms = 0, conv_flops = 0, gemm_ms = 0, gemm_flops = 0, gn_ms = 0, other_ms = 0;
     long launches = 0;
@@ -74,6 +85,7 @@ public:
     const PatchSpec& patch_spec(int device) const;
     long cached_input(int device, int layer, float* dst, int* nchw4);
     uint64_t total_macs() const { return total_macs_; }
+    const std::vector<TraceEvent>& trace(int device) const;
     std::vector<uint64_t> step_device_macs(int step) const;
     CommVolumes volumes() const { return volumes_; }
     ProfileTotals profile() const { return prof_; }
@@ -122,6 +134,10 @@ private:
     std::vector<int> posted_;      // per layer: last step whose gather exchange was posted
     std::vector<int> gn_posted_;   // per layer: last step whose GN stats were posted
     uint64_t total_macs_ = 0;
+    // RawTrace mirror (record_trace): per device events + the reference's cache-step state
+    std::vector<std::vector<TraceEvent>> trace_;
+    std::vector<std::vector<int>> tr_act_step_, tr_gn_step_;
+    void record_trace(int s, int kind);   // kind: 0 reference, 1 sync, 2 displaced, 3 naive
     std::vector<std::vector<uint64_t>> step_device_macs_;
     CommVolumes volumes_;
     ProfileTotals prof_;

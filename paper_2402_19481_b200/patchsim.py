@@ -276,6 +276,21 @@ class PatchRunner:
         return dict(zip(["allgather_recv", "allgather_sent", "halo_recv", "halo_sent",
                          "statreduce_recv", "statreduce_sent"], (int(x) for x in v)))
 
+    def trace(self, device=0):
+        """RawTrace events of one device (PatchRunner::trace(), trace.hpp:18-35) as tuples
+        (device, step, layer, kind, prim, macs, bytes_recv, bytes_sent, tag)."""
+        n = N.lib().pp_runner_trace(self._r, device, None, 0)
+        if n < 0:
+            N.check(-1)
+        out = np.zeros((max(n, 1), 9), dtype=np.uint64)
+        N.lib().pp_runner_trace(self._r, device, _p(out), n)
+        rows = []
+        for r in out[:n]:
+            v = [int(x) for x in r]
+            v[2] = v[2] - (1 << 64) if v[2] >= (1 << 63) else v[2]
+            rows.append(tuple(v))
+        return rows
+
     def sample(self, x_T, timesteps, alpha_bar, trajectory=False):
         """sample() (proj/src/sampler.cpp:76-95) with the loop on the GPU."""
         x_T = _f32(x_T)

@@ -5,6 +5,8 @@ Tolerances (BASELINE.json north_star): relative L2 <= 1e-3 in fp32-accumulate mo
 (fp32 storage, TF32 tensor cores) and <= 2e-2 in bf16.  Patch partitioning and halo
 indexing are integer logic and are compared bit-exactly elsewhere.
 """
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -203,3 +205,54 @@ def test_fused_conv_groupnorm_forward(dtype, monkeypatch):
     r = P.PatchRunner(P.build_model(cfg, 77), cond, hw, hw, mode="reference", dtype=dtype)
     eps = r.run_step(x, 700, 0)
     assert rel(eps, ref) <= EPS_TOL[dtype], rel(eps, ref)
+
+
+def _ref_lib():
+    from oracle import ref as R
+    if not R.available():
+        pytest.skip("oracle/_ref (reference build) not available")
+    return R
+
+
+@pytest.mark.parametrize("mode,n,warmup", [("displaced", 2, 1), ("displaced", 4, 0), ("sync-pp", 2, 4),
+                                           ("reference", 1, 4), ("naive", 2, 4), ("displaced", 1, 1)])
+def test_trace_matches_reference(mode, n, warmup):
+    # RawTrace (proj/include/patchsim/trace.hpp:18-35) of the B200 runner == the reference
+    # PatchRunner's trace for the same run_step calls, event by event
+    R = _ref_lib()
+    cfg, hw = TOY, 32
+    cond = O.random_condition(cfg.cond_dim, 7)
+    x = O.random_normal(1, cfg.in_channels, hw, hw, 1234)
+    rm = R.Model(dataclasses.astuple(cfg), 42)
+    rr = R.PatchRunner(rm, cond, hw, hw, mode=mode, n_devices=n, warmup=warmup)
+    pr = P.PatchRunner(P.build_model(cfg, 42), cond, hw, hw, mode=mode, n_devices=n,
+                       warmup_steps=warmup, dtype="bf16")
+    for s, t in enumerate([750, 500, 250, 0]):
+        rr.step("run_step", x, t, s)
+        pr.run_step(x, t, s)
+    for d in range(pr.n_devices):
+        assert pr.trace(d) == rr.trace(d), d
+
+
+def test_trace_after_graph_sample_matches_reference():
+    R = _ref_lib()
+    cfg, hw = TOY, 32
+    cond = O.random_condition(cfg.cond_dim, 7)
+    x = O.random_normal(1, cfg.in_channels, hw, hw, 1234)
+    abar = O.make_schedule()
+    plan = O.make_plan(1000, 4)
+    pr = P.PatchRunner(P.build_model(cfg, 42), cond, hw, hw, mode="displaced", n_devices=2,
+                       warmup_steps=1, dtype="bf16")
+    pr.sample(x, plan, abar)
+    pr.sample(x, plan, abar)   # second call replays the captured CUDA graph
+    # every sample() is a fresh run (run_sampling builds a new PatchRunner, runtime.cpp:494-526)
+    expect = {0: [], 1: []}
+    for _ in range(2):
+        rr = R.PatchRunner(R.Model(dataclasses.astuple(cfg), 42), cond, hw, hw, mode="displaced",
+                           n_devices=2, warmup=1)
+        for s, t in enumerate(plan):
+            rr.step("run_step", x, int(t), s)
+        for d in range(2):
+            expect[d] += rr.trace(d)
+    for d in range(2):
+        assert pr.trace(d) == expect[d], d
