@@ -28,7 +28,8 @@ namespace pp {
 
 namespace {
 
-constexpr int kThreads = 224;   // warp 0: TMA, 1: MMA, 2-5: epilogue, 6: TMA
+constexpr int kThreads = 352;   // warp 0: TMA, 1: MMA, 2-5 + 7-10: epilogue, 6: TMA
+constexpr int kEpiThreads = 256;
 constexpr int kTileM = 128;
 constexpr int kBlockBytes = 128;   // K block = 128 bytes of each operand row
 constexpr int kTmemCols = 512;     // 2 accumulators x 256 columns
@@ -40,7 +41,7 @@ __device__ __forceinline__ float round_tf32(float x) {
     return __uint_as_float(r);
 }
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 struct TileCoord {
     int m, ty, tx, nt, split;
@@ -289,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int s = 0; s < 2; ++s) {
             ptx::mbar_init(&st.tfull_bar[s], 1);
-            ptx::mbar_init(&st.tempty_bar[s], 4 * P);
+            ptx::mbar_init(&st.tempty_bar[s], 8 * P);
         }
         ptx::fence_barrier_init();
         ptx::fence_proxy_async();
@@ -315,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int conv = a.mode != 0;
     const int a_box_bytes = conv ? a.rows_box * a.w_box * kBlockBytes : int(a_slot);
 
-    if (warp == 0 || warp == kThreads / 32 - 1) {
+    if (warp == 0 || warp == 6) {
         // ===== TMA producers: two warps, stage-interleaved (warp-uniform loops, one elected
         // lane issues).  One stage = kps consecutive 128-byte K blocks: kps A boxes and one
         // 3-D B box, completing on one full barrier.  Both warps walk the same (tile, K)
@@ -539,11 +540,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc_phase ^= 1;
             }
         }
-    } else if (warp >= 2 && warp <= 5) {
-        // ===== epilogue (warps 2..5; TMEM lane quarter = warp % 4) =====
+    } else if ((warp >= 2 && warp <= 5) || warp >= 7) {
+        // ===== epilogue (warps 2-5 and 7-10; TMEM lane quarter = warp % 4, two warps per
+        // quarter: `half` 0 takes the even 16-column chunks, half 1 the odd ones) =====
         const int quarter = warp & 3;
+        const int half = warp >= 7 ? 1 : 0;
         const int r = quarter * 32 + lane;  // tile row owned by this thread
-        const int et = threadIdx.x - 64;    // 0..127
+        const int et = warp <= 5 ? int(threadIdx.x) - 64 : int(threadIdx.x) - 96;   // 0..255
         float* sgn_warp = st.gn + quarter * 2 * a.block_n;   // [block_n / cpg][2] used
         // accumulator release: the MMA issuer (the leader's, for a pair) waits for 4*P warps
         const uint32_t tempty_leader = kPair ? ptx::mapa(ptx::smem_u32(st.tempty_bar), 0) : 0u;
@@ -589,7 +592,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int eb_out = (kTF32 || a.out_f32) ? 4 : 2;
             uint8_t* srow = stage_out ? smem + size_t(r) * a.block_n * eb_out : nullptr;
             uint8_t* srow1 = a.gn_apply ? nullptr : srow;   // fused GN: pass 1 stores nothing
-            for (int c = et; c < a.block_n; c += 128)
+            for (int c = et; c < a.block_n; c += kEpiThreads)
                 sbias[c] = (a.bias && nbase + c < a.n_valid) ? a.bias[nbase + c] : 0.0f;
             ptx::mbar_wait(&st.tfull_bar[cur], cur_phase);
             ptx::tc_fence_after();
@@ -616,7 +619,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float4* part = reinterpret_cast<float4*>(a.partial) +
                                size_t(tile_id) * (kTileM / 4) * a.block_n + r;
                 if (first) {
-                    for (int c0 = 0; c0 < a.block_n; c0 += 16) {
+                    for (int c0 = half * 16; c0 < a.block_n; c0 += 32) {
                         float v[16];
                         ptx::tmem_ld16(t_row + c0, v);
 #pragma unroll
@@ -639,33 +642,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __threadfence();
                 }
                 epi_bar();
-                // 64 partial columns (16 loads) in flight per round trip
-                for (int cb = 0; cb < a.block_n; cb += 64) {
-                    const int nc = min(64, a.block_n - cb);
-                    float o[64];
+                for (int c0 = half * 16; c0 < a.block_n; c0 += 32) {
+                    float o[16], v[16];
                     if (valid) {
 #pragma unroll
-                        for (int j = 0; j < 64; j += 4) {
-                            if (j < nc) {
-                                const float4 q = __ldcg(part + size_t((cb + j) / 4) * kTileM);
-                                o[j] = q.x; o[j + 1] = q.y; o[j + 2] = q.z; o[j + 3] = q.w;
-                            }
+                        for (int j = 0; j < 16; j += 4) {
+                            const float4 q = __ldcg(part + size_t((c0 + j) / 4) * kTileM);
+                            o[j] = q.x; o[j + 1] = q.y; o[j + 2] = q.z; o[j + 3] = q.w;
                         }
                     }
+                    ptx::tmem_ld16(t_row + c0, v);
+                    if (valid) {
 #pragma unroll
-                    for (int c1 = 0; c1 < 64; c1 += 16) {
-                        if (c1 < nc) {
-                            float v[16];
-                            ptx::tmem_ld16(t_row + cb + c1, v);
-                            if (valid) {
-#pragma unroll
-                                for (int j = 0; j < 16; ++j) v[j] = v[j] + o[c1 + j];
-                            }
-                            if (a.gn_apply) ptx::tmem_st16(t_row + cb + c1, v);   // acc + partial
-                            finish_chunk<kTF32>(a, v, sbias, cb + c1, nbase + cb + c1, p, valid,
-                                                sgn_warp, lane, srow1);
-                        }
+                        for (int j = 0; j < 16; ++j) v[j] = v[j] + o[j];
                     }
+                    if (a.gn_apply) ptx::tmem_st16(t_row + c0, v);   // acc + partial
+                    finish_chunk<kTF32>(a, v, sbias, c0, nbase + c0, p, valid, sgn_warp, lane, srow1);
                 }
                 if (!a.gn_apply) release(cur);
                 if (et == 0) {
@@ -673,7 +665,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     *ready = 0u;
                 }
             } else {
-                for (int c0 = 0; c0 < a.block_n; c0 += 16) {
+                for (int c0 = half * 16; c0 < a.block_n; c0 += 32) {
                     float v[16];
                     ptx::tmem_ld16(t_row + c0, v);
                     finish_chunk<kTF32>(a, v, sbias, c0, nbase + c0, p, valid, sgn_warp, lane, srow1);
@@ -703,7 +695,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int sub = et & 7;
                 const unsigned gmask = 0xFFu << (lane & 24);
                 const int n_e = 4 * cpg;
-                for (int gl = et >> 3; gl < gn_here; gl += 16) {
+                for (int gl = et >> 3; gl < gn_here; gl += kEpiThreads / 8) {
                     double s = 0.0, q = 0.0;
                     for (int e = sub; e < n_e; e += 8) {
                         const int w = e / cpg;
@@ -737,7 +729,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // in flight), the P partials are added in order -> deterministic
                     const int G = a.gn_groups;
                     int P = 1;
-                    while (P * 2 * gn_here <= 128 && P * 2 * gn_here <= 2 * a.block_n) P *= 2;
+                    while (P * 2 * gn_here <= kEpiThreads && P * 2 * gn_here <= 2 * a.block_n) P *= 2;
                     double* sfold = reinterpret_cast<double*>(st.gn);   // [P][gn_here][2]
                     if (et < P * gn_here) {
                         const int gl = et % gn_here, part = et / gn_here;
@@ -760,7 +752,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         sfold[(part * gn_here + gl) * 2 + 1] = q;
                     }
                     epi_bar();
-                    for (int gl = et; gl < gn_here; gl += 128) {
+                    for (int gl = et; gl < gn_here; gl += kEpiThreads) {
                         double s = 0.0, q = 0.0;
                         for (int part = 0; part < P; ++part) {
                             s += sfold[(part * gn_here + gl) * 2];
@@ -793,7 +785,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float* s_sc = st.gn;
                 float* s_sh = s_sc + a.block_n;
                 float* s_te = s_sh + a.block_n;
-                for (int c = et; c < a.block_n && !(a.debug & 64); c += 128) {
+                for (int c = et; c < a.block_n && !(a.debug & 64); c += kEpiThreads) {
                     const int g = (nbase + c) / a.gn_cpg;
                     const double m = __ldcg(a.gn_out + g * 2), q = __ldcg(a.gn_out + g * 2 + 1);
                     const double var = __dsub_rn(q, __dmul_rn(m, m));
@@ -812,7 +804,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 ptx::tmem_wait_st();
                 const bool f32out = kTF32 || a.out_f32;
-                for (int c0 = 0; c0 < a.block_n && !(a.debug & 128); c0 += 16) {
+                for (int c0 = half * 16; c0 < a.block_n && !(a.debug & 128); c0 += 32) {
                     float v[16], cb[16], cs[16], ch[16];
                     ptx::tmem_ld16(t_row + c0, v);
 #pragma unroll
@@ -1304,7 +1296,21 @@ void launch_variant(const GemmPlan& p, cudaStream_t s) {
                p.tmA, p.tmB, p.tmD, p.a);
 }
 
-void launch_gemm(const GemmPlan& p, cudaStream_t s) {
+void launch_gemm(const GemmPlan& p0, cudaStream_t s) {
+    // PP_DEBUG_GEMM=<bits>: timing experiments only (results are wrong): kernel debug flags
+    // applied to every GEMM launch (1 no MMA, 2 no TMA, 4 no epilogue work)
+    static const int dbg = [] {
+        const char* v = std::getenv("PP_DEBUG_GEMM");
+        return v ? std::atoi(v) : 0;
+    }();
+    GemmPlan pd;
+    const GemmPlan* pp_ = &p0;
+    if (dbg) {
+        pd = p0;
+        pd.a.debug = dbg;
+        pp_ = &pd;
+    }
+    const GemmPlan& p = *pp_;
     const bool tf32 = p.elem == Elem::F32;
     if (tf32)
         p.pair ? launch_variant<true, true>(p, s) : launch_variant<true, false>(p, s);

@@ -658,7 +658,15 @@ void Program::gn_stats(const Group& g, int par) {
     count(1);
 }
 
+// PP_SKIP=<letters>: timing experiments only (results are wrong): g = GroupNorm passes,
+// o = other pointwise / attention-side kernels are not launched
+static bool skip_kind(char k) {
+    static const char* v = std::getenv("PP_SKIP");
+    return v && std::strchr(v, k);
+}
+
 void Program::gn_apply(const Group& g, int mode, int par_cur, int par_prev) {
+    if (skip_kind('g')) return;
     const Act& in = input_of(g.first);
     const LayerX& x = lx[g.first];
     const Layer& d = m->layers[g.first];
@@ -695,6 +703,7 @@ void Program::gn_apply(const Group& g, int mode, int par_cur, int par_prev) {
 }
 
 void Program::simple(const Group& g, int par) {
+    if (skip_kind('o')) return;
     const Layer& d = m->layers[g.first];
     const Act& in = input_of(g.first);
     const int L = int(m->layers.size());
