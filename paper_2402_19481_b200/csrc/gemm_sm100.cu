@@ -28,8 +28,10 @@ namespace pp {
 
 namespace {
 
-constexpr int kThreads = 352;   // warp 0: TMA, 1: MMA, 2-5 + 7-10: epilogue, 6: TMA
-constexpr int kEpiThreads = 256;
+// warp 0: TMA, 1: MMA, 6: TMA, the rest epilogue: kEpiPerQuarter warps per TMEM lane quarter
+constexpr int kEpiPerQuarter = 3;
+constexpr int kEpiThreads = 128 * kEpiPerQuarter;
+constexpr int kThreads = 96 + kEpiThreads;
 constexpr int kTileM = 128;
 constexpr int kBlockBytes = 128;   // K block = 128 bytes of each operand row
 constexpr int kTmemCols = 512;     // 2 accumulators x 256 columns
@@ -41,7 +43,9 @@ __device__ __forceinline__ float round_tf32(float x) {
     return __uint_as_float(r);
 }
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+}
 
 struct TileCoord {
     int m, ty, tx, nt, split;
@@ -127,7 +131,7 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
                     const float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                     if (srow)
                         *reinterpret_cast<float4*>(srow + (c0 + j) * 4) = o;
-                    else if (!a.gn_apply)
+                    else if (!a.gn_apply && !(a.debug & 512))
                         *reinterpret_cast<float4*>(dst + j) = o;
                 }
             } else {
@@ -178,7 +182,7 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
                     }
                     if (srow)
                         *reinterpret_cast<uint4*>(srow + (c0 + j) * 2) = o;
-                    else if (!a.gn_apply)
+                    else if (!a.gn_apply && !(a.debug & 512))
                         *reinterpret_cast<uint4*>(dst + j) = o;
                 }
             } else {
@@ -207,7 +211,7 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
             }
         }
     }
-    if (a.gn_groups) {
+    if (a.gn_groups && !(a.debug & 256)) {
         // Column sums over the warp's 32 rows (invalid rows contribute 0) by a butterfly
         // transpose-reduce: each xor step halves the columns a lane keeps, so 16 columns
         // cost 16+8+4+2+1 shuffles per quantity instead of 16*5.  Lane l ends up with the
@@ -290,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int s = 0; s < 2; ++s) {
             ptx::mbar_init(&st.tfull_bar[s], 1);
-            ptx::mbar_init(&st.tempty_bar[s], 8 * P);
+            ptx::mbar_init(&st.tempty_bar[s], 4 * kEpiPerQuarter * P);
         }
         ptx::fence_barrier_init();
         ptx::fence_proxy_async();
@@ -540,13 +544,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc_phase ^= 1;
             }
         }
-    } else if ((warp >= 2 && warp <= 5) || warp >= 7) {
-        // ===== epilogue (warps 2-5 and 7-10; TMEM lane quarter = warp % 4, two warps per
-        // quarter: `half` 0 takes the even 16-column chunks, half 1 the odd ones) =====
+    } else if (warp >= 2 && warp != 6) {
+        // ===== epilogue (warps 2-5 and 7..; TMEM lane quarter = warp % 4, kEpiPerQuarter warps
+        // per quarter: warp `half` of its quarter takes the 16-column chunks half, half + K, ...
         const int quarter = warp & 3;
-        const int half = warp >= 7 ? 1 : 0;
+        const int half = warp <= 5 ? 0 : (warp - 3) / 4;   // 7-10 -> 1, 11-14 -> 2
         const int r = quarter * 32 + lane;  // tile row owned by this thread
-        const int et = warp <= 5 ? int(threadIdx.x) - 64 : int(threadIdx.x) - 96;   // 0..255
+        const int et = warp <= 5 ? int(threadIdx.x) - 64 : int(threadIdx.x) - 96;   // 0..kEpiThreads-1
+        constexpr int kCS = 16 * kEpiPerQuarter;   // chunk stride of one warp
         float* sgn_warp = st.gn + quarter * 2 * a.block_n;   // [block_n / cpg][2] used
         // accumulator release: the MMA issuer (the leader's, for a pair) waits for 4*P warps
         const uint32_t tempty_leader = kPair ? ptx::mapa(ptx::smem_u32(st.tempty_bar), 0) : 0u;
@@ -619,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float4* part = reinterpret_cast<float4*>(a.partial) +
                                size_t(tile_id) * (kTileM / 4) * a.block_n + r;
                 if (first) {
-                    for (int c0 = half * 16; c0 < a.block_n; c0 += 32) {
+                    for (int c0 = half * 16; c0 < a.block_n; c0 += kCS) {
                         float v[16];
                         ptx::tmem_ld16(t_row + c0, v);
 #pragma unroll
@@ -642,7 +647,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __threadfence();
                 }
                 epi_bar();
-                for (int c0 = half * 16; c0 < a.block_n; c0 += 32) {
+                for (int c0 = half * 16; c0 < a.block_n; c0 += kCS) {
                     float o[16], v[16];
                     if (valid) {
 #pragma unroll
@@ -665,14 +670,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     *ready = 0u;
                 }
             } else {
-                for (int c0 = half * 16; c0 < a.block_n; c0 += 32) {
+                for (int c0 = half * 16; c0 < a.block_n; c0 += kCS) {
                     float v[16];
                     ptx::tmem_ld16(t_row + c0, v);
                     finish_chunk<kTF32>(a, v, sbias, c0, nbase + c0, p, valid, sgn_warp, lane, srow1);
                 }
                 if (!a.gn_apply) release(cur);
             }
-            if (stage_out && !a.gn_apply) {
+            if (stage_out && !a.gn_apply && !(a.debug & 512)) {
                 ptx::fence_proxy_async();   // staged rows -> visible to the TMA engine
                 epi_bar();
                 if (et == 0) {
@@ -684,7 +689,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::bulk_wait_all();
                 }
             }
-            if (a.gn_groups) {
+            if (a.gn_groups && !(a.debug & 256)) {
                 epi_bar();
                 const int cpg = a.gn_cpg;
                 const int g0 = nbase / cpg;
@@ -804,7 +809,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 ptx::tmem_wait_st();
                 const bool f32out = kTF32 || a.out_f32;
-                for (int c0 = half * 16; c0 < a.block_n && !(a.debug & 128); c0 += 32) {
+                for (int c0 = half * 16; c0 < a.block_n && !(a.debug & 128); c0 += kCS) {
                     float v[16], cb[16], cs[16], ch[16];
                     ptx::tmem_ld16(t_row + c0, v);
 #pragma unroll
