@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (a.b_static && tile0 < total_tiles && !(a.debug & 2)) {
             const TileCoord tc = decode_tile<P>(a, tile0, rank);
             const int kb0 = tc.split * a.kb_per_split;
-            const int kb1 = min(kb0 + a.kb_per_split, a.k_blocks);
+            const int kb1 = (a.debug & 1024) ? kb0 + 1 : min(kb0 + a.kb_per_split, a.k_blocks);
             pre = min(stages, (kb1 - kb0 + kps - 1) / kps);
             const int bcoord = tc.nt * a.block_n + rank * (a.block_n / a.n_sub / P);
             for (int i = pw; i < pre; i += 2) {
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = tile0; t < total_tiles; t += tile_step) {
             const TileCoord tc = decode_tile<P>(a, t, rank);
             const int kb0 = tc.split * a.kb_per_split;
-            const int kb1 = min(kb0 + a.kb_per_split, a.k_blocks);
+            const int kb1 = (a.debug & 1024) ? kb0 + 1 : min(kb0 + a.kb_per_split, a.k_blocks);
             const int oy0 = tc.ty * a.rows_box, ox0 = tc.tx * a.w_box;
             const int bcoord = tc.nt * a.block_n + rank * (a.block_n / a.n_sub / P);
             const int arow = tc.ty * kTileM;
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = tile0; t < total_tiles; t += tile_step) {
             const TileCoord tc = decode_tile<P>(a, t, 0);
             const int kb0 = tc.split * a.kb_per_split;
-            const int kb1 = min(kb0 + a.kb_per_split, a.k_blocks);
+            const int kb1 = (a.debug & 1024) ? kb0 + 1 : min(kb0 + a.kb_per_split, a.k_blocks);
             ptx::mbar_wait(&st.tempty_bar[acc], acc_phase ^ 1);
             ptx::tc_fence_after();
             const uint32_t d_tmem = tmem_base + uint32_t(acc * 256);
