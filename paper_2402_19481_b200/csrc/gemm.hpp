@@ -41,6 +41,13 @@ struct GemmArgs {
     int kps;                  // 128-byte K blocks per pipeline stage (1 or 2)
     int n_sub;                // MMAs per K step along N (2: block_n > 256, N = block_n / 2 each)
     int n_acc;                // TMEM accumulators in the MMA <-> epilogue ring (1 or 2)
+    // slab mode (stride-1 conv, rows_box == 1): A from a 2-slot ring of im2col slabs
+    // [3 rows][slab_px = w_box + 2][128 B] shared by the nine taps of a channel chunk; the
+    // virtual K index is chunk * 10 + tap (tap 9 empty), B comes from a 4-D map
+    int slab;
+    int slab_px;
+    uint32_t slab_bytes;      // smem per slot (1024-aligned)
+    uint32_t slab_box_bytes;  // TMA bytes per slab
     uint32_t idesc;           // tcgen05 instruction descriptor
     // epilogue
     void* out;                // output base (already offset to pixel 0 of the band)

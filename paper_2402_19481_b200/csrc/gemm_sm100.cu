@@ -71,6 +71,8 @@ struct SmemTail {
     uint64_t* empty_bar;
     uint64_t* tfull_bar;
     uint64_t* tempty_bar;
+    uint64_t* slab_full;    // [2] A-slab ring (slab mode)
+    uint64_t* slab_empty;   // [2]
     uint32_t* tmem_slot;
     int* flags;        // [4]
     float* bias;       // [2][block_n]
@@ -79,7 +81,7 @@ struct SmemTail {
 
 // Sized by block_n so that the fused-GN variant keeps the same pipeline depth.
 __host__ __device__ inline size_t tail_bytes(int stages, bool gn, int block_n) {
-    return size_t(2 * stages + 4) * 8 + 16 + 16 + size_t(2) * block_n * 4 +
+    return size_t(2 * stages + 8) * 8 + 16 + 16 + size_t(2) * block_n * 4 +
            (gn ? size_t(4) * block_n * 2 * 4 : 0);
 }
 
@@ -91,6 +93,14 @@ __host__ __device__ inline size_t tail_bytes(int stages, bool gn, int block_n) {
 template <bool kPair>
 __device__ __forceinline__ void load_b(uint8_t* sb, const CUtensorMap* tm, uint64_t* bar,
                                        uint32_t bar_cl, int bcoord, int kb, const GemmArgs& a) {
+    if (a.slab) {   // virtual K block kb = chunk * 10 + tap (two taps per stage, tap 9 is OOB)
+        const int chunk = kb / 10, tap = kb - chunk * 10;
+        if (kPair)
+            ptx::tma_load_4d_pair(sb, tm, bar_cl, 0, bcoord, chunk, tap);
+        else
+            ptx::tma_load_4d(sb, tm, bar, 0, bcoord, chunk, tap);
+        return;
+    }
     const int hrow = a.block_n / a.n_sub;                 // weight rows per N half
     const int brows = hrow / (kPair ? 2 : 1);             // rows this CTA stages per half
     for (int h = 0; h < a.n_sub; ++h) {
@@ -264,17 +274,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int kps = a.kps;                                      // K blocks per stage (1 or 2)
     const uint32_t a_slot = kTileM * kBlockBytes;               // one A box slot
     const uint32_t b_slot = uint32_t(a.block_n / P) * kBlockBytes;
-    const uint32_t a_stage_bytes = kps * a_slot;
+    // slab mode (stride-1 conv, one output row per tile): A comes from a 2-slot ring of im2col
+    // slabs (3 input rows x (w_box + 2) pixels x 128 B per channel chunk) that serve all nine
+    // taps; the stage ring then holds B only
+    const uint32_t a_stage_bytes = a.slab ? 0u : kps * a_slot;
+    uint8_t* const ring = smem + (a.slab ? 2u * a.slab_bytes : 0u);
     const uint32_t b_stage_bytes = kps * b_slot;
     const uint32_t stage_bytes = a_stage_bytes + b_stage_bytes;
     SmemTail st;
     {
-        uint8_t* p = smem + size_t(stages) * stage_bytes;
+        uint8_t* p = ring + size_t(stages) * stage_bytes;
         st.full_bar = reinterpret_cast<uint64_t*>(p);
         st.empty_bar = st.full_bar + stages;
         st.tfull_bar = st.empty_bar + stages;
         st.tempty_bar = st.tfull_bar + 2;
-        st.tmem_slot = reinterpret_cast<uint32_t*>(st.tempty_bar + 2);
+        st.slab_full = st.tempty_bar + 2;
+        st.slab_empty = st.slab_full + 2;
+        st.tmem_slot = reinterpret_cast<uint32_t*>(st.slab_empty + 2);
         st.flags = reinterpret_cast<int*>(st.tmem_slot + 4);
         st.bias = reinterpret_cast<float*>(st.flags + 4);
         st.gn = st.bias + 2 * a.block_n;
@@ -293,6 +309,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&st.empty_bar[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
+            ptx::mbar_init(&st.slab_full[s], 1);
+            ptx::mbar_init(&st.slab_empty[s], 1);
             ptx::mbar_init(&st.tfull_bar[s], 1);
             ptx::mbar_init(&st.tempty_bar[s], 4 * kEpiPerQuarter * P);
         }
@@ -318,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int total_tiles = (m_tiles + P - 1) / P * a.n_tiles * a.splits;
     const int tile0 = blockIdx.x / P, tile_step = gridDim.x / P;
     const int conv = a.mode != 0;
-    const int a_box_bytes = conv ? a.rows_box * a.w_box * kBlockBytes : int(a_slot);
+    const int a_box_bytes = a.slab ? 0 : conv ? a.rows_box * a.w_box * kBlockBytes : int(a_slot);
 
     if (warp == 0 || warp == 6) {
         // ===== TMA producers: two warps, stage-interleaved (warp-uniform loops, one elected
@@ -345,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int bcoord = tc.nt * a.block_n + rank * (a.block_n / a.n_sub / P);
             for (int i = pw; i < pre; i += 2) {
                 if (ptx::elect_one()) {
-                    uint8_t* sb = smem + size_t(i) * stage_bytes + a_stage_bytes;
+                    uint8_t* sb = ring + size_t(i) * stage_bytes + a_stage_bytes;
                     const int nk = min(kps, kb1 - (kb0 + i * kps));
                     if (rank == 0)
                         ptx::mbar_arrive_expect_tx(&st.full_bar[i],
@@ -373,6 +391,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         pdl_wait();
         int it = 0;
+        int sl_slot = 0;          // slab mode: A-slab ring slot / phase (both producer warps)
+        uint32_t sl_phase = 0;
+        const uint32_t slab_leader = kPair ? ptx::mapa(ptx::smem_u32(st.slab_full), 0) : 0u;
         for (int t = tile0; t < total_tiles; t += tile_step) {
             const TileCoord tc = decode_tile<P>(a, t, rank);
             const int kb0 = tc.split * a.kb_per_split;
@@ -388,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int nk = min(kps, kb1 - kb);
                 if ((it & 1) == pw) {
                     ptx::mbar_wait(&st.empty_bar[stage], phase ^ 1);
-                    uint8_t* sa = smem + size_t(stage) * stage_bytes;
+                    uint8_t* sa = ring + size_t(stage) * stage_bytes;
                     uint8_t* sb = sa + a_stage_bytes;
                     if (ptx::elect_one()) {
                         if (a.debug & 2) {   // micro-benchmark: barriers only, no data movement
@@ -399,8 +420,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 ptx::mbar_arrive_expect_tx(&st.full_bar[stage],
                                                            P * (nk * a_box_bytes + b_stage_bytes));
                             const uint32_t fb = kPair ? full_leader + uint32_t(stage) * 8u : 0u;
+                            if (a.slab && kb % 10 == 0) {
+                                // first stage of a channel chunk: its im2col slab (3 input rows
+                                // x (w_box + 2) pixels, TMA zero-fill = the left/right padding)
+                                ptx::mbar_wait(&st.slab_empty[sl_slot], sl_phase ^ 1);
+                                if (rank == 0)
+                                    ptx::mbar_arrive_expect_tx(&st.slab_full[sl_slot],
+                                                               P * a.slab_box_bytes);
+                                uint8_t* dst = smem + size_t(sl_slot) * a.slab_bytes;
+                                const int ch = kb / 10;
+                                if (kPair)
+                                    ptx::tma_load_5d_pair(dst, &tmA, slab_leader + uint32_t(sl_slot) * 8u,
+                                                          ch * kel, 0, ox0 - 1, 0, oy0);
+                                else
+                                    ptx::tma_load_5d(dst, &tmA, &st.slab_full[sl_slot], ch * kel, 0,
+                                                     ox0 - 1, 0, oy0);
+                            }
                             int c_j = cj, c_x = kx, c_y = ky;
-                            for (int j = 0; j < nk; ++j) {
+                            for (int j = 0; j < nk && !a.slab; ++j) {
                                 uint8_t* dst = sa + j * a_slot;
                                 if (!conv) {
                                     if (kPair)
@@ -436,6 +473,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __syncwarp();
                 }
                 ++it;
+                if (a.slab && kb % 10 == 8 && ++sl_slot == 2) {
+                    sl_slot = 0;
+                    sl_phase ^= 1;
+                }
                 for (int j = 0; j < nk; ++j) {
                     if (++cj == a.cin_chunks) {
                         cj = 0;
@@ -456,9 +497,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // Descriptors: stage s, block j, K step k = base + s * (stage_bytes >> 4) +
         // j * (slot >> 4) + 2 * k (the start address field is addr >> 4; +32 bytes per
         // 16-element bf16 / 8-element tf32 step).
-        const uint32_t smem0 = ptx::smem_u32(smem);
+        const uint32_t smem0 = ptx::smem_u32(ring);
         const uint64_t desc_a0 = ptx::smem_desc_sw128(smem0);
         const uint64_t desc_b0 = ptx::smem_desc_sw128(smem0 + a_stage_bytes);
+        const uint32_t slab0 = ptx::smem_u32(smem);   // slab mode: slot s at slab0 + s * slab_bytes
         const uint64_t desc_stride = stage_bytes >> 4;
         const uint64_t a_next = a_slot >> 4, b_next = b_slot >> 4;
         const uint32_t b_half = uint32_t(a.block_n / 2 / P) * kBlockBytes;   // n_sub == 2
@@ -466,6 +508,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t phase = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
+        int ms_slot = 0;          // slab mode: A-slab ring slot / phase
+        uint32_t ms_phase = 0;
         for (int t = tile0; t < total_tiles; t += tile_step) {
             const TileCoord tc = decode_tile<P>(a, t, 0);
             const int kb0 = tc.split * a.kb_per_split;
@@ -474,6 +518,65 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tc_fence_after();
             const uint32_t d_tmem = tmem_base + uint32_t(acc * 256);
             for (int kb = kb0; kb < kb1; kb += kps) {
+                if (a.slab) {
+                    // one stage = taps (sg, sg + 1) of channel chunk kb / 10 (tap 9 does not
+                    // exist): A rows of tap (ky, kx) start (ky * slab_px + kx) 128-byte rows
+                    // into the slab (a start address that is not swizzle-atom aligned)
+                    const int sg = kb % 10;
+                    if (sg == 0) {
+                        ptx::mbar_wait(&st.slab_full[ms_slot], ms_phase);
+                        ptx::tc_fence_after();
+                    }
+                    ptx::mbar_wait(&st.full_bar[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint64_t db = desc_b0 + uint64_t(stage) * desc_stride;
+                    const uint32_t sbase = slab0 + uint32_t(ms_slot) * a.slab_bytes;
+                    if (ptx::elect_one()) {
+                        if (!(a.debug & 1)) {
+#pragma unroll
+                            for (int j = 0; j < 2; ++j) {
+                                const int tap = sg + j;
+                                if (tap < 9) {
+                                    const int ky = tap / 3, kx = tap - 3 * ky;
+                                    const uint32_t off = uint32_t(ky * a.slab_px + kx);
+                                    // the SW128 XOR pattern is applied to absolute smem address
+                                    // bits (as TMA wrote it), so an unaligned start needs no base
+                                    // offset (measured: setting bits 49-51 breaks it)
+                                    const uint64_t da = ptx::smem_desc_sw128(sbase + off * kBlockBytes);
+                                    const uint32_t acc0 = (kb > kb0 || j > 0) ? 1u : 0u;
+                                    if (kPair) {
+                                        if (kTF32)
+                                            ptx::mma4_tf32_pair(d_tmem, da, db + j * b_next, a.idesc, acc0);
+                                        else
+                                            ptx::mma4_bf16_pair(d_tmem, da, db + j * b_next, a.idesc, acc0);
+                                    } else {
+                                        if (kTF32)
+                                            ptx::mma4_tf32(d_tmem, da, db + j * b_next, a.idesc, acc0);
+                                        else
+                                            ptx::mma4_bf16(d_tmem, da, db + j * b_next, a.idesc, acc0);
+                                    }
+                                }
+                            }
+                        }
+                        if (kPair) {
+                            ptx::mma_commit_pair(&st.empty_bar[stage], 3);
+                            if (sg == 8) ptx::mma_commit_pair(&st.slab_empty[ms_slot], 3);
+                        } else {
+                            ptx::mma_commit(&st.empty_bar[stage]);
+                            if (sg == 8) ptx::mma_commit(&st.slab_empty[ms_slot]);
+                        }
+                    }
+                    __syncwarp();
+                    if (sg == 8 && ++ms_slot == 2) {
+                        ms_slot = 0;
+                        ms_phase ^= 1;
+                    }
+                    if (++stage == stages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                    continue;
+                }
                 const bool two = kb + 1 < kb1 && kps == 2;
                 ptx::mbar_wait(&st.full_bar[stage], phase);
                 ptx::tc_fence_after();
@@ -1020,14 +1123,16 @@ uint32_t make_idesc(Elem e, int n, int m) {
     return d;
 }
 
-size_t smem_for(int block_n, int stages, bool gn, int pair, int kps) {
-    return size_t(stages) * kps * (kTileM * kBlockBytes + block_n / (pair ? 2 : 1) * kBlockBytes) +
-           1024 + tail_bytes(stages, gn, block_n);
+size_t smem_for(int block_n, int stages, bool gn, int pair, int kps, uint32_t slab_bytes = 0) {
+    const size_t a_stage = slab_bytes ? 0 : kTileM * kBlockBytes;
+    return size_t(2) * slab_bytes +
+           size_t(stages) * kps * (a_stage + block_n / (pair ? 2 : 1) * kBlockBytes) + 1024 +
+           tail_bytes(stages, gn, block_n);
 }
 
-int stages_for(int block_n, bool gn, int pair, int kps) {
+int stages_for(int block_n, bool gn, int pair, int kps, uint32_t slab_bytes = 0) {
     int s = 8;
-    while (s > 2 && smem_for(block_n, s, gn, pair, kps) > size_t(kSmemMax)) --s;
+    while (s > 2 && smem_for(block_n, s, gn, pair, kps, slab_bytes) > size_t(kSmemMax)) --s;
     return s;
 }
 
@@ -1141,11 +1246,16 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
     a.n_sub = bn > 256 ? 2 : 1;
     a.n_acc = bn > 256 ? 1 : 2;
     a.kps = a.n_sub == 2 ? 1 : choose_kps(bn, gn, pair);
+    if (a.slab) {
+        if (a.n_sub != 1) throw std::invalid_argument("slab conv: wide tiles unsupported");
+        a.kps = 2;   // one stage = two taps of a chunk
+    }
     a.splits = splits;
     a.kb_per_split = (k_blocks + splits - 1) / splits;
     a.kb_per_split = (a.kb_per_split + a.kps - 1) / a.kps * a.kps;   // whole stages per split
+    if (a.slab) a.kb_per_split = (a.kb_per_split + 9) / 10 * 10;       // whole channel chunks
     a.splits = (k_blocks + a.kb_per_split - 1) / a.kb_per_split;
-    a.stages = stages_for(bn, gn, pair, a.kps);
+    a.stages = stages_for(bn, gn, pair, a.kps, a.slab ? a.slab_bytes : 0u);
     a.idesc = make_idesc(p.elem, bn / a.n_sub, pair ? 2 * kTileM : kTileM);
     a.out = ep.out;
     a.out_ld = ep.out_ld;
@@ -1180,7 +1290,7 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
     const int P = pair ? 2 : 1;
     const int units = (m_tiles + P - 1) / P * a.n_tiles * a.splits;
     p.grid = P * std::min(units, num_sms / P);
-    p.smem = smem_for(bn, a.stages, gn, pair, a.kps);
+    p.smem = smem_for(bn, a.stages, gn, pair, a.kps, a.slab ? a.slab_bytes : 0u);
 }
 
 }  // namespace
@@ -1222,7 +1332,20 @@ void plan_conv(GemmPlan& p, Elem e, const void* in, int rows_in, int W, int C_in
     a.out_w = out_w;
     a.cin_chunks = C_in_pad / kel;
     a.m_pix = out_rows * out_w;
-    const int k_blocks = 9 * a.cin_chunks;
+    // slab mode: stride 1, one output row per tile (w_box > 64), unless PP_SLAB=0
+    static const bool slab_env = [] {
+        const char* v = std::getenv("PP_SLAB");
+        return !(v && v[0] == '0');
+    }();
+    a.slab = (slab_env && stride == 1 && a.rows_box == 1 && wb + 2 <= 256 && force_block_n <= 256 &&
+              !ep.gn_apply && !std::getenv("PP_WIDE"))
+                 ? 1 : 0;
+    if (a.slab) {
+        a.slab_px = wb + 2;
+        a.slab_box_bytes = uint32_t(3 * a.slab_px * kBlockBytes);
+        a.slab_bytes = (a.slab_box_bytes + 1023u) / 1024u * 1024u;
+    }
+    const int k_blocks = a.slab ? 10 * a.cin_chunks : 9 * a.cin_chunks;
 
     // A: 5-D view of the padded band [rows_in+2][W][C_in_pad]
     const int rows_pad = rows_in + 2;
@@ -1237,12 +1360,24 @@ void plan_conv(GemmPlan& p, Elem e, const void* in, int rows_in, int W, int C_in
         strides[0] = pix; strides[1] = 2 * pix; strides[2] = pix * W; strides[3] = 2 * pix * W;
     }
     box[0] = kel; box[1] = 1; box[2] = wb; box[3] = 1; box[4] = a.rows_box;
+    if (a.slab) {
+        box[2] = a.slab_px;
+        box[4] = 3;
+    }
     encode(&p.tmA, e, 5, in, dims, strides, box);
     finish_plan(p, a.tiles_y * a.tiles_x, n_pad, k_blocks, ep, sc, num_sms, force_splits,
                 force_block_n);
     // B: weights [n_pad][9*C_in_pad] viewed as [K blocks][n_pad][kel]: one box = kps blocks
-    encode_b(&p.tmB, e, weights, n_pad, 9 * C_in_pad, 9LL * C_in_pad,
-             a.block_n / (p.pair ? 2 : 1) / a.n_sub, a.kps);
+    if (a.slab) {
+        // B as [tap][chunk][n][kel]: box {kel, rows, 1 chunk, 2 taps}
+        uint64_t d[4] = {uint64_t(kel), uint64_t(n_pad), uint64_t(a.cin_chunks), 9};
+        uint64_t st[3] = {uint64_t(9) * C_in_pad * eb, uint64_t(kBlockBytes), uint64_t(C_in_pad) * eb};
+        uint32_t b[4] = {uint32_t(kel), uint32_t(a.block_n / (p.pair ? 2 : 1)), 1, 2};
+        encode(&p.tmB, e, 4, weights, d, st, b);
+    } else {
+        encode_b(&p.tmB, e, weights, n_pad, 9 * C_in_pad, 9LL * C_in_pad,
+                 a.block_n / (p.pair ? 2 : 1) / a.n_sub, a.kps);
+    }
     p.flops = 2.0 * a.m_pix * double(ep.n_valid) * 9.0 * C_in_pad;
     a.b_static = 1;   // conv weights
     plan_output_map(p, true);
