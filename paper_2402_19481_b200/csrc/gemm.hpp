@@ -84,6 +84,8 @@ struct GemmArgs {
     const void* b_base;       // B tensor (weights) and its size: with b_static, every CTA
     long long b_bytes;        // prefetches its 1/grid slice into L2 at kernel start
     int tma_store;            // 1: the CTA's last tile is stored through tmD (smem staging)
+    int up_w;                 // > 0: store the nearest-2x upsample (output row p of an up_w-wide
+                              //      map -> 2x2 block of the 2 up_w-wide output)
     int b_static;             // 1: B is weights (not written by an earlier kernel on the stream):
                               //    its first boxes are prefetched before griddepcontrol.wait
     int debug;                // micro-benchmarks only: bit0 = no MMA, bit1 = no TMA loads
@@ -114,6 +116,7 @@ struct EpilogueSpec {
     // GroupNorm statistics of the output (groups == 0: off)
     int gn_groups = 0;
     double* gn_out = nullptr;
+    int up_w = 0;             // plain GEMM: > 0 = fused nearest-2x upsample of the output
     // fused GroupNorm apply (requires gn_groups): `out` receives GN(conv) [SiLU] [+temb]
     // [+skip]; the raw conv output is never stored
     bool gn_apply = false;

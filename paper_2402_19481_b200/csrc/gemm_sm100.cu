@@ -122,9 +122,16 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = v[j] * a.scale + sbias[c0 + j];
     const bool full = n0 + 16 <= a.n_valid;
+    // fused nearest 2x upsample of the output (up_w = input width): row p -> the 2x2 block
+    long long prow = p;
+    if (a.up_w) {
+        const long long py = p / a.up_w, px = p - py * a.up_w;
+        prow = (2 * py) * (2LL * a.up_w) + 2 * px;
+    }
+    const long long up_dy = 2LL * a.up_w * a.out_ld;   // elements to the row below
     if (valid) {
         if (kTF32 || a.out_f32) {
-            float* dst = reinterpret_cast<float*>(a.out) + p * a.out_ld + n0;
+            float* dst = reinterpret_cast<float*>(a.out) + prow * a.out_ld + n0;
             const float* res =
                 a.residual ? reinterpret_cast<const float*>(a.residual) + p * a.res_ld + n0 : nullptr;
             if (full && (a.out_ld % 4) == 0 && (!res || (a.res_ld % 4) == 0)) {
@@ -139,10 +146,16 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
                         v[j + 2] = round_tf32(v[j + 2]); v[j + 3] = round_tf32(v[j + 3]);
                     }
                     const float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                    if (srow)
+                    if (srow) {
                         *reinterpret_cast<float4*>(srow + (c0 + j) * 4) = o;
-                    else if (!a.gn_apply && !(a.debug & 512))
+                    } else if (!a.gn_apply && !(a.debug & 512)) {
                         *reinterpret_cast<float4*>(dst + j) = o;
+                        if (a.up_w) {
+                            *reinterpret_cast<float4*>(dst + a.out_ld + j) = o;
+                            *reinterpret_cast<float4*>(dst + up_dy + j) = o;
+                            *reinterpret_cast<float4*>(dst + up_dy + a.out_ld + j) = o;
+                        }
+                    }
                 }
             } else {
 #pragma unroll
@@ -164,7 +177,7 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
                 }
             }
         } else {
-            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(a.out) + p * a.out_ld + n0;
+            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(a.out) + prow * a.out_ld + n0;
             const __nv_bfloat16* res =
                 a.residual ? reinterpret_cast<const __nv_bfloat16*>(a.residual) + p * a.res_ld + n0
                            : nullptr;
@@ -190,10 +203,16 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
                         v[j + 2 * i] = back.x;
                         v[j + 2 * i + 1] = back.y;
                     }
-                    if (srow)
+                    if (srow) {
                         *reinterpret_cast<uint4*>(srow + (c0 + j) * 2) = o;
-                    else if (!a.gn_apply && !(a.debug & 512))
+                    } else if (!a.gn_apply && !(a.debug & 512)) {
                         *reinterpret_cast<uint4*>(dst + j) = o;
+                        if (a.up_w) {
+                            *reinterpret_cast<uint4*>(dst + a.out_ld + j) = o;
+                            *reinterpret_cast<uint4*>(dst + up_dy + j) = o;
+                            *reinterpret_cast<uint4*>(dst + up_dy + a.out_ld + j) = o;
+                        }
+                    }
                 }
             } else {
 #pragma unroll
@@ -1098,6 +1117,7 @@ void plan_output_map(GemmPlan& p, bool conv) {
     if (std::getenv("PP_NO_TMA_STORE")) return;
     if ((uint64_t(a.out_ld) * eb) % 16 || (reinterpret_cast<uintptr_t>(a.out) % 16)) return;
     if (a.block_n > 256) return;   // TMA box dims are <= 256
+    if (a.up_w) return;            // fused upsample: four row stores per output row
     if (conv) {
         uint64_t d[3] = {uint64_t(a.n_valid), uint64_t(a.out_w), uint64_t(a.out_rows)};
         uint64_t st[2] = {uint64_t(a.out_ld) * eb, uint64_t(a.out_w) * a.out_ld * eb};
@@ -1412,6 +1432,9 @@ void plan_gemm(GemmPlan& p, Elem e, const void* A, int M, int K, long long lda, 
     encode_b(&p.tmB, e, B, N, K, ldb, a.block_n / (p.pair ? 2 : 1) / a.n_sub, a.kps);
     p.flops = 2.0 * double(M) * N * K;
     a.b_static = b_static ? 1 : 0;
+    a.up_w = ep.up_w;
+    if (ep.up_w && (ep.n_valid % 16 || ep.out_ld % 8 || ep.gn_groups))
+        throw std::invalid_argument("plan_gemm: fused upsample needs full 16-column tiles");
     plan_output_map(p, false);
     a.b_base = B;
     a.b_bytes = b_static ? ((long long)(N - 1) * ldb + K) * (long long)eb / 16 * 16 : 0;

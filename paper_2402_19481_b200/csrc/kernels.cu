@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(256, (STATS ? 2 : 3))
     gn_pass_kernel(const T* __restrict__ x, T* __restrict__ y, int pix, int C, int ld, int G,
                    const GnCombine cb, const float* __restrict__ gamma,
                    const float* __restrict__ beta, int do_silu, const float* __restrict__ temb,
-                   const T* __restrict__ skip, int round_tf32, const GnStatsOut so) {
+                   const T* __restrict__ skip, int round_tf32, const GnStatsOut so, int up_w) {
     constexpr int VEC = Vec<T>::N;
     const int vx = blockDim.x, vy = blockDim.y;
     const int tx = threadIdx.x, ty = threadIdx.y;
@@ -333,7 +333,20 @@ __global__ void __launch_bounds__(256, (STATS ? 2 : 3))
                     }
                     uint4 o;
                     store_vec<T>(reinterpret_cast<T*>(&o), f, round_tf32 != 0);
-                    *reinterpret_cast<uint4*>(y + (size_t(pp) * nvec + cv) * VEC) = o;
+                    if (up_w) {
+                        // fused nearest 2x upsample (upsample_nearest2x, tensor.cpp:323-334):
+                        // low-res pixel (py, px) -> the 2x2 block at (2py, 2px) of a 2W-wide map
+                        const int py = pp / up_w, px = pp - py * up_w;
+                        const size_t q = (size_t(2 * py) * (2 * up_w) + 2 * px) * nvec + cv;
+                        const size_t row = size_t(2 * up_w) * nvec;
+                        uint4* yv = reinterpret_cast<uint4*>(y);
+                        yv[q] = o;
+                        yv[q + nvec] = o;
+                        yv[q + row] = o;
+                        yv[q + row + nvec] = o;
+                    } else {
+                        *reinterpret_cast<uint4*>(y + (size_t(pp) * nvec + cv) * VEC) = o;
+                    }
                     if (STATS) load_vec<T>(reinterpret_cast<const T*>(&o), f);   // stored values
                 }
                 if (STATS) {
@@ -767,14 +780,14 @@ void gn_stats(Elem e, const void* x, long long pix, int C, int ld, int groups, d
                            static_cast<const T*>(x), static_cast<T*>(nullptr), int(pix), C, ld,
                            groups, cb, static_cast<const float*>(nullptr),
                            static_cast<const float*>(nullptr), 0, static_cast<const float*>(nullptr),
-                           static_cast<const T*>(nullptr), 0, so));
+                           static_cast<const T*>(nullptr), 0, so, 0));
     CUDA_CHECK(cudaGetLastError());
 }
 
 void gn_apply(Elem e, const void* x, void* y, long long pix, int C, int ld, int groups,
               const GnCombine& cb, const float* gamma, const float* beta, bool do_silu,
               const float* temb, const void* skip, bool round_tf32, cudaStream_t s,
-              const GnStatsOut* out_stats) {
+              const GnStatsOut* out_stats, int up_w) {
     if (groups > 1024) throw std::invalid_argument("group_norm_apply: too many groups");
     const int VEC = e == Elem::BF16 ? 8 : 4;
     if (pix * (ld / VEC) >= (1LL << 31)) throw std::invalid_argument("group_norm_apply: band too large");
@@ -785,12 +798,12 @@ void gn_apply(Elem e, const void* x, void* y, long long pix, int C, int ld, int 
         DISPATCH(e, launch_pdl(gn_pass_kernel<T, true, true, kGnUStats>, sh.grid, sh.block, 0, s, 1,
                                static_cast<const T*>(x), static_cast<T*>(y), int(pix), C, ld, groups,
                                cb, gamma, beta, do_silu ? 1 : 0, temb, static_cast<const T*>(skip),
-                               round_tf32 ? 1 : 0, *out_stats));
+                               round_tf32 ? 1 : 0, *out_stats, up_w));
     } else {
         DISPATCH(e, launch_pdl(gn_pass_kernel<T, true, false, kGnU>, sh.grid, sh.block, 0, s, 1,
                                static_cast<const T*>(x), static_cast<T*>(y), int(pix), C, ld, groups,
                                cb, gamma, beta, do_silu ? 1 : 0, temb, static_cast<const T*>(skip),
-                               round_tf32 ? 1 : 0, GnStatsOut{}));
+                               round_tf32 ? 1 : 0, GnStatsOut{}, up_w));
     }
     CUDA_CHECK(cudaGetLastError());
 }

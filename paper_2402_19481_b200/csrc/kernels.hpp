@@ -51,7 +51,9 @@ struct GnStatsOut {
 void gn_apply(Elem e, const void* x, void* y, long long pix, int C, int ld, int groups,
               const GnCombine& cb, const float* gamma, const float* beta, bool silu,
               const float* temb, const void* skip, bool round_tf32, cudaStream_t s,
-              const GnStatsOut* out_stats = nullptr);
+              const GnStatsOut* out_stats = nullptr, int up_w = 0);
+// up_w > 0: y is the nearest-2x upsample of the result (y is [2 rows][2 up_w] per input row;
+// up_w = the input width in pixels)
 
 // ---- pointwise (proj/src/tensor.cpp:297-334, model.cpp:278-298) ---------------------------
 void silu(Elem e, const void* x, void* y, long long n, bool round_tf32, cudaStream_t s);

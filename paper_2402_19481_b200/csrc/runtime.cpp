@@ -361,6 +361,12 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
             if (g.kind == Kind::SelfAttn && gc.kind == Kind::CrossAttn && gc.skip == g.last &&
                 srcs_count.count(g.last) == 1 && gc.last != L - 1 && !std::getenv("PP_NO_XATTN_MERGE"))
                 merged_into_prev[gi + 1] = 1;
+            // Linear / GroupNorm group -> Upsample of its output: the producer stores the
+            // nearest-2x upsample directly (its own output is not materialised)
+            if ((g.kind == Kind::Linear || g.kind == Kind::GroupNorm) && gc.kind == Kind::Upsample &&
+                gc.first == gc.last && !srcs_count.count(g.last) && gc.last != L - 1 &&
+                !std::getenv("PP_NO_UP_MERGE"))
+                merged_into_prev[gi + 1] = 1;
         }
     }
 
@@ -414,6 +420,12 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
                           e2, sc, sms);
             } else if (d.kind == Kind::Linear) {
                 e2.bias = lw.bias;
+                if (gi + 1 < groups.size() && merged_into_prev[gi + 1]) {
+                    const Group& gu = groups[gi + 1];
+                    e2.out = act[gu.last].interior(eb);
+                    e2.out_ld = act[gu.last].ld;
+                    e2.up_w = in.w;
+                }
                 plan_gemm(plans[gi][p], e, in.interior(eb), int(in.pix()), in.ld, in.ld, lw.w,
                           d.out_ch, in.ld, e2, sc, sms, 0, 0, /*b_static=*/true);
             } else if (d.kind == Kind::SelfAttn) {
@@ -469,6 +481,7 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
                 continue;
             if (gq.kind != Kind::GroupNorm || !fused_stats[gq.first] || srcs.count(g.last)) continue;
             if (gq.last + 1 < L && fused_stats[gq.last + 1] == 2) continue;   // output stats wanted
+            if (gi + 2 < groups.size() && merged_into_prev[gi + 2]) continue;   // fused upsample
             const Layer& dn = m->layers[gq.first];
             const LayerWeights& lw = wts->L[g.first];
             const LayerWeights& lg = wts->L[gq.first];
@@ -693,11 +706,14 @@ void Program::gn_apply(const Group& g, int mode, int par_cur, int par_prev) {
         so.ticket = gn_ticket;
         so.out = lx[next].stats[par_cur] + size_t(band) * dn.groups * 2;
     }
+    const size_t gi = size_t(&g - groups.data());
+    const bool up = gi + 1 < groups.size() && merged_into_prev[gi + 1];   // fused Upsample
     run_timed(CAT_GN, 0, [&] {
-        const Act& out = act[g.last];
+        const Act& out = act[up ? groups[gi + 1].last : g.last];
         pp::gn_apply(e, in.interior(eb), out.interior(eb), in.pix(), in.C, in.ld, d.groups, cb,
                      lw.gamma, lw.beta, g.silu, g.temb >= 0 ? temb_ptr(g.temb) : nullptr,
-                     g.skip >= 0 ? act[g.skip].interior(eb) : nullptr, rnd, cs, &so);
+                     g.skip >= 0 ? act[g.skip].interior(eb) : nullptr, rnd, cs, &so,
+                     up ? in.w : 0);
     });
     count(1);
 }
