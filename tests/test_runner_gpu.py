@@ -256,3 +256,30 @@ def test_trace_after_graph_sample_matches_reference():
             expect[d] += rr.trace(d)
     for d in range(2):
         assert pr.trace(d) == expect[d], d
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_reference_forward_wide_latent(dtype):
+    # a 128-pixel-wide latent puts the level-0 convs on the slab path (one im2col slab per
+    # channel chunk serves all nine taps) and on CTA pairs; same parity bar as the toy sizes
+    cfg, h, w = TOY, 64, 128
+    om = O.build_model(ocfg(cfg), 17)
+    cond = O.random_condition(cfg.cond_dim, 18)
+    x = O.random_normal(1, cfg.in_channels, h, w, 19)
+    ref = O.forward_full(om, x, 400, cond)
+    r = P.PatchRunner(P.build_model(cfg, 17), cond, h, w, mode="reference", dtype=dtype)
+    eps = r.run_step(x, 400, 0)
+    assert rel(eps, ref) <= EPS_TOL[dtype], rel(eps, ref)
+
+
+def test_displaced_wide_latent_matches_oracle():
+    cfg, h, w = TOY, 64, 128
+    res = O.run_sampling(ocfg(cfg), "displaced", 2, h, w, 4, 1)
+    m = P.build_model(cfg, 42)
+    cond = O.random_condition(cfg.cond_dim, 7)
+    x = O.random_normal(1, cfg.in_channels, h, w, 1234)
+    abar = O.make_schedule()
+    plan = O.make_plan(1000, 4)
+    r = P.PatchRunner(m, cond, h, w, mode="displaced", n_devices=2, warmup_steps=1, dtype="bf16")
+    x0, _ = r.sample(x, plan, abar)
+    assert rel(x0, res["x0"]) <= TOL["bf16"], rel(x0, res["x0"])
