@@ -13,6 +13,7 @@
 // 2 = std::runtime_error (proj/src/cli.cpp:145-154 maps them to exit 2 / 1).
 #include "patchsim/costmodel.hpp"
 #include "patchsim/model.hpp"
+#include "patchsim/io.hpp"
 #include "patchsim/runtime.hpp"
 #include "patchsim/sampler.hpp"
 #include "patchsim/tensor.hpp"
@@ -194,6 +195,28 @@ long ref_runner_trace(void* rp, int dev, uint64_t* out9, long cap) {
         o[6] = e.bytes_recv; o[7] = e.bytes_sent; o[8] = e.tag;
     }
     return n;
+}
+
+// ---- artifacts (proj/src/io.cpp) --------------------------------------------------
+int ref_write_tnsr(const float* x, int n, int c, int h, int w, const char* path) {
+    return guard([&] { write_tnsr(make(n, c, h, w, x), path); });
+}
+int ref_read_tnsr_dims(const char* path, int* dims4) {
+    return guard([&] {
+        const Tensor t = read_tnsr(path);
+        dims4[0] = t.n; dims4[1] = t.c; dims4[2] = t.h; dims4[3] = t.w;
+    });
+}
+int ref_read_tnsr(const char* path, float* dst) {
+    return guard([&] { put(read_tnsr(path), dst); });
+}
+int ref_write_pgm(const float* x, int n, int c, int h, int w, double lo, double hi, const char* path) {
+    return guard([&] { write_pgm(make(n, c, h, w, x), path, lo, hi); });
+}
+double ref_psnr(const float* a, const float* b, int n, int c, int h, int w, double peak) {
+    double r = 0;
+    guard([&] { r = psnr(make(n, c, h, w, a), make(n, c, h, w, b), peak); });
+    return r;
 }
 
 // ---- run_sampling ----------------------------------------------------------------
