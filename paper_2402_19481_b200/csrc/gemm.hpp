@@ -43,7 +43,7 @@ struct GemmArgs {
     int n_acc;                // TMEM accumulators in the MMA <-> epilogue ring (1 or 2)
     // slab mode (stride-1 conv, rows_box == 1): A from a 2-slot ring of im2col slabs
     // [3 rows][slab_px = w_box + 2][128 B] shared by the nine taps of a channel chunk; the
-    // virtual K index is chunk * 10 + tap (tap 9 empty), B comes from a 4-D map
+    // K index is chunk * 9 + tap (three taps per stage), B comes from a 4-D map
     int slab;
     int slab_px;
     uint32_t slab_bytes;      // smem per slot (1024-aligned)

@@ -93,8 +93,8 @@ __host__ __device__ inline size_t tail_bytes(int stages, bool gn, int block_n) {
 template <bool kPair>
 __device__ __forceinline__ void load_b(uint8_t* sb, const CUtensorMap* tm, uint64_t* bar,
                                        uint32_t bar_cl, int bcoord, int kb, const GemmArgs& a) {
-    if (a.slab) {   // virtual K block kb = chunk * 10 + tap (two taps per stage, tap 9 is OOB)
-        const int chunk = kb / 10, tap = kb - chunk * 10;
+    if (a.slab) {   // K block kb = chunk * 9 + tap; one stage = three taps
+        const int chunk = kb / 9, tap = kb - chunk * 9;
         if (kPair)
             ptx::tma_load_4d_pair(sb, tm, bar_cl, 0, bcoord, chunk, tap);
         else
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 ptx::mbar_arrive_expect_tx(&st.full_bar[stage],
                                                            P * (nk * a_box_bytes + b_stage_bytes));
                             const uint32_t fb = kPair ? full_leader + uint32_t(stage) * 8u : 0u;
-                            if (a.slab && kb % 10 == 0) {
+                            if (a.slab && kb % 9 == 0) {
                                 // first stage of a channel chunk: its im2col slab (3 input rows
                                 // x (w_box + 2) pixels, TMA zero-fill = the left/right padding)
                                 ptx::mbar_wait(&st.slab_empty[sl_slot], sl_phase ^ 1);
@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     ptx::mbar_arrive_expect_tx(&st.slab_full[sl_slot],
                                                                P * a.slab_box_bytes);
                                 uint8_t* dst = smem + size_t(sl_slot) * a.slab_bytes;
-                                const int ch = kb / 10;
+                                const int ch = kb / 9;
                                 if (kPair)
                                     ptx::tma_load_5d_pair(dst, &tmA, slab_leader + uint32_t(sl_slot) * 8u,
                                                           ch * kel, 0, ox0 - 1, 0, oy0);
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __syncwarp();
                 }
                 ++it;
-                if (a.slab && kb % 10 == 8 && ++sl_slot == 2) {
+                if (a.slab && kb % 9 == 6 && ++sl_slot == 2) {
                     sl_slot = 0;
                     sl_phase ^= 1;
                 }
@@ -538,10 +538,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t d_tmem = tmem_base + uint32_t(acc * 256);
             for (int kb = kb0; kb < kb1; kb += kps) {
                 if (a.slab) {
-                    // one stage = taps (sg, sg + 1) of channel chunk kb / 10 (tap 9 does not
-                    // exist): A rows of tap (ky, kx) start (ky * slab_px + kx) 128-byte rows
-                    // into the slab (a start address that is not swizzle-atom aligned)
-                    const int sg = kb % 10;
+                    // one stage = taps sg .. sg + 2 (one kernel row) of channel chunk kb / 9:
+                    // A rows of tap (ky, kx) start (ky * slab_px + kx) 128-byte rows into the
+                    // slab (a start address that is not swizzle-atom aligned)
+                    const int sg = kb % 9;
                     if (sg == 0) {
                         ptx::mbar_wait(&st.slab_full[ms_slot], ms_phase);
                         ptx::tc_fence_after();
@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (ptx::elect_one()) {
                         if (!(a.debug & 1)) {
 #pragma unroll
-                            for (int j = 0; j < 2; ++j) {
+                            for (int j = 0; j < 3; ++j) {
                                 const int tap = sg + j;
                                 if (tap < 9) {
                                     const int ky = tap / 3, kx = tap - 3 * ky;
@@ -579,14 +579,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                         if (kPair) {
                             ptx::mma_commit_pair(&st.empty_bar[stage], 3);
-                            if (sg == 8) ptx::mma_commit_pair(&st.slab_empty[ms_slot], 3);
+                            if (sg == 6) ptx::mma_commit_pair(&st.slab_empty[ms_slot], 3);
                         } else {
                             ptx::mma_commit(&st.empty_bar[stage]);
-                            if (sg == 8) ptx::mma_commit(&st.slab_empty[ms_slot]);
+                            if (sg == 6) ptx::mma_commit(&st.slab_empty[ms_slot]);
                         }
                     }
                     __syncwarp();
-                    if (sg == 8 && ++ms_slot == 2) {
+                    if (sg == 6 && ++ms_slot == 2) {
                         ms_slot = 0;
                         ms_phase ^= 1;
                     }
@@ -1268,12 +1268,12 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
     a.kps = a.n_sub == 2 ? 1 : choose_kps(bn, gn, pair);
     if (a.slab) {
         if (a.n_sub != 1) throw std::invalid_argument("slab conv: wide tiles unsupported");
-        a.kps = 2;   // one stage = two taps of a chunk
+        a.kps = 3;   // one stage = three taps (one kernel row) of a chunk
     }
     a.splits = splits;
     a.kb_per_split = (k_blocks + splits - 1) / splits;
     a.kb_per_split = (a.kb_per_split + a.kps - 1) / a.kps * a.kps;   // whole stages per split
-    if (a.slab) a.kb_per_split = (a.kb_per_split + 9) / 10 * 10;       // whole channel chunks
+    if (a.slab) a.kb_per_split = (a.kb_per_split + 8) / 9 * 9;         // whole channel chunks
     a.splits = (k_blocks + a.kb_per_split - 1) / a.kb_per_split;
     a.stages = stages_for(bn, gn, pair, a.kps, a.slab ? a.slab_bytes : 0u);
     a.idesc = make_idesc(p.elem, bn / a.n_sub, pair ? 2 * kTileM : kTileM);
@@ -1365,7 +1365,7 @@ void plan_conv(GemmPlan& p, Elem e, const void* in, int rows_in, int W, int C_in
         a.slab_box_bytes = uint32_t(3 * a.slab_px * kBlockBytes);
         a.slab_bytes = (a.slab_box_bytes + 1023u) / 1024u * 1024u;
     }
-    const int k_blocks = a.slab ? 10 * a.cin_chunks : 9 * a.cin_chunks;
+    const int k_blocks = 9 * a.cin_chunks;
 
     // A: 5-D view of the padded band [rows_in+2][W][C_in_pad]
     const int rows_pad = rows_in + 2;
@@ -1389,10 +1389,10 @@ void plan_conv(GemmPlan& p, Elem e, const void* in, int rows_in, int W, int C_in
                 force_block_n);
     // B: weights [n_pad][9*C_in_pad] viewed as [K blocks][n_pad][kel]: one box = kps blocks
     if (a.slab) {
-        // B as [tap][chunk][n][kel]: box {kel, rows, 1 chunk, 2 taps}
+        // B as [tap][chunk][n][kel]: box {kel, rows, 1 chunk, 3 taps}
         uint64_t d[4] = {uint64_t(kel), uint64_t(n_pad), uint64_t(a.cin_chunks), 9};
         uint64_t st[3] = {uint64_t(9) * C_in_pad * eb, uint64_t(kBlockBytes), uint64_t(C_in_pad) * eb};
-        uint32_t b[4] = {uint32_t(kel), uint32_t(a.block_n / (p.pair ? 2 : 1)), 1, 2};
+        uint32_t b[4] = {uint32_t(kel), uint32_t(a.block_n / (p.pair ? 2 : 1)), 1, 3};
         encode(&p.tmB, e, 4, weights, d, st, b);
     } else {
         encode_b(&p.tmB, e, weights, n_pad, 9 * C_in_pad, 9LL * C_in_pad,
