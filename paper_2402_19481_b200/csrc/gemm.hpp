@@ -100,6 +100,7 @@ struct GemmPlan {
     size_t smem = 0;
     Elem elem = Elem::BF16;
     int pair = 0;             // 1: CTA-pair (cta_group::2, M = 256) kernel, clusters of 2
+    int mc = 0;               // 1: clusters of two pairs sharing B by TMA multicast (needs pair)
     double flops = 0;         // algorithmic 2*M*N*K of the layer (for rooflines)
 };
 

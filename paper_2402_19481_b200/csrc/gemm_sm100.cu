@@ -53,13 +53,14 @@ struct TileCoord {
 
 // Work unit t -> (split, N tile, M unit); the CTA's M tile is unit * P + rank (P = CTAs
 // per cluster).  m >= tiles_y * tiles_x only for the peer of an odd last unit.
-template <int P>
+template <int P, int Q = 1>
 __device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int t, int rank) {
+    // Q = CTA pairs per cluster sharing one B tile (multicast): unit = Q pair units
     TileCoord c;
     c.split = t % a.splits;
     int rest = t / a.splits;
     c.nt = rest % a.n_tiles;
-    c.m = (rest / a.n_tiles) * P + rank;
+    c.m = ((rest / a.n_tiles) * Q + rank / P) * P + rank % P;
     c.tx = c.m % a.tiles_x;
     c.ty = c.m / a.tiles_x;
     return c;
@@ -90,9 +91,26 @@ __host__ __device__ inline size_t tail_bytes(int stages, bool gn, int block_n) {
 // (rows * kps) slots apart; in a CTA pair each CTA loads its share (rank) of every half.
 // bcoord = first weight row of this CTA's share of half 0.  kPair: complete_tx on the
 // leader's barrier (shared::cluster address bar_cl), else on the local barrier bar.
-template <bool kPair>
+template <bool kPair, bool kMC>
 __device__ __forceinline__ void load_b(uint8_t* sb, const CUtensorMap* tm, uint64_t* bar,
-                                       uint32_t bar_cl, int bcoord, int kb, const GemmArgs& a) {
+                                       uint32_t bar_cl, int bcoord, int kb, const GemmArgs& a,
+                                       int pid, int crank) {
+    if (kMC) {
+        // this CTA's quarter of the stage (rows pid * q of its pair half), one box per K
+        // block, multicast to itself and the same-rank CTA of the other pair
+        const int q = a.block_n / 4;
+        const uint16_t mask = uint16_t((1u << crank) | (1u << (crank ^ 2)));
+        for (int j = 0; j < a.kps; ++j) {
+            uint8_t* dst = sb + size_t(j) * (a.block_n / 2) * kBlockBytes + size_t(pid) * q * kBlockBytes;
+            if (a.slab) {
+                const int k = kb + j, chunk = k / 9, tap = k - chunk * 9;
+                ptx::tma_load_4d_pair_mc(dst, tm, bar_cl, 0, bcoord, chunk, tap, mask);
+            } else {
+                ptx::tma_load_3d_pair_mc(dst, tm, bar_cl, 0, bcoord, kb + j, mask);
+            }
+        }
+        return;
+    }
     if (a.slab) {   // K block kb = chunk * 9 + tap; one stage = three taps
         const int chunk = kb / 9, tap = kb - chunk * 9;
         if (kPair)
@@ -280,11 +298,15 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
 // (rank 0) issues M=256 MMAs that read both CTAs' smem, and each CTA's TMEM receives its
 // own 128 rows, so the epilogue is unchanged.  Per SM this halves the B bytes staged and
 // read per MMA (the single-CTA kernel is shared-memory-bandwidth bound at block_n <= 256).
-template <bool kTF32, bool kPair>
+template <bool kTF32, bool kPair, bool kMC>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmD, const GemmArgs a) {
     constexpr int P = kPair ? 2 : 1;
+    // kMC: clusters of two CTA pairs on the same N tile; each B quarter is loaded once and
+    // multicast to the two CTAs that need it (B bytes per SM halved again)
+    constexpr int Q = kMC ? 2 : 1;
+    constexpr int CL = P * Q;   // CTAs per cluster
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte aligned base derived from smem_raw by pointer arithmetic (not an integer
     // cast), so the compiler keeps the shared address space: LDS/STS for the tail arrays
@@ -317,7 +339,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
-    const int rank = kPair ? int(ptx::cluster_ctarank()) : 0;
+    const int crank = kPair ? int(ptx::cluster_ctarank()) : 0;   // rank in the cluster
+    const int rank = crank & 1;            // rank in the CTA pair
+    const int pid = kMC ? crank >> 1 : 0;  // pair index in the cluster
+    const uint32_t ldr = uint32_t(crank & ~1);                // the pair's leader CTA
+    const uint16_t pair_mask = uint16_t(3u << ldr);
 
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmA);
@@ -325,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (a.tma_store) ptx::prefetch_tmap(&tmD);
         for (int s = 0; s < stages; ++s) {
             ptx::mbar_init(&st.full_bar[s], 1);
-            ptx::mbar_init(&st.empty_bar[s], 1);
+            ptx::mbar_init(&st.empty_bar[s], Q);   // one MMA commit per pair sharing the stage
         }
         for (int s = 0; s < 2; ++s) {
             ptx::mbar_init(&st.slab_full[s], 1);
@@ -352,8 +378,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     pdl_trigger();   // the next kernel on the stream may start its own prologue now
 
     const int m_tiles = a.tiles_y * a.tiles_x;
-    const int total_tiles = (m_tiles + P - 1) / P * a.n_tiles * a.splits;
-    const int tile0 = blockIdx.x / P, tile_step = gridDim.x / P;
+    const int total_tiles = ((m_tiles + P - 1) / P + Q - 1) / Q * a.n_tiles * a.splits;
+    const int tile0 = blockIdx.x / CL, tile_step = gridDim.x / CL;
     const int conv = a.mode != 0;
     const int a_box_bytes = a.slab ? 0 : conv ? a.rows_box * a.w_box * kBlockBytes : int(a_slot);
 
@@ -369,17 +395,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t phase = 0;
         const int kel = kTF32 ? 32 : 64;  // elements per 128-byte K block
         // pair: every box completes on the leader's full barrier
-        const uint32_t full_leader = kPair ? ptx::mapa(ptx::smem_u32(st.full_bar), 0) : 0u;
+        const uint32_t full_leader = kPair ? ptx::mapa(ptx::smem_u32(st.full_bar), ldr) : 0u;
         // PDL: the weights (B) do not depend on the previous kernel, so the first tile's
         // first `pre` stages get their B boxes (and are armed for A + B) before waiting for
         // it; only the A boxes (activations) wait.
         int pre = 0;
         if (a.b_static && tile0 < total_tiles && !(a.debug & 2)) {
-            const TileCoord tc = decode_tile<P>(a, tile0, rank);
+            const TileCoord tc = decode_tile<P, Q>(a, tile0, crank);
             const int kb0 = tc.split * a.kb_per_split;
             const int kb1 = (a.debug & 1024) ? kb0 + 1 : min(kb0 + a.kb_per_split, a.k_blocks);
             pre = min(stages, (kb1 - kb0 + kps - 1) / kps);
-            const int bcoord = tc.nt * a.block_n + rank * (a.block_n / a.n_sub / P);
+            const int bcoord = tc.nt * a.block_n + rank * (a.block_n / a.n_sub / P) +
+                               pid * (a.block_n / a.n_sub / P / Q);
             for (int i = pw; i < pre; i += 2) {
                 if (ptx::elect_one()) {
                     uint8_t* sb = ring + size_t(i) * stage_bytes + a_stage_bytes;
@@ -387,8 +414,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (rank == 0)
                         ptx::mbar_arrive_expect_tx(&st.full_bar[i],
                                                    P * (nk * a_box_bytes + b_stage_bytes));
-                    load_b<kPair>(sb, &tmB, &st.full_bar[i], full_leader + uint32_t(i) * 8u, bcoord,
-                                  kb0 + i * kps, a);
+                    load_b<kPair, kMC>(sb, &tmB, &st.full_bar[i], full_leader + uint32_t(i) * 8u, bcoord,
+                                       kb0 + i * kps, a, pid, crank);
                 }
                 __syncwarp();
             }
@@ -412,13 +439,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         int it = 0;
         int sl_slot = 0;          // slab mode: A-slab ring slot / phase (both producer warps)
         uint32_t sl_phase = 0;
-        const uint32_t slab_leader = kPair ? ptx::mapa(ptx::smem_u32(st.slab_full), 0) : 0u;
+        const uint32_t slab_leader = kPair ? ptx::mapa(ptx::smem_u32(st.slab_full), ldr) : 0u;
         for (int t = tile0; t < total_tiles; t += tile_step) {
-            const TileCoord tc = decode_tile<P>(a, t, rank);
+            const TileCoord tc = decode_tile<P, Q>(a, t, crank);
             const int kb0 = tc.split * a.kb_per_split;
             const int kb1 = (a.debug & 1024) ? kb0 + 1 : min(kb0 + a.kb_per_split, a.k_blocks);
             const int oy0 = tc.ty * a.rows_box, ox0 = tc.tx * a.w_box;
-            const int bcoord = tc.nt * a.block_n + rank * (a.block_n / a.n_sub / P);
+            const int bcoord = tc.nt * a.block_n + rank * (a.block_n / a.n_sub / P) +
+                               pid * (a.block_n / a.n_sub / P / Q);
             const int arow = tc.ty * kTileM;
             // conv K position of block kb0: tap (ky, kx), channel chunk cj
             int cj = kb0 % a.cin_chunks;
@@ -485,7 +513,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 }
                             }
                             if (!b_done) {
-                                load_b<kPair>(sb, &tmB, &st.full_bar[stage], fb, bcoord, kb, a);
+                                load_b<kPair, kMC>(sb, &tmB, &st.full_bar[stage], fb, bcoord, kb, a, pid,
+                                                   crank);
                             }
                         }
                     }
@@ -530,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int ms_slot = 0;          // slab mode: A-slab ring slot / phase
         uint32_t ms_phase = 0;
         for (int t = tile0; t < total_tiles; t += tile_step) {
-            const TileCoord tc = decode_tile<P>(a, t, 0);
+            const TileCoord tc = decode_tile<P, Q>(a, t, crank);
             const int kb0 = tc.split * a.kb_per_split;
             const int kb1 = (a.debug & 1024) ? kb0 + 1 : min(kb0 + a.kb_per_split, a.k_blocks);
             ptx::mbar_wait(&st.tempty_bar[acc], acc_phase ^ 1);
@@ -578,8 +607,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                         if (kPair) {
-                            ptx::mma_commit_pair(&st.empty_bar[stage], 3);
-                            if (sg == 6) ptx::mma_commit_pair(&st.slab_empty[ms_slot], 3);
+                            ptx::mma_commit_pair(&st.empty_bar[stage], kMC ? uint16_t(0xF) : pair_mask);
+                            if (sg == 6) ptx::mma_commit_pair(&st.slab_empty[ms_slot], pair_mask);
                         } else {
                             ptx::mma_commit(&st.empty_bar[stage]);
                             if (sg == 6) ptx::mma_commit(&st.slab_empty[ms_slot]);
@@ -644,7 +673,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                     if (kPair)
-                        ptx::mma_commit_pair(&st.empty_bar[stage], 3);
+                        ptx::mma_commit_pair(&st.empty_bar[stage], kMC ? uint16_t(0xF) : pair_mask);
                     else
                         ptx::mma_commit(&st.empty_bar[stage]);
                 }
@@ -656,7 +685,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (ptx::elect_one()) {
                 if (kPair)
-                    ptx::mma_commit_pair(&st.tfull_bar[acc], 3);
+                    ptx::mma_commit_pair(&st.tfull_bar[acc], pair_mask);
                 else
                     ptx::mma_commit(&st.tfull_bar[acc]);
             }
@@ -676,7 +705,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr int kCS = 16 * kEpiPerQuarter;   // chunk stride of one warp
         float* sgn_warp = st.gn + quarter * 2 * a.block_n;   // [block_n / cpg][2] used
         // accumulator release: the MMA issuer (the leader's, for a pair) waits for 4*P warps
-        const uint32_t tempty_leader = kPair ? ptx::mapa(ptx::smem_u32(st.tempty_bar), 0) : 0u;
+        const uint32_t tempty_leader = kPair ? ptx::mapa(ptx::smem_u32(st.tempty_bar), ldr) : 0u;
         auto release = [&](int which) {
             ptx::tc_fence_before();
             __syncwarp();
@@ -696,7 +725,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc = 0;
                 acc_phase ^= 1;
             }
-            const TileCoord tc = decode_tile<P>(a, t, rank);
+            const TileCoord tc = decode_tile<P, Q>(a, t, crank);
             const int m_tile = tc.m;
             const int tile_id = m_tile * a.n_tiles + tc.nt;
             long long p;
@@ -1308,8 +1337,17 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
         a.gn_err = ep.gn_err;
     }
     const int P = pair ? 2 : 1;
-    const int units = (m_tiles + P - 1) / P * a.n_tiles * a.splits;
-    p.grid = P * std::min(units, num_sms / P);
+    // clusters of two pairs sharing B by TMA multicast: parity-tested but measured slower on
+    // B200 (4-CTA clusters lock two pairs into step and strand SMs: L01 32 vs 24 us, 8192^3
+    // GEMM 1.16 vs 0.55 ms), so opt-in (PP_MC=1)
+    static const bool mc_env = [] {
+        const char* v = std::getenv("PP_MC");
+        return v && v[0] == '1';
+    }();
+    p.mc = (mc_env && pair && a.n_sub == 1 && bn % 32 == 0 && (m_tiles + 1) / 2 >= 2) ? 1 : 0;
+    const int Q = p.mc ? 2 : 1;
+    const int units = ((m_tiles + P - 1) / P + Q - 1) / Q * a.n_tiles * a.splits;
+    p.grid = P * Q * std::min(units, num_sms / (P * Q));
     p.smem = smem_for(bn, a.stages, gn, pair, a.kps, a.slab ? a.slab_bytes : 0u);
 }
 
@@ -1392,11 +1430,12 @@ void plan_conv(GemmPlan& p, Elem e, const void* in, int rows_in, int W, int C_in
         // B as [tap][chunk][n][kel]: box {kel, rows, 1 chunk, 3 taps}
         uint64_t d[4] = {uint64_t(kel), uint64_t(n_pad), uint64_t(a.cin_chunks), 9};
         uint64_t st[3] = {uint64_t(9) * C_in_pad * eb, uint64_t(kBlockBytes), uint64_t(C_in_pad) * eb};
-        uint32_t b[4] = {uint32_t(kel), uint32_t(a.block_n / (p.pair ? 2 : 1)), 1, 3};
+        uint32_t b[4] = {uint32_t(kel), uint32_t(a.block_n / (p.pair ? 2 : 1) / (p.mc ? 2 : 1)), 1,
+                         p.mc ? 1u : 3u};
         encode(&p.tmB, e, 4, weights, d, st, b);
     } else {
         encode_b(&p.tmB, e, weights, n_pad, 9 * C_in_pad, 9LL * C_in_pad,
-                 a.block_n / (p.pair ? 2 : 1) / a.n_sub, a.kps);
+                 a.block_n / (p.pair ? 2 : 1) / a.n_sub / (p.mc ? 2 : 1), p.mc ? 1 : a.kps);
     }
     p.flops = 2.0 * a.m_pix * double(ep.n_valid) * 9.0 * C_in_pad;
     a.b_static = 1;   // conv weights
@@ -1429,7 +1468,8 @@ void plan_gemm(GemmPlan& p, Elem e, const void* A, int M, int K, long long lda, 
     uint32_t ab[2] = {uint32_t(kel), uint32_t(kTileM)};
     encode(&p.tmA, e, 2, A, ad, as, ab);
     finish_plan(p, a.tiles_y, n_pad, K / kel, ep, sc, num_sms, force_splits, force_block_n);
-    encode_b(&p.tmB, e, B, N, K, ldb, a.block_n / (p.pair ? 2 : 1) / a.n_sub, a.kps);
+    encode_b(&p.tmB, e, B, N, K, ldb, a.block_n / (p.pair ? 2 : 1) / a.n_sub / (p.mc ? 2 : 1),
+             p.mc ? 1 : a.kps);
     p.flops = 2.0 * double(M) * N * K;
     a.b_static = b_static ? 1 : 0;
     a.up_w = ep.up_w;
@@ -1440,7 +1480,7 @@ void plan_gemm(GemmPlan& p, Elem e, const void* A, int M, int K, long long lda, 
     a.b_bytes = b_static ? ((long long)(N - 1) * ldb + K) * (long long)eb / 16 * 16 : 0;
 }
 
-template <bool kTF32, bool kPair>
+template <bool kTF32, bool kPair, bool kMC>
 void launch_variant(const GemmPlan& p, cudaStream_t s) {
     // the dynamic-smem attribute is per device: remember which devices have it
     static std::mutex mu;
@@ -1450,13 +1490,13 @@ void launch_variant(const GemmPlan& p, cudaStream_t s) {
     {
         std::lock_guard<std::mutex> lk(mu);
         if (!(done >> dev & 1ull)) {
-            CUDA_CHECK(cudaFuncSetAttribute(gemm_kernel<kTF32, kPair>,
+            CUDA_CHECK(cudaFuncSetAttribute(gemm_kernel<kTF32, kPair, kMC>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
             done |= 1ull << dev;
         }
     }
-    launch_pdl(gemm_kernel<kTF32, kPair>, dim3(p.grid), dim3(kThreads), p.smem, s, kPair ? 2 : 1,
-               p.tmA, p.tmB, p.tmD, p.a);
+    launch_pdl(gemm_kernel<kTF32, kPair, kMC>, dim3(p.grid), dim3(kThreads), p.smem, s,
+               kMC ? 4 : kPair ? 2 : 1, p.tmA, p.tmB, p.tmD, p.a);
 }
 
 void launch_gemm(const GemmPlan& p0, cudaStream_t s) {
@@ -1475,10 +1515,15 @@ void launch_gemm(const GemmPlan& p0, cudaStream_t s) {
     }
     const GemmPlan& p = *pp_;
     const bool tf32 = p.elem == Elem::F32;
-    if (tf32)
-        p.pair ? launch_variant<true, true>(p, s) : launch_variant<true, false>(p, s);
-    else
-        p.pair ? launch_variant<false, true>(p, s) : launch_variant<false, false>(p, s);
+    if (tf32) {
+        if (p.mc) launch_variant<true, true, true>(p, s);
+        else if (p.pair) launch_variant<true, true, false>(p, s);
+        else launch_variant<true, false, false>(p, s);
+    } else {
+        if (p.mc) launch_variant<false, true, true>(p, s);
+        else if (p.pair) launch_variant<false, true, false>(p, s);
+        else launch_variant<false, false, false>(p, s);
+    }
 }
 
 }  // namespace pp

@@ -193,6 +193,28 @@ __device__ __forceinline__ void tma_load_4d_pair(void* dst, const CUtensorMap* m
         "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
         : "memory");
 }
+// CTA-pair TMA with cluster multicast: the box lands at the same offset in every CTA of
+// `mask`; its bytes complete on the mbarrier at bar_cluster's offset in each destination's pair
+// leader.
+__device__ __forceinline__ void tma_load_3d_pair_mc(void* dst, const CUtensorMap* m,
+                                                    uint32_t bar_cluster, int c0, int c1, int c2,
+                                                    uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_pair_mc(void* dst, const CUtensorMap* m,
+                                                    uint32_t bar_cluster, int c0, int c1, int c2,
+                                                    int c3, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".multicast::cluster [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+        "h"(mask)
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_5d_pair(void* dst, const CUtensorMap* m,
                                                  uint32_t bar_cluster, int c0, int c1, int c2,
                                                  int c3, int c4) {

@@ -1,5 +1,6 @@
 """tcgen05 GEMM / implicit-GEMM conv kernel vs a plain torch fp32/fp64 reference."""
 import ctypes as C
+import os
 
 import pytest
 
@@ -149,3 +150,28 @@ def test_conv_wide_tile(rows, W, C, co):
                                     1, None, 0, force, 320, None))
         err = (out.double() - ref).norm() / ref.norm()
         assert err < 1e-5, (force, err)
+
+
+@pytest.mark.parametrize("M,Nn,K", [(1024, 1024, 1280), (1000, 640, 576), (384, 320, 2880)])
+def test_gemm_pair_multicast(M, Nn, K, monkeypatch):
+    # opt-in clusters of two CTA pairs sharing B by TMA multicast (PP_MC=1, read once per
+    # process: run in a subprocess so the setting cannot leak into other tests)
+    import subprocess
+    import sys
+    code = (
+        "import torch, ctypes as C\n"
+        "from paper_2402_19481_b200 import _native as N\n"
+        f"M, Nn, K = {M}, {Nn}, {K}\n"
+        "g = torch.Generator(device='cuda').manual_seed(3)\n"
+        "A = torch.randn(M, K, device='cuda', generator=g).bfloat16()\n"
+        "B = torch.randn(Nn, K, device='cuda', generator=g).bfloat16()\n"
+        "D = torch.zeros(M, Nn, device='cuda')\n"
+        "p = lambda t: C.c_void_p(t.data_ptr())\n"
+        "N.check(N.lib().pp_dev_gemm(0, p(A), M, K, K, p(B), Nn, K, None, p(D), Nn, 1, 16, 0, None))\n"
+        "ref = A.double() @ B.double().T\n"
+        "print(((D.double() - ref).norm() / ref.norm()).item())\n")
+    env = dict(os.environ, PP_MC="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         timeout=120)
+    assert out.returncode == 0, out.stderr
+    assert float(out.stdout.strip().splitlines()[-1]) < 1e-5
