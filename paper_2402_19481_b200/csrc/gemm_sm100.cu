@@ -111,12 +111,16 @@ __device__ __forceinline__ void load_b(uint8_t* sb, const CUtensorMap* tm, uint6
         }
         return;
     }
-    if (a.slab) {   // K block kb = chunk * 9 + tap; one stage = three taps
+    if (a.slab) {   // K block kb = chunk * 9 + tap; one stage = kps taps (per N half)
         const int chunk = kb / 9, tap = kb - chunk * 9;
-        if (kPair)
-            ptx::tma_load_4d_pair(sb, tm, bar_cl, 0, bcoord, chunk, tap);
-        else
-            ptx::tma_load_4d(sb, tm, bar, 0, bcoord, chunk, tap);
+        const int hrow = a.block_n / a.n_sub, brows = hrow / (kPair ? 2 : 1);
+        for (int h = 0; h < a.n_sub; ++h) {
+            uint8_t* dst = sb + size_t(h) * brows * kBlockBytes * a.kps;
+            if (kPair)
+                ptx::tma_load_4d_pair(dst, tm, bar_cl, 0, bcoord + h * hrow, chunk, tap);
+            else
+                ptx::tma_load_4d(dst, tm, bar, 0, bcoord + h * hrow, chunk, tap);
+        }
         return;
     }
     const int hrow = a.block_n / a.n_sub;                 // weight rows per N half
@@ -521,7 +525,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __syncwarp();
                 }
                 ++it;
-                if (a.slab && kb % 9 == 6 && ++sl_slot == 2) {
+                if (a.slab && kb % 9 + kps >= 9 && ++sl_slot == 2) {
                     sl_slot = 0;
                     sl_phase ^= 1;
                 }
@@ -552,6 +556,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t desc_stride = stage_bytes >> 4;
         const uint64_t a_next = a_slot >> 4, b_next = b_slot >> 4;
         const uint32_t b_half = uint32_t(a.block_n / 2 / P) * kBlockBytes;   // n_sub == 2
+        const uint32_t b_sub = uint32_t(a.block_n / a.n_sub / P) * kBlockBytes;  // slab: one tap, one half
         int stage = 0;
         uint32_t phase = 0;
         int acc = 0;
@@ -581,8 +586,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t sbase = slab0 + uint32_t(ms_slot) * a.slab_bytes;
                     if (ptx::elect_one()) {
                         if (!(a.debug & 1)) {
-#pragma unroll
-                            for (int j = 0; j < 3; ++j) {
+                            for (int j = 0; j < kps; ++j) {
                                 const int tap = sg + j;
                                 if (tap < 9) {
                                     const int ky = tap / 3, kx = tap - 3 * ky;
@@ -592,30 +596,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     // offset (measured: setting bits 49-51 breaks it)
                                     const uint64_t da = ptx::smem_desc_sw128(sbase + off * kBlockBytes);
                                     const uint32_t acc0 = (kb > kb0 || j > 0) ? 1u : 0u;
-                                    if (kPair) {
-                                        if (kTF32)
-                                            ptx::mma4_tf32_pair(d_tmem, da, db + j * b_next, a.idesc, acc0);
-                                        else
-                                            ptx::mma4_bf16_pair(d_tmem, da, db + j * b_next, a.idesc, acc0);
-                                    } else {
-                                        if (kTF32)
-                                            ptx::mma4_tf32(d_tmem, da, db + j * b_next, a.idesc, acc0);
-                                        else
-                                            ptx::mma4_bf16(d_tmem, da, db + j * b_next, a.idesc, acc0);
+                                    // N halves (wide tile): B rows of half h follow the kps
+                                    // slots of half h - 1, accumulator columns h * block_n / 2
+                                    for (int h = 0; h < a.n_sub; ++h) {
+                                        const uint64_t dbj = db + (uint64_t(h * kps + j) * b_sub >> 4);
+                                        const uint32_t dh = d_tmem + uint32_t(h * (a.block_n / 2));
+                                        if (kPair) {
+                                            if (kTF32)
+                                                ptx::mma4_tf32_pair(dh, da, dbj, a.idesc, acc0);
+                                            else
+                                                ptx::mma4_bf16_pair(dh, da, dbj, a.idesc, acc0);
+                                        } else {
+                                            if (kTF32)
+                                                ptx::mma4_tf32(dh, da, dbj, a.idesc, acc0);
+                                            else
+                                                ptx::mma4_bf16(dh, da, dbj, a.idesc, acc0);
+                                        }
                                     }
                                 }
                             }
                         }
                         if (kPair) {
                             ptx::mma_commit_pair(&st.empty_bar[stage], kMC ? uint16_t(0xF) : pair_mask);
-                            if (sg == 6) ptx::mma_commit_pair(&st.slab_empty[ms_slot], pair_mask);
+                            if (sg + kps >= 9) ptx::mma_commit_pair(&st.slab_empty[ms_slot], pair_mask);
                         } else {
                             ptx::mma_commit(&st.empty_bar[stage]);
-                            if (sg == 6) ptx::mma_commit(&st.slab_empty[ms_slot]);
+                            if (sg + kps >= 9) ptx::mma_commit(&st.slab_empty[ms_slot]);
                         }
                     }
                     __syncwarp();
-                    if (sg == 6 && ++ms_slot == 2) {
+                    if (sg + kps >= 9 && ++ms_slot == 2) {
                         ms_slot = 0;
                         ms_phase ^= 1;
                     }
@@ -1296,8 +1306,9 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
     a.n_acc = bn > 256 ? 1 : 2;
     a.kps = a.n_sub == 2 ? 1 : choose_kps(bn, gn, pair);
     if (a.slab) {
-        if (a.n_sub != 1) throw std::invalid_argument("slab conv: wide tiles unsupported");
-        a.kps = 3;   // one stage = three taps (one kernel row) of a chunk
+        // one stage = three taps (one kernel row) of a chunk; a wide tile (two N halves, 8
+        // MMAs per tap) takes one tap per stage
+        a.kps = a.n_sub == 2 ? 1 : 3;
     }
     a.splits = splits;
     a.kb_per_split = (k_blocks + splits - 1) / splits;
@@ -1395,8 +1406,7 @@ void plan_conv(GemmPlan& p, Elem e, const void* in, int rows_in, int W, int C_in
         const char* v = std::getenv("PP_SLAB");
         return !(v && v[0] == '0');
     }();
-    a.slab = (slab_env && stride == 1 && a.rows_box == 1 && wb + 2 <= 256 && force_block_n <= 256 &&
-              !ep.gn_apply && !std::getenv("PP_WIDE"))
+    a.slab = (slab_env && stride == 1 && a.rows_box == 1 && wb + 2 <= 256 && !ep.gn_apply)
                  ? 1 : 0;
     if (a.slab) {
         a.slab_px = wb + 2;
@@ -1430,8 +1440,9 @@ void plan_conv(GemmPlan& p, Elem e, const void* in, int rows_in, int W, int C_in
         // B as [tap][chunk][n][kel]: box {kel, rows, 1 chunk, 3 taps}
         uint64_t d[4] = {uint64_t(kel), uint64_t(n_pad), uint64_t(a.cin_chunks), 9};
         uint64_t st[3] = {uint64_t(9) * C_in_pad * eb, uint64_t(kBlockBytes), uint64_t(C_in_pad) * eb};
-        uint32_t b[4] = {uint32_t(kel), uint32_t(a.block_n / (p.pair ? 2 : 1) / (p.mc ? 2 : 1)), 1,
-                         p.mc ? 1u : 3u};
+        uint32_t b[4] = {uint32_t(kel),
+                         uint32_t(a.block_n / (p.pair ? 2 : 1) / (p.mc ? 2 : 1) / a.n_sub), 1,
+                         p.mc ? 1u : uint32_t(a.kps)};
         encode(&p.tmB, e, 4, weights, d, st, b);
     } else {
         encode_b(&p.tmB, e, weights, n_pad, 9 * C_in_pad, 9LL * C_in_pad,
