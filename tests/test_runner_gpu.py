@@ -283,3 +283,46 @@ def test_displaced_wide_latent_matches_oracle():
     r = P.PatchRunner(m, cond, h, w, mode="displaced", n_devices=2, warmup_steps=1, dtype="bf16")
     x0, _ = r.sample(x, plan, abar)
     assert rel(x0, res["x0"]) <= TOL["bf16"], rel(x0, res["x0"])
+
+
+SDXL = P.ModelConfig(4, 320, 3, 32, 2048, -1)   # the SDXL-shape graph
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_sdxl_shape_forward_matches_reference_build(dtype):
+    # the benchmark's model (320/640/1280 channels, GN32, d=1280 attention, 77.4M params) at a
+    # 32x32 latent: one eps against the reference's own CPU path (oracle/_ref), same weights
+    R = _ref_lib()
+    hw = 32
+    cond = O.random_condition(2048, 7)
+    x = O.random_normal(1, 4, hw, hw, 1234)
+    rr = R.PatchRunner(R.Model(dataclasses.astuple(SDXL), 42), cond, hw, hw, mode="reference")
+    ref = rr.step("run_step", x, 980, 0)
+    r = P.PatchRunner(P.build_model(SDXL, 42), cond, hw, hw, mode="reference", dtype=dtype)
+    eps = r.run_step(x, 980, 0)
+    assert rel(eps, ref) <= EPS_TOL[dtype], rel(eps, ref)
+
+
+def test_sdxl_shape_displaced_two_bands_matches_reference_build():
+    # displaced patch parallelism at the real channel counts: 2 bands, warm-up 1, 3 steps of
+    # DDIM through run_step on both sides (halo rows, full K/V and GN statistics exchanged)
+    R = _ref_lib()
+    hw = 32
+    cond = O.random_condition(2048, 7)
+    x = O.random_normal(1, 4, hw, hw, 1234)
+    abar = O.make_schedule()
+    plan = [980, 960, 940]
+    rr = R.PatchRunner(R.Model(dataclasses.astuple(SDXL), 42), cond, hw, hw, mode="displaced",
+                       n_devices=2, warmup=1)
+    pr = P.PatchRunner(P.build_model(SDXL, 42), cond, hw, hw, mode="displaced", n_devices=2,
+                       warmup_steps=1, dtype="bf16")
+    xr, xp = x.copy(), x.copy()
+    for s, t in enumerate(plan):
+        er = rr.step("run_step", xr, t, s)
+        ep = pr.run_step(xp, t, s)
+        assert rel(ep, er) <= EPS_TOL["bf16"], (s, rel(ep, er))
+        tn = plan[s + 1] if s + 1 < len(plan) else -1
+        a_t, a_n = O.alpha_bar_at(abar, t), O.alpha_bar_at(abar, tn)
+        xr = O.ddim_update(xr, er, a_t, a_n)
+        xp = O.ddim_update(xp, ep, a_t, a_n)
+    assert rel(xp, xr) <= TOL["bf16"], rel(xp, xr)
