@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--latent", type=int, default=128, help="latent side (image = 8x)")
+    ap.add_argument("--latent-w", type=int, default=0,
+                    help="latent width when not square (e.g. 160x240 = 1280x1920 image)")
     ap.add_argument("--num-steps", type=int, default=50)
     ap.add_argument("--mode", default="displaced")
     ap.add_argument("--warmup-steps", type=int, default=4, help="displaced: sync warm-up steps")
@@ -66,11 +68,11 @@ def dist_env():
 def workload(args, n):
     return {
         "workload": f"SDXL-shape UNet (4->320/640/1280 ch, GN32, d=1280 self-attn, 77.4M params, "
-                    f"random init seed 42), {8 * args.latent}x{8 * args.latent} image "
-                    f"({args.latent}x{args.latent} latent), {args.num_steps}-step DDIM-eta0 "
+                    f"random init seed 42), {8 * args.latent}x{8 * (args.latent_w or args.latent)} image "
+                    f"({args.latent}x{args.latent_w or args.latent} latent), {args.num_steps}-step DDIM-eta0 "
                     f"(Euler) sampling, displaced patch parallelism over {n} row band(s), "
                     f"{args.warmup_steps} synchronous warm-up steps",
-        "latent": [args.latent, args.latent],
+        "latent": [args.latent, args.latent_w or args.latent],
         "sampling_steps": args.num_steps,
         "mode": args.mode if n > 1 else "displaced (N=1: identical to reference mode)",
         "patches": n,
@@ -243,7 +245,7 @@ def main():
 
     model = P.build_model(P.ModelConfig(*SDXL), SEEDS[0])
     cond = P.random_condition(2048, SEEDS[2])
-    H = W = args.latent
+    H, W = args.latent, (args.latent_w or args.latent)
     runner = P.PatchRunner(model, cond, H, W, mode=args.mode if n > 1 else "displaced",
                            n_devices=n, warmup_steps=args.warmup_steps, dtype=args.dtype,
                            world=world, rank=rank, nccl_id=nccl_id, device=local)
