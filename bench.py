@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--warmup-steps", type=int, default=4, help="displaced: sync warm-up steps")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
+                    help="N>1 (torchrun): NCCL, or CUDA IPC peer buffers + copy engines")
     return ap.parse_args()
 
 
@@ -77,6 +79,7 @@ def workload(args, n):
         "mode": args.mode if n > 1 else "displaced (N=1: identical to reference mode)",
         "patches": n,
         "parallelism": f"pp{n}",
+        **({"transport": args.transport} if n > 1 and os.environ.get("WORLD_SIZE", "1") != "1" else {}),
         "l2": "flushed between timed generations (256 MiB device write)",
         "timed_unit": "one full generation (x_T -> x0)",
     }
@@ -238,7 +241,7 @@ def main():
     if world == 1 and n > 1 and torch.cuda.device_count() < n:
         n = args.gpus   # in-process bands share the visible devices
     nccl_id = None
-    if world > 1:
+    if world > 1 and args.transport == "nccl":
         obj = [P.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
@@ -248,7 +251,10 @@ def main():
     H, W = args.latent, (args.latent_w or args.latent)
     runner = P.PatchRunner(model, cond, H, W, mode=args.mode if n > 1 else "displaced",
                            n_devices=n, warmup_steps=args.warmup_steps, dtype=args.dtype,
-                           world=world, rank=rank, nccl_id=nccl_id, device=local)
+                           world=world, rank=rank, nccl_id=nccl_id, device=local,
+                           transport=args.transport)
+    if world > 1 and args.transport == "ipc":
+        runner.connect_ipc()
     abar = P.make_schedule(1000)
     plan = P.make_plan(1000, args.num_steps)
     x_T = P.random_normal(1, 4, H, W, SEEDS[1])

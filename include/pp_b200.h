@@ -50,6 +50,9 @@ extern "C" {
 #define PP_GN_CORRECTED 0
 #define PP_GN_STALE 1
 #define PP_GN_SEPARATE 2
+/* exchange transport of the multi-process layout (world > 1) */
+#define PP_TRANSPORT_NCCL 0
+#define PP_TRANSPORT_IPC 1
 /* step entries, PatchRunner::run_step / step_* (proj/include/patchsim/runtime.hpp:64-71) */
 #define PP_STEP_RUN 0
 #define PP_STEP_REFERENCE 1
@@ -136,6 +139,9 @@ typedef struct {
     const void* nccl_id;
     int device;       /* CUDA device of band 0 (world == 1) or of this rank */
     int profile;      /* record per-kernel CUDA events (pp_runner_profile) */
+    int transport;    /* world > 1: PP_TRANSPORT_NCCL (nccl_id) or PP_TRANSPORT_IPC (CUDA IPC
+                       * peer mappings + copy engines; pp_runner_ipc_export / _connect before
+                       * the first step; no CUDA-graph capture) */
 } pp_runner_opts;
 PP_API void pp_runner_opts_default(pp_runner_opts* o);
 
@@ -183,6 +189,13 @@ PP_API double pp_runner_last_device_ms(const pp_runner* r);
 PP_API int pp_runner_set_profile(pp_runner* r, int on);
 /* ncclGetUniqueId for the multi-process (one rank per GPU) layout */
 PP_API int pp_nccl_unique_id(void* out128);
+/* PP_TRANSPORT_IPC: this rank's CUDA IPC handle blob (receive buffers + flags); *size = its
+ * byte count, copied to out when cap suffices.  Replaces the hub registration of
+ * CollectiveHub (proj/src/collectives.cpp:62-115) for one-process-per-GPU runs. */
+PP_API int pp_runner_ipc_export(pp_runner* r, void* out, long cap, long* size);
+/* every rank's blob concatenated in rank order (per_rank bytes each); opens the peers'
+ * mappings.  Must precede the first step. */
+PP_API int pp_runner_ipc_connect(pp_runner* r, const void* blobs, long per_rank);
 /* host stitching of a rank-ordered band all-gather [n][c][rows][w] into NCHW (c, n*rows, w),
  * as run_workers stitches eps rows (proj/src/runtime.cpp:368-377) */
 PP_API int pp_assemble_bands(const float* gathered, int n_bands, int c, int rows, int w,

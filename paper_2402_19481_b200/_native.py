@@ -17,6 +17,7 @@ PP_OK, PP_EINVAL, PP_ERUNTIME, PP_ECUDA, PP_ENCCL = 0, 1, 2, 3, 4
 DTYPES = {"bf16": 0, "fp32": 1}
 MODES = {"reference": 0, "naive": 1, "sync-pp": 2, "displaced": 3}
 GN_SCHEMES = {"corrected": 0, "stale": 1, "separate": 2}
+TRANSPORTS = {"nccl": 0, "ipc": 1}
 ENTRIES = {"run_step": 0, "reference": 1, "naive": 2, "sync": 3, "displaced": 4}
 
 
@@ -74,7 +75,7 @@ class RunnerOpts(C.Structure):
     _fields_ = [("mode", C.c_int), ("n_devices", C.c_int), ("warmup_steps", C.c_int),
                 ("gn_scheme", C.c_int), ("dtype", C.c_int), ("world", C.c_int),
                 ("rank", C.c_int), ("nccl_id", C.c_void_p), ("device", C.c_int),
-                ("profile", C.c_int)]
+                ("profile", C.c_int), ("transport", C.c_int)]
 
 
 _V, _I, _L, _D, _U64, _F = C.c_void_p, C.c_int, C.c_long, C.c_double, C.c_uint64, C.c_float
@@ -122,6 +123,8 @@ SIGNATURES = {
     "pp_runner_last_device_ms": (_D, [_V]),
     "pp_runner_set_profile": (_I, [_V, _I]),
     "pp_nccl_unique_id": (_I, [_V]),
+    "pp_runner_ipc_export": (_I, [_V, _V, _L, _V]),
+    "pp_runner_ipc_connect": (_I, [_V, _V, _L]),
     "pp_assemble_bands": (_I, [_V, _I, _I, _I, _I, _V]),
     "pp_dev_gemm_bench": (_I, [_I, _I, _I, _I, _I, _I, _I, _I, _I, _V]),
     "pp_dev_gn_bench": (_I, [_I, _LL, _I, _I, _I, _I, _V]),

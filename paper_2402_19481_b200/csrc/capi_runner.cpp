@@ -46,7 +46,10 @@ pp::RunnerOptions opts_of(const pp_runner_opts* o) {
     r.elem = pp::elem_of(o->dtype);
     r.world = o->world < 1 ? 1 : o->world;
     r.rank = o->rank;
-    if (r.world > 1) {
+    r.transport = o->transport;
+    if (r.transport != PP_TRANSPORT_NCCL && r.transport != PP_TRANSPORT_IPC)
+        throw std::invalid_argument("pp_runner_create: bad transport");
+    if (r.world > 1 && r.transport == PP_TRANSPORT_NCCL) {
         need(o->nccl_id, "pp_runner_create(nccl_id)");
         const uint8_t* p = static_cast<const uint8_t*>(o->nccl_id);
         r.nccl_id.assign(p, p + 128);
@@ -293,6 +296,7 @@ PP_API void pp_runner_opts_default(pp_runner_opts* o) {
     o->nccl_id = nullptr;
     o->device = 0;
     o->profile = 0;
+    o->transport = PP_TRANSPORT_NCCL;
 }
 
 PP_API int pp_runner_create(const pp_model* m, const float* cond, int cond_dim, int h, int w,
@@ -424,6 +428,25 @@ PP_API int pp_assemble_bands(const float* gathered, int n_bands, int c, int rows
         need(out, "pp_assemble_bands");
         if (n_bands < 1 || c < 1 || rows < 1 || w < 1) throw std::invalid_argument("pp_assemble_bands: bad shape");
         pp::assemble_bands(gathered, n_bands, c, rows, w, out);
+    });
+}
+
+PP_API int pp_runner_ipc_export(pp_runner* r, void* out, long cap, long* size) {
+    return pp::guard([&] {
+        need(r, "pp_runner_ipc_export");
+        need(size, "pp_runner_ipc_export(size)");
+        const auto blob = r->r->ipc_export();
+        *size = long(blob.size());
+        if (out && cap >= *size) std::memcpy(out, blob.data(), blob.size());
+    });
+}
+
+PP_API int pp_runner_ipc_connect(pp_runner* r, const void* blobs, long per_rank) {
+    return pp::guard([&] {
+        need(r, "pp_runner_ipc_connect");
+        need(blobs, "pp_runner_ipc_connect");
+        if (per_rank <= 0) throw std::invalid_argument("pp_runner_ipc_connect: bad blob size");
+        r->r->ipc_connect(static_cast<const uint8_t*>(blobs), size_t(per_rank));
     });
 }
 

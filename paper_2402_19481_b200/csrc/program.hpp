@@ -186,5 +186,10 @@ public:
 std::unique_ptr<Transport> make_inproc_transport(std::vector<Program*> bands);
 std::unique_ptr<Transport> make_nccl_transport(Program* band, int world, int rank,
                                                const std::vector<uint8_t>& id);
+// Copy-engine transport over CUDA IPC peer mappings (world > 1, no NCCL on the data path):
+// export this rank's handle blob, then connect with every rank's blob (rank order).
+std::unique_ptr<Transport> make_ipc_transport(Program* band, int world, int rank);
+std::vector<uint8_t> ipc_export(Transport& t);
+void ipc_connect(Transport& t, const uint8_t* blobs, size_t per_rank);
 
 }  // namespace pp

@@ -791,7 +791,9 @@ Runner::Runner(const Model& m, const std::vector<float>& cond, int h, int w, con
             const int dev = o_.device;
             bands_.push_back(std::make_unique<Program>(this, m_, weights_for(dev), dev, o_.rank, n_dev_,
                                                        h, w, specs_[o_.rank], o_.elem, o_.profile));
-            transport_ = make_nccl_transport(bands_[0].get(), o_.world, o_.rank, o_.nccl_id);
+            transport_ = o_.transport == 1
+                             ? make_ipc_transport(bands_[0].get(), o_.world, o_.rank)
+                             : make_nccl_transport(bands_[0].get(), o_.world, o_.rank, o_.nccl_id);
         } else {
             for (int d = 0; d < n_dev_; ++d) {
                 const int dev = (o_.device + d) % ndev;
@@ -807,6 +809,18 @@ Runner::Runner(const Model& m, const std::vector<float>& cond, int h, int w, con
     }
 }
 
+std::vector<uint8_t> Runner::ipc_export() {
+    if (!transport_ || o_.world < 2 || o_.transport != 1)
+        throw std::invalid_argument("pp_runner_ipc_export: runner does not use the IPC transport");
+    return pp::ipc_export(*transport_);
+}
+
+void Runner::ipc_connect(const uint8_t* blobs, size_t per_rank) {
+    if (!transport_ || o_.world < 2 || o_.transport != 1)
+        throw std::invalid_argument("pp_runner_ipc_connect: runner does not use the IPC transport");
+    pp::ipc_connect(*transport_, blobs, per_rank);
+}
+
 const DeviceWeights* Runner::weights_for(int dev) {
     for (auto& wp : weights_)
         if (wp->dev == dev) return wp.get();
@@ -817,6 +831,7 @@ const DeviceWeights* Runner::weights_for(int dev) {
 Runner::~Runner() {
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     for (auto ev : graph_events_) cudaEventDestroy(ev);
+    transport_.reset();   // uses the bands' streams and buffers
     bands_.clear();
     naive_rows_.clear();
     naive_cols_.clear();
@@ -1368,7 +1383,9 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
     // ~80 launches and ~30 exchange copies per step become one graph launch.
     bool same_dev = true;
     for (auto& b : bands_) same_dev &= b->dev == bands_[0]->dev;
-    const bool use_graph = !traj && !o_.profile && graphs_enabled_ && (o_.world > 1 || same_dev);
+    // (the IPC transport's flag sequence numbers advance per exchange: not capturable)
+    const bool use_graph = !traj && !o_.profile && graphs_enabled_ && (o_.world > 1 || same_dev) &&
+                           !(o_.world > 1 && o_.transport == 1);
     std::vector<double> key(ts, ts + n);
     for (int i = 0; i < n; ++i) key.push_back(abar_at(ts[i]));
     key.push_back(o_.mode);
@@ -1444,8 +1461,17 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
                 DeviceGuard g(b->dev);
                 nhwc_f32_to_nchw(b->x_state, C, b->stem.rows, w_, b->band_nchw, nullptr, b->cs);
             }
-            std::vector<float> img(size_t(C) * h_ * w_);
+            if (o_.world > 1) {   // every rank records the whole image (rank-ordered gather)
+                Program& b = *bands_[0];
+                DeviceGuard g(b.dev);
+                const size_t band_n = size_t(C) * b.stem.rows * w_;
+                transport_->gather_floats(b, b.band_nchw, b.x_full, band_n);
+                CUDA_CHECK(cudaMemcpyAsync(h_eps_, b.x_full, band_n * n_dev_ * 4, cudaMemcpyDeviceToHost, b.cs));
+                CUDA_CHECK(cudaStreamSynchronize(b.cs));
+                assemble_bands(h_eps_, n_dev_, C, b.stem.rows, w_, traj + size_t(i) * C * h_ * w_);
+            }
             for (auto& b : bands_) {
+                if (o_.world > 1) break;
                 DeviceGuard g(b->dev);
                 const int rows = b->stem.rows;
                 std::vector<float> band(size_t(C) * rows * w_);

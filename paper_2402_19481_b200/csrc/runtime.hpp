@@ -38,7 +38,8 @@ struct RunnerOptions {
     int gn_scheme = GN_CORRECTED;
     Elem elem = Elem::BF16;
     int world = 1, rank = 0;          // world > 1: one band per process, NCCL exchange
-    std::vector<uint8_t> nccl_id;     // 128-byte ncclUniqueId (world > 1)
+    std::vector<uint8_t> nccl_id;     // 128-byte ncclUniqueId (world > 1, NCCL transport)
+    int transport = 0;                // world > 1: 0 NCCL, 1 CUDA IPC + copy engines
     int device = 0;                   // CUDA device of band 0 / of this rank
     bool profile = false;
 };
@@ -95,6 +96,9 @@ public:
     double last_device_ms() const { return last_device_ms_; }
     int n_devices() const { return n_dev_; }
     void set_profile(bool on);
+    // IPC transport (world > 1, transport 1): this rank's handle blob, then every rank's blob
+    std::vector<uint8_t> ipc_export();
+    void ipc_connect(const uint8_t* blobs, size_t per_rank);
 
 private:
     friend struct Program;

@@ -8,10 +8,22 @@
 //  * NcclTransport: one band per process (torchrun / one rank per GPU).  Halos are
 //    ncclSend/ncclRecv pairs with the two neighbours, K/V and GroupNorm statistics are
 //    in-place ncclAllGather, all on the comm stream; consumers wait on its event.
-// Both replace CollectiveHub (proj/src/collectives.cpp:62-232).
+//  * IpcTransport: one band per process, no NCCL on the data path (SURVEY.md §8f row 3:
+//    copy-engine transport).  Every rank exports CUDA IPC handles of its receive buffers
+//    (halo rows, K/V map, GroupNorm statistics, the full-image gather buffer) and of a flag
+//    array; the sender PUSHES its rows with cudaMemcpyAsync on its comm stream (copy engines
+//    over NVLink / NVSwitch, no SM time) and orders them with stream memory operations on the
+//    flags (cuStreamWriteValue32 into the peer's flag after the copies -- the write carries a
+//    memory fence -- and cuStreamWaitValue32 GEQ on the local flag), so no host round trip
+//    and no SM polls.  Per layer and per peer two monotone counters: READY (the peer's compute
+//    stream reached this exchange, so it finished reading the parity buffer about to be
+//    overwritten -- the same ordering the in-process transport takes from the receivers'
+//    `ready` events) and ARRIVED (the peer's rows for exchange k have landed).
+// All replace CollectiveHub (proj/src/collectives.cpp:62-232).
 #include "program.hpp"
 #include "util.hpp"
 
+#include <cuda.h>
 #include <nccl.h>
 
 #include <cstring>
@@ -196,6 +208,237 @@ private:
     ncclComm_t comm_ = nullptr;
 };
 
+// ---------------------------------------------------------------- IPC (copy-engine) transport
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WriteValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+template <class F>
+F driver_fn(const char* name) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    CUDA_CHECK(cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess)
+        throw std::runtime_error(std::string("IPC transport: driver entry point ") + name + " unavailable");
+    return reinterpret_cast<F>(fn);
+}
+
+constexpr uint32_t kIpcMagic = 0x50504331u;   // "PPC1"
+
+class IpcTransport final : public Transport {
+public:
+    // flags layout (uint32): [READY][L][world], [ARRIVED][L][world], [GREADY][world], [GARRIVED][world]
+    IpcTransport(Program* b, int world, int rank) : b_(b), world_(world), rank_(rank) {
+        L_ = int(b->lx.size());
+        DeviceGuard g(b->dev);
+        n_flags_ = size_t(2 * L_ + 2) * world_;
+        flags_ = static_cast<uint32_t*>(b->alloc(n_flags_ * 4));
+        wait_ = driver_fn<WaitValueFn>("cuStreamWaitValue32");
+        write_ = driver_fn<WriteValueFn>("cuStreamWriteValue32");
+        seq_.assign(L_, 0);
+        last_.assign(L_, {0u, 0u});
+        senders_.assign(L_, {});
+        peers_.resize(world_);
+    }
+    ~IpcTransport() override {
+        DeviceGuard g(b_->dev);
+        cudaStreamSynchronize(b_->xs);
+        cudaStreamSynchronize(b_->cs);
+        for (void* p : opened_) cudaIpcCloseMemHandle(p);
+    }
+
+    // the receive buffers a peer pushes into, in a fixed order all ranks agree on
+    std::vector<void*> exported() const {
+        std::vector<void*> v;
+        for (int l = 0; l < L_; ++l) {
+            const auto& x = b_->lx[l];
+            for (int p = 0; p < 2; ++p) {
+                if (x.halo_recv[p]) v.push_back(x.halo_recv[p]);
+                if (x.kv[p]) v.push_back(x.kv[p]);
+                if (x.stats[p]) v.push_back(x.stats[p]);
+            }
+        }
+        v.push_back(b_->x_full);
+        v.push_back(flags_);
+        return v;
+    }
+
+    std::vector<uint8_t> export_blob() const {
+        const auto bufs = exported();
+        std::vector<uint8_t> out(16 + bufs.size() * sizeof(cudaIpcMemHandle_t));
+        const uint32_t hdr[4] = {kIpcMagic, uint32_t(rank_), uint32_t(world_), uint32_t(bufs.size())};
+        std::memcpy(out.data(), hdr, 16);
+        DeviceGuard g(b_->dev);
+        for (size_t i = 0; i < bufs.size(); ++i) {
+            cudaIpcMemHandle_t h;
+            CUDA_CHECK(cudaIpcGetMemHandle(&h, bufs[i]));
+            std::memcpy(out.data() + 16 + i * sizeof(h), &h, sizeof(h));
+        }
+        return out;
+    }
+
+    void connect(const uint8_t* blobs, size_t per_rank) {
+        const size_t nb = exported().size();
+        if (per_rank != 16 + nb * sizeof(cudaIpcMemHandle_t))
+            throw std::invalid_argument("pp_runner_ipc_connect: handle blob size mismatch");
+        DeviceGuard g(b_->dev);
+        for (int r = 0; r < world_; ++r) {
+            const uint8_t* blob = blobs + size_t(r) * per_rank;
+            uint32_t hdr[4];
+            std::memcpy(hdr, blob, 16);
+            if (hdr[0] != kIpcMagic || hdr[1] != uint32_t(r) || hdr[2] != uint32_t(world_) || hdr[3] != nb)
+                throw std::invalid_argument("pp_runner_ipc_connect: blob " + std::to_string(r) +
+                                            " is not rank " + std::to_string(r) + "'s handle set");
+            if (r == rank_) continue;
+            auto& v = peers_[r];
+            v.resize(nb);
+            for (size_t i = 0; i < nb; ++i) {
+                cudaIpcMemHandle_t h;
+                std::memcpy(&h, blob + 16 + i * sizeof(h), sizeof(h));
+                CUDA_CHECK(cudaIpcOpenMemHandle(&v[i], h, cudaIpcMemLazyEnablePeerAccess));
+                opened_.push_back(v[i]);
+            }
+        }
+        // index of each layer's buffers in the exported order
+        idx_.assign(L_, {});
+        size_t k = 0;
+        for (int l = 0; l < L_; ++l) {
+            const auto& x = b_->lx[l];
+            for (int p = 0; p < 2; ++p) {
+                if (x.halo_recv[p]) idx_[l][p] = k++;
+                if (x.kv[p]) idx_[l][p] = k++;
+                if (x.stats[p]) idx_[l][p] = k++;
+            }
+        }
+        connected_ = true;
+    }
+
+    void halo(int l, int par, bool top_only) override {
+        std::vector<std::pair<int, std::pair<size_t, size_t>>> out;   // peer, (src off, dst off)
+        const size_t rb = b_->lx[l].row_bytes;
+        if (rank_ + 1 < world_) out.push_back({rank_ + 1, {rb, 0}});   // last row -> row above e+1
+        if (rank_ > 0 && !top_only) out.push_back({rank_ - 1, {0, rb}});
+        std::vector<int> from;
+        if (rank_ > 0) from.push_back(rank_ - 1);
+        if (rank_ + 1 < world_ && !top_only) from.push_back(rank_ + 1);
+        push(l, par, out, rb, static_cast<const char*>(b_->lx[l].send_rows[par]), from);
+    }
+
+    void kv(int l, int par) override {
+        const size_t bb = b_->lx[l].band_bytes;
+        std::vector<std::pair<int, std::pair<size_t, size_t>>> out;
+        std::vector<int> from;
+        for (int d = 0; d < world_; ++d)
+            if (d != rank_) {
+                out.push_back({d, {size_t(rank_) * bb, size_t(rank_) * bb}});
+                from.push_back(d);
+            }
+        push(l, par, out, bb, static_cast<const char*>(b_->lx[l].kv[par]), from);
+    }
+
+    void stats(int l, int par) override {
+        const size_t eb = size_t(b_->lx[l].G) * 2 * sizeof(double);
+        std::vector<std::pair<int, std::pair<size_t, size_t>>> out;
+        std::vector<int> from;
+        for (int d = 0; d < world_; ++d)
+            if (d != rank_) {
+                out.push_back({d, {size_t(rank_) * eb, size_t(rank_) * eb}});
+                from.push_back(d);
+            }
+        push(l, par, out, eb, reinterpret_cast<const char*>(b_->lx[l].stats[par]), from);
+    }
+
+    void wait(Program& b, int l, int par) override {
+        const uint32_t k = last_[l][par];
+        if (k == 0) return;   // nothing exchanged into this parity yet
+        for (int p : senders_[l]) wait_ge(b.cs, flag(ARRIVED, l, p), k);
+    }
+
+    void gather_floats(Program& b, const float* send, float* recv, size_t count) override {
+        need_connected();
+        if (recv != b.x_full) throw std::logic_error("IPC gather_floats: recv must be the band's x_full");
+        const uint32_t k = ++gseq_;
+        DeviceGuard g(b.dev);
+        for (int p = 0; p < world_; ++p)
+            if (p != rank_) write(b.cs, peer_flag(p, GREADY, 0, rank_), k);
+        for (int p = 0; p < world_; ++p)
+            if (p != rank_) wait_ge(b.cs, flag(GREADY, 0, p), k);
+        const size_t off = size_t(rank_) * count;
+        CUDA_CHECK(cudaMemcpyAsync(recv + off, send, count * 4, cudaMemcpyDeviceToDevice, b.cs));
+        const size_t xi = peers_idx_x_full();
+        for (int p = 0; p < world_; ++p)
+            if (p != rank_)
+                CUDA_CHECK(cudaMemcpyAsync(static_cast<float*>(peers_[p][xi]) + off, send, count * 4,
+                                           cudaMemcpyDeviceToDevice, b.cs));
+        for (int p = 0; p < world_; ++p)
+            if (p != rank_) write(b.cs, peer_flag(p, GARRIVED, 0, rank_), k);
+        for (int p = 0; p < world_; ++p)
+            if (p != rank_) wait_ge(b.cs, flag(GARRIVED, 0, p), k);
+    }
+
+private:
+    enum { READY = 0, ARRIVED = 1, GREADY = 2, GARRIVED = 3 };
+    size_t flag_index(int kind, int l, int p) const {
+        if (kind <= ARRIVED) return (size_t(kind) * L_ + l) * world_ + p;
+        return (size_t(2) * L_ + (kind - GREADY)) * world_ + p;
+    }
+    CUdeviceptr flag(int kind, int l, int p) const {
+        return reinterpret_cast<CUdeviceptr>(flags_ + flag_index(kind, l, p));
+    }
+    CUdeviceptr peer_flag(int peer, int kind, int l, int p) const {
+        return reinterpret_cast<CUdeviceptr>(static_cast<uint32_t*>(peers_[peer].back()) +
+                                             flag_index(kind, l, p));
+    }
+    size_t peers_idx_x_full() const { return exported().size() - 2; }
+    void need_connected() const {
+        if (!connected_)
+            throw std::runtime_error("IPC transport not connected (pp_runner_ipc_connect)");
+    }
+    void wait_ge(cudaStream_t s, CUdeviceptr a, uint32_t v) {
+        const CUresult r = wait_(reinterpret_cast<CUstream>(s), a, v, CU_STREAM_WAIT_VALUE_GEQ);
+        if (r != CUDA_SUCCESS) throw CudaError("cuStreamWaitValue32 failed (" + std::to_string(int(r)) + ")");
+    }
+    void write(cudaStream_t s, CUdeviceptr a, uint32_t v) {
+        const CUresult r = write_(reinterpret_cast<CUstream>(s), a, v, CU_STREAM_WRITE_VALUE_DEFAULT);
+        if (r != CUDA_SUCCESS) throw CudaError("cuStreamWriteValue32 failed (" + std::to_string(int(r)) + ")");
+    }
+
+    // exchange k of layer l into parity `par`: READY handshake with the receivers, copies into
+    // their parity buffers, ARRIVED after the copies (the flag write is fenced behind them)
+    void push(int l, int par, const std::vector<std::pair<int, std::pair<size_t, size_t>>>& out,
+              size_t bytes, const char* src, const std::vector<int>& from) {
+        need_connected();
+        Program& s = *b_;
+        DeviceGuard g(s.dev);
+        const uint32_t k = ++seq_[l];
+        last_[l][par] = k;
+        senders_[l] = from;
+        CUDA_CHECK(cudaStreamWaitEvent(s.xs, s.ready[l], 0));
+        for (int p : from) write(s.xs, peer_flag(p, READY, l, rank_), k);   // I reached exchange k
+        for (const auto& o : out) wait_ge(s.xs, flag(READY, l, o.first), k);
+        const size_t bi = idx_[l][par];
+        for (const auto& o : out)
+            CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(peers_[o.first][bi]) + o.second.second,
+                                       src + o.second.first, bytes, cudaMemcpyDeviceToDevice, s.xs));
+        for (const auto& o : out) write(s.xs, peer_flag(o.first, ARRIVED, l, rank_), k);
+        CUDA_CHECK(cudaEventRecord(s.sent[l][par], s.xs));
+    }
+
+    Program* b_;
+    int world_, rank_, L_ = 0;
+    uint32_t* flags_ = nullptr;
+    size_t n_flags_ = 0;
+    WaitValueFn wait_ = nullptr;
+    WriteValueFn write_ = nullptr;
+    std::vector<uint32_t> seq_;
+    std::vector<std::array<uint32_t, 2>> last_;
+    std::vector<std::vector<int>> senders_;
+    std::vector<std::array<size_t, 2>> idx_;
+    std::vector<std::vector<void*>> peers_;
+    std::vector<void*> opened_;
+    uint32_t gseq_ = 0;
+    bool connected_ = false;
+};
+
 }  // namespace
 
 std::unique_ptr<Transport> make_inproc_transport(std::vector<Program*> bands) {
@@ -205,6 +448,22 @@ std::unique_ptr<Transport> make_inproc_transport(std::vector<Program*> bands) {
 std::unique_ptr<Transport> make_nccl_transport(Program* band, int world, int rank,
                                                const std::vector<uint8_t>& id) {
     return std::make_unique<NcclTransport>(band, world, rank, id);
+}
+
+std::unique_ptr<Transport> make_ipc_transport(Program* band, int world, int rank) {
+    return std::make_unique<IpcTransport>(band, world, rank);
+}
+
+std::vector<uint8_t> ipc_export(Transport& t) {
+    auto* p = dynamic_cast<IpcTransport*>(&t);
+    if (!p) throw std::invalid_argument("pp_runner_ipc_export: runner does not use the IPC transport");
+    return p->export_blob();
+}
+
+void ipc_connect(Transport& t, const uint8_t* blobs, size_t per_rank) {
+    auto* p = dynamic_cast<IpcTransport*>(&t);
+    if (!p) throw std::invalid_argument("pp_runner_ipc_connect: runner does not use the IPC transport");
+    p->connect(blobs, per_rank);
 }
 
 }  // namespace pp

@@ -185,6 +185,7 @@ class RunnerOptions:
     nccl_id: bytes | None = None
     device: int = 0
     profile: bool = False
+    transport: str = "nccl"          # world > 1: "nccl" or "ipc" (CUDA IPC + copy engines)
 
 
 class PatchRunner:
@@ -209,11 +210,38 @@ class PatchRunner:
         o.nccl_id = C.cast(self._id, C.c_void_p) if self._id is not None else None
         o.device = opts.device
         o.profile = int(opts.profile)
+        if opts.transport not in N.TRANSPORTS:
+            raise InvalidArgument(f"unknown transport '{opts.transport}'")
+        o.transport = N.TRANSPORTS[opts.transport]
         h_ = C.c_void_p()
         N.check(N.lib().pp_runner_create(model._h, _p(cond), cond.size, h, w, C.byref(o),
                                          C.byref(h_)))
         self._r = h_
         self.n_devices = 1 if opts.mode == "reference" else opts.n_devices
+
+    def ipc_handles(self) -> bytes:
+        """This rank's CUDA IPC handle blob (transport "ipc"), to be all-gathered."""
+        n = C.c_long()
+        N.check(N.lib().pp_runner_ipc_export(self._r, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        N.check(N.lib().pp_runner_ipc_export(self._r, buf, n.value, C.byref(n)))
+        return buf.raw
+
+    def ipc_connect(self, blobs) -> None:
+        """Open every rank's receive buffers (blobs in rank order)."""
+        blobs = [bytes(b) for b in blobs]
+        if len({len(b) for b in blobs}) != 1:
+            raise InvalidArgument("ipc_connect: blobs differ in size")
+        flat = C.create_string_buffer(b"".join(blobs), len(blobs) * len(blobs[0]))
+        N.check(N.lib().pp_runner_ipc_connect(self._r, flat, len(blobs[0])))
+
+    def connect_ipc(self, group=None) -> None:
+        """all-gather the handle blobs over torch.distributed (any backend) and connect."""
+        import torch.distributed as dist
+        mine = self.ipc_handles()
+        allb = [None] * dist.get_world_size(group)
+        dist.all_gather_object(allb, mine, group=group)
+        self.ipc_connect(allb)
 
     def close(self):
         if getattr(self, "_r", None) and N._lib is not None:

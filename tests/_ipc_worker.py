@@ -1,0 +1,91 @@
+"""Worker of tests/test_ipc_gpu.py: one rank of a world-2 run with the copy-engine (CUDA IPC)
+transport, both ranks on cuda:0 (the pool has one GPU per box; CUDA IPC maps a buffer of
+another process on the same device exactly as on a peer).  Rank 0 repeats the run in-process
+(world 1, two bands: the in-process transport, itself parity-tested against the oracle) and
+writes the comparison to argv[1]."""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2402_19481_b200 import patchsim as P  # noqa: E402
+
+
+def main():
+    out_path = sys.argv[1]
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    torch.cuda.set_device(0)
+    cfg = P.ModelConfig()
+    h = w = 32
+    steps = 6
+    model = P.build_model(cfg, 42)
+    cond = P.random_condition(cfg.cond_dim, 7)
+    x_T = P.random_normal(1, cfg.in_channels, h, w, 1234)
+    abar = P.make_schedule(1000)
+    plan = P.make_plan(1000, steps)
+    res = {}
+    for mode, warmup in (("displaced", 1), ("sync-pp", 0), ("displaced", 0)):
+        for dtype in ("bf16", "fp32"):
+            r = P.PatchRunner(model, cond, h, w, mode=mode, n_devices=world, warmup_steps=warmup,
+                              dtype=dtype, world=world, rank=rank, device=0, transport="ipc")
+            r.connect_ipc()
+            x0, _ = r.sample(x_T, plan, abar)
+            x0b, traj = r.sample(x_T, plan, abar, trajectory=True)   # per-step gathers
+            eps = r.run_step(x_T, int(plan[0]), 0)
+            vol = r.volumes()
+            dist.barrier()   # nobody frees an exported buffer while a peer still maps it
+            r.close()
+            dist.barrier()
+            if rank == 0:
+                ref = P.PatchRunner(model, cond, h, w, mode=mode, n_devices=world,
+                                    warmup_steps=warmup, dtype=dtype, device=0)
+                rx0, _ = ref.sample(x_T, plan, abar)
+                _, rtraj = ref.sample(x_T, plan, abar, trajectory=True)
+                reps = ref.run_step(x_T, int(plan[0]), 0)
+                key = f"{mode}/w{warmup}/{dtype}"
+                res[key] = {
+                    "x0_equal": bool(np.array_equal(x0, rx0)),
+                    "x0_replay_equal": bool(np.array_equal(x0, x0b)),
+                    "traj_equal": bool(np.array_equal(traj, rtraj)),
+                    "eps_equal": bool(np.array_equal(eps, reps)),
+                    "x0_rel": float(np.linalg.norm(x0 - rx0) / np.linalg.norm(rx0)),
+                    "finite": bool(np.isfinite(x0).all()),
+                    "volumes_equal": vol == ref.volumes(),
+                }
+                ref.close()
+            dist.barrier()
+    # bad blob: wrong rank order is rejected with the reference's error class
+    r = P.PatchRunner(model, cond, h, w, mode="displaced", n_devices=world, warmup_steps=1,
+                      world=world, rank=rank, device=0, transport="ipc")
+    mine = r.ipc_handles()
+    allb = [None] * world
+    dist.all_gather_object(allb, mine)
+    try:
+        r.ipc_connect(list(reversed(allb)))
+        res_bad = "accepted"
+    except P.InvalidArgument as e:
+        res_bad = "InvalidArgument: " + str(e)
+    try:
+        P.PatchRunner(model, cond, h, w, mode="displaced", n_devices=world, world=world,
+                      rank=rank, device=0, transport="bogus")
+        res_tp = "accepted"
+    except P.InvalidArgument as e:
+        res_tp = "InvalidArgument: " + str(e)
+    dist.barrier()
+    r.close()
+    dist.barrier()
+    if rank == 0:
+        res["bad_blob"] = res_bad
+        res["bad_transport"] = res_tp
+        with open(out_path, "w") as f:
+            json.dump(res, f, indent=1)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

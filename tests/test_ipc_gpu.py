@@ -1,0 +1,51 @@
+"""Copy-engine transport (CUDA IPC peer mappings + stream memory operations, SURVEY.md §8f
+row 3): a world-2 / world-4 run, one process per band, must be bitwise identical to the in-process
+multi-band run (same kernels, same data; only the exchange mechanism differs) in every mode,
+dtype, with and without trajectories, and through the step API."""
+import json
+import os
+import signal
+import socket
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_ipc_transport_matches_inprocess(tmp_path, world):
+    # world 4: interior bands exchange halos with both neighbours
+    out = tmp_path / "ipc.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tests", "_ipc_worker.py"), str(out)]
+    # own process group: a hung exchange is killed with both workers, never left on the GPU
+    p = subprocess.Popen(cmd, cwd=ROOT, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True,
+                         start_new_session=True)
+    try:
+        log, _ = p.communicate(timeout=300)
+    except subprocess.TimeoutExpired:
+        os.killpg(p.pid, signal.SIGKILL)
+        log, _ = p.communicate()
+        pytest.fail(f"IPC world-{world} run timed out:\n" + log[-3000:])
+    assert p.returncode == 0, log[-5000:]
+    res = json.loads(out.read_text())
+    for key in [k for k in res if "/" in k]:
+        r = res[key]
+        assert r["finite"], key
+        assert r["x0_equal"] and r["traj_equal"] and r["eps_equal"], (key, r)
+        assert r["x0_replay_equal"], (key, r)
+        assert r["volumes_equal"], (key, r)
+    assert res["bad_blob"].startswith("InvalidArgument"), res["bad_blob"]
+    assert res["bad_transport"].startswith("InvalidArgument"), res["bad_transport"]
