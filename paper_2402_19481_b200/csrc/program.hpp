@@ -124,6 +124,7 @@ struct Program {
     const float* temb_ptr(int l) const {
         return temb_step_base ? temb_step_base + size_t(temb_slot[l]) * temb_ldt : temb_out[l];
     }
+    std::vector<int> temb_plan_key;   // timesteps the table holds
     void prepare_temb_plan(const int* ts, int n);
     void use_temb_step(int i) {
         temb_step_base = i < 0 ? nullptr : temb_plan + size_t(i) * n_temb * temb_ldt;

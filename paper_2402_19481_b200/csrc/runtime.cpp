@@ -562,6 +562,10 @@ void Program::record_ready(int l) { CUDA_CHECK(cudaEventRecord(ready[l], cs)); }
 
 void Program::prepare_temb_plan(const int* ts, int n) {
     if (!n_temb) return;
+    // the projections depend only on the timesteps (the weights are fixed per runner)
+    std::vector<int> key(ts, ts + n);
+    if (key == temb_plan_key) return;
+    temb_plan_key.clear();
     DeviceGuard dg(dev);
     const int dim = m->time_dim();
     std::vector<float> embs(size_t(n) * dim);
@@ -581,6 +585,7 @@ void Program::prepare_temb_plan(const int* ts, int n) {
     CUDA_CHECK(cudaMemcpy(temb_embs, embs.data(), embs.size() * 4, cudaMemcpyHostToDevice));
     time_projection_plan(temb_dev, n_temb, temb_max_c, temb_embs, n, dim, temb_plan, temb_ldt, cs);
     CUDA_CHECK(cudaStreamSynchronize(cs));
+    temb_plan_key = std::move(key);
 }
 
 void Program::time_projection(int t) {
