@@ -797,15 +797,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // publish: CTA barrier, then one gpu-scope fence + flag (the fence is
                     // cumulative over the other threads' stores ordered before the barrier)
                     epi_bar();
-                    if (et == 0) {
-                        __threadfence();
-                        atomicExch(ready, 1u);
-                    }
+                    if (et == 0) ptx::st_release_gpu(ready, 1u);
                     continue;
                 }
                 if (et == 0) {
                     while (ptx::ld_acquire_gpu(ready) == 0u) __nanosleep(64);
-                    __threadfence();
                 }
                 epi_bar();
                 for (int c0 = half * 16; c0 < a.block_n; c0 += kCS) {
@@ -884,10 +880,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // the last M tile of this N tile folds the N tile's groups (the N tiles fold
                 // disjoint groups in parallel); counter gn_ticket[1 + nt]
                 if (et == 0) {
-                    __threadfence();   // cumulative over the partials stored before the barrier
-                    const bool last = atomicAdd(a.gn_ticket + 1 + tc.nt, 1u) == unsigned(m_tiles - 1);
-                    if (last) __threadfence();
-                    st.flags[2] = last;
+                    // release: cumulative over the partials stored before the barrier;
+                    // acquire: the folding CTA sees every other tile's partials
+                    st.flags[2] = ptx::atom_add_acq_rel_gpu(a.gn_ticket + 1 + tc.nt, 1u) ==
+                                  unsigned(m_tiles - 1);
                 }
                 epi_bar();
                 if (st.flags[2]) {

@@ -156,6 +156,14 @@ constexpr int kGnUStats = 8;   // pixels per thread with statistics (fewer block
 
 constexpr int kGnRange = 32;   // blocks per first-level statistics fold
 
+// gpu-scope acq_rel ticket (release: cumulative over the block's partials stored before the
+// preceding __syncthreads; acquire: the folding block sees the other blocks' partials)
+__device__ __forceinline__ unsigned int atom_add_acq_rel(unsigned int* p, unsigned int v) {
+    unsigned int old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
 // dst[g] = sum_{k < n} src[k * G + g] / div (double2 = (sum, sum_sq)), fixed order: thread
 // (part, g) sums k = part, part + parts, ...; the parts are added in order through smem
 // (scratch >= 2 * parts * G doubles).  Reads with ld.global.cg (partials of other blocks).
@@ -405,9 +413,7 @@ __global__ void __launch_bounds__(256, (STATS ? 2 : 3))
     double2* part2 = part1 + size_t(nblk) * Gs;
     __syncthreads();
     if (tid == 0) {
-        __threadfence();
-        is_last = atomicAdd(so.ticket + 1 + r, 1u) == unsigned(rsize - 1);
-        if (is_last) __threadfence();
+        is_last = atom_add_acq_rel(so.ticket + 1 + r, 1u) == unsigned(rsize - 1);
     }
     __syncthreads();
     if (!is_last) return;
@@ -416,9 +422,7 @@ __global__ void __launch_bounds__(256, (STATS ? 2 : 3))
     if (tid == 0) so.ticket[1 + r] = 0u;
     __syncthreads();
     if (tid == 0) {
-        __threadfence();
-        is_last = atomicAdd(so.ticket, 1u) == unsigned(nrange - 1);
-        if (is_last) __threadfence();
+        is_last = atom_add_acq_rel(so.ticket, 1u) == unsigned(nrange - 1);
     }
     __syncthreads();
     if (!is_last) return;
