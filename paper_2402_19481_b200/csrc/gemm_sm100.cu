@@ -843,7 +843,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     else
                         ptx::tma_store_2d(&tmD, smem, nbase, tc.ty * kTileM);
                     ptx::bulk_commit();
-                    ptx::bulk_wait_all();
+                    ptx::bulk_wait_read();
                 }
             }
             if (a.gn_groups && !(a.debug & 256)) {

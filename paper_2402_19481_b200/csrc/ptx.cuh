@@ -143,6 +143,11 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_all() {
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
+// the bulk stores have finished READING shared memory (the staging can be reused / the CTA
+// can exit; the global writes complete with the grid)
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
 
 // Multicast variant: the box lands at the same CTA-relative smem offset in every CTA of
 // `mask` (cluster ranks) and completes `bytes` on each destination CTA's mbarrier at the
