@@ -1218,7 +1218,8 @@ double tile_eff(int pair, int bn) {
 // over SM pairs); split-K pays a partial write + read.
 //   force_splits: bits 0-3 = splits (0 auto), bit 4 = force pair, bit 5 = force single CTA
 void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int gn_cpg, int force_splits,
-                   int force_block_n, int& block_n, int& splits, int& pair, bool one_wave = false) {
+                   int force_block_n, int& block_n, int& splits, int& pair, bool one_wave = false,
+                   bool gemm = false) {
     double best = 1e300;
     block_n = 16;
     splits = 1;
@@ -1262,6 +1263,29 @@ void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int gn_cpg
         }
     }
     if (force_block_n) block_n = force_block_n;
+    // Plain GEMMs that fit one wave of single-CTA tiles (the 1024-token attention S / PV and
+    // linear layers): each CTA runs a short K loop once, so the time is latency, not
+    // shared-memory throughput -- the smallest per-CTA tile that still fits one wave wins
+    // (measured, scripts/attn_gemm_sweep.py: PV 8.3 us at block_n 80 vs 10.8 us at pair 160).
+    if (gemm && !force_block_n && !fs && !force_pair && !one_wave && !gn_cpg) {
+        double lbest = 1e300;
+        int lbn = 0;
+        for (int bn = 256; bn >= 64; bn -= 16) {   // >= 64: the measured range
+            if (n_pad % bn) continue;
+            const long long tiles = (long long)m_tiles * (n_pad / bn);
+            if (tiles > num_sms) continue;
+            const double cost = double(k_blocks) * 2.0 * bn + 2500.0;
+            if (cost < lbest) {
+                lbest = cost;
+                lbn = bn;
+            }
+        }
+        if (lbn) {
+            block_n = lbn;
+            splits = 1;
+            pair = 0;
+        }
+    }
 }
 
 void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const EpilogueSpec& ep,
@@ -1278,7 +1302,7 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
     }
     int bn, splits, pair;
     choose_tiling(m_tiles, n_pad, k_blocks, num_sms, cpg, force_splits, force_block_n, bn, splits,
-                  pair, ep.gn_apply);
+                  pair, ep.gn_apply, a.mode == 0);
     if (ep.gn_apply) {
         if (!gn) throw std::invalid_argument("fused GroupNorm apply needs the statistics epilogue");
         if (ep.residual) throw std::invalid_argument("fused GroupNorm apply: conv residual unsupported");
