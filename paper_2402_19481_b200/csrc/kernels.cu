@@ -556,6 +556,80 @@ __global__ void softmax_kernel(const float* __restrict__ S, int ns, long long ld
         pr[j] = from_float<T>(expf(s[j] * scale - mx) * inv, true);
 }
 
+// Row softmax with the row held in registers: one read of S (float4, streaming) instead of
+// three, NV float4 per thread, 256 threads per row; same per-element formula as
+// softmax_kernel (expf(s * scale - max) * (1 / sum)).  Needs ns, lds, ldp % 4 == 0.
+template <int NV>
+__device__ __forceinline__ float block_reduce_256(float v, bool is_max, float* red) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const float w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = is_max ? fmaxf(v, w) : v + w;
+    }
+    __syncthreads();   // red may still be read from the previous reduction
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    v = red[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) v = is_max ? fmaxf(v, red[w]) : v + red[w];
+    return v;
+}
+
+template <class T, int NV>
+__global__ void __launch_bounds__(256) softmax_reg_kernel(const float* __restrict__ S, int ns,
+                                                          long long lds, float scale,
+                                                          T* __restrict__ P, long long ldp) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ float red[8];
+    const int row = blockIdx.x;
+    const int n4 = ns >> 2;
+    const float4* s4 = reinterpret_cast<const float4*>(S + (long long)row * lds);
+    float4 v[NV];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const int j = threadIdx.x + i * 256;
+        if (j < n4) {
+            v[i] = __ldcs(s4 + j);
+            v[i].x *= scale;
+            v[i].y *= scale;
+            v[i].z *= scale;
+            v[i].w *= scale;
+            mx = fmaxf(mx, fmaxf(fmaxf(v[i].x, v[i].y), fmaxf(v[i].z, v[i].w)));
+        }
+    }
+    mx = block_reduce_256<NV>(mx, true, red);
+    float sum = 0.0f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        if (threadIdx.x + i * 256 < n4) {
+            v[i].x = expf(v[i].x - mx);
+            v[i].y = expf(v[i].y - mx);
+            v[i].z = expf(v[i].z - mx);
+            v[i].w = expf(v[i].w - mx);
+            sum += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+        }
+    }
+    sum = block_reduce_256<NV>(sum, false, red);
+    const float inv = 1.0f / sum;
+    T* pr = P + (long long)row * ldp;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const int j = threadIdx.x + i * 256;
+        if (j < n4) {
+            const T a = from_float<T>(v[i].x * inv, true), b = from_float<T>(v[i].y * inv, true);
+            const T c = from_float<T>(v[i].z * inv, true), d = from_float<T>(v[i].w * inv, true);
+            if constexpr (sizeof(T) == 2) {
+                __align__(8) T q[4] = {a, b, c, d};
+                *reinterpret_cast<uint2*>(pr + 4 * j) = *reinterpret_cast<const uint2*>(q);
+            } else {
+                *reinterpret_cast<float4*>(pr + 4 * j) = make_float4(a, b, c, d);
+            }
+        }
+    }
+}
+
 template <class T>
 __global__ void transpose_kernel(const T* __restrict__ V, int ns, int C, long long ldv,
                                  T* __restrict__ Vt, long long ldt) {
@@ -863,7 +937,23 @@ void upsample2x(Elem e, const void* x, void* y, int rows, int W, int ld, cudaStr
 
 void softmax_rows(Elem e, const float* S, int m, int ns, long long lds, float scale, void* P,
                   long long ldp, cudaStream_t s) {
-    DISPATCH(e, launch_pdl(softmax_kernel<T>, dim3(m), dim3(256), 0, s, 1, S, ns, lds, scale, static_cast<T*>(P), ldp));
+    const bool vec = ns % 4 == 0 && lds % 4 == 0 && ldp % 4 == 0 && ns <= 16 * 1024 &&
+                     reinterpret_cast<uintptr_t>(S) % 16 == 0 && reinterpret_cast<uintptr_t>(P) % 16 == 0;
+    if (vec) {
+        const int per = (ns / 4 + 255) / 256;   // float4 per thread
+#define PP_SOFTMAX_REG(NV)                                                                          \
+    DISPATCH(e, launch_pdl(softmax_reg_kernel<T, NV>, dim3(m), dim3(256), 0, s, 1, S, ns, lds, scale, \
+                           static_cast<T*>(P), ldp))
+        if (per <= 1) PP_SOFTMAX_REG(1);
+        else if (per <= 2) PP_SOFTMAX_REG(2);
+        else if (per <= 4) PP_SOFTMAX_REG(4);
+        else if (per <= 8) PP_SOFTMAX_REG(8);
+        else PP_SOFTMAX_REG(16);
+#undef PP_SOFTMAX_REG
+    } else {
+        DISPATCH(e, launch_pdl(softmax_kernel<T>, dim3(m), dim3(256), 0, s, 1, S, ns, lds, scale,
+                               static_cast<T*>(P), ldp));
+    }
     CUDA_CHECK(cudaGetLastError());
 }
 
