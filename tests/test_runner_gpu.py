@@ -326,3 +326,34 @@ def test_sdxl_shape_displaced_two_bands_matches_reference_build():
         xr = O.ddim_update(xr, er, a_t, a_n)
         xp = O.ddim_update(xp, ep, a_t, a_n)
     assert rel(xp, xr) <= TOL["bf16"], rel(xp, xr)
+
+
+@pytest.mark.parametrize("entry,mode,n", [("run_step", "reference", 1), ("run_step", "sync-pp", 2),
+                                          ("step_naive", "naive", 2)])
+def test_non_finite_input_is_reported(entry, mode, n):
+    # Tensor::require_finite (proj/src/tensor.cpp:36-42) on the step's eps
+    # (proj/src/runtime.cpp:346-394): runtime_error "<who>: non-finite value in tensor (1,C,H,W)"
+    m = P.build_model(TINY, 97)
+    cond = O.random_condition(8, 98)
+    r = P.PatchRunner(m, cond, 16, 16, mode=mode, n_devices=n, dtype="bf16")
+    x = O.random_normal(1, 2, 16, 16, 99)
+    x[0, 1, 7, 3] = np.nan
+    # run_step dispatches Reference mode to step_reference, which names itself (runtime.cpp:394)
+    who = {"naive": "step_naive", "reference": "step_reference"}.get(mode, "run_step")
+    with pytest.raises(P.RuntimeFailure, match=rf"{who}: non-finite value in tensor \(1,2,16,16\)"):
+        getattr(r, entry)(x, 500, 0)
+    # the runner stays usable after the error (flags are reset)
+    x[0, 1, 7, 3] = 0.0
+    eps = getattr(r, entry)(x, 500, 0)
+    assert np.isfinite(eps).all()
+
+
+def test_non_finite_x_T_in_sample_is_reported():
+    # sample() -> the executor's require_finite on eps (proj/src/sampler.cpp:76-95)
+    m = P.build_model(TINY, 97)
+    cond = O.random_condition(8, 98)
+    r = P.PatchRunner(m, cond, 16, 16, mode="displaced", n_devices=2, warmup_steps=1, dtype="bf16")
+    x = O.random_normal(1, 2, 16, 16, 99)
+    x[0, 0, 0, 0] = np.inf
+    with pytest.raises(P.RuntimeFailure, match="non-finite value in tensor"):
+        r.sample(x, P.make_plan(1000, 4), P.make_schedule(1000))
