@@ -45,6 +45,7 @@ struct GemmArgs {
     // [3 rows][slab_px = w_box + 2][128 B] shared by the nine taps of a channel chunk; the
     // K index is chunk * 9 + tap (three taps per stage), B comes from a 4-D map
     int slab;
+    int slab_slots;           // slab ring depth (2..4: deeper when small block_n leaves smem free)
     int slab_px;
     uint32_t slab_bytes;      // smem per slot (1024-aligned)
     uint32_t slab_box_bytes;  // TMA bytes per slab

@@ -72,17 +72,19 @@ struct SmemTail {
     uint64_t* empty_bar;
     uint64_t* tfull_bar;
     uint64_t* tempty_bar;
-    uint64_t* slab_full;    // [2] A-slab ring (slab mode)
-    uint64_t* slab_empty;   // [2]
+    uint64_t* slab_full;    // [kMaxSlabSlots] A-slab ring (slab mode)
+    uint64_t* slab_empty;   // [kMaxSlabSlots]
     uint32_t* tmem_slot;
     int* flags;        // [4]
     float* bias;       // [2][block_n]
     float* gn;         // [4 warps][block_n cols][2]  (also the GN fold scratch)
 };
 
+constexpr int kMaxSlabSlots = 4;
+
 // Sized by block_n so that the fused-GN variant keeps the same pipeline depth.
 __host__ __device__ inline size_t tail_bytes(int stages, bool gn, int block_n) {
-    return size_t(2 * stages + 8) * 8 + 16 + 16 + size_t(2) * block_n * 4 +
+    return size_t(2 * stages + 4 + 2 * kMaxSlabSlots) * 8 + 16 + 16 + size_t(2) * block_n * 4 +
            (gn ? size_t(4) * block_n * 2 * 4 : 0);
 }
 
@@ -319,11 +321,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int kps = a.kps;                                      // K blocks per stage (1 or 2)
     const uint32_t a_slot = kTileM * kBlockBytes;               // one A box slot
     const uint32_t b_slot = uint32_t(a.block_n / P) * kBlockBytes;
-    // slab mode (stride-1 conv, one output row per tile): A comes from a 2-slot ring of im2col
+    // slab mode (stride-1 conv, one output row per tile): A comes from a 2-4 slot ring of im2col
     // slabs (3 input rows x (w_box + 2) pixels x 128 B per channel chunk) that serve all nine
     // taps; the stage ring then holds B only
     const uint32_t a_stage_bytes = a.slab ? 0u : kps * a_slot;
-    uint8_t* const ring = smem + (a.slab ? 2u * a.slab_bytes : 0u);
+    uint8_t* const ring = smem + (a.slab ? uint32_t(a.slab_slots) * a.slab_bytes : 0u);
     const uint32_t b_stage_bytes = kps * b_slot;
     const uint32_t stage_bytes = a_stage_bytes + b_stage_bytes;
     SmemTail st;
@@ -334,8 +336,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         st.tfull_bar = st.empty_bar + stages;
         st.tempty_bar = st.tfull_bar + 2;
         st.slab_full = st.tempty_bar + 2;
-        st.slab_empty = st.slab_full + 2;
-        st.tmem_slot = reinterpret_cast<uint32_t*>(st.slab_empty + 2);
+        st.slab_empty = st.slab_full + kMaxSlabSlots;
+        st.tmem_slot = reinterpret_cast<uint32_t*>(st.slab_empty + kMaxSlabSlots);
         st.flags = reinterpret_cast<int*>(st.tmem_slot + 4);
         st.bias = reinterpret_cast<float*>(st.flags + 4);
         st.gn = st.bias + 2 * a.block_n;
@@ -357,9 +359,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&st.full_bar[s], 1);
             ptx::mbar_init(&st.empty_bar[s], Q);   // one MMA commit per pair sharing the stage
         }
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < kMaxSlabSlots; ++s) {
             ptx::mbar_init(&st.slab_full[s], 1);
             ptx::mbar_init(&st.slab_empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
             ptx::mbar_init(&st.tfull_bar[s], 1);
             ptx::mbar_init(&st.tempty_bar[s], 4 * kEpiPerQuarter * P);
         }
@@ -525,7 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __syncwarp();
                 }
                 ++it;
-                if (a.slab && kb % 9 + kps >= 9 && ++sl_slot == 2) {
+                if (a.slab && kb % 9 + kps >= 9 && ++sl_slot == a.slab_slots) {
                     sl_slot = 0;
                     sl_phase ^= 1;
                 }
@@ -625,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                     __syncwarp();
-                    if (sg + kps >= 9 && ++ms_slot == 2) {
+                    if (sg + kps >= 9 && ++ms_slot == a.slab_slots) {
                         ms_slot = 0;
                         ms_phase ^= 1;
                     }
@@ -1178,16 +1182,17 @@ uint32_t make_idesc(Elem e, int n, int m) {
     return d;
 }
 
-size_t smem_for(int block_n, int stages, bool gn, int pair, int kps, uint32_t slab_bytes = 0) {
+size_t smem_for(int block_n, int stages, bool gn, int pair, int kps, uint32_t slab_bytes = 0,
+                int slab_slots = 2) {
     const size_t a_stage = slab_bytes ? 0 : kTileM * kBlockBytes;
-    return size_t(2) * slab_bytes +
+    return size_t(slab_slots) * slab_bytes +
            size_t(stages) * kps * (a_stage + block_n / (pair ? 2 : 1) * kBlockBytes) + 1024 +
            tail_bytes(stages, gn, block_n);
 }
 
-int stages_for(int block_n, bool gn, int pair, int kps, uint32_t slab_bytes = 0) {
+int stages_for(int block_n, bool gn, int pair, int kps, uint32_t slab_bytes = 0, int slab_slots = 2) {
     int s = 8;
-    while (s > 2 && smem_for(block_n, s, gn, pair, kps, slab_bytes) > size_t(kSmemMax)) --s;
+    while (s > 2 && smem_for(block_n, s, gn, pair, kps, slab_bytes, slab_slots) > size_t(kSmemMax)) --s;
     return s;
 }
 
@@ -1336,6 +1341,23 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
     if (a.slab) a.kb_per_split = (a.kb_per_split + 8) / 9 * 9;         // whole channel chunks
     a.splits = (k_blocks + a.kb_per_split - 1) / a.kb_per_split;
     a.stages = stages_for(bn, gn, pair, a.kps, a.slab ? a.slab_bytes : 0u);
+    a.slab_slots = 2;
+    if (a.slab) {
+        // deeper slab ring where smem is left over (small block_n: the head conv), never at the
+        // cost of B stages; a slab per channel chunk, so no more slots than chunks.
+        // PP_SLAB_SLOTS=n forces n (experiments)
+        static const int forced_slots = [] {
+            const char* v = std::getenv("PP_SLAB_SLOTS");
+            return v ? std::atoi(v) : 0;
+        }();
+        for (int s = kMaxSlabSlots; s > 2; --s) {
+            if (forced_slots && s != forced_slots) continue;
+            if (s > a.cin_chunks) continue;
+            if (smem_for(bn, a.stages, gn, pair, a.kps, a.slab_bytes, s) > size_t(kSmemMax)) continue;
+            a.slab_slots = s;
+            break;
+        }
+    }
     a.idesc = make_idesc(p.elem, bn / a.n_sub, pair ? 2 * kTileM : kTileM);
     a.out = ep.out;
     a.out_ld = ep.out_ld;
@@ -1379,7 +1401,7 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
     const int Q = p.mc ? 2 : 1;
     const int units = ((m_tiles + P - 1) / P + Q - 1) / Q * a.n_tiles * a.splits;
     p.grid = P * Q * std::min(units, num_sms / (P * Q));
-    p.smem = smem_for(bn, a.stages, gn, pair, a.kps, a.slab ? a.slab_bytes : 0u);
+    p.smem = smem_for(bn, a.stages, gn, pair, a.kps, a.slab ? a.slab_bytes : 0u, a.slab_slots);
 }
 
 }  // namespace
