@@ -173,15 +173,15 @@ __device__ void fold_fixed(const double2* src, int n, int G, double2* dst, doubl
     if (tid < parts * G) {
         const int g = tid % G, pt = tid / G;
         double a = 0.0, b = 0.0;
-        for (int k0 = pt; k0 < n; k0 += 4 * parts) {
-            double2 v[4];
+        for (int k0 = pt; k0 < n; k0 += 8 * parts) {
+            double2 v[8];   // one round of loads covers a 32-block range (parts >= 4)
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < 8; ++u) {
                 const int k = k0 + u * parts;
                 v[u] = k < n ? __ldcg(src + size_t(k) * G + g) : make_double2(0.0, 0.0);
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < 8; ++u) {
                 a += v[u].x;
                 b += v[u].y;
             }
