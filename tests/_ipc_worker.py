@@ -62,6 +62,11 @@ def main():
     # bad blob: wrong rank order is rejected with the reference's error class
     r = P.PatchRunner(model, cond, h, w, mode="displaced", n_devices=world, warmup_steps=1,
                       world=world, rank=rank, device=0, transport="ipc")
+    try:   # a step before the handles are exchanged
+        r.run_step(x_T, int(plan[0]), 0)
+        res_nc = "accepted"
+    except P.RuntimeFailure as e:
+        res_nc = "RuntimeFailure: " + str(e)
     mine = r.ipc_handles()
     allb = [None] * world
     dist.all_gather_object(allb, mine)
@@ -81,6 +86,7 @@ def main():
     dist.barrier()
     if rank == 0:
         res["bad_blob"] = res_bad
+        res["not_connected"] = res_nc
         res["bad_transport"] = res_tp
         with open(out_path, "w") as f:
             json.dump(res, f, indent=1)

@@ -49,3 +49,4 @@ def test_ipc_transport_matches_inprocess(tmp_path, world):
         assert r["volumes_equal"], (key, r)
     assert res["bad_blob"].startswith("InvalidArgument"), res["bad_blob"]
     assert res["bad_transport"].startswith("InvalidArgument"), res["bad_transport"]
+    assert res["not_connected"].startswith("RuntimeFailure") and "not connected" in res["not_connected"]
