@@ -59,8 +59,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
-// Polling load with acquire semantics at gpu scope (no read-modify-write: many pollers of one
-// flag do not serialise on the L2 atomic unit).
 // gpu-scope acq_rel read-modify-write / release store: the ticket and flag protocols'
 // ordering without the MEMBAR.SC.GPU a __threadfence() compiles to (cumulative over the
 // stores other threads of the CTA ordered before a preceding bar.sync)
@@ -73,6 +71,8 @@ __device__ __forceinline__ void st_release_gpu(unsigned int* p, unsigned int v) 
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Polling load with acquire semantics at gpu scope (no read-modify-write: many pollers of one
+// flag do not serialise on the L2 atomic unit).
 __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
     unsigned int v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
