@@ -561,6 +561,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t a_next = a_slot >> 4, b_next = b_slot >> 4;
         const uint32_t b_half = uint32_t(a.block_n / 2 / P) * kBlockBytes;   // n_sub == 2
         const uint32_t b_sub = uint32_t(a.block_n / a.n_sub / P) * kBlockBytes;  // slab: one tap, one half
+        // loop-invariant launch parameters, read once (the issue loop is on the critical path)
+        const bool do_mma = !(a.debug & 1);
+        const bool wide = a.n_sub == 2;
+        const bool slab = a.slab != 0;
+        const int n_sub = a.n_sub;
+        const uint32_t idesc = a.idesc;
         int stage = 0;
         uint32_t phase = 0;
         int acc = 0;
@@ -575,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tc_fence_after();
             const uint32_t d_tmem = tmem_base + uint32_t(acc * 256);
             for (int kb = kb0; kb < kb1; kb += kps) {
-                if (a.slab) {
+                if (slab) {
                     // one stage = taps sg .. sg + 2 (one kernel row) of channel chunk kb / 9:
                     // A rows of tap (ky, kx) start (ky * slab_px + kx) 128-byte rows into the
                     // slab (a start address that is not swizzle-atom aligned)
@@ -589,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint64_t db = desc_b0 + uint64_t(stage) * desc_stride;
                     const uint32_t sbase = slab0 + uint32_t(ms_slot) * a.slab_bytes;
                     if (ptx::elect_one()) {
-                        if (!(a.debug & 1)) {
+                        if (do_mma) {
                             for (int j = 0; j < kps; ++j) {
                                 const int tap = sg + j;
                                 if (tap < 9) {
@@ -602,19 +608,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     const uint32_t acc0 = (kb > kb0 || j > 0) ? 1u : 0u;
                                     // N halves (wide tile): B rows of half h follow the kps
                                     // slots of half h - 1, accumulator columns h * block_n / 2
-                                    for (int h = 0; h < a.n_sub; ++h) {
+                                    for (int h = 0; h < n_sub; ++h) {
                                         const uint64_t dbj = db + (uint64_t(h * kps + j) * b_sub >> 4);
                                         const uint32_t dh = d_tmem + uint32_t(h * (a.block_n / 2));
                                         if (kPair) {
                                             if (kTF32)
-                                                ptx::mma4_tf32_pair(dh, da, dbj, a.idesc, acc0);
+                                                ptx::mma4_tf32_pair(dh, da, dbj, idesc, acc0);
                                             else
-                                                ptx::mma4_bf16_pair(dh, da, dbj, a.idesc, acc0);
+                                                ptx::mma4_bf16_pair(dh, da, dbj, idesc, acc0);
                                         } else {
                                             if (kTF32)
-                                                ptx::mma4_tf32(dh, da, dbj, a.idesc, acc0);
+                                                ptx::mma4_tf32(dh, da, dbj, idesc, acc0);
                                             else
-                                                ptx::mma4_bf16(dh, da, dbj, a.idesc, acc0);
+                                                ptx::mma4_bf16(dh, da, dbj, idesc, acc0);
                                         }
                                     }
                                 }
@@ -645,7 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint64_t da = desc_a0 + uint64_t(stage) * desc_stride;
                 const uint64_t db = desc_b0 + uint64_t(stage) * desc_stride;
                 if (ptx::elect_one()) {
-                    if (!(a.debug & 1) && a.n_sub == 2) {
+                    if (do_mma && wide) {
                         // wide tile (block_n > 256): two N halves per K step, each an MMA of
                         // N = block_n / 2 into its own TMEM column range, sharing the A tile
                         const uint32_t acc0 = kb > kb0 ? 1u : 0u;
@@ -655,34 +661,34 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const uint32_t dh = d_tmem + uint32_t(h * (a.block_n / 2));
                             if (kPair) {
                                 if (kTF32)
-                                    ptx::mma4_tf32_pair(dh, da, db + h * bh, a.idesc, acc0);
+                                    ptx::mma4_tf32_pair(dh, da, db + h * bh, idesc, acc0);
                                 else
-                                    ptx::mma4_bf16_pair(dh, da, db + h * bh, a.idesc, acc0);
+                                    ptx::mma4_bf16_pair(dh, da, db + h * bh, idesc, acc0);
                             } else if (kTF32) {
-                                ptx::mma4_tf32(dh, da, db + h * bh, a.idesc, acc0);
-                                if (two) ptx::mma4_tf32(dh, da + a_next, db + b_next + h * bh, a.idesc, 1u);
+                                ptx::mma4_tf32(dh, da, db + h * bh, idesc, acc0);
+                                if (two) ptx::mma4_tf32(dh, da + a_next, db + b_next + h * bh, idesc, 1u);
                             } else {
-                                ptx::mma4_bf16(dh, da, db + h * bh, a.idesc, acc0);
-                                if (two) ptx::mma4_bf16(dh, da + a_next, db + b_next + h * bh, a.idesc, 1u);
+                                ptx::mma4_bf16(dh, da, db + h * bh, idesc, acc0);
+                                if (two) ptx::mma4_bf16(dh, da + a_next, db + b_next + h * bh, idesc, 1u);
                             }
                         }
-                    } else if (!(a.debug & 1)) {
+                    } else if (do_mma) {
                         const uint32_t acc0 = kb > kb0 ? 1u : 0u;
                         if (kPair) {
                             if (kTF32) {
-                                ptx::mma4_tf32_pair(d_tmem, da, db, a.idesc, acc0);
-                                if (two) ptx::mma4_tf32_pair(d_tmem, da + a_next, db + b_next, a.idesc, 1u);
+                                ptx::mma4_tf32_pair(d_tmem, da, db, idesc, acc0);
+                                if (two) ptx::mma4_tf32_pair(d_tmem, da + a_next, db + b_next, idesc, 1u);
                             } else {
-                                ptx::mma4_bf16_pair(d_tmem, da, db, a.idesc, acc0);
-                                if (two) ptx::mma4_bf16_pair(d_tmem, da + a_next, db + b_next, a.idesc, 1u);
+                                ptx::mma4_bf16_pair(d_tmem, da, db, idesc, acc0);
+                                if (two) ptx::mma4_bf16_pair(d_tmem, da + a_next, db + b_next, idesc, 1u);
                             }
                         } else {
                             if (kTF32) {
-                                ptx::mma4_tf32(d_tmem, da, db, a.idesc, acc0);
-                                if (two) ptx::mma4_tf32(d_tmem, da + a_next, db + b_next, a.idesc, 1u);
+                                ptx::mma4_tf32(d_tmem, da, db, idesc, acc0);
+                                if (two) ptx::mma4_tf32(d_tmem, da + a_next, db + b_next, idesc, 1u);
                             } else {
-                                ptx::mma4_bf16(d_tmem, da, db, a.idesc, acc0);
-                                if (two) ptx::mma4_bf16(d_tmem, da + a_next, db + b_next, a.idesc, 1u);
+                                ptx::mma4_bf16(d_tmem, da, db, idesc, acc0);
+                                if (two) ptx::mma4_bf16(d_tmem, da + a_next, db + b_next, idesc, 1u);
                             }
                         }
                     }
