@@ -444,6 +444,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
         }
         pdl_wait();
+        // loop-invariant launch parameters, read once
+        const bool no_tma = a.debug & 2;
+        const bool slab = a.slab != 0;
+        const bool stride2 = a.mode == 2;
+        const int cin_chunks = a.cin_chunks;
         int it = 0;
         int sl_slot = 0;          // slab mode: A-slab ring slot / phase (both producer warps)
         uint32_t sl_phase = 0;
@@ -467,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint8_t* sa = ring + size_t(stage) * stage_bytes;
                     uint8_t* sb = sa + a_stage_bytes;
                     if (ptx::elect_one()) {
-                        if (a.debug & 2) {   // micro-benchmark: barriers only, no data movement
+                        if (no_tma) {   // micro-benchmark: barriers only, no data movement
                             ptx::mbar_arrive(&st.full_bar[stage]);
                         } else {
                             const bool b_done = it < pre;   // armed + B issued before pdl_wait
@@ -475,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 ptx::mbar_arrive_expect_tx(&st.full_bar[stage],
                                                            P * (nk * a_box_bytes + b_stage_bytes));
                             const uint32_t fb = kPair ? full_leader + uint32_t(stage) * 8u : 0u;
-                            if (a.slab && kb % 9 == 0) {
+                            if (slab && kb % 9 == 0) {
                                 // first stage of a channel chunk: its im2col slab (3 input rows
                                 // x (w_box + 2) pixels, TMA zero-fill = the left/right padding)
                                 ptx::mbar_wait(&st.slab_empty[sl_slot], sl_phase ^ 1);
@@ -492,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                      ox0 - 1, 0, oy0);
                             }
                             int c_j = cj, c_x = kx, c_y = ky;
-                            for (int j = 0; j < nk && !a.slab; ++j) {
+                            for (int j = 0; j < nk && !slab; ++j) {
                                 uint8_t* dst = sa + j * a_slot;
                                 if (!conv) {
                                     if (kPair)
@@ -502,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                          (kb + j) * kel, arow);
                                 } else {
                                     int c1 = 0, c2 = ox0 + c_x - 1, c3 = 0, c4 = oy0 + c_y;
-                                    if (a.mode == 2) {
+                                    if (stride2) {
                                         c1 = c_x == 1 ? 0 : 1; c2 = ox0 + (c_x == 0 ? -1 : 0);
                                         c3 = c_y == 1 ? 1 : 0; c4 = oy0 + (c_y == 2 ? 1 : 0);
                                     }
@@ -511,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     else
                                         ptx::tma_load_5d(dst, &tmA, &st.full_bar[stage], c_j * kel,
                                                          c1, c2, c3, c4);
-                                    if (++c_j == a.cin_chunks) {
+                                    if (++c_j == cin_chunks) {
                                         c_j = 0;
                                         if (++c_x == 3) {
                                             c_x = 0;
@@ -529,12 +534,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __syncwarp();
                 }
                 ++it;
-                if (a.slab && kb % 9 + kps >= 9 && ++sl_slot == a.slab_slots) {
+                if (slab && kb % 9 + kps >= 9 && ++sl_slot == a.slab_slots) {
                     sl_slot = 0;
                     sl_phase ^= 1;
                 }
                 for (int j = 0; j < nk; ++j) {
-                    if (++cj == a.cin_chunks) {
+                    if (++cj == cin_chunks) {
                         cj = 0;
                         if (++kx == 3) {
                             kx = 0;
