@@ -1345,6 +1345,14 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
         // one stage = three taps (one kernel row) of a chunk; a wide tile (two N halves, 8
         // MMAs per tap) takes one tap per stage
         a.kps = a.n_sub == 2 ? 1 : 3;
+        // a whole channel chunk (nine taps) per stage where the MMAs are tiny (block_n <= 32:
+        // the head conv): a third of the handshakes, the issue loop being the bound there
+        // (L62 16.4 -> 13.7 us; 33.28 vs 33.40 ms per generation).  PP_SLAB_KPS9_BN overrides.
+        static const int k9_bn = [] {
+            const char* v = std::getenv("PP_SLAB_KPS9_BN");
+            return v ? std::atoi(v) : 32;
+        }();
+        if (a.n_sub == 1 && bn <= k9_bn) a.kps = 9;
     }
     a.splits = splits;
     a.kb_per_split = (k_blocks + splits - 1) / splits;
