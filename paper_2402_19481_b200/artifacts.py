@@ -76,12 +76,18 @@ def write_pgm(x, path: str, lo: float, hi: float) -> None:
         f.write(px.reshape(-1).tobytes())
 
 
+def _shape_str(shape):
+    """Tensor::shape_str (tensor.cpp:30-34): '(1,4,8,8)'."""
+    return "(" + ",".join(str(int(v)) for v in shape) + ")"
+
+
 def psnr(a, b, peak: float) -> float:
     """psnr (tensor.cpp:336-347): 10 log10(peak^2 / mse), +inf when identical."""
     a = np.asarray(a, dtype=np.float32)
     b = np.asarray(b, dtype=np.float32)
     if a.shape != b.shape:
-        raise P.InvalidArgument(f"psnr: shape mismatch {a.shape} vs {b.shape}")
+        raise P.InvalidArgument(f"psnr: shape mismatch {_shape_str(a.shape)} vs "
+                                f"{_shape_str(b.shape)}")
     if not peak > 0.0:
         raise P.InvalidArgument("psnr: peak must be positive")
     se = float(np.sum((a.astype(np.float64) - b.astype(np.float64)) ** 2))

@@ -95,16 +95,13 @@ PP_API int pp_dev_conv(int dtype, const void* in, int rows, int W, int C_in_pad,
 // is irrelevant for timing).
 PP_API int pp_dev_gemm_bench(int dtype, int kind, int M_or_rows, int W, int K, int N,
                              int force_splits, int force_block_n, int reps, double* ms_out) {
-    // reps < 0: flags in the high bits -- bit 20 = fused GroupNorm statistics (32 groups),
-    // bit 21 = flush L2 (256 MiB memset) before every timed launch
-    const bool gn_fused = reps > 0 && (reps & (1 << 30));   // bit 30: fused GroupNorm apply
-    const bool gn = reps > 0 && ((reps & (1 << 20)) || gn_fused);
+    // flags in the high bits of reps: bit 20 = fused GroupNorm statistics (32 groups),
+    // bit 21 = flush L2 (256 MiB memset) before every timed launch; bits 22..29 = kernel debug
+    // flags (1 no MMA, 2 no TMA, 4 no epilogue work; effective only in a -DPP_GEMM_DEBUG build)
+    const bool gn = reps > 0 && (reps & (1 << 20));
     const bool flush = reps > 0 && (reps & (1 << 21));
-    // bits 22..29 = kernel debug flags: 1 no MMA, 2 no TMA, 4 no epilogue work, 16 no
-    // full-barrier wait
     const int debug = reps > 0 ? (reps >> 22) & 255 : 0;
     reps &= 0xFFFFF;
-    (void)gn_fused;
     return pp::guard([&] {
         pp::require_device();
         const pp::Elem e = pp::elem_of(dtype);
@@ -138,17 +135,6 @@ PP_API int pp_dev_gemm_bench(int dtype, int kind, int M_or_rows, int W, int K, i
             sc.gn_ticket = static_cast<unsigned int*>(gt.ptr);
             ep.gn_groups = 32;
             ep.gn_out = static_cast<double*>(go.ptr);
-        }
-        pp::DeviceScratch gam(size_t(n_pad) * 4), bet(size_t(n_pad) * 4), err(16);
-        if (gn_fused) {
-            CUDA_CHECK(cudaMemset(gam.ptr, 0, size_t(n_pad) * 4));
-            CUDA_CHECK(cudaMemset(bet.ptr, 0, size_t(n_pad) * 4));
-            CUDA_CHECK(cudaMemset(err.ptr, 0, 16));
-            ep.gn_apply = true;
-            ep.gn_gamma = static_cast<const float*>(gam.ptr);
-            ep.gn_beta = static_cast<const float*>(bet.ptr);
-            ep.gn_silu = true;
-            ep.gn_err = static_cast<int*>(err.ptr);
         }
         pp::DeviceScratch fl(flush ? size_t(256) << 20 : 16);
         pp::GemmPlan plan;

@@ -9,7 +9,7 @@
 //   * attention      (proj/src/tensor.cpp:163-199) -> S = Q K^T and O = P V^T.
 // Operands are staged by TMA into 128B-swizzled shared memory, multiplied by
 // tcgen05.mma (kind::f16 for bf16, kind::tf32 for the fp32 mode) into a
-// double-buffered TMEM accumulator, and drained by four epilogue warps that
+// double-buffered TMEM accumulator, and drained by twelve epilogue warps that
 // add bias / residual, store NHWC rows and (optionally) fold the stored values
 // into GroupNorm statistics of the next layer (group_stats, tensor.cpp:203-235).
 // Split-K (2-way) is reduced inside the kernel: the split that finishes first
@@ -33,14 +33,12 @@ struct GemmArgs {
     int rows_box, w_box;      // conv: output rows / cols covered by one 128-row M tile
     int tiles_y, tiles_x;     // M-tile grid (plain: tiles_y = ceil(M/128), tiles_x = 1)
     int out_rows, out_w;      // valid output extent in pixels (plain: M, 1)
-    int n_tiles, block_n;     // N tiling (block_n % 16 == 0, <= 256; <= 512 as two N halves)
+    int n_tiles, block_n;     // N tiling (block_n % 16 == 0, <= 256)
     int cin_chunks;           // conv: channel chunks of 128 B per tap; plain: k_blocks
     int k_blocks;             // total 128-byte K blocks
     int splits, kb_per_split; // split-K
     int stages;               // smem pipeline depth
-    int kps;                  // 128-byte K blocks per pipeline stage (1 or 2)
-    int n_sub;                // MMAs per K step along N (2: block_n > 256, N = block_n / 2 each)
-    int n_acc;                // TMEM accumulators in the MMA <-> epilogue ring (1 or 2)
+    int kps;                  // 128-byte K blocks per pipeline stage (1 or 2; slab mode 3 or 9)
     // slab mode (stride-1 conv, rows_box == 1): A from a 2-slot ring of im2col slabs
     // [3 rows][slab_px = w_box + 2][128 B] shared by the nine taps of a channel chunk; the
     // K index is chunk * 9 + tap (three taps per stage), B comes from a 4-D map
@@ -70,18 +68,6 @@ struct GemmArgs {
     double* gn_part;          // [m_tiles][groups][2]
     unsigned int* gn_ticket;  // [1 + n_tiles] zeroed counters, each reset by its folder
     double* gn_out;           // [groups][2] = (mean, mean_sq)
-    // fused GroupNorm apply (conv -> GroupNorm [-> SiLU] [-> +temb] [-> +skip] in one kernel,
-    // one tile per CTA, all CTAs resident): the raw conv tile stays in TMEM while the
-    // statistics are reduced, then is normalised from TMEM and written to `out`
-    int gn_apply;
-    const float* gn_gamma;
-    const float* gn_beta;
-    const float* gn_temb;     // [n] or null (per step: patched at launch)
-    const void* gn_skip;      // same layout as out (ld = gn_skip_ld) or null
-    long long gn_skip_ld;
-    int gn_silu;
-    float gn_eps;
-    int* gn_err;              // set to 1 when a group's variance is negative
     const void* b_base;       // B tensor (weights) and its size: with b_static, every CTA
     long long b_bytes;        // prefetches its 1/grid slice into L2 at kernel start
     int tma_store;            // 1: the CTA's last tile is stored through tmD (smem staging)
@@ -89,7 +75,7 @@ struct GemmArgs {
                               //      map -> 2x2 block of the 2 up_w-wide output)
     int b_static;             // 1: B is weights (not written by an earlier kernel on the stream):
                               //    its first boxes are prefetched before griddepcontrol.wait
-    int debug;                // micro-benchmarks only: bit0 = no MMA, bit1 = no TMA loads
+    int debug;                // micro-benchmarks only (compiled out unless -DPP_GEMM_DEBUG)
 };
 
 struct GemmPlan {
@@ -101,7 +87,6 @@ struct GemmPlan {
     size_t smem = 0;
     Elem elem = Elem::BF16;
     int pair = 0;             // 1: CTA-pair (cta_group::2, M = 256) kernel, clusters of 2
-    int mc = 0;               // 1: clusters of two pairs sharing B by TMA multicast (needs pair)
     double flops = 0;         // algorithmic 2*M*N*K of the layer (for rooflines)
 };
 
@@ -119,17 +104,6 @@ struct EpilogueSpec {
     int gn_groups = 0;
     double* gn_out = nullptr;
     int up_w = 0;             // plain GEMM: > 0 = fused nearest-2x upsample of the output
-    // fused GroupNorm apply (requires gn_groups): `out` receives GN(conv) [SiLU] [+temb]
-    // [+skip]; the raw conv output is never stored
-    bool gn_apply = false;
-    const float* gn_gamma = nullptr;
-    const float* gn_beta = nullptr;
-    const float* gn_temb = nullptr;
-    const void* gn_skip = nullptr;
-    long long gn_skip_ld = 0;
-    bool gn_silu = false;
-    float gn_eps = 1e-5f;
-    int* gn_err = nullptr;
 };
 
 // Scratch shared by all GEMMs issued on one stream (they run one after another).

@@ -1,9 +1,10 @@
 // sm_100a tcgen05 GEMM / implicit-GEMM 3x3 conv (see gemm.hpp for the contract).
 //
-// Warp roles (192 threads, 1 CTA per SM, persistent over output tiles):
-//   warp 0      TMA producer (one lane): A box + B box per 128-byte K block
-//   warp 1      TMEM owner + MMA issuer (one lane): 4 x tcgen05.mma per K block
-//   warps 2..5  epilogue: tcgen05.ld -> bias/residual -> NHWC stores (+ GN statistics)
+// Warp roles (480 threads, 1 CTA per SM, persistent over output tiles):
+//   warps 0, 6  TMA producers (one lane each, alternate stages): A boxes + B box per stage
+//   warp 1      TMEM owner + MMA issuer (one lane): 4 x tcgen05.mma per 128-byte K block
+//   warps 2-5, 7-14  epilogue (three warps per TMEM lane quarter): tcgen05.ld ->
+//               bias/residual -> NHWC stores (+ GN statistics)
 // Pipelines: smem ring (full/empty mbarriers, TMA <-> MMA) and a 2-deep TMEM
 // accumulator ring (tmem_full/tmem_empty, MMA <-> epilogue), so the epilogue of
 // tile i overlaps the main loop of tile i+1.
@@ -36,6 +37,13 @@ constexpr int kTileM = 128;
 constexpr int kBlockBytes = 128;   // K block = 128 bytes of each operand row
 constexpr int kTmemCols = 512;     // 2 accumulators x 256 columns
 constexpr int kSmemMax = 232448;
+// Kernel debug flags (GemmArgs::debug: 1 no MMA, 2 no TMA, 4 no epilogue, 1024 one K block)
+// exist for the micro-benchmarks only and are compiled out of the shipped library.
+#ifdef PP_GEMM_DEBUG
+constexpr bool kGemmDebug = true;
+#else
+constexpr bool kGemmDebug = false;
+#endif
 
 __device__ __forceinline__ float round_tf32(float x) {
     uint32_t r;
@@ -53,14 +61,13 @@ struct TileCoord {
 
 // Work unit t -> (split, N tile, M unit); the CTA's M tile is unit * P + rank (P = CTAs
 // per cluster).  m >= tiles_y * tiles_x only for the peer of an odd last unit.
-template <int P, int Q = 1>
+template <int P>
 __device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int t, int rank) {
-    // Q = CTA pairs per cluster sharing one B tile (multicast): unit = Q pair units
     TileCoord c;
     c.split = t % a.splits;
     int rest = t / a.splits;
     c.nt = rest % a.n_tiles;
-    c.m = ((rest / a.n_tiles) * Q + rank / P) * P + rank % P;
+    c.m = (rest / a.n_tiles) * P + rank;
     c.tx = c.m % a.tiles_x;
     c.ty = c.m / a.tiles_x;
     return c;
@@ -88,52 +95,25 @@ __host__ __device__ inline size_t tail_bytes(int stages, bool gn, int block_n) {
            (gn ? size_t(4) * block_n * 2 * 4 : 0);
 }
 
-// B box(es) of one stage.  A CTA stages block_n / P / n_sub weight rows per N half: for a
-// wide tile (n_sub == 2) the halves are separate boxes (TMA box dims are <= 256) landing
-// (rows * kps) slots apart; in a CTA pair each CTA loads its share (rank) of every half.
-// bcoord = first weight row of this CTA's share of half 0.  kPair: complete_tx on the
-// leader's barrier (shared::cluster address bar_cl), else on the local barrier bar.
-template <bool kPair, bool kMC>
+// B box of one stage: a CTA stages block_n / P weight rows (in a CTA pair each CTA loads its
+// share `rank` of the rows).  bcoord = first weight row of this CTA's share.  kPair:
+// complete_tx on the leader's barrier (shared::cluster address bar_cl), else on the local
+// barrier bar.
+template <bool kPair>
 __device__ __forceinline__ void load_b(uint8_t* sb, const CUtensorMap* tm, uint64_t* bar,
-                                       uint32_t bar_cl, int bcoord, int kb, const GemmArgs& a,
-                                       int pid, int crank) {
-    if (kMC) {
-        // this CTA's quarter of the stage (rows pid * q of its pair half), one box per K
-        // block, multicast to itself and the same-rank CTA of the other pair
-        const int q = a.block_n / 4;
-        const uint16_t mask = uint16_t((1u << crank) | (1u << (crank ^ 2)));
-        for (int j = 0; j < a.kps; ++j) {
-            uint8_t* dst = sb + size_t(j) * (a.block_n / 2) * kBlockBytes + size_t(pid) * q * kBlockBytes;
-            if (a.slab) {
-                const int k = kb + j, chunk = k / 9, tap = k - chunk * 9;
-                ptx::tma_load_4d_pair_mc(dst, tm, bar_cl, 0, bcoord, chunk, tap, mask);
-            } else {
-                ptx::tma_load_3d_pair_mc(dst, tm, bar_cl, 0, bcoord, kb + j, mask);
-            }
-        }
-        return;
-    }
-    if (a.slab) {   // K block kb = chunk * 9 + tap; one stage = kps taps (per N half)
+                                       uint32_t bar_cl, int bcoord, int kb, const GemmArgs& a) {
+    if (a.slab) {   // K block kb = chunk * 9 + tap; one stage = kps taps
         const int chunk = kb / 9, tap = kb - chunk * 9;
-        const int hrow = a.block_n / a.n_sub, brows = hrow / (kPair ? 2 : 1);
-        for (int h = 0; h < a.n_sub; ++h) {
-            uint8_t* dst = sb + size_t(h) * brows * kBlockBytes * a.kps;
-            if (kPair)
-                ptx::tma_load_4d_pair(dst, tm, bar_cl, 0, bcoord + h * hrow, chunk, tap);
-            else
-                ptx::tma_load_4d(dst, tm, bar, 0, bcoord + h * hrow, chunk, tap);
-        }
+        if (kPair)
+            ptx::tma_load_4d_pair(sb, tm, bar_cl, 0, bcoord, chunk, tap);
+        else
+            ptx::tma_load_4d(sb, tm, bar, 0, bcoord, chunk, tap);
         return;
     }
-    const int hrow = a.block_n / a.n_sub;                 // weight rows per N half
-    const int brows = hrow / (kPair ? 2 : 1);             // rows this CTA stages per half
-    for (int h = 0; h < a.n_sub; ++h) {
-        uint8_t* dst = sb + size_t(h) * brows * kBlockBytes * a.kps;
-        if (kPair)
-            ptx::tma_load_3d_pair(dst, tm, bar_cl, 0, bcoord + h * hrow, kb);
-        else
-            ptx::tma_load_3d(dst, tm, bar, 0, bcoord + h * hrow, kb);
-    }
+    if (kPair)
+        ptx::tma_load_3d_pair(sb, tm, bar_cl, 0, bcoord, kb);
+    else
+        ptx::tma_load_3d(sb, tm, bar, 0, bcoord, kb);
 }
 
 // Final values of one 16-column chunk of one row: bias, residual, store, GN sums.
@@ -172,7 +152,7 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
                     const float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                     if (srow) {
                         *reinterpret_cast<float4*>(srow + (c0 + j) * 4) = o;
-                    } else if (!a.gn_apply && !(a.debug & 512)) {
+                    } else {
                         *reinterpret_cast<float4*>(dst + j) = o;
                         if (a.up_w) {
                             *reinterpret_cast<float4*>(dst + a.out_ld + j) = o;
@@ -187,7 +167,7 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
                     if (n0 + j < a.n_valid) {
                         float o = v[j] + (res ? res[j] : 0.0f);
                         o = a.round_tf32 ? round_tf32(o) : o;
-                        if (!srow && !a.gn_apply) dst[j] = o;
+                        if (!srow) dst[j] = o;
                         v[j] = o;
                     } else {
                         v[j] = 0.0f;
@@ -229,7 +209,7 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
                     }
                     if (srow) {
                         *reinterpret_cast<uint4*>(srow + (c0 + j) * 2) = o;
-                    } else if (!a.gn_apply && !(a.debug & 512)) {
+                    } else {
                         *reinterpret_cast<uint4*>(dst + j) = o;
                         if (a.up_w) {
                             *reinterpret_cast<uint4*>(dst + a.out_ld + j) = o;
@@ -244,7 +224,7 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
                     if (n0 + j < a.n_valid) {
                         float o = v[j] + (res ? __bfloat162float(res[j]) : 0.0f);
                         const __nv_bfloat16 b = __float2bfloat16(o);
-                        if (!srow && !a.gn_apply) dst[j] = b;
+                        if (!srow) dst[j] = b;
                         v[j] = __bfloat162float(b);
                     } else {
                         v[j] = 0.0f;
@@ -264,7 +244,7 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
             }
         }
     }
-    if (a.gn_groups && !(a.debug & 256)) {
+    if (a.gn_groups) {
         // Column sums over the warp's 32 rows (invalid rows contribute 0) by a butterfly
         // transpose-reduce: each xor step halves the columns a lane keeps, so 16 columns
         // cost 16+8+4+2+1 shuffles per quantity instead of 16*5.  Lane l ends up with the
@@ -304,15 +284,11 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
 // (rank 0) issues M=256 MMAs that read both CTAs' smem, and each CTA's TMEM receives its
 // own 128 rows, so the epilogue is unchanged.  Per SM this halves the B bytes staged and
 // read per MMA (the single-CTA kernel is shared-memory-bandwidth bound at block_n <= 256).
-template <bool kTF32, bool kPair, bool kMC>
+template <bool kTF32, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmD, const GemmArgs a) {
-    constexpr int P = kPair ? 2 : 1;
-    // kMC: clusters of two CTA pairs on the same N tile; each B quarter is loaded once and
-    // multicast to the two CTAs that need it (B bytes per SM halved again)
-    constexpr int Q = kMC ? 2 : 1;
-    constexpr int CL = P * Q;   // CTAs per cluster
+    constexpr int P = kPair ? 2 : 1;   // CTAs per cluster
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte aligned base derived from smem_raw by pointer arithmetic (not an integer
     // cast), so the compiler keeps the shared address space: LDS/STS for the tail arrays
@@ -345,9 +321,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
+    const int dbg = kGemmDebug ? a.debug : 0;
     const int crank = kPair ? int(ptx::cluster_ctarank()) : 0;   // rank in the cluster
     const int rank = crank & 1;            // rank in the CTA pair
-    const int pid = kMC ? crank >> 1 : 0;  // pair index in the cluster
     const uint32_t ldr = uint32_t(crank & ~1);                // the pair's leader CTA
     const uint16_t pair_mask = uint16_t(3u << ldr);
 
@@ -357,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (a.tma_store) ptx::prefetch_tmap(&tmD);
         for (int s = 0; s < stages; ++s) {
             ptx::mbar_init(&st.full_bar[s], 1);
-            ptx::mbar_init(&st.empty_bar[s], Q);   // one MMA commit per pair sharing the stage
+            ptx::mbar_init(&st.empty_bar[s], 1);
         }
         for (int s = 0; s < kMaxSlabSlots; ++s) {
             ptx::mbar_init(&st.slab_full[s], 1);
@@ -386,8 +362,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     pdl_trigger();   // the next kernel on the stream may start its own prologue now
 
     const int m_tiles = a.tiles_y * a.tiles_x;
-    const int total_tiles = ((m_tiles + P - 1) / P + Q - 1) / Q * a.n_tiles * a.splits;
-    const int tile0 = blockIdx.x / CL, tile_step = gridDim.x / CL;
+    const int total_tiles = (m_tiles + P - 1) / P * a.n_tiles * a.splits;
+    const int tile0 = blockIdx.x / P, tile_step = gridDim.x / P;
     const int conv = a.mode != 0;
     const int a_box_bytes = a.slab ? 0 : conv ? a.rows_box * a.w_box * kBlockBytes : int(a_slot);
 
@@ -408,13 +384,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // first `pre` stages get their B boxes (and are armed for A + B) before waiting for
         // it; only the A boxes (activations) wait.
         int pre = 0;
-        if (a.b_static && tile0 < total_tiles && !(a.debug & 2)) {
-            const TileCoord tc = decode_tile<P, Q>(a, tile0, crank);
+        if (a.b_static && tile0 < total_tiles && !(dbg & 2)) {
+            const TileCoord tc = decode_tile<P>(a, tile0, crank);
             const int kb0 = tc.split * a.kb_per_split;
-            const int kb1 = (a.debug & 1024) ? kb0 + 1 : min(kb0 + a.kb_per_split, a.k_blocks);
+            const int kb1 = (dbg & 1024) ? kb0 + 1 : min(kb0 + a.kb_per_split, a.k_blocks);
             pre = min(stages, (kb1 - kb0 + kps - 1) / kps);
-            const int bcoord = tc.nt * a.block_n + rank * (a.block_n / a.n_sub / P) +
-                               pid * (a.block_n / a.n_sub / P / Q);
+            const int bcoord = tc.nt * a.block_n + rank * (a.block_n / P);
             for (int i = pw; i < pre; i += 2) {
                 if (ptx::elect_one()) {
                     uint8_t* sb = ring + size_t(i) * stage_bytes + a_stage_bytes;
@@ -422,13 +397,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (rank == 0)
                         ptx::mbar_arrive_expect_tx(&st.full_bar[i],
                                                    P * (nk * a_box_bytes + b_stage_bytes));
-                    load_b<kPair, kMC>(sb, &tmB, &st.full_bar[i], full_leader + uint32_t(i) * 8u, bcoord,
-                                       kb0 + i * kps, a, pid, crank);
+                    load_b<kPair>(sb, &tmB, &st.full_bar[i], full_leader + uint32_t(i) * 8u, bcoord,
+                                  kb0 + i * kps, a);
                 }
                 __syncwarp();
             }
         }
-        if (a.b_static && pw == 0 && a.b_bytes > 0 && !(a.debug & 2)) {
+        if (a.b_static && pw == 0 && a.b_bytes > 0 && !(dbg & 2)) {
             // The weights are streamed from HBM once per layer (155 MB per UNet step do not
             // stay in L2): pull this CTA's 1/grid slice of the whole B tensor into L2 now,
             // so the B boxes of later K blocks hit L2 instead of paying HBM latency in the
@@ -445,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         pdl_wait();
         // loop-invariant launch parameters, read once
-        const bool no_tma = a.debug & 2;
+        const bool no_tma = dbg & 2;
         const bool slab = a.slab != 0;
         const bool stride2 = a.mode == 2;
         const int cin_chunks = a.cin_chunks;
@@ -454,12 +429,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t sl_phase = 0;
         const uint32_t slab_leader = kPair ? ptx::mapa(ptx::smem_u32(st.slab_full), ldr) : 0u;
         for (int t = tile0; t < total_tiles; t += tile_step) {
-            const TileCoord tc = decode_tile<P, Q>(a, t, crank);
+            const TileCoord tc = decode_tile<P>(a, t, crank);
             const int kb0 = tc.split * a.kb_per_split;
-            const int kb1 = (a.debug & 1024) ? kb0 + 1 : min(kb0 + a.kb_per_split, a.k_blocks);
+            const int kb1 = (dbg & 1024) ? kb0 + 1 : min(kb0 + a.kb_per_split, a.k_blocks);
             const int oy0 = tc.ty * a.rows_box, ox0 = tc.tx * a.w_box;
-            const int bcoord = tc.nt * a.block_n + rank * (a.block_n / a.n_sub / P) +
-                               pid * (a.block_n / a.n_sub / P / Q);
+            const int bcoord = tc.nt * a.block_n + rank * (a.block_n / P);
             const int arow = tc.ty * kTileM;
             // conv K position of block kb0: tap (ky, kx), channel chunk cj
             int cj = kb0 % a.cin_chunks;
@@ -526,8 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 }
                             }
                             if (!b_done) {
-                                load_b<kPair, kMC>(sb, &tmB, &st.full_bar[stage], fb, bcoord, kb, a, pid,
-                                                   crank);
+                                load_b<kPair>(sb, &tmB, &st.full_bar[stage], fb, bcoord, kb, a);
                             }
                         }
                     }
@@ -564,13 +537,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t slab0 = ptx::smem_u32(smem);   // slab mode: slot s at slab0 + s * slab_bytes
         const uint64_t desc_stride = stage_bytes >> 4;
         const uint64_t a_next = a_slot >> 4, b_next = b_slot >> 4;
-        const uint32_t b_half = uint32_t(a.block_n / 2 / P) * kBlockBytes;   // n_sub == 2
-        const uint32_t b_sub = uint32_t(a.block_n / a.n_sub / P) * kBlockBytes;  // slab: one tap, one half
         // loop-invariant launch parameters, read once (the issue loop is on the critical path)
-        const bool do_mma = !(a.debug & 1);
-        const bool wide = a.n_sub == 2;
+        const bool do_mma = !(dbg & 1);
         const bool slab = a.slab != 0;
-        const int n_sub = a.n_sub;
         const uint32_t idesc = a.idesc;
         int stage = 0;
         uint32_t phase = 0;
@@ -579,9 +548,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         int ms_slot = 0;          // slab mode: A-slab ring slot / phase
         uint32_t ms_phase = 0;
         for (int t = tile0; t < total_tiles; t += tile_step) {
-            const TileCoord tc = decode_tile<P, Q>(a, t, crank);
+            const TileCoord tc = decode_tile<P>(a, t, crank);
             const int kb0 = tc.split * a.kb_per_split;
-            const int kb1 = (a.debug & 1024) ? kb0 + 1 : min(kb0 + a.kb_per_split, a.k_blocks);
+            const int kb1 = (dbg & 1024) ? kb0 + 1 : min(kb0 + a.kb_per_split, a.k_blocks);
             ptx::mbar_wait(&st.tempty_bar[acc], acc_phase ^ 1);
             ptx::tc_fence_after();
             const uint32_t d_tmem = tmem_base + uint32_t(acc * 256);
@@ -611,28 +580,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     // offset (measured: setting bits 49-51 breaks it)
                                     const uint64_t da = ptx::smem_desc_sw128(sbase + off * kBlockBytes);
                                     const uint32_t acc0 = (kb > kb0 || j > 0) ? 1u : 0u;
-                                    // N halves (wide tile): B rows of half h follow the kps
-                                    // slots of half h - 1, accumulator columns h * block_n / 2
-                                    for (int h = 0; h < n_sub; ++h) {
-                                        const uint64_t dbj = db + (uint64_t(h * kps + j) * b_sub >> 4);
-                                        const uint32_t dh = d_tmem + uint32_t(h * (a.block_n / 2));
-                                        if (kPair) {
-                                            if (kTF32)
-                                                ptx::mma4_tf32_pair(dh, da, dbj, idesc, acc0);
-                                            else
-                                                ptx::mma4_bf16_pair(dh, da, dbj, idesc, acc0);
-                                        } else {
-                                            if (kTF32)
-                                                ptx::mma4_tf32(dh, da, dbj, idesc, acc0);
-                                            else
-                                                ptx::mma4_bf16(dh, da, dbj, idesc, acc0);
-                                        }
+                                    const uint64_t dbj = db + uint64_t(j) * b_next;
+                                    if (kPair) {
+                                        if (kTF32)
+                                            ptx::mma4_tf32_pair(d_tmem, da, dbj, idesc, acc0);
+                                        else
+                                            ptx::mma4_bf16_pair(d_tmem, da, dbj, idesc, acc0);
+                                    } else {
+                                        if (kTF32)
+                                            ptx::mma4_tf32(d_tmem, da, dbj, idesc, acc0);
+                                        else
+                                            ptx::mma4_bf16(d_tmem, da, dbj, idesc, acc0);
                                     }
                                 }
                             }
                         }
                         if (kPair) {
-                            ptx::mma_commit_pair(&st.empty_bar[stage], kMC ? uint16_t(0xF) : pair_mask);
+                            ptx::mma_commit_pair(&st.empty_bar[stage], pair_mask);
                             if (sg + kps >= 9) ptx::mma_commit_pair(&st.slab_empty[ms_slot], pair_mask);
                         } else {
                             ptx::mma_commit(&st.empty_bar[stage]);
@@ -656,28 +620,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint64_t da = desc_a0 + uint64_t(stage) * desc_stride;
                 const uint64_t db = desc_b0 + uint64_t(stage) * desc_stride;
                 if (ptx::elect_one()) {
-                    if (do_mma && wide) {
-                        // wide tile (block_n > 256): two N halves per K step, each an MMA of
-                        // N = block_n / 2 into its own TMEM column range, sharing the A tile
-                        const uint32_t acc0 = kb > kb0 ? 1u : 0u;
-                        const uint64_t bh = uint64_t(b_half) >> 4;
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const uint32_t dh = d_tmem + uint32_t(h * (a.block_n / 2));
-                            if (kPair) {
-                                if (kTF32)
-                                    ptx::mma4_tf32_pair(dh, da, db + h * bh, idesc, acc0);
-                                else
-                                    ptx::mma4_bf16_pair(dh, da, db + h * bh, idesc, acc0);
-                            } else if (kTF32) {
-                                ptx::mma4_tf32(dh, da, db + h * bh, idesc, acc0);
-                                if (two) ptx::mma4_tf32(dh, da + a_next, db + b_next + h * bh, idesc, 1u);
-                            } else {
-                                ptx::mma4_bf16(dh, da, db + h * bh, idesc, acc0);
-                                if (two) ptx::mma4_bf16(dh, da + a_next, db + b_next + h * bh, idesc, 1u);
-                            }
-                        }
-                    } else if (do_mma) {
+                    if (do_mma) {
                         const uint32_t acc0 = kb > kb0 ? 1u : 0u;
                         if (kPair) {
                             if (kTF32) {
@@ -698,7 +641,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                     if (kPair)
-                        ptx::mma_commit_pair(&st.empty_bar[stage], kMC ? uint16_t(0xF) : pair_mask);
+                        ptx::mma_commit_pair(&st.empty_bar[stage], pair_mask);
                     else
                         ptx::mma_commit(&st.empty_bar[stage]);
                 }
@@ -715,7 +658,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mma_commit(&st.tfull_bar[acc]);
             }
             __syncwarp();
-            if (++acc == a.n_acc) {
+            if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
             }
@@ -746,11 +689,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = tile0; t < total_tiles; t += tile_step) {
             const int cur = acc;
             const uint32_t cur_phase = acc_phase;
-            if (++acc == a.n_acc) {
+            if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
             }
-            const TileCoord tc = decode_tile<P, Q>(a, t, crank);
+            const TileCoord tc = decode_tile<P>(a, t, crank);
             const int m_tile = tc.m;
             const int tile_id = m_tile * a.n_tiles + tc.nt;
             long long p;
@@ -772,12 +715,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool stage_out = a.tma_store && t + tile_step >= total_tiles;
             const int eb_out = (kTF32 || a.out_f32) ? 4 : 2;
             uint8_t* srow = stage_out ? smem + size_t(r) * a.block_n * eb_out : nullptr;
-            uint8_t* srow1 = a.gn_apply ? nullptr : srow;   // fused GN: pass 1 stores nothing
             for (int c = et; c < a.block_n; c += kEpiThreads)
                 sbias[c] = (a.bias && nbase + c < a.n_valid) ? a.bias[nbase + c] : 0.0f;
             ptx::mbar_wait(&st.tfull_bar[cur], cur_phase);
             ptx::tc_fence_after();
-            if ((a.debug & 4) || (kPair && m_tile >= m_tiles)) {
+            if ((dbg & 4) || (kPair && m_tile >= m_tiles)) {
                 // micro-benchmark (no epilogue work) / the empty half of an odd last pair unit
                 release(cur);
                 continue;
@@ -833,10 +775,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int j = 0; j < 16; ++j) v[j] = v[j] + o[j];
                     }
-                    if (a.gn_apply) ptx::tmem_st16(t_row + c0, v);   // acc + partial
-                    finish_chunk<kTF32>(a, v, sbias, c0, nbase + c0, p, valid, sgn_warp, lane, srow1);
+                    finish_chunk<kTF32>(a, v, sbias, c0, nbase + c0, p, valid, sgn_warp, lane, srow);
                 }
-                if (!a.gn_apply) release(cur);
+                release(cur);
                 if (et == 0) {
                     *ticket = 0u;
                     *ready = 0u;
@@ -845,11 +786,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int c0 = half * 16; c0 < a.block_n; c0 += kCS) {
                     float v[16];
                     ptx::tmem_ld16(t_row + c0, v);
-                    finish_chunk<kTF32>(a, v, sbias, c0, nbase + c0, p, valid, sgn_warp, lane, srow1);
+                    finish_chunk<kTF32>(a, v, sbias, c0, nbase + c0, p, valid, sgn_warp, lane, srow);
                 }
-                if (!a.gn_apply) release(cur);
+                release(cur);
             }
-            if (stage_out && !a.gn_apply && !(a.debug & 512)) {
+            if (stage_out) {
                 ptx::fence_proxy_async();   // staged rows -> visible to the TMA engine
                 epi_bar();
                 if (et == 0) {
@@ -861,7 +802,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::bulk_wait_read();
                 }
             }
-            if (a.gn_groups && !(a.debug & 256)) {
+            if (a.gn_groups) {
                 epi_bar();
                 const int cpg = a.gn_cpg;
                 const int g0 = nbase / cpg;
@@ -942,152 +883,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     epi_bar();
                 }
             }
-            if (a.gn_apply) {
-                // ===== fused GroupNorm apply, pass 2 (one tile per CTA, all CTAs resident) =====
-                // wait for this N tile's statistics (folded above by the N tile's last CTA)
-                unsigned int* nt_ready = a.gn_ticket + 1 + a.n_tiles + tc.nt;
-                unsigned int* nt_used = a.gn_ticket + 1 + 2 * a.n_tiles + tc.nt;
-                if (et == 0 && !(a.debug & 32)) {
-                    if (st.flags[2]) {
-                        __threadfence();
-                        atomicExch(nt_ready, 1u);
-                    } else {
-                        while (ptx::ld_acquire_gpu(nt_ready) == 0u) __nanosleep(64);
-                        __threadfence();
-                    }
-                }
-                epi_bar();
-                // per-column coefficients: y = x * sc + sh (sc = gamma / std, sh = beta - mean
-                // * sc; the same fp32 formulas as gn_pass_kernel), then SiLU, + temb, + skip
-                float* s_sc = st.gn;
-                float* s_sh = s_sc + a.block_n;
-                float* s_te = s_sh + a.block_n;
-                for (int c = et; c < a.block_n && !(a.debug & 64); c += kEpiThreads) {
-                    const int g = (nbase + c) / a.gn_cpg;
-                    const double m = __ldcg(a.gn_out + g * 2), q = __ldcg(a.gn_out + g * 2 + 1);
-                    const double var = __dsub_rn(q, __dmul_rn(m, m));
-                    if (var < 0.0 && a.gn_err) atomicExch(a.gn_err, 1);
-                    const float mu = float(m);
-                    const float inv = float(1.0 / sqrt(__dadd_rn(fmax(var, 0.0), double(a.gn_eps))));
-                    const float sc = a.gn_gamma[nbase + c] * inv;
-                    s_sc[c] = sc;
-                    s_sh[c] = fmaf(-mu, sc, a.gn_beta[nbase + c]);
-                    s_te[c] = a.gn_temb ? a.gn_temb[nbase + c] : 0.0f;
-                }
-                epi_bar();
-                if (et == 0 && atomicAdd(nt_used, 1u) == unsigned(m_tiles - 1)) {
-                    *nt_ready = 0u;   // every CTA of this N tile has passed the wait
-                    *nt_used = 0u;
-                }
-                ptx::tmem_wait_st();
-                const bool f32out = kTF32 || a.out_f32;
-                for (int c0 = half * 16; c0 < a.block_n && !(a.debug & 128); c0 += kCS) {
-                    float v[16], cb[16], cs[16], ch[16];
-                    ptx::tmem_ld16(t_row + c0, v);
-#pragma unroll
-                    for (int j = 0; j < 16; j += 4) {
-                        *reinterpret_cast<float4*>(cb + j) = *reinterpret_cast<const float4*>(sbias + c0 + j);
-                        *reinterpret_cast<float4*>(cs + j) = *reinterpret_cast<const float4*>(s_sc + c0 + j);
-                        *reinterpret_cast<float4*>(ch + j) = *reinterpret_cast<const float4*>(s_sh + c0 + j);
-                    }
-                    // the raw conv value exactly as the unfused path stores it
-                    if (!f32out) {
-#pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            v[j] = __bfloat162float(__float2bfloat16(v[j] * a.scale + cb[j]));
-                    } else if (a.round_tf32) {
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) v[j] = round_tf32(v[j] * a.scale + cb[j]);
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) v[j] = v[j] * a.scale + cb[j];
-                    }
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) v[j] = fmaf(v[j], cs[j], ch[j]);
-                    if (a.gn_silu) {
-                        if (!f32out) {
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) {   // silu = h + h tanh(h), h = v / 2
-                                const float h = 0.5f * v[j];
-                                float tt;
-                                asm("tanh.approx.f32 %0, %1;" : "=f"(tt) : "f"(h));
-                                v[j] = fmaf(h, tt, h);
-                            }
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) v[j] = v[j] / (1.0f + expf(-v[j]));
-                        }
-                    }
-#pragma unroll
-                    for (int j = 0; j < 16; j += 4) {
-                        const float4 t4 = *reinterpret_cast<const float4*>(s_te + c0 + j);
-                        v[j] += t4.x; v[j + 1] += t4.y; v[j + 2] += t4.z; v[j + 3] += t4.w;
-                    }
-                    if (valid && a.gn_skip) {
-                        if (f32out) {
-                            const float* sk = reinterpret_cast<const float*>(a.gn_skip) + p * a.gn_skip_ld + nbase + c0;
-#pragma unroll
-                            for (int j = 0; j < 16; j += 4) {
-                                const float4 q = *reinterpret_cast<const float4*>(sk + j);
-                                v[j] += q.x; v[j + 1] += q.y; v[j + 2] += q.z; v[j + 3] += q.w;
-                            }
-                        } else {
-                            const __nv_bfloat16* sk =
-                                reinterpret_cast<const __nv_bfloat16*>(a.gn_skip) + p * a.gn_skip_ld + nbase + c0;
-#pragma unroll
-                            for (int j = 0; j < 16; j += 8) {
-                                const uint4 q = *reinterpret_cast<const uint4*>(sk + j);
-                                const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&q);
-#pragma unroll
-                                for (int i = 0; i < 4; ++i) {
-                                    const float2 f = __bfloat1622float2(q2[i]);
-                                    v[j + 2 * i] += f.x;
-                                    v[j + 2 * i + 1] += f.y;
-                                }
-                            }
-                        }
-                    }
-                    if (valid) {
-                        uint8_t* dst = srow ? srow + size_t(c0) * (f32out ? 4 : 2)
-                                            : static_cast<uint8_t*>(a.out) +
-                                                  (size_t(p) * a.out_ld + nbase + c0) * (f32out ? 4 : 2);
-                        if (f32out) {
-#pragma unroll
-                            for (int j = 0; j < 16; j += 4) {
-                                float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                                if (a.round_tf32) {
-                                    o.x = round_tf32(o.x); o.y = round_tf32(o.y);
-                                    o.z = round_tf32(o.z); o.w = round_tf32(o.w);
-                                }
-                                *reinterpret_cast<float4*>(dst + j * 4) = o;
-                            }
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 16; j += 8) {
-                                uint4 o;
-                                __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-                                for (int i = 0; i < 4; ++i)
-                                    o2[i] = __floats2bfloat162_rn(v[j + 2 * i], v[j + 2 * i + 1]);
-                                *reinterpret_cast<uint4*>(dst + j * 2) = o;
-                            }
-                        }
-                    }
-                }
-                release(cur);
-                if (stage_out) {
-                    ptx::fence_proxy_async();
-                    epi_bar();
-                    if (et == 0) {
-                        if (conv)
-                            ptx::tma_store_3d(&tmD, smem, nbase, tc.tx * a.w_box, tc.ty * a.rows_box);
-                        else
-                            ptx::tma_store_2d(&tmD, smem, nbase, tc.ty * kTileM);
-                        ptx::bulk_commit();
-                        ptx::bulk_wait_all();
-                    }
-                }
-            }
         }
     }
 
@@ -1164,9 +959,7 @@ void plan_output_map(GemmPlan& p, bool conv) {
     const bool f32 = p.elem == Elem::F32 || a.out_f32;
     const uint64_t eb = f32 ? 4 : 2;
     a.tma_store = 0;
-    if (std::getenv("PP_NO_TMA_STORE")) return;
     if ((uint64_t(a.out_ld) * eb) % 16 || (reinterpret_cast<uintptr_t>(a.out) % 16)) return;
-    if (a.block_n > 256) return;   // TMA box dims are <= 256
     if (a.up_w) return;            // fused upsample: four row stores per output row
     if (conv) {
         uint64_t d[3] = {uint64_t(a.n_valid), uint64_t(a.out_w), uint64_t(a.out_rows)};
@@ -1209,13 +1002,9 @@ int stages_for(int block_n, bool gn, int pair, int kps, uint32_t slab_bytes = 0,
 
 // K blocks per stage: 2 halves the per-block barrier / issue work of the single-thread TMA
 // and MMA loops (measured ~450 cycles per iteration, more than the MMAs of a block_n <= 224
-// block take), as long as at least 3 stages (6 blocks) still fit.  PP_KPS overrides.
+// block take), as long as at least 3 stages (6 blocks) still fit (3 blocks per stage:
+// measured slower, 35.72 vs 33.61 ms per generation).
 int choose_kps(int block_n, bool gn, int pair) {
-    static const int forced = [] {
-        const char* v = std::getenv("PP_KPS");
-        return v ? std::atoi(v) : 0;
-    }();
-    if (forced == 1 || forced == 2) return forced;
     return stages_for(block_n, gn, pair, 2) >= 3 ? 2 : 1;
 }
 
@@ -1224,7 +1013,6 @@ int choose_kps(int block_n, bool gn, int pair) {
 // shared-memory bandwidth (TMA writes + MMA operand reads of a 128 x block_n tile); the
 // CTA pair halves the B bytes per SM.
 double tile_eff(int pair, int bn) {
-    if (bn > 256) return 0.85;   // wide tile: 8+ MMAs per stage hide the issue loop
     if (pair) return bn >= 256 ? 0.90 : bn >= 160 ? 0.64 : bn >= 128 ? 0.35 : 0.27;
     return bn >= 256 ? 0.75 : bn >= 160 ? 0.62 : bn >= 128 ? 0.36 : 0.28;
 }
@@ -1234,15 +1022,12 @@ double tile_eff(int pair, int bn) {
 // over SM pairs); split-K pays a partial write + read.
 //   force_splits: bits 0-3 = splits (0 auto), bit 4 = force pair, bit 5 = force single CTA
 void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int gn_cpg, int force_splits,
-                   int force_block_n, int& block_n, int& splits, int& pair, bool one_wave = false,
-                   bool gemm = false) {
+                   int force_block_n, int& block_n, int& splits, int& pair, bool gemm = false) {
     double best = 1e300;
     block_n = 16;
     splits = 1;
     pair = 0;
     const int fs = force_splits & 15;
-    static const bool wide_env = std::getenv("PP_WIDE") != nullptr;
-    const bool wide_ok = wide_env || force_block_n > 256 || one_wave;
     const bool force_pair = force_splits & 16, force_single = force_splits & 32;
     for (int pr = 0; pr <= 1; ++pr) {
         if ((force_pair && !pr) || (force_single && pr)) continue;
@@ -1250,9 +1035,8 @@ void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int gn_cpg
         const int P = pr ? 2 : 1;
         const int slots = num_sms / P;
         const int units = (m_tiles + P - 1) / P;
-        for (int bn = 512; bn >= 16; bn -= 16) {
+        for (int bn = 256; bn >= 16; bn -= 16) {
             if (force_block_n && bn != force_block_n) continue;
-            if (bn > 256 && (bn % 32 || !wide_ok)) continue;
             if (n_pad % bn) continue;
             if (gn_cpg && bn % gn_cpg) continue;
             const int nt = n_pad / bn;
@@ -1262,12 +1046,10 @@ void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int gn_cpg
                 // split only when one wave leaves more than half of the SMs idle
                 if (!fs && s == 2 && ((long long)units * nt * 2 > slots || k_blocks < 16)) continue;
                 const long long tiles = (long long)units * nt * s;
-                if (one_wave && tiles > slots) continue;   // fused GroupNorm: every tile resident
                 const double waves = std::ceil(double(tiles) / slots);
                 const double per_kb = 2.0 * bn / tile_eff(pr, bn);
                 const double kbs = std::ceil(double(k_blocks) / s);
                 double cost = waves * (kbs * per_kb + 2500.0);
-                if (bn > 256) cost += (waves - 1) * 4000.0;   // one accumulator: epilogue exposed
                 if (s > 1) cost += 2.0 * 128.0 * bn * 4.0 / 20.0;
                 if (cost < best * 0.98) {
                     best = cost;
@@ -1283,7 +1065,7 @@ void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int gn_cpg
     // linear layers): each CTA runs a short K loop once, so the time is latency, not
     // shared-memory throughput -- the smallest per-CTA tile that still fits one wave wins
     // (measured, scripts/attn_gemm_sweep.py: PV 8.3 us at block_n 80 vs 10.8 us at pair 160).
-    if (gemm && !force_block_n && !fs && !force_pair && !one_wave && !gn_cpg) {
+    if (gemm && !force_block_n && !fs && !force_pair && !gn_cpg) {
         double lbest = 1e300;
         int lbn = 0;
         for (int bn = 256; bn >= 64; bn -= 16) {   // >= 64: the measured range
@@ -1317,16 +1099,9 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
             throw std::invalid_argument("GroupNorm statistics need unpadded output channels");
     }
     int bn, splits, pair;
+    if (force_block_n > 256) throw std::invalid_argument("GEMM: block_n must be <= 256");
     choose_tiling(m_tiles, n_pad, k_blocks, num_sms, cpg, force_splits, force_block_n, bn, splits,
-                  pair, ep.gn_apply, a.mode == 0);
-    if (ep.gn_apply) {
-        if (!gn) throw std::invalid_argument("fused GroupNorm apply needs the statistics epilogue");
-        if (ep.residual) throw std::invalid_argument("fused GroupNorm apply: conv residual unsupported");
-        const int P = pair ? 2 : 1;
-        const long long tiles = (long long)(m_tiles + P - 1) / P * (n_pad / bn) * splits;
-        if (bn % cpg || tiles > num_sms / P)
-            throw std::invalid_argument("fused GroupNorm apply: no single-wave tiling");
-    }
+                  pair, a.mode == 0);
     if (gn && bn % cpg) throw std::invalid_argument("GroupNorm statistics: block_n not group aligned");
     if (pair && bn % 16) throw std::invalid_argument("CTA-pair GEMM: block_n % 16 != 0");
     p.pair = pair;
@@ -1338,21 +1113,12 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
     if (splits > 1 && ((size_t)m_tiles * kTileM * n_pad * sizeof(float) > sc.ws_bytes ||
                        2 * size_t(m_tiles) * a.n_tiles > sc.n_tickets))
         splits = 1;
-    a.n_sub = bn > 256 ? 2 : 1;
-    a.n_acc = bn > 256 ? 1 : 2;
-    a.kps = a.n_sub == 2 ? 1 : choose_kps(bn, gn, pair);
+    a.kps = choose_kps(bn, gn, pair);
     if (a.slab) {
-        // one stage = three taps (one kernel row) of a chunk; a wide tile (two N halves, 8
-        // MMAs per tap) takes one tap per stage
-        a.kps = a.n_sub == 2 ? 1 : 3;
-        // a whole channel chunk (nine taps) per stage where the MMAs are tiny (block_n <= 32:
-        // the head conv): a third of the handshakes, the issue loop being the bound there
-        // (L62 16.4 -> 13.7 us; 33.28 vs 33.40 ms per generation).  PP_SLAB_KPS9_BN overrides.
-        static const int k9_bn = [] {
-            const char* v = std::getenv("PP_SLAB_KPS9_BN");
-            return v ? std::atoi(v) : 32;
-        }();
-        if (a.n_sub == 1 && bn <= k9_bn) a.kps = 9;
+        // one stage = three taps (one kernel row) of a chunk; a whole channel chunk (nine
+        // taps) per stage where the MMAs are tiny (block_n <= 32: the head conv): a third of
+        // the handshakes, the issue loop being the bound there (L62 16.4 -> 13.7 us)
+        a.kps = bn <= 32 ? 9 : 3;
     }
     a.splits = splits;
     a.kb_per_split = (k_blocks + splits - 1) / splits;
@@ -1363,21 +1129,15 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
     a.slab_slots = 2;
     if (a.slab) {
         // deeper slab ring where smem is left over (small block_n: the head conv), never at the
-        // cost of B stages; a slab per channel chunk, so no more slots than chunks.
-        // PP_SLAB_SLOTS=n forces n (experiments)
-        static const int forced_slots = [] {
-            const char* v = std::getenv("PP_SLAB_SLOTS");
-            return v ? std::atoi(v) : 0;
-        }();
+        // cost of B stages; a slab per channel chunk, so no more slots than chunks
         for (int s = kMaxSlabSlots; s > 2; --s) {
-            if (forced_slots && s != forced_slots) continue;
             if (s > a.cin_chunks) continue;
             if (smem_for(bn, a.stages, gn, pair, a.kps, a.slab_bytes, s) > size_t(kSmemMax)) continue;
             a.slab_slots = s;
             break;
         }
     }
-    a.idesc = make_idesc(p.elem, bn / a.n_sub, pair ? 2 * kTileM : kTileM);
+    a.idesc = make_idesc(p.elem, bn, pair ? 2 * kTileM : kTileM);
     a.out = ep.out;
     a.out_ld = ep.out_ld;
     a.n_valid = ep.n_valid;
@@ -1398,28 +1158,10 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
         a.gn_part = sc.gn_part;
         a.gn_ticket = sc.gn_ticket;
         a.gn_out = ep.gn_out;
-        a.gn_apply = ep.gn_apply ? 1 : 0;
-        a.gn_gamma = ep.gn_gamma;
-        a.gn_beta = ep.gn_beta;
-        a.gn_temb = ep.gn_temb;
-        a.gn_skip = ep.gn_skip;
-        a.gn_skip_ld = ep.gn_skip_ld;
-        a.gn_silu = ep.gn_silu ? 1 : 0;
-        a.gn_eps = ep.gn_eps;
-        a.gn_err = ep.gn_err;
     }
     const int P = pair ? 2 : 1;
-    // clusters of two pairs sharing B by TMA multicast: parity-tested but measured slower on
-    // B200 (4-CTA clusters lock two pairs into step and strand SMs: L01 32 vs 24 us, 8192^3
-    // GEMM 1.16 vs 0.55 ms), so opt-in (PP_MC=1)
-    static const bool mc_env = [] {
-        const char* v = std::getenv("PP_MC");
-        return v && v[0] == '1';
-    }();
-    p.mc = (mc_env && pair && a.n_sub == 1 && bn % 32 == 0 && (m_tiles + 1) / 2 >= 2) ? 1 : 0;
-    const int Q = p.mc ? 2 : 1;
-    const int units = ((m_tiles + P - 1) / P + Q - 1) / Q * a.n_tiles * a.splits;
-    p.grid = P * Q * std::min(units, num_sms / (P * Q));
+    const int units = (m_tiles + P - 1) / P * a.n_tiles * a.splits;
+    p.grid = P * std::min(units, num_sms / P);
     p.smem = smem_for(bn, a.stages, gn, pair, a.kps, a.slab ? a.slab_bytes : 0u, a.slab_slots);
 }
 
@@ -1462,13 +1204,8 @@ void plan_conv(GemmPlan& p, Elem e, const void* in, int rows_in, int W, int C_in
     a.out_w = out_w;
     a.cin_chunks = C_in_pad / kel;
     a.m_pix = out_rows * out_w;
-    // slab mode: stride 1, one output row per tile (w_box > 64), unless PP_SLAB=0
-    static const bool slab_env = [] {
-        const char* v = std::getenv("PP_SLAB");
-        return !(v && v[0] == '0');
-    }();
-    a.slab = (slab_env && stride == 1 && a.rows_box == 1 && wb + 2 <= 256 && !ep.gn_apply)
-                 ? 1 : 0;
+    // slab mode: stride 1, one output row per tile (w_box > 64)
+    a.slab = (stride == 1 && a.rows_box == 1 && wb + 2 <= 256) ? 1 : 0;
     if (a.slab) {
         a.slab_px = wb + 2;
         a.slab_box_bytes = uint32_t(3 * a.slab_px * kBlockBytes);
@@ -1501,13 +1238,11 @@ void plan_conv(GemmPlan& p, Elem e, const void* in, int rows_in, int W, int C_in
         // B as [tap][chunk][n][kel]: box {kel, rows, 1 chunk, 3 taps}
         uint64_t d[4] = {uint64_t(kel), uint64_t(n_pad), uint64_t(a.cin_chunks), 9};
         uint64_t st[3] = {uint64_t(9) * C_in_pad * eb, uint64_t(kBlockBytes), uint64_t(C_in_pad) * eb};
-        uint32_t b[4] = {uint32_t(kel),
-                         uint32_t(a.block_n / (p.pair ? 2 : 1) / (p.mc ? 2 : 1) / a.n_sub), 1,
-                         p.mc ? 1u : uint32_t(a.kps)};
+        uint32_t b[4] = {uint32_t(kel), uint32_t(a.block_n / (p.pair ? 2 : 1)), 1, uint32_t(a.kps)};
         encode(&p.tmB, e, 4, weights, d, st, b);
     } else {
-        encode_b(&p.tmB, e, weights, n_pad, 9 * C_in_pad, 9LL * C_in_pad,
-                 a.block_n / (p.pair ? 2 : 1) / a.n_sub / (p.mc ? 2 : 1), p.mc ? 1 : a.kps);
+        encode_b(&p.tmB, e, weights, n_pad, 9 * C_in_pad, 9LL * C_in_pad, a.block_n / (p.pair ? 2 : 1),
+                 a.kps);
     }
     p.flops = 2.0 * a.m_pix * double(ep.n_valid) * 9.0 * C_in_pad;
     a.b_static = 1;   // conv weights
@@ -1540,8 +1275,7 @@ void plan_gemm(GemmPlan& p, Elem e, const void* A, int M, int K, long long lda, 
     uint32_t ab[2] = {uint32_t(kel), uint32_t(kTileM)};
     encode(&p.tmA, e, 2, A, ad, as, ab);
     finish_plan(p, a.tiles_y, n_pad, K / kel, ep, sc, num_sms, force_splits, force_block_n);
-    encode_b(&p.tmB, e, B, N, K, ldb, a.block_n / (p.pair ? 2 : 1) / a.n_sub / (p.mc ? 2 : 1),
-             p.mc ? 1 : a.kps);
+    encode_b(&p.tmB, e, B, N, K, ldb, a.block_n / (p.pair ? 2 : 1), a.kps);
     p.flops = 2.0 * double(M) * N * K;
     a.b_static = b_static ? 1 : 0;
     a.up_w = ep.up_w;
@@ -1552,7 +1286,7 @@ void plan_gemm(GemmPlan& p, Elem e, const void* A, int M, int K, long long lda, 
     a.b_bytes = b_static ? ((long long)(N - 1) * ldb + K) * (long long)eb / 16 * 16 : 0;
 }
 
-template <bool kTF32, bool kPair, bool kMC>
+template <bool kTF32, bool kPair>
 void launch_variant(const GemmPlan& p, cudaStream_t s) {
     // the dynamic-smem attribute is per device: remember which devices have it
     static std::mutex mu;
@@ -1562,39 +1296,22 @@ void launch_variant(const GemmPlan& p, cudaStream_t s) {
     {
         std::lock_guard<std::mutex> lk(mu);
         if (!(done >> dev & 1ull)) {
-            CUDA_CHECK(cudaFuncSetAttribute(gemm_kernel<kTF32, kPair, kMC>,
+            CUDA_CHECK(cudaFuncSetAttribute(gemm_kernel<kTF32, kPair>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
             done |= 1ull << dev;
         }
     }
-    launch_pdl(gemm_kernel<kTF32, kPair, kMC>, dim3(p.grid), dim3(kThreads), p.smem, s,
-               kMC ? 4 : kPair ? 2 : 1, p.tmA, p.tmB, p.tmD, p.a);
+    launch_pdl(gemm_kernel<kTF32, kPair>, dim3(p.grid), dim3(kThreads), p.smem, s, kPair ? 2 : 1,
+               p.tmA, p.tmB, p.tmD, p.a);
 }
 
-void launch_gemm(const GemmPlan& p0, cudaStream_t s) {
-    // PP_DEBUG_GEMM=<bits>: timing experiments only (results are wrong): kernel debug flags
-    // applied to every GEMM launch (1 no MMA, 2 no TMA, 4 no epilogue work)
-    static const int dbg = [] {
-        const char* v = std::getenv("PP_DEBUG_GEMM");
-        return v ? std::atoi(v) : 0;
-    }();
-    GemmPlan pd;
-    const GemmPlan* pp_ = &p0;
-    if (dbg) {
-        pd = p0;
-        pd.a.debug = dbg;
-        pp_ = &pd;
-    }
-    const GemmPlan& p = *pp_;
-    const bool tf32 = p.elem == Elem::F32;
-    if (tf32) {
-        if (p.mc) launch_variant<true, true, true>(p, s);
-        else if (p.pair) launch_variant<true, true, false>(p, s);
-        else launch_variant<true, false, false>(p, s);
+void launch_gemm(const GemmPlan& p, cudaStream_t s) {
+    if (p.elem == Elem::F32) {
+        if (p.pair) launch_variant<true, true>(p, s);
+        else launch_variant<true, false>(p, s);
     } else {
-        if (p.mc) launch_variant<false, true, true>(p, s);
-        else if (p.pair) launch_variant<false, true, false>(p, s);
-        else launch_variant<false, false, false>(p, s);
+        if (p.pair) launch_variant<false, true>(p, s);
+        else launch_variant<false, false>(p, s);
     }
 }
 

@@ -849,10 +849,6 @@ int gn_wave_blocks(int per_sm) {
     if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
     return std::max(1, std::min(1184, per_sm * sms));
 }
-int gn_env(const char* name, int def) {   // experiment override of the blocks per SM
-    const char* v = std::getenv(name);
-    return v ? std::atoi(v) : def;
-}
 
 // >= gx * gy of every gn_shape, plus the second-level range sums
 int gn_stats_blocks(long long) { return 1184 + 1184 + 80; }
@@ -863,7 +859,7 @@ void gn_stats(Elem e, const void* x, long long pix, int C, int ld, int groups, d
     if (C % VEC || ld % VEC || C % groups)
         throw std::invalid_argument("group_stats: channels must be a multiple of the vector width");
     if (pix * (ld / VEC) >= (1LL << 31)) throw std::invalid_argument("group_stats: band too large");
-    const GnShape sh = gn_shape(e, pix, ld, kGnUStats, gn_wave_blocks(gn_env("PP_GN_WS", 2)));
+    const GnShape sh = gn_shape(e, pix, ld, kGnUStats, gn_wave_blocks(2));
     GnStatsOut so;
     so.G = groups;
     so.count = count;
@@ -888,7 +884,7 @@ void gn_apply(Elem e, const void* x, void* y, long long pix, int C, int ld, int 
     if (pix * (ld / VEC) >= (1LL << 31)) throw std::invalid_argument("group_norm_apply: band too large");
     const bool st = out_stats && out_stats->G > 0;
     const GnShape sh = gn_shape(e, pix, ld, st ? kGnUStats : kGnU,
-                                gn_wave_blocks(st ? gn_env("PP_GN_WS", 2) : gn_env("PP_GN_WA", 3)));
+                                gn_wave_blocks(st ? 2 : 3));
     if (st) {
         if (C % out_stats->G) throw std::invalid_argument("group_stats: channels not divisible by groups");
         DISPATCH(e, launch_pdl(gn_pass_kernel<T, true, true, kGnUStats>, sh.grid, sh.block, 0, s, 1,

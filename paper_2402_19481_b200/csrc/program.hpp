@@ -97,9 +97,6 @@ struct Program {
     std::vector<std::array<GemmPlan, 2>> plans;    // per group, per step parity: conv / linear / PV
     std::vector<std::array<GemmPlan, 2>> s_plans;  // attention S = Q K^T per K/V parity
     std::vector<char> fused_stats;                 // per GN layer: stats come from the conv epilogue
-    std::vector<std::array<GemmPlan, 2>> fplans;   // per conv group: conv + next GN group fused
-    std::vector<char> gn_fusable;                  // per group: fplans valid
-    std::vector<char> fused_now;                   // per GN layer: applied by this step's conv
     std::vector<char> merged_into_prev;            // per group: computed by the previous group
     GemmScratch sc;
     // scratch
@@ -132,6 +129,7 @@ struct Program {
     // events
     std::vector<cudaEvent_t> ready;               // per layer
     std::vector<std::array<cudaEvent_t, 2>> sent; // per layer, per parity
+    cudaEvent_t gather_ev = nullptr;              // compute <-> comm stream join (gathers)
     std::vector<void*> allocs;
     // profiling
     struct Timed {
@@ -160,7 +158,7 @@ struct Program {
     void time_projection(int t);
     void pack_halo(const Group& g, int par);
     void unpack_halo(const Group& g, int par);
-    void conv(const Group& g, int par, bool gn_fresh = false);
+    void conv(const Group& g, int par);
     void pack_kv(const Group& g, int par);
     void scatter_kv(const Group& g, int par);
     void attention(const Group& g, int par, int par_out);

@@ -233,6 +233,7 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
     rnd = e == Elem::F32;
     CUDA_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     CUDA_CHECK(cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaEventCreateWithFlags(&gather_ev, cudaEventDisableTiming));
     const int L = int(m->layers.size());
     groups = fuse_layers(*m);
     std::vector<char> mat(L, 0);
@@ -359,13 +360,12 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
             const Group& g = groups[gi];
             const Group& gc = groups[gi + 1];
             if (g.kind == Kind::SelfAttn && gc.kind == Kind::CrossAttn && gc.skip == g.last &&
-                srcs_count.count(g.last) == 1 && gc.last != L - 1 && !std::getenv("PP_NO_XATTN_MERGE"))
+                srcs_count.count(g.last) == 1 && gc.last != L - 1)
                 merged_into_prev[gi + 1] = 1;
             // Linear / GroupNorm group -> Upsample of its output: the producer stores the
             // nearest-2x upsample directly (its own output is not materialised)
             if ((g.kind == Kind::Linear || g.kind == Kind::GroupNorm) && gc.kind == Kind::Upsample &&
-                gc.first == gc.last && !srcs_count.count(g.last) && gc.last != L - 1 &&
-                !std::getenv("PP_NO_UP_MERGE"))
+                gc.first == gc.last && !srcs_count.count(g.last) && gc.last != L - 1)
                 merged_into_prev[gi + 1] = 1;
         }
     }
@@ -459,61 +459,6 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
             m->layers[g.first].out_ch % m->layers[next].groups == 0)
             fused_stats[next] = 2;
     }
-    // Single band: conv -> GroupNorm group in ONE kernel (the raw conv tile stays in TMEM
-    // while the statistics are reduced, then is normalised and stored; the raw conv output is
-    // never written).  Needs fresh statistics (one band: no cross-band reduction), a conv
-    // output nothing else reads, and a single-wave tiling; otherwise the two-kernel path.
-    fplans.resize(groups.size());
-    gn_fusable.assign(groups.size(), 0);
-    fused_now.assign(L, 0);
-    // Measured on B200 (scripts/fused_diag.py): the second TMEM pass runs on the 4 epilogue
-    // warps only and costs more than the separate 720-thread/SM GroupNorm pass it replaces
-    // (41.8 vs 33.5 + 5.4 us at 64^2 x 640), so the fused path is opt-in (PP_GN_FUSE=1).
-    if (nb == 1 && std::getenv("PP_GN_FUSE")) {
-        std::set<int> srcs;
-        for (const Layer& d : m->layers)
-            if (d.kind == Kind::AddSkip) srcs.insert(d.skip_source);
-        for (size_t gi = 0; gi + 1 < groups.size(); ++gi) {
-            const Group& g = groups[gi];
-            const Group& gq = groups[gi + 1];
-            const Layer& d = m->layers[g.first];
-            if (!(d.kind == Kind::Conv || d.kind == Kind::DownConv) || g.skip >= 0 || g.last != g.first)
-                continue;
-            if (gq.kind != Kind::GroupNorm || !fused_stats[gq.first] || srcs.count(g.last)) continue;
-            if (gq.last + 1 < L && fused_stats[gq.last + 1] == 2) continue;   // output stats wanted
-            if (gi + 2 < groups.size() && merged_into_prev[gi + 2]) continue;   // fused upsample
-            const Layer& dn = m->layers[gq.first];
-            const LayerWeights& lw = wts->L[g.first];
-            const LayerWeights& lg = wts->L[gq.first];
-            const Act& in = input_of(g.first);
-            try {
-                for (int p = 0; p < 2; ++p) {
-                    EpilogueSpec ep;
-                    ep.out = act[gq.last].interior(eb);
-                    ep.out_ld = act[gq.last].ld;
-                    ep.out_f32 = e == Elem::F32;
-                    ep.round_tf32 = rnd;
-                    ep.n_valid = d.out_ch;
-                    ep.bias = lw.bias;
-                    ep.gn_groups = dn.groups;
-                    ep.gn_out = lx[gq.first].stats[p] + size_t(band) * dn.groups * 2;
-                    ep.gn_apply = true;
-                    ep.gn_gamma = lg.gamma;
-                    ep.gn_beta = lg.beta;
-                    ep.gn_skip = gq.skip >= 0 ? act[gq.skip].interior(eb) : nullptr;
-                    ep.gn_skip_ld = gq.skip >= 0 ? act[gq.skip].ld : 0;
-                    ep.gn_silu = gq.silu;
-                    ep.gn_eps = dn.eps;
-                    ep.gn_err = flags + 1;
-                    plan_conv(fplans[gi][p], e, in.base, in.rows, in.w, in.ld, d.stride, lw.w,
-                              lw.n_pad, ep, sc, sms);
-                }
-                gn_fusable[gi] = 1;
-            } catch (const std::invalid_argument&) {
-                gn_fusable[gi] = 0;
-            }
-        }
-    }
     set_profile(profile);
     CUDA_CHECK(cudaDeviceSynchronize());
 }
@@ -538,6 +483,7 @@ Program::~Program() {
         for (auto ev : pr)
             if (ev) cudaEventDestroy(ev);
     for (auto ev : event_pool) cudaEventDestroy(ev);
+    if (gather_ev) cudaEventDestroy(gather_ev);
     for (void* p : allocs) cudaFree(p);
     if (cs) cudaStreamDestroy(cs);
     if (xs) cudaStreamDestroy(xs);
@@ -619,19 +565,8 @@ void Program::unpack_halo(const Group& g, int par) {
                                    x.row_bytes, cudaMemcpyDeviceToDevice, cs));
 }
 
-void Program::conv(const Group& g, int par, bool gn_fresh) {
+void Program::conv(const Group& g, int par) {
     const size_t gi = size_t(&g - groups.data());
-    if (gn_fresh && gn_fusable[gi]) {
-        // conv + the following GroupNorm group in one kernel (see the Program constructor)
-        const Group& gq = groups[gi + 1];
-        GemmPlan p = fplans[gi][par];
-        p.a.gn_temb = gq.temb >= 0 ? temb_ptr(gq.temb) : nullptr;
-        fused_now[gq.first] = 1;
-        run_timed(CAT_CONV, p.flops, [&] { launch_gemm(p, cs); });
-        count(1);
-        return;
-    }
-    if (gi + 1 < groups.size()) fused_now[groups[gi + 1].first] = 0;
     const GemmPlan& p = plans[gi][par];
     run_timed(CAT_CONV, p.flops, [&] { launch_gemm(p, cs); });
     count(1);
@@ -676,15 +611,7 @@ void Program::gn_stats(const Group& g, int par) {
     count(1);
 }
 
-// PP_SKIP=<letters>: timing experiments only (results are wrong): g = GroupNorm passes,
-// o = other pointwise / attention-side kernels are not launched
-static bool skip_kind(char k) {
-    static const char* v = std::getenv("PP_SKIP");
-    return v && std::strchr(v, k);
-}
-
 void Program::gn_apply(const Group& g, int mode, int par_cur, int par_prev) {
-    if (skip_kind('g')) return;
     const Act& in = input_of(g.first);
     const LayerX& x = lx[g.first];
     const Layer& d = m->layers[g.first];
@@ -724,7 +651,6 @@ void Program::gn_apply(const Group& g, int mode, int par_cur, int par_prev) {
 }
 
 void Program::simple(const Group& g, int par) {
-    if (skip_kind('o')) return;
     const Layer& d = m->layers[g.first];
     const Act& in = input_of(g.first);
     const int L = int(m->layers.size());
@@ -1038,10 +964,7 @@ void Runner::run_bands(std::vector<std::unique_ptr<Program>>& progs, int t, int 
                 volumes_.halo_recv += per_band;
                 volumes_.halo_sent += per_band;
             }
-            // fused conv + GroupNorm needs this step's own fresh statistics: one band and not
-            // the Stale scheme of a displaced step
-            const bool gn_fresh = !multi && !(displaced && o_.gn_scheme == GN_STALE);
-            each([&](Program& b, const Group& g) { b.conv(g, pcur, gn_fresh); });
+            each([&](Program& b, const Group& g) { b.conv(g, pcur); });
             if (exchanging) posted_[l] = s;
         } else if (d.kind == Kind::SelfAttn) {
             if (multi) {
@@ -1061,12 +984,6 @@ void Runner::run_bands(std::vector<std::unique_ptr<Program>>& progs, int t, int 
             each([&](Program& b, const Group& g) { b.attention(g, nb_pu, pcur); });
             if (exchanging) posted_[l] = s;
         } else if (d.kind == Kind::GroupNorm) {
-            if (!multi && progs[0]->fused_now[l]) {
-                // already applied by the fused conv kernel (single band, fresh statistics)
-                each([&](Program& b, const Group&) { b.record_ready(l); });
-                if (exchanging) gn_posted_[l] = s;
-                continue;
-            }
             each([&](Program& b, const Group& g) {
                 if (!b.fused_stats[l]) b.gn_stats(g, pcur);
                 b.record_ready(l);
@@ -1411,6 +1328,10 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
         for (auto& b : bands_)
             if (b.get() != &b0) CUDA_CHECK(cudaStreamWaitEvent(b->cs, b0.ready[0], 0));
     };
+    // The per-plan time-embedding table is read by the captured graph: refresh it for this
+    // plan before any replay (a no-op when it already holds these timesteps; an eager run of
+    // another plan may have rewritten it in place since the capture).
+    for (auto& b : bands_) b->prepare_temb_plan(ts, n);
     if (use_graph && graph_exec_ && key == graph_key_) {
         Program& b0 = *bands_[0];
         DeviceGuard g(b0.dev);
@@ -1434,7 +1355,6 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
                             : (o_.mode == MODE_DISPLACED && i >= 1 + o_.warmup) ? 2
                                                                                 : 1);
     } else {
-    for (auto& b : bands_) b->prepare_temb_plan(ts, n);   // outside any capture (synchronous)
     const uint64_t macs0 = total_macs_;
     const auto step_macs0 = step_device_macs_;
     const CommVolumes vol0 = volumes_;

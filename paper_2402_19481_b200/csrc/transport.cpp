@@ -198,8 +198,16 @@ public:
     }
 
     void gather_floats(Program& b, const float* send, float* recv, size_t count) override {
+        // One communicator, one stream: the gather runs on the comm stream after every
+        // exchange already queued there (a displaced step leaves its posts in flight), and
+        // the compute stream waits for it.  Two NCCL operations of one communicator never
+        // run concurrently on different streams.
         DeviceGuard g(b.dev);
-        NCCL_CHECK(ncclAllGather(send, recv, count, ncclFloat32, comm_, b.cs));
+        CUDA_CHECK(cudaEventRecord(b.gather_ev, b.cs));
+        CUDA_CHECK(cudaStreamWaitEvent(b.xs, b.gather_ev, 0));
+        NCCL_CHECK(ncclAllGather(send, recv, count, ncclFloat32, comm_, b.xs));
+        CUDA_CHECK(cudaEventRecord(b.gather_ev, b.xs));
+        CUDA_CHECK(cudaStreamWaitEvent(b.cs, b.gather_ev, 0));
     }
 
 private:
@@ -351,6 +359,9 @@ public:
         const uint32_t k = last_[l][par];
         if (k == 0) return;   // nothing exchanged into this parity yet
         for (int p : senders_[l]) wait_ge(b.cs, flag(ARRIVED, l, p), k);
+        // this rank's own pushes out of the parity buffers must also be complete before the
+        // compute stream overwrites them (scatter_kv rewrites the own slot of kv[par])
+        CUDA_CHECK(cudaStreamWaitEvent(b.cs, b.sent[l][par], 0));
     }
 
     void gather_floats(Program& b, const float* send, float* recv, size_t count) override {

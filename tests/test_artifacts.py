@@ -128,3 +128,11 @@ def test_cli_end_to_end(tmp_path):
     assert float(metrics["psnr_db"]) > 30.0
     assert int(metrics["total_macs"]) > 0 and float(metrics["device_ms"]) > 0
     assert (out / "x0.pgm").exists() and (out / "trace.txt").exists()
+
+
+def test_psnr_shape_mismatch_message():
+    # require(a.same_shape(b), "psnr: shape mismatch " + a.shape_str() + ...) (tensor.cpp:337)
+    a = np.zeros((1, 4, 6, 9), np.float32)
+    b = np.zeros((1, 4, 6, 8), np.float32)
+    with pytest.raises(P.InvalidArgument, match=r"^psnr: shape mismatch \(1,4,6,9\) vs \(1,4,6,8\)$"):
+        A.psnr(a, b, 1.0)

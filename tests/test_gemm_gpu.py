@@ -115,63 +115,3 @@ def test_conv_residual_bf16():
     ref = conv_ref(inp, w, bias, 1) + res.double()
     err = (out.double() - ref).norm() / ref.norm()
     assert err < 1e-2, err
-
-
-@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
-@pytest.mark.parametrize("M,Nn,K,bn", [(1000, 640, 576, 320), (256, 320, 2880, 320), (300, 384, 256, 384),
-                                       (128, 512, 128, 512)])
-def test_gemm_wide_tile(dtype, M, Nn, K, bn):
-    # block_n > 256: two N-half MMAs per K step into one TMEM accumulator
-    g = torch.Generator(device="cuda").manual_seed(M + bn)
-    A = torch.randn(M, K, device="cuda", generator=g)
-    B = torch.randn(Nn, K, device="cuda", generator=g)
-    bias = torch.randn(Nn, device="cuda", generator=g)
-    if dtype == "bf16":
-        A, B = A.bfloat16(), B.bfloat16()
-    else:
-        A, B = _tf32(A), _tf32(B)
-    for splits in (1, 2, 1 | PAIR, 2 | PAIR):
-        D = gemm(dtype, A, B, bias, splits=splits if splits & PAIR else splits | SINGLE, bn=bn)
-        ref = A.double() @ B.double().T + bias.double()
-        err = (D.double() - ref).norm() / ref.norm()
-        assert err < 1e-5, (splits, err)
-
-
-@pytest.mark.parametrize("rows,W,C,co", [(4, 128, 64, 320), (3, 64, 128, 320)])
-def test_conv_wide_tile(rows, W, C, co):
-    g = torch.Generator(device="cuda").manual_seed(rows * 7 + W)
-    inp = torch.randn(rows + 2, W, C, device="cuda", generator=g).bfloat16()
-    w = (torch.randn(co, 3, 3, C, device="cuda", generator=g) / (3 * C ** 0.5)).bfloat16()
-    bias = torch.randn(co, device="cuda", generator=g)
-    ref = conv_ref(inp, w, bias, 1)
-    for force in (SINGLE, PAIR):
-        out = torch.zeros(rows, W, co, device="cuda", dtype=torch.float32)
-        N.check(N.lib().pp_dev_conv(0, _p(inp), rows, W, C, 1, _p(w), co, co, _p(bias), _p(out), co,
-                                    1, None, 0, force, 320, None))
-        err = (out.double() - ref).norm() / ref.norm()
-        assert err < 1e-5, (force, err)
-
-
-@pytest.mark.parametrize("M,Nn,K", [(1024, 1024, 1280), (1000, 640, 576), (384, 320, 2880)])
-def test_gemm_pair_multicast(M, Nn, K, monkeypatch):
-    # opt-in clusters of two CTA pairs sharing B by TMA multicast (PP_MC=1, read once per
-    # process: run in a subprocess so the setting cannot leak into other tests)
-    import subprocess
-    import sys
-    code = (
-        "import torch, ctypes as C\n"
-        "from paper_2402_19481_b200 import _native as N\n"
-        f"M, Nn, K = {M}, {Nn}, {K}\n"
-        "g = torch.Generator(device='cuda').manual_seed(3)\n"
-        "A = torch.randn(M, K, device='cuda', generator=g).bfloat16()\n"
-        "B = torch.randn(Nn, K, device='cuda', generator=g).bfloat16()\n"
-        "D = torch.zeros(M, Nn, device='cuda')\n"
-        "p = lambda t: C.c_void_p(t.data_ptr())\n"
-        "N.check(N.lib().pp_dev_gemm(0, p(A), M, K, K, p(B), Nn, K, None, p(D), Nn, 1, 16, 0, None))\n"
-        "ref = A.double() @ B.double().T\n"
-        "print(((D.double() - ref).norm() / ref.norm()).item())\n")
-    env = dict(os.environ, PP_MC="1")
-    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
-                         timeout=120)
-    assert out.returncode == 0, out.stderr
-    assert float(out.stdout.strip().splitlines()[-1]) < 1e-5
