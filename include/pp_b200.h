@@ -131,10 +131,10 @@ typedef struct {
     int warmup_steps; /* displaced: sync steps after the first (default 4) */
     int gn_scheme;    /* PP_GN_* */
     int dtype;        /* PP_DTYPE_* */
-    /* process layout: world == 1 runs all n_devices bands in this process (one CUDA
-     * device per band, round-robin over the visible devices); world == n_devices runs
-     * band `rank` only, exchanging with the other ranks over NCCL (nccl_id = the
-     * 128-byte ncclUniqueId shared by all ranks) */
+    /* process layout: world == 1 runs all n_devices bands in this process, on CUDA device
+     * `device` (a single-GPU simulation of the N-device run); world == n_devices runs
+     * band `rank` only on its own GPU, exchanging with the other ranks over NCCL
+     * (nccl_id = the 128-byte ncclUniqueId shared by all ranks) or CUDA IPC */
     int world, rank;
     const void* nccl_id;
     int device;       /* CUDA device of band 0 (world == 1) or of this rank */
@@ -142,6 +142,10 @@ typedef struct {
     int transport;    /* world > 1: PP_TRANSPORT_NCCL (nccl_id) or PP_TRANSPORT_IPC (CUDA IPC
                        * peer mappings + copy engines; pp_runner_ipc_export / _connect before
                        * the first step; no CUDA-graph capture) */
+    int no_comm;      /* ablation only, the paper's "No Comm." row: every
+                       * exchange (halo rows, K/V, GroupNorm statistics) is skipped and each
+                       * band normalises with its own statistics; compute is identical, the
+                       * results are NOT the reference's.  Default 0. */
 } pp_runner_opts;
 PP_API void pp_runner_opts_default(pp_runner_opts* o);
 

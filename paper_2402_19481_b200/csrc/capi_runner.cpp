@@ -56,6 +56,7 @@ pp::RunnerOptions opts_of(const pp_runner_opts* o) {
     }
     r.device = o->device;
     r.profile = o->profile != 0;
+    r.no_comm = o->no_comm != 0;
     return r;
 }
 
@@ -297,6 +298,7 @@ PP_API void pp_runner_opts_default(pp_runner_opts* o) {
     o->device = 0;
     o->profile = 0;
     o->transport = PP_TRANSPORT_NCCL;
+    o->no_comm = 0;
 }
 
 PP_API int pp_runner_create(const pp_model* m, const float* cond, int cond_dim, int h, int w,

@@ -726,8 +726,10 @@ Runner::Runner(const Model& m, const std::vector<float>& cond, int h, int w, con
                              ? make_ipc_transport(bands_[0].get(), o_.world, o_.rank)
                              : make_nccl_transport(bands_[0].get(), o_.world, o_.rank, o_.nccl_id);
         } else {
+            // all local bands on one device: multi-GPU runs are one process per GPU
+            // (world > 1), so no host thread ever drives several GPUs' launches
             for (int d = 0; d < n_dev_; ++d) {
-                const int dev = (o_.device + d) % ndev;
+                const int dev = o_.device;
                 bands_.push_back(std::make_unique<Program>(this, m_, weights_for(dev), dev, d, n_dev_,
                                                            h, w, specs_[d], o_.elem, o_.profile));
             }
@@ -931,7 +933,7 @@ void Runner::run_bands(std::vector<std::unique_ptr<Program>>& progs, int t, int 
     if (displaced) check_displaced_ready(s);
     const int pcur = s & 1, pprev = (s + 1) & 1;
     const int pu = displaced ? pprev : pcur;
-    const bool multi = exchanging && n_dev_ > 1;
+    const bool multi = exchanging && n_dev_ > 1 && !o_.no_comm;
     const int nb_pu = multi ? pu : pcur;
     for (auto& b : progs) {
         DeviceGuard g(b->dev);
@@ -989,7 +991,9 @@ void Runner::run_bands(std::vector<std::unique_ptr<Program>>& progs, int t, int 
                 b.record_ready(l);
             });
             int mode;
-            if (!displaced) {
+            if (o_.no_comm) {
+                mode = GN_USE_LOCAL;
+            } else if (!displaced) {
                 mode = multi ? GN_USE_GLOBAL : GN_USE_LOCAL;
             } else {
                 mode = o_.gn_scheme == GN_CORRECTED ? GN_USE_CORRECTED
@@ -1529,8 +1533,9 @@ long Runner::cached_input(int device, int layer, float* dst, int* nchw4) {
     CUDA_CHECK(cudaStreamSynchronize(b->xs));
     std::fill(dst, dst + count, std::nanf(""));
     const Program::Act& in = b->input_of(layer);
-    // rows this band holds: the full K/V map (self-attention) or own band + halo rows (convs)
-    int r0 = ri.row_start - 1, r1 = ri.row_end + 1;
+    // rows this band holds: the full K/V map (self-attention) or own band + halo rows (convs;
+    // a stride-2 DownConv reads only the row above its band, derive_patch_spec / conv2d_region)
+    int r0 = ri.row_start - 1, r1 = ri.row_end + (d.stride == 2 ? 0 : 1);
     const void* src = in.base;
     long long src_ld = in.ld;
     if (d.kind == Kind::SelfAttn && n_dev_ > 1) {

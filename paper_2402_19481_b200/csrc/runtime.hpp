@@ -40,8 +40,9 @@ struct RunnerOptions {
     int world = 1, rank = 0;          // world > 1: one band per process, NCCL exchange
     std::vector<uint8_t> nccl_id;     // 128-byte ncclUniqueId (world > 1, NCCL transport)
     int transport = 0;                // world > 1: 0 NCCL, 1 CUDA IPC + copy engines
-    int device = 0;                   // CUDA device of band 0 / of this rank
+    int device = 0;                   // CUDA device of every local band / of this rank
     bool profile = false;
+    bool no_comm = false;             // ablation ("No Comm."): exchanges skipped, local GN stats
 };
 
 struct CommVolumes {

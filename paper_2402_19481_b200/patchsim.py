@@ -186,6 +186,7 @@ class RunnerOptions:
     device: int = 0
     profile: bool = False
     transport: str = "nccl"          # world > 1: "nccl" or "ipc" (CUDA IPC + copy engines)
+    no_comm: bool = False            # ablation only ("No Comm."): exchanges skipped
 
 
 class PatchRunner:
@@ -213,6 +214,7 @@ class PatchRunner:
         if opts.transport not in N.TRANSPORTS:
             raise InvalidArgument(f"unknown transport '{opts.transport}'")
         o.transport = N.TRANSPORTS[opts.transport]
+        o.no_comm = int(opts.no_comm)
         h_ = C.c_void_p()
         N.check(N.lib().pp_runner_create(model._h, _p(cond), cond.size, h, w, C.byref(o),
                                          C.byref(h_)))
