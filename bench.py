@@ -363,7 +363,6 @@ def roofline_from(kernels, flops_per_gen, dev_s, peaks):
         "gemm_ms_per_generation": gemm_us / 1e3,
         "all_kernels_ms_per_generation": all_us / 1e3,
         "gemm_share_of_generation": (gemm_us * 1e-6) / dev_s if dev_s else None,
-        "timing": "CUPTI kernel records of one pipelined generation (torch.profiler), graph replay",
         "traffic_source": traffic_src,
         "top_kernels_ms": {k[:80]: round(us / 1e3, 3) for k, (us, _) in top},
     }
@@ -426,9 +425,23 @@ def main():
     macs_per_gen = model.total_macs(H, W) * args.num_steps // n
     roofline = None
     try:
-        kern = pipelined_kernel_times(torch, runner, x_T, plan, abar)
+        # per-kernel device time without PDL early starts (a PDL kernel launches while its
+        # predecessor drains and waits in griddepcontrol.wait, so its CUPTI span would include
+        # that wait): a fresh runner captures the same loop with the attribute off
+        from paper_2402_19481_b200 import _native as NAT
+        NAT.lib().pp_set_pdl(0)
+        rp = make_runner(H, W, args.dtype)
+        rp.sample(x_T, plan, abar)
+        kern = pipelined_kernel_times(torch, rp, x_T, plan, abar)
+        dev_nopdl = timer.run(rp, x_T, plan, abar, 3, 1)["dev_s"]
+        rp.close()
+        NAT.lib().pp_set_pdl(1)
         if any("gemm_kernel" in k for k in kern):
-            roofline = roofline_from(kern, 2.0 * macs_per_gen, dev, peaks)
+            roofline = roofline_from(kern, 2.0 * macs_per_gen, dev_nopdl, peaks)
+            roofline["generation_s_without_pdl"] = dev_nopdl
+            roofline["timing"] = ("CUPTI kernel records (torch.profiler) of one graph-replayed "
+                                  "generation captured with PDL off: kernels back to back, warm "
+                                  "L2 as in the pipeline, no event serialisation")
     except Exception as e:  # fall back to the event-instrumented pass, labelled
         roofline = {"error": f"profiler: {e!r}"[:200]}
     if roofline is None or "achieved" not in roofline:

@@ -62,6 +62,10 @@ extern "C" {
 
 PP_API const char* pp_last_error(void);
 PP_API int pp_version(void);
+/* programmatic dependent launch on (1, default) / off (0) for later launches and graph
+ * captures; off is a measurement control (strictly serialised kernels, exact per-kernel
+ * device times), results are identical either way */
+PP_API void pp_set_pdl(int on);
 /* number of visible CUDA devices with compute capability 10.x (0 on a CPU-only host) */
 PP_API int pp_device_count(void);
 

@@ -85,6 +85,7 @@ _LL, _SZ = C.c_longlong, C.c_size_t
 SIGNATURES = {
     "pp_last_error": (C.c_char_p, []),
     "pp_version": (_I, []),
+    "pp_set_pdl": (None, [_I]),
     "pp_device_count": (_I, []),
     "pp_model_build": (_I, [_V, _U64, _V]),
     "pp_model_from_pool": (_I, [_V, _V, _SZ, _V]),

@@ -1,6 +1,7 @@
 // C ABI: error plumbing, device queries and the device-pointer GEMM / conv entries.
 #include "capi_common.hpp"
 #include "gemm.hpp"
+#include "pdl.cuh"
 
 #include <cuda_runtime.h>
 
@@ -13,6 +14,8 @@ extern "C" {
 PP_API const char* pp_last_error(void) { return pp::g_last_error.c_str(); }
 
 PP_API int pp_version(void) { return 1; }
+
+PP_API void pp_set_pdl(int on) { pp::pdl_flag().store(on ? 1 : 0); }
 
 PP_API int pp_device_count(void) {
     int n = 0;

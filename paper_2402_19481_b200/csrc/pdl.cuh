@@ -6,12 +6,15 @@
 //   pdl_wait()    before the first read of data produced by an earlier kernel on the stream
 //                 (and before the first global write: kernel i may still read that buffer)
 //   pdl_trigger() lets the dependent grid launch once every CTA of this grid has called it
-// Both are no-ops for a launch without the attribute.  PP_PDL=0 disables the attribute.
+// Both are no-ops for a launch without the attribute.  PP_PDL=0 (or pp_set_pdl(0), a
+// measurement control: kernels then run strictly back to back, so per-kernel device times
+// from CUPTI carry no early-start wait) disables the attribute for later launches / captures.
 #pragma once
 #include "util.hpp"
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdlib>
 #include <utility>
 
@@ -22,13 +25,14 @@ __device__ __forceinline__ void pdl_trigger() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-inline bool pdl_enabled() {
-    static const bool on = [] {
+inline std::atomic<int>& pdl_flag() {
+    static std::atomic<int> on{[] {
         const char* v = std::getenv("PP_PDL");
-        return !(v && v[0] == '0');
-    }();
+        return (v && v[0] == '0') ? 0 : 1;
+    }()};
     return on;
 }
+inline bool pdl_enabled() { return pdl_flag().load(std::memory_order_relaxed) != 0; }
 
 // kernel<<<grid, block, smem, stream>>>(args...) with the PDL attribute (and an optional
 // cluster dimension).
