@@ -430,6 +430,26 @@ __global__ void __launch_bounds__(256, (STATS ? 2 : 3))
     if (tid == 0) *so.ticket = 0u;
 }
 
+// ---------------------------------------------------------------- context exchange
+__global__ void __launch_bounds__(256) copy_chunks_kernel(const CopyChunk* __restrict__ chunks) {
+    const CopyChunk c = chunks[blockIdx.x];
+    const uint4* src = static_cast<const uint4*>(c.src);
+    uint4* dst = static_cast<uint4*>(c.dst);
+    const int n = int(c.bytes / 16);
+    for (int i = threadIdx.x; i < n; i += 256) dst[i] = __ldcg(src + i);
+}
+
+__global__ void __launch_bounds__(256) copy_rows_kernel(const RowCopies c, long long nv) {
+    pdl_wait();
+    pdl_trigger();
+    const int k = blockIdx.y;
+    if (!c.src[k]) return;
+    const uint4* src = static_cast<const uint4*>(c.src[k]);
+    uint4* dst = static_cast<uint4*>(c.dst[k]);
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < nv; i += 256LL * gridDim.x)
+        dst[i] = __ldcg(src + i);
+}
+
 // ---------------------------------------------------------------- pointwise
 template <class T>
 __global__ void silu_kernel(const T* __restrict__ x, T* __restrict__ y, long long nv, int r) {
@@ -921,6 +941,22 @@ void add_channel(Elem e, const void* x, const float* vec, const void* skip, void
     DISPATCH(e, launch_pdl(add_channel_kernel<T>, dim3(grid_for(pix * ld / VEC, 256)), dim3(256), 0, s, 1, 
                     static_cast<const T*>(x), vec, static_cast<const T*>(skip), static_cast<T*>(o),
                     pix, ld, r ? 1 : 0));
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void copy_chunks(const CopyChunk* chunks, int n, cudaStream_t s) {
+    if (n <= 0) return;
+    copy_chunks_kernel<<<n, 256, 0, s>>>(chunks);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void copy_rows(const RowCopies& c, unsigned long long bytes, cudaStream_t s) {
+    int k = 0;
+    for (int i = 0; i < 4; ++i) k += c.src[i] != nullptr;
+    if (!k || !bytes) return;
+    const long long v = (long long)(bytes / 16);
+    const int per = int(std::min<long long>(std::max<long long>((v + 255) / 256, 1), 64));
+    launch_pdl(copy_rows_kernel, dim3(per, 4), dim3(256), 0, s, 1, c, v);
     CUDA_CHECK(cudaGetLastError());
 }
 

@@ -72,6 +72,24 @@ void softmax_rows(Elem e, const float* S, int m, int ns, long long lds, float sc
 void transpose(Elem e, const void* V, int ns, int C, long long ldv, void* Vt, long long ldt,
                cudaStream_t s);
 
+// ---- context exchange (displaced patch parallelism) ----------------------------------------
+// A batch of exchange copies in ONE launch (in-process transport: every band's halo rows,
+// K/V band and GroupNorm statistics of a batch of layers): chunk i = {src, dst, bytes},
+// 16-byte aligned, bytes <= 64 KiB (one block per chunk).
+struct CopyChunk {
+    const void* src;
+    void* dst;
+    unsigned long long bytes;
+};
+void copy_chunks(const CopyChunk* chunks_dev, int n, cudaStream_t s);
+// Up to four equal-size row copies (null src = skipped) in one small launch: halo pack /
+// unpack and the K/V own-band copies on the compute stream.
+struct RowCopies {
+    const void* src[4];
+    void* dst[4];
+};
+void copy_rows(const RowCopies& c, unsigned long long bytes, cudaStream_t s);
+
 // ---- time embedding / condition projection ----------------------------------------------
 // proj[l][c] for every AddTimeEmb layer in one launch: proj = W_l emb + b_l (fp64
 // accumulate, fp32 result; layer_time_emb, model.cpp:278-289).  `emb` is the host

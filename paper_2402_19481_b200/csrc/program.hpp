@@ -156,16 +156,22 @@ struct Program {
 
     // per-step pieces (issued by Runner in layer order)
     void time_projection(int t);
-    void pack_halo(const Group& g, int par);
-    void unpack_halo(const Group& g, int par);
+    void halo_rows(const Group& g, int par_pack, int par_unpack);
     void conv(const Group& g, int par);
-    void pack_kv(const Group& g, int par);
-    void scatter_kv(const Group& g, int par);
+    void own_kv(const Group& g, int par_post, int par_use);
     void attention(const Group& g, int par, int par_out);
     void gn_stats(const Group& g, int par);
     void gn_apply(const Group& g, int combine_mode, int par_cur, int par_prev);
     void simple(const Group& g, int par);
     void record_ready(int l);
+};
+
+// One exchange of a batch: layer and what moves (halo rows, K/V band, GroupNorm statistics).
+struct XItem {
+    enum Kind { HALO = 0, KV = 1, STATS = 2 };
+    int layer = 0;
+    int kind = HALO;
+    bool top_only = false;   // halo of a stride-2 DownConv: only the row above is needed
 };
 
 class Transport {
@@ -176,6 +182,21 @@ public:
     virtual void halo(int l, int par, bool top_only) = 0;
     virtual void kv(int l, int par) = 0;
     virtual void stats(int l, int par) = 0;
+    // Displaced steps: the layers' posts of one step, exchanged together into parity `par`
+    // (their consumers read them one step later).  Precondition: every local band recorded
+    // ready[l] for every listed layer; afterwards sent[l][par] of every listed layer marks the
+    // exchange, so wait() is unchanged.  Default: one exchange per item.
+    // Every exchange this runner will issue (the displaced batches and the single-layer
+    // exchanges of synchronous steps), announced once before any capture: a transport may
+    // build its device-side tables here (no allocation or synchronous copy during a capture).
+    virtual void prepare(const std::vector<std::vector<XItem>>& exchanges) { (void)exchanges; }
+    virtual void batch(const std::vector<XItem>& items, int par) {
+        for (const XItem& it : items) {
+            if (it.kind == XItem::HALO) halo(it.layer, par, it.top_only);
+            else if (it.kind == XItem::KV) kv(it.layer, par);
+            else stats(it.layer, par);
+        }
+    }
     // Make band b's compute stream wait until the (l, par) exchange has landed.
     virtual void wait(Program& b, int l, int par) = 0;
     // All-gather equal float chunks (rank order) on band b's compute stream (NCCL only).

@@ -543,26 +543,36 @@ void Program::time_projection(int t) {
     count(1);
 }
 
-void Program::pack_halo(const Group& g, int par) {
-    const Act& in = input_of(g.first);
-    const LayerX& x = lx[g.first];
-    char* dst = static_cast<char*>(x.send_rows[par]);
-    const char* src = static_cast<const char*>(in.interior(eb));
-    CUDA_CHECK(cudaMemcpyAsync(dst, src, x.row_bytes, cudaMemcpyDeviceToDevice, cs));
-    CUDA_CHECK(cudaMemcpyAsync(dst + x.row_bytes, src + size_t(in.rows - 1) * x.row_bytes,
-                               x.row_bytes, cudaMemcpyDeviceToDevice, cs));
-}
-
-void Program::unpack_halo(const Group& g, int par) {
+// Halo pack (own first / last row -> send_rows[par_pack]) and / or unpack (halo_recv[par_unpack]
+// -> the band's rows -1 and rows: the row above from band-1, the row below from band+1, which a
+// stride-2 DownConv does not read); -1 = skip.  One small kernel on the compute stream.
+void Program::halo_rows(const Group& g, int par_pack, int par_unpack) {
     const Act& in = input_of(g.first);
     const LayerX& x = lx[g.first];
     const Layer& d = m->layers[g.first];
-    char* base = static_cast<char*>(in.base);
-    const char* src = static_cast<const char*>(x.halo_recv[par]);
-    if (band > 0) CUDA_CHECK(cudaMemcpyAsync(base, src, x.row_bytes, cudaMemcpyDeviceToDevice, cs));
-    if (band < nb - 1 && d.stride == 1)
-        CUDA_CHECK(cudaMemcpyAsync(base + size_t(in.rows + 1) * x.row_bytes, src + x.row_bytes,
-                                   x.row_bytes, cudaMemcpyDeviceToDevice, cs));
+    RowCopies c{};
+    if (par_pack >= 0) {
+        char* dst = static_cast<char*>(x.send_rows[par_pack]);
+        const char* src = static_cast<const char*>(in.interior(eb));
+        c.src[0] = src;
+        c.dst[0] = dst;
+        c.src[1] = src + size_t(in.rows - 1) * x.row_bytes;
+        c.dst[1] = dst + x.row_bytes;
+    }
+    if (par_unpack >= 0) {
+        char* base = static_cast<char*>(in.base);
+        const char* src = static_cast<const char*>(x.halo_recv[par_unpack]);
+        if (band > 0) {
+            c.src[2] = src;
+            c.dst[2] = base;
+        }
+        if (band < nb - 1 && d.stride == 1) {
+            c.src[3] = src + x.row_bytes;
+            c.dst[3] = base + size_t(in.rows + 1) * x.row_bytes;
+        }
+    }
+    copy_rows(c, x.row_bytes, cs);
+    count(1);
 }
 
 void Program::conv(const Group& g, int par) {
@@ -572,14 +582,22 @@ void Program::conv(const Group& g, int par) {
     count(1);
 }
 
-void Program::pack_kv(const Group& g, int par) {
+// The band's own K/V rows (its layer input) into its slot of the full map kv[par] for each
+// given parity (-1 = skip): the post (par_post) and, in a displaced step, the map the
+// attention reads (the other bands' rows stale, par_use).
+void Program::own_kv(const Group& g, int par_post, int par_use) {
     const Act& in = input_of(g.first);
     const LayerX& x = lx[g.first];
-    CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(x.kv[par]) + size_t(band) * x.band_bytes,
-                               in.interior(eb), x.band_bytes, cudaMemcpyDeviceToDevice, cs));
+    RowCopies c{};
+    int k = 0;
+    for (int par : {par_post, par_use}) {
+        if (par < 0) continue;
+        c.src[k] = in.interior(eb);
+        c.dst[k++] = static_cast<char*>(x.kv[par]) + size_t(band) * x.band_bytes;
+    }
+    copy_rows(c, x.band_bytes, cs);
+    count(1);
 }
-
-void Program::scatter_kv(const Group& g, int par) { pack_kv(g, par); }
 
 void Program::attention(const Group& g, int par, int par_out) {
     const size_t gi = size_t(&g - groups.data());
@@ -725,6 +743,7 @@ Runner::Runner(const Model& m, const std::vector<float>& cond, int h, int w, con
             transport_ = o_.transport == 1
                              ? make_ipc_transport(bands_[0].get(), o_.world, o_.rank)
                              : make_nccl_transport(bands_[0].get(), o_.world, o_.rank, o_.nccl_id);
+            plan_exchanges();
         } else {
             // all local bands on one device: multi-GPU runs are one process per GPU
             // (world > 1), so no host thread ever drives several GPUs' launches
@@ -737,6 +756,7 @@ Runner::Runner(const Model& m, const std::vector<float>& cond, int h, int w, con
                 std::vector<Program*> ps;
                 for (auto& b : bands_) ps.push_back(b.get());
                 transport_ = make_inproc_transport(ps);
+                plan_exchanges();
             }
         }
     }
@@ -940,10 +960,17 @@ void Runner::run_bands(std::vector<std::unique_ptr<Program>>& progs, int t, int 
         b->time_projection(t);
     }
     const std::vector<Group>& groups = progs[0]->groups;
+    // Displaced steps post their context for the NEXT step, so the posts are batched
+    // (plan_exchanges): one exchange for the layers of the first half of the step (issued at
+    // mid-step, consumed by the first half of step s+1) and one for the rest (issued at the
+    // end of the step).  A synchronous step exchanges every layer on the spot.
+    const int L = int(m_.layers.size());
     for (size_t gi = 0; gi < groups.size(); ++gi) {
         const Group& g0 = groups[gi];
         const int l = g0.first;
         const Layer& d = m_.layers[l];
+        if (multi && displaced && 2 * l >= L && 2 * (gi ? groups[gi - 1].first : 0) < L)
+            transport_->batch(xbatch_[0], pcur);
         auto each = [&](auto&& fn) {
             for (auto& b : progs) {
                 DeviceGuard g(b->dev);
@@ -951,16 +978,26 @@ void Runner::run_bands(std::vector<std::unique_ptr<Program>>& progs, int t, int 
             }
         };
         if (d.kind == Kind::Conv || d.kind == Kind::DownConv) {
-            if (multi) {
+            if (multi && displaced) {
+                // the halo rows of step s-1 were exchanged a step ago: wait for them, then
+                // unpack them and pack this step's rows in one launch; post in the batch
                 each([&](Program& b, const Group& g) {
-                    b.pack_halo(g, pcur);
+                    transport_->wait(b, l, pu);
+                    b.halo_rows(g, pcur, pu);
+                    b.record_ready(l);
+                });
+            } else if (multi) {
+                each([&](Program& b, const Group& g) {
+                    b.halo_rows(g, pcur, -1);
                     b.record_ready(l);
                 });
                 transport_->halo(l, pcur, d.stride == 2);
                 each([&](Program& b, const Group& g) {
                     transport_->wait(b, l, pu);
-                    b.unpack_halo(g, pu);
+                    b.halo_rows(g, -1, pu);
                 });
+            }
+            if (multi) {
                 const size_t row = bands_[0]->lx[l].row_bytes;
                 const uint64_t per_band = (d.stride == 2 ? 1 : 2) * uint64_t(n_dev_ - 1) * row;
                 volumes_.halo_recv += per_band;
@@ -969,16 +1006,23 @@ void Runner::run_bands(std::vector<std::unique_ptr<Program>>& progs, int t, int 
             each([&](Program& b, const Group& g) { b.conv(g, pcur); });
             if (exchanging) posted_[l] = s;
         } else if (d.kind == Kind::SelfAttn) {
-            if (multi) {
+            if (multi && displaced) {
+                // stale K/V of step s-1 (exchanged a step ago) + this band's fresh rows; this
+                // step's rows posted to the other parity
                 each([&](Program& b, const Group& g) {
-                    b.pack_kv(g, pcur);
+                    transport_->wait(b, l, pu);
+                    b.own_kv(g, pcur, pu);
+                    b.record_ready(l);
+                });
+            } else if (multi) {
+                each([&](Program& b, const Group& g) {
+                    b.own_kv(g, pcur, -1);
                     b.record_ready(l);
                 });
                 transport_->kv(l, pcur);
-                each([&](Program& b, const Group& g) {
-                    transport_->wait(b, l, pu);
-                    if (displaced) b.scatter_kv(g, pu);
-                });
+                each([&](Program& b, const Group&) { transport_->wait(b, l, pu); });
+            }
+            if (multi) {
                 const uint64_t v = uint64_t(bands_[0]->lx[l].band_bytes) * (n_dev_ - 1) * n_dev_;
                 volumes_.allgather_recv += v;
                 volumes_.allgather_sent += v;
@@ -1001,7 +1045,7 @@ void Runner::run_bands(std::vector<std::unique_ptr<Program>>& progs, int t, int 
                                                     : GN_USE_LOCAL;
             }
             if (multi) {
-                transport_->stats(l, pcur);
+                if (!displaced) transport_->stats(l, pcur);
                 each([&](Program& b, const Group&) { transport_->wait(b, l, pu); });
                 const uint64_t v = uint64_t(d.groups) * 16 * (n_dev_ - 1) * n_dev_;
                 volumes_.statreduce_recv += v;
@@ -1015,6 +1059,37 @@ void Runner::run_bands(std::vector<std::unique_ptr<Program>>& progs, int t, int 
             each([&](Program& b, const Group& g) { b.simple(g, pcur); });
         }
     }
+    if (multi && displaced) transport_->batch(xbatch_[1], pcur);
+}
+
+void Runner::plan_exchanges() {
+    // one entry per exchange layer in step order; the first batch holds the layers of the
+    // groups that start in the first half of the layer list (run_bands issues it before the
+    // first group starting at or past L/2)
+    const int L = int(m_.layers.size());
+    xbatch_.assign(2, {});
+    std::vector<std::vector<XItem>> singles;
+    for (const Group& g : bands_[0]->groups) {
+        const Layer& d = m_.layers[g.first];
+        XItem it;
+        it.layer = g.first;
+        if (d.kind == Kind::Conv || d.kind == Kind::DownConv) {
+            it.kind = XItem::HALO;
+            it.top_only = d.stride == 2;
+        } else if (d.kind == Kind::SelfAttn) {
+            it.kind = XItem::KV;
+        } else if (d.kind == Kind::GroupNorm) {
+            it.kind = XItem::STATS;
+        } else {
+            continue;
+        }
+        xbatch_[2 * g.first >= L ? 1 : 0].push_back(it);
+        singles.push_back({it});
+    }
+    std::vector<std::vector<XItem>> all = singles;
+    all.push_back(xbatch_[0]);
+    all.push_back(xbatch_[1]);
+    transport_->prepare(all);
 }
 
 void Runner::load_x(const float* x) {

@@ -70,6 +70,7 @@ struct ProfileTotals {
 struct DeviceWeights;  // packed weights on one CUDA device
 struct Program;        // one band compiled for one CUDA device
 class Transport;
+struct XItem;
 
 class Runner {
 public:
@@ -143,6 +144,9 @@ private:
     std::vector<std::vector<TraceEvent>> trace_;
     std::vector<std::vector<int>> tr_act_step_, tr_gn_step_;
     void record_trace(int s, int kind);   // kind: 0 reference, 1 sync, 2 displaced, 3 naive
+    // the two exchange batches of a displaced step (layers of the first / second half)
+    std::vector<std::vector<XItem>> xbatch_;
+    void plan_exchanges();
     std::vector<std::vector<uint64_t>> step_device_macs_;
     CommVolumes volumes_;
     ProfileTotals prof_;

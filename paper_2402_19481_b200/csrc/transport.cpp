@@ -26,7 +26,9 @@
 #include <cuda.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
+#include <map>
 #include <stdexcept>
 #include <string>
 
@@ -50,80 +52,48 @@ struct DeviceGuard {
             throw NcclError(std::string("NCCL error '") + ncclGetErrorString(r_) + "' (" #x ")"); \
     } while (0)
 
+// All bands in this process, on one device.  An exchange (one layer of a synchronous step, or
+// a displaced step's batch of layers) is ONE copy kernel on band 0's comm stream that moves
+// every band's halo rows / K/V band / GroupNorm statistics into the receivers' parity buffers,
+// after every band's ready event (the receivers' event orders the writes after their previous
+// reads of the same parity buffer); each band's sent[l][par] is recorded behind it.  The chunk
+// tables are built once per (batch, parity) and stay on the device, so the exchange is
+// graph-capturable and costs one kernel node.
 class InProcTransport final : public Transport {
 public:
-    explicit InProcTransport(std::vector<Program*> b) : bands_(std::move(b)) {
-        // peer access where the hardware allows it (NVLink / NVSwitch)
-        for (Program* a : bands_)
-            for (Program* c : bands_) {
-                if (a->dev == c->dev) continue;
-                int ok = 0;
-                cudaDeviceCanAccessPeer(&ok, a->dev, c->dev);
-                if (ok) {
-                    DeviceGuard g(a->dev);
-                    const cudaError_t e = cudaDeviceEnablePeerAccess(c->dev, 0);
-                    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CUDA_CHECK(e);
-                    cudaGetLastError();
-                }
-            }
+    explicit InProcTransport(std::vector<Program*> b) : bands_(std::move(b)) {}
+    ~InProcTransport() override {
+        DeviceGuard g(bands_[0]->dev);
+        cudaStreamSynchronize(bands_[0]->xs);
+        for (auto& kv : tables_) cudaFree(kv.second.first);
     }
 
-    void halo(int l, int par, bool top_only) override {
-        const int n = int(bands_.size());
-        for (int e = 0; e < n; ++e) {
-            Program& s = *bands_[e];
-            DeviceGuard g(s.dev);
-            CUDA_CHECK(cudaStreamWaitEvent(s.xs, s.ready[l], 0));
-            if (e > 0) CUDA_CHECK(cudaStreamWaitEvent(s.xs, bands_[e - 1]->ready[l], 0));
-            if (e + 1 < n) CUDA_CHECK(cudaStreamWaitEvent(s.xs, bands_[e + 1]->ready[l], 0));
-            const size_t rb = s.lx[l].row_bytes;
-            const char* src = static_cast<const char*>(s.lx[l].send_rows[par]);
-            if (e + 1 < n)  // my last row is the row above band e+1
-                CUDA_CHECK(cudaMemcpyAsync(bands_[e + 1]->lx[l].halo_recv[par], src + rb, rb,
-                                           cudaMemcpyDefault, s.xs));
-            if (e > 0 && !top_only)  // my first row is the row below band e-1
-                CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(bands_[e - 1]->lx[l].halo_recv[par]) + rb,
-                                           src, rb, cudaMemcpyDefault, s.xs));
-            CUDA_CHECK(cudaEventRecord(s.sent[l][par], s.xs));
-        }
+    void halo(int l, int par, bool top_only) override { batch({XItem{l, XItem::HALO, top_only}}, par); }
+    void kv(int l, int par) override { batch({XItem{l, XItem::KV, false}}, par); }
+    void stats(int l, int par) override { batch({XItem{l, XItem::STATS, false}}, par); }
+
+    void prepare(const std::vector<std::vector<XItem>>& exchanges) override {
+        DeviceGuard g(bands_[0]->dev);
+        for (const auto& items : exchanges)
+            for (int par = 0; par < 2; ++par) table(items, par);
     }
 
-    void kv(int l, int par) override {
-        const int n = int(bands_.size());
-        for (int e = 0; e < n; ++e) {
-            Program& s = *bands_[e];
-            DeviceGuard g(s.dev);
-            for (Program* o : bands_) CUDA_CHECK(cudaStreamWaitEvent(s.xs, o->ready[l], 0));
-            const size_t bb = s.lx[l].band_bytes;
-            const char* src = static_cast<const char*>(s.lx[l].kv[par]) + size_t(e) * bb;
-            for (int d = 0; d < n; ++d) {
-                if (d == e) continue;
-                CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(bands_[d]->lx[l].kv[par]) + size_t(e) * bb,
-                                           src, bb, cudaMemcpyDefault, s.xs));
-            }
-            CUDA_CHECK(cudaEventRecord(s.sent[l][par], s.xs));
-        }
-    }
-
-    void stats(int l, int par) override {
-        const int n = int(bands_.size());
-        for (int e = 0; e < n; ++e) {
-            Program& s = *bands_[e];
-            DeviceGuard g(s.dev);
-            for (Program* o : bands_) CUDA_CHECK(cudaStreamWaitEvent(s.xs, o->ready[l], 0));
-            const size_t eb = size_t(s.lx[l].G) * 2 * sizeof(double);
-            const char* src = reinterpret_cast<const char*>(s.lx[l].stats[par]) + size_t(e) * eb;
-            for (int d = 0; d < n; ++d) {
-                if (d == e) continue;
-                CUDA_CHECK(cudaMemcpyAsync(reinterpret_cast<char*>(bands_[d]->lx[l].stats[par]) + size_t(e) * eb,
-                                           src, eb, cudaMemcpyDefault, s.xs));
-            }
-            CUDA_CHECK(cudaEventRecord(s.sent[l][par], s.xs));
-        }
+    void batch(const std::vector<XItem>& items, int par) override {
+        if (items.empty()) return;
+        Program& s0 = *bands_[0];
+        DeviceGuard g(s0.dev);
+        int lmax = 0;
+        for (const XItem& it : items) lmax = std::max(lmax, it.layer);
+        for (Program* o : bands_) CUDA_CHECK(cudaStreamWaitEvent(s0.xs, o->ready[lmax], 0));
+        const auto& t = table(items, par);
+        copy_chunks(t.first, t.second, s0.xs);
+        for (const XItem& it : items)
+            for (Program* o : bands_) CUDA_CHECK(cudaEventRecord(o->sent[it.layer][par], s0.xs));
     }
 
     void wait(Program& b, int l, int par) override {
-        for (Program* o : bands_) CUDA_CHECK(cudaStreamWaitEvent(b.cs, o->sent[l][par], 0));
+        // every band's sent event of this exchange is recorded at the same point of one stream
+        CUDA_CHECK(cudaStreamWaitEvent(b.cs, bands_[0]->sent[l][par], 0));
     }
 
     void gather_floats(Program&, const float*, float*, size_t) override {
@@ -131,7 +101,55 @@ public:
     }
 
 private:
+    using Table = std::pair<CopyChunk*, int>;
+    const Table& table(const std::vector<XItem>& items, int par) {
+        std::vector<int> key{par};
+        for (const XItem& it : items) key.insert(key.end(), {it.layer, it.kind, int(it.top_only)});
+        auto f = tables_.find(key);
+        if (f != tables_.end()) return f->second;
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        CUDA_CHECK(cudaStreamIsCapturing(bands_[0]->xs, &cap));
+        if (cap != cudaStreamCaptureStatusNone)
+            throw std::logic_error("in-process transport: exchange not announced by prepare()");
+        std::vector<CopyChunk> ch;
+        auto add = [&](const void* src, void* dst, size_t bytes) {
+            for (size_t off = 0; off < bytes; off += kChunk)
+                ch.push_back(CopyChunk{static_cast<const char*>(src) + off, static_cast<char*>(dst) + off,
+                                       (unsigned long long)std::min(kChunk, bytes - off)});
+        };
+        const int n = int(bands_.size());
+        for (const XItem& it : items) {
+            const int l = it.layer;
+            for (int e = 0; e < n; ++e) {
+                Program& s = *bands_[e];
+                if (it.kind == XItem::HALO) {
+                    const size_t rb = s.lx[l].row_bytes;
+                    const char* src = static_cast<const char*>(s.lx[l].send_rows[par]);
+                    if (e + 1 < n)   // my last row is the row above band e+1
+                        add(src + rb, bands_[e + 1]->lx[l].halo_recv[par], rb);
+                    if (e > 0 && !it.top_only)   // my first row is the row below band e-1
+                        add(src, static_cast<char*>(bands_[e - 1]->lx[l].halo_recv[par]) + rb, rb);
+                } else {
+                    const size_t bb = it.kind == XItem::KV ? s.lx[l].band_bytes
+                                                           : size_t(s.lx[l].G) * 2 * sizeof(double);
+                    auto buf = [&](Program& p) -> char* {
+                        return it.kind == XItem::KV ? static_cast<char*>(p.lx[l].kv[par])
+                                                    : reinterpret_cast<char*>(p.lx[l].stats[par]);
+                    };
+                    for (int d = 0; d < n; ++d)
+                        if (d != e) add(buf(s) + size_t(e) * bb, buf(*bands_[d]) + size_t(e) * bb, bb);
+                }
+            }
+        }
+        CopyChunk* dev = nullptr;
+        CUDA_CHECK(cudaMalloc(&dev, std::max<size_t>(ch.size(), 1) * sizeof(CopyChunk)));
+        CUDA_CHECK(cudaMemcpy(dev, ch.data(), ch.size() * sizeof(CopyChunk), cudaMemcpyHostToDevice));
+        return tables_.emplace(key, Table{dev, int(ch.size())}).first->second;
+    }
+
+    static constexpr size_t kChunk = size_t(64) << 10;
     std::vector<Program*> bands_;
+    std::map<std::vector<int>, Table> tables_;
 };
 
 class NcclTransport final : public Transport {
@@ -154,43 +172,48 @@ public:
     }
 
     void halo(int l, int par, bool top_only) override {
+        batch({XItem{l, XItem::HALO, top_only}}, par);
+    }
+    void kv(int l, int par) override { batch({XItem{l, XItem::KV, false}}, par); }
+    void stats(int l, int par) override { batch({XItem{l, XItem::STATS, false}}, par); }
+
+    // Every item of the batch in ONE NCCL group (one kernel on the comm stream): halo rows as
+    // send/recv with the two neighbours, K/V bands and GroupNorm statistics as in-place
+    // all-gathers.
+    void batch(const std::vector<XItem>& items, int par) override {
+        if (items.empty()) return;
         Program& s = *b_;
         DeviceGuard g(s.dev);
-        CUDA_CHECK(cudaStreamWaitEvent(s.xs, s.ready[l], 0));
-        const size_t rb = s.lx[l].row_bytes;
-        char* send = static_cast<char*>(s.lx[l].send_rows[par]);
-        char* recv = static_cast<char*>(s.lx[l].halo_recv[par]);
+        int lmax = 0;
+        for (const XItem& it : items) lmax = std::max(lmax, it.layer);
+        CUDA_CHECK(cudaStreamWaitEvent(s.xs, s.ready[lmax], 0));   // cs order: every item packed
         NCCL_CHECK(ncclGroupStart());
-        if (rank_ > 0) {
-            NCCL_CHECK(ncclRecv(recv, rb, ncclUint8, rank_ - 1, comm_, s.xs));
-            if (!top_only) NCCL_CHECK(ncclSend(send, rb, ncclUint8, rank_ - 1, comm_, s.xs));
-        }
-        if (rank_ + 1 < world_) {
-            NCCL_CHECK(ncclSend(send + rb, rb, ncclUint8, rank_ + 1, comm_, s.xs));
-            if (!top_only) NCCL_CHECK(ncclRecv(recv + rb, rb, ncclUint8, rank_ + 1, comm_, s.xs));
+        for (const XItem& it : items) {
+            const int l = it.layer;
+            if (it.kind == XItem::HALO) {
+                const size_t rb = s.lx[l].row_bytes;
+                char* send = static_cast<char*>(s.lx[l].send_rows[par]);
+                char* recv = static_cast<char*>(s.lx[l].halo_recv[par]);
+                if (rank_ > 0) {
+                    NCCL_CHECK(ncclRecv(recv, rb, ncclUint8, rank_ - 1, comm_, s.xs));
+                    if (!it.top_only) NCCL_CHECK(ncclSend(send, rb, ncclUint8, rank_ - 1, comm_, s.xs));
+                }
+                if (rank_ + 1 < world_) {
+                    NCCL_CHECK(ncclSend(send + rb, rb, ncclUint8, rank_ + 1, comm_, s.xs));
+                    if (!it.top_only) NCCL_CHECK(ncclRecv(recv + rb, rb, ncclUint8, rank_ + 1, comm_, s.xs));
+                }
+            } else if (it.kind == XItem::KV) {
+                const size_t bb = s.lx[l].band_bytes;
+                char* buf = static_cast<char*>(s.lx[l].kv[par]);
+                NCCL_CHECK(ncclAllGather(buf + size_t(rank_) * bb, buf, bb, ncclUint8, comm_, s.xs));
+            } else {
+                const size_t cnt = size_t(s.lx[l].G) * 2;
+                double* buf = s.lx[l].stats[par];
+                NCCL_CHECK(ncclAllGather(buf + size_t(rank_) * cnt, buf, cnt, ncclFloat64, comm_, s.xs));
+            }
         }
         NCCL_CHECK(ncclGroupEnd());
-        CUDA_CHECK(cudaEventRecord(s.sent[l][par], s.xs));
-    }
-
-    void kv(int l, int par) override {
-        Program& s = *b_;
-        DeviceGuard g(s.dev);
-        CUDA_CHECK(cudaStreamWaitEvent(s.xs, s.ready[l], 0));
-        const size_t bb = s.lx[l].band_bytes;
-        char* buf = static_cast<char*>(s.lx[l].kv[par]);
-        NCCL_CHECK(ncclAllGather(buf + size_t(rank_) * bb, buf, bb, ncclUint8, comm_, s.xs));
-        CUDA_CHECK(cudaEventRecord(s.sent[l][par], s.xs));
-    }
-
-    void stats(int l, int par) override {
-        Program& s = *b_;
-        DeviceGuard g(s.dev);
-        CUDA_CHECK(cudaStreamWaitEvent(s.xs, s.ready[l], 0));
-        const size_t cnt = size_t(s.lx[l].G) * 2;
-        double* buf = s.lx[l].stats[par];
-        NCCL_CHECK(ncclAllGather(buf + size_t(rank_) * cnt, buf, cnt, ncclFloat64, comm_, s.xs));
-        CUDA_CHECK(cudaEventRecord(s.sent[l][par], s.xs));
+        for (const XItem& it : items) CUDA_CHECK(cudaEventRecord(s.sent[it.layer][par], s.xs));
     }
 
     void wait(Program& b, int l, int par) override {
