@@ -10,6 +10,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <vector>
 
 namespace {
@@ -198,41 +199,70 @@ PP_API int pp_linear(int dtype, const float* tokens, int n, int t, int in_f, con
 
 PP_API int pp_attention(int dtype, const float* q, const float* k, const float* v, int n, int m,
                         int s, int d, int dv, float scale, float* out) {
-    // attention (proj/src/tensor.cpp:163-199): S = Q K^T (tcgen05), row softmax, O = P V
+    // attention (proj/src/tensor.cpp:163-199) through the product path: S = Q K^T tcgen05
+    // GEMM with the softmax in its epilogue (per key tile row max) -> attn_rescale (row max,
+    // row sum) -> O = P V tcgen05 GEMM (bf16: V MN-major; 1/l in the epilogue)
     return pp::guard([&] {
+        if (m <= 0 || s <= 0 || d <= 0 || dv <= 0)
+            throw std::invalid_argument("attention: empty operand");
         pp::require_device();
         const Elem e = pp::elem_of(dtype);
         const int kel = int(128 / pp::elem_bytes(e));
-        const int sp = round_up(s, std::max(kel, 16));
+        const int dp = round_up(d, kel), dvp = round_up(dv, kel);
+        const int sp = round_up(s, 64);
+        const size_t eb = pp::elem_bytes(e);
         for (int b = 0; b < n; ++b) {
-            const auto Q = to_host(q + size_t(b) * m * d, size_t(m) * d);
-            const auto K = to_host(k + size_t(b) * s * d, size_t(s) * d);
-            std::vector<float> S = gemm_host(e, Q, m, d, K, s, nullptr);
-            // softmax rows on the device (the product kernel), P padded to sp columns
-            DevF32 dS(S.data(), S.size());
-            pp::DeviceScratch dP(size_t(m) * sp * pp::elem_bytes(e) + 16);
-            CUDA_CHECK(cudaMemset(dP.ptr, 0, size_t(m) * sp * pp::elem_bytes(e) + 16));
-            pp::softmax_rows(e, dS.p(), m, s, s, scale, dP.ptr, sp, 0);
-            // V^T [dv][sp] via the device transpose
-            std::vector<float> Vh = to_host(v + size_t(b) * s * dv, size_t(s) * dv);
-            DevElems dV(Vh, e, true);
-            const int ntp = round_up(dv, 16);
-            pp::DeviceScratch dVt(size_t(ntp) * sp * pp::elem_bytes(e) + 16);
-            CUDA_CHECK(cudaMemset(dVt.ptr, 0, size_t(ntp) * sp * pp::elem_bytes(e) + 16));
-            pp::transpose(e, dV.mem.ptr, s, dv, dv, dVt.ptr, sp, 0);
-            DevF32 dO(size_t(m) * dv);
+            // padded row-major copies (zero channels beyond d / dv)
+            std::vector<float> Q(size_t(m) * dp, 0.0f), K(size_t(s) * dp, 0.0f), V(size_t(s) * dvp, 0.0f);
+            for (int i = 0; i < m; ++i)
+                std::memcpy(&Q[size_t(i) * dp], q + (size_t(b) * m + i) * d, size_t(d) * 4);
+            for (int j = 0; j < s; ++j) {
+                std::memcpy(&K[size_t(j) * dp], k + (size_t(b) * s + j) * d, size_t(d) * 4);
+                std::memcpy(&V[size_t(j) * dvp], v + (size_t(b) * s + j) * dv, size_t(dv) * 4);
+            }
+            DevElems dQ(Q, e, true), dK(K, e, true), dV(V, e, true);
+            pp::DeviceScratch dP(size_t(m) * sp * eb + 16);
+            CUDA_CHECK(cudaMemset(dP.ptr, 0, size_t(m) * sp * eb + 16));
+            DevF32 rscale{size_t(m)};
+            DevF32 dO(size_t(m) * dvp);
+            Scratch sc(size_t(8) * m * std::max(sp, dvp) * 4 + 1024);
+            const int sms = pp::device_sm_count();
+            pp::EpilogueSpec es;
+            es.out = dP.ptr;
+            es.out_ld = sp;
+            es.out_f32 = e == Elem::F32;
+            es.round_tf32 = e == Elem::F32;
+            es.n_valid = s;
+            es.sm_rowmax = rscale.p();   // placeholder: marks the softmax epilogue
+            es.sm_scale = scale;
+            es.sm_ld = m;
+            pp::GemmPlan splan, pvplan;
+            pp::plan_gemm(splan, e, dQ.mem.ptr, m, dp, dp, dK.mem.ptr, s, dp, es, sc.sc, sms);
+            DevF32 rowmax{size_t(splan.a.n_tiles) * m};
+            splan.a.sm_rowmax = rowmax.p();
             pp::EpilogueSpec ep;
             ep.out = dO.p();
-            ep.out_ld = dv;
-            ep.n_valid = dv;
+            ep.out_ld = dvp;
+            ep.n_valid = dvp;
             ep.out_f32 = true;
-            Scratch sc(size_t(8) * m * ntp * 4 + 1024);
-            pp::GemmPlan plan;
-            pp::plan_gemm(plan, e, dP.ptr, m, sp, sp, dVt.ptr, dv, sp, ep, sc.sc, pp::device_sm_count());
-            pp::launch_gemm(plan, 0);
+            ep.row_scale = rscale.p();
+            std::unique_ptr<pp::DeviceScratch> dVt;
+            if (e == Elem::BF16) {
+                pp::plan_gemm_bmn(pvplan, e, dP.ptr, m, sp, sp, dV.mem.ptr, s, dvp, dvp, ep, sc.sc, sms);
+            } else {   // TF32: B K-major only, V^T by the transpose kernel
+                dVt.reset(new pp::DeviceScratch(size_t(dvp) * sp * eb + 16));
+                CUDA_CHECK(cudaMemset(dVt->ptr, 0, size_t(dvp) * sp * eb + 16));
+                pp::transpose(e, dV.mem.ptr, s, dvp, dvp, dVt->ptr, sp, 0);
+                pp::plan_gemm(pvplan, e, dP.ptr, m, sp, sp, dVt->ptr, dvp, sp, ep, sc.sc, sms);
+            }
+            pp::launch_gemm(splan, 0);
+            pp::attn_rescale(e, dP.ptr, sp, m, s, rowmax.p(), splan.a.n_tiles, splan.a.block_n, m,
+                             rscale.p(), e == Elem::F32, 0);
+            pp::launch_gemm(pvplan, 0);
             CUDA_CHECK(cudaDeviceSynchronize());
-            const auto o = dO.get(size_t(m) * dv);
-            std::memcpy(out + size_t(b) * m * dv, o.data(), o.size() * 4);
+            const auto o = dO.get(size_t(m) * dvp);
+            for (int i = 0; i < m; ++i)
+                std::memcpy(out + (size_t(b) * m + i) * dv, &o[size_t(i) * dvp], size_t(dv) * 4);
         }
     });
 }

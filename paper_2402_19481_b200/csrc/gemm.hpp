@@ -76,6 +76,18 @@ struct GemmArgs {
     int b_static;             // 1: B is weights (not written by an earlier kernel on the stream):
                               //    its first boxes are prefetched before griddepcontrol.wait
     int debug;                // micro-benchmarks only (compiled out unless -DPP_GEMM_DEBUG)
+    // attention (tensor.cpp:163-199) as two GEMMs around a TMEM-side softmax:
+    //  S GEMM (sm_rowmax != null): the epilogue finds each row's max over the tile's keys in
+    //    TMEM, stores P = exp(S * sm_scale - tile max) (<= 1) and the tile max (log2 units) at
+    //    sm_rowmax[nt * sm_ld + r]; attn_rescale then brings every tile to the row max and
+    //    sums the row;
+    //  PV GEMM (row_scale != null): row r of the accumulator is multiplied by row_scale[r]
+    //    (1 / row sum).
+    float* sm_rowmax;
+    float sm_scale;
+    int sm_ld;
+    const float* row_scale;
+    int b_mn;                 // B operand MN-major: B = [K][N] with N contiguous (V rows)
 };
 
 struct GemmPlan {
@@ -104,6 +116,11 @@ struct EpilogueSpec {
     int gn_groups = 0;
     double* gn_out = nullptr;
     int up_w = 0;             // plain GEMM: > 0 = fused nearest-2x upsample of the output
+    // attention epilogues (GemmArgs::sm_* / row_scale)
+    float* sm_rowmax = nullptr;
+    float sm_scale = 0.0f;
+    int sm_ld = 0;
+    const float* row_scale = nullptr;
 };
 
 // Scratch shared by all GEMMs issued on one stream (they run one after another).
@@ -130,7 +147,16 @@ void plan_gemm(GemmPlan& p, Elem e, const void* A, int M, int K, long long lda, 
                int N, long long ldb, const EpilogueSpec& ep, const GemmScratch& sc, int num_sms,
                int force_splits = 0, int force_block_n = 0, bool b_static = false);
 
+// Attention PV GEMM: D[M][N] = P[M][K] * V[K][N] with V row-major (N contiguous, leading
+// dim ldv): the B operand is staged MN-major by TMA straight from V (no transpose).
+// V has v_rows <= K rows; rows v_rows..K-1 read as zero.
+void plan_gemm_bmn(GemmPlan& p, Elem e, const void* A, int M, int K, long long lda, const void* V,
+                   int v_rows, int N, long long ldv, const EpilogueSpec& ep, const GemmScratch& sc,
+                   int num_sms);
+
 void launch_gemm(const GemmPlan& p, cudaStream_t s);
+
+
 
 int device_sm_count();
 

@@ -91,17 +91,27 @@ constexpr int kMaxSlabSlots = 4;
 
 // Sized by block_n so that the fused-GN variant keeps the same pipeline depth.
 __host__ __device__ inline size_t tail_bytes(int stages, bool gn, int block_n) {
+    // gn: the GroupNorm column-sum scratch [4][block_n][2], also the attention epilogues' row
+    // scratch (>= 3 x 128 floats)
     return size_t(2 * stages + 4 + 2 * kMaxSlabSlots) * 8 + 16 + 16 + size_t(2) * block_n * 4 +
-           (gn ? size_t(4) * block_n * 2 * 4 : 0);
+           (gn ? (block_n >= 48 ? size_t(4) * block_n * 2 * 4 : size_t(384) * 4) : 0);
 }
 
 // B box of one stage: a CTA stages block_n / P weight rows (in a CTA pair each CTA loads its
 // share `rank` of the rows).  bcoord = first weight row of this CTA's share.  kPair:
 // complete_tx on the leader's barrier (shared::cluster address bar_cl), else on the local
 // barrier bar.
-template <bool kPair>
+template <bool kPair, bool kBmn = false>
 __device__ __forceinline__ void load_b(uint8_t* sb, const CUtensorMap* tm, uint64_t* bar,
-                                       uint32_t bar_cl, int bcoord, int kb, const GemmArgs& a) {
+                                       uint32_t bar_cl, int bcoord, int kb, const GemmArgs& a,
+                                       int kel = 0) {
+    if (kBmn) {   // V [K][N] (MN-major): box {kel N, kps * kel K rows, block_n / P / kel chunks}
+        if (kPair)
+            ptx::tma_load_3d_pair(sb, tm, bar_cl, 0, kb * kel, bcoord / kel);
+        else
+            ptx::tma_load_3d(sb, tm, bar, 0, kb * kel, bcoord / kel);
+        return;
+    }
     if (a.slab) {   // K block kb = chunk * 9 + tap; one stage = kps taps
         const int chunk = kb / 9, tap = kb - chunk * 9;
         if (kPair)
@@ -149,15 +159,35 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
                         v[j] = round_tf32(v[j]); v[j + 1] = round_tf32(v[j + 1]);
                         v[j + 2] = round_tf32(v[j + 2]); v[j + 3] = round_tf32(v[j + 3]);
                     }
-                    const float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                    if (srow) {
-                        *reinterpret_cast<float4*>(srow + (c0 + j) * 4) = o;
-                    } else {
-                        *reinterpret_cast<float4*>(dst + j) = o;
+                }
+                if (!srow && (a.out_ld % 8) == 0) {
+                    // two 256-bit stores: whole 32-byte sectors
+#pragma unroll
+                    for (int j = 0; j < 16; j += 8) {
+                        const uint4 lo = make_uint4(__float_as_uint(v[j]), __float_as_uint(v[j + 1]),
+                                                    __float_as_uint(v[j + 2]), __float_as_uint(v[j + 3]));
+                        const uint4 hi = make_uint4(__float_as_uint(v[j + 4]), __float_as_uint(v[j + 5]),
+                                                    __float_as_uint(v[j + 6]), __float_as_uint(v[j + 7]));
+                        ptx::st_global_v8(dst + j, lo, hi);
                         if (a.up_w) {
-                            *reinterpret_cast<float4*>(dst + a.out_ld + j) = o;
-                            *reinterpret_cast<float4*>(dst + up_dy + j) = o;
-                            *reinterpret_cast<float4*>(dst + up_dy + a.out_ld + j) = o;
+                            ptx::st_global_v8(dst + a.out_ld + j, lo, hi);
+                            ptx::st_global_v8(dst + up_dy + j, lo, hi);
+                            ptx::st_global_v8(dst + up_dy + a.out_ld + j, lo, hi);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; j += 4) {
+                        const float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                        if (srow) {
+                            *reinterpret_cast<float4*>(srow + (c0 + j) * 4) = o;
+                        } else {
+                            *reinterpret_cast<float4*>(dst + j) = o;
+                            if (a.up_w) {
+                                *reinterpret_cast<float4*>(dst + a.out_ld + j) = o;
+                                *reinterpret_cast<float4*>(dst + up_dy + j) = o;
+                                *reinterpret_cast<float4*>(dst + up_dy + a.out_ld + j) = o;
+                            }
                         }
                     }
                 }
@@ -186,6 +216,7 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
                 a.residual ? reinterpret_cast<const __nv_bfloat16*>(a.residual) + p * a.res_ld + n0
                            : nullptr;
             if (full && (a.out_ld % 8) == 0 && (!res || (a.res_ld % 8) == 0)) {
+                uint4 o[2];
 #pragma unroll
                 for (int j = 0; j < 16; j += 8) {
                     if (res) {
@@ -198,8 +229,7 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
                             v[j + 2 * i + 1] += f.y;
                         }
                     }
-                    uint4 o;
-                    __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+                    __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o[j / 8]);
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         o2[i] = __floats2bfloat162_rn(v[j + 2 * i], v[j + 2 * i + 1]);
@@ -207,14 +237,26 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
                         v[j + 2 * i] = back.x;
                         v[j + 2 * i + 1] = back.y;
                     }
-                    if (srow) {
-                        *reinterpret_cast<uint4*>(srow + (c0 + j) * 2) = o;
-                    } else {
-                        *reinterpret_cast<uint4*>(dst + j) = o;
+                }
+                if (srow) {
+                    *reinterpret_cast<uint4*>(srow + c0 * 2) = o[0];
+                    *reinterpret_cast<uint4*>(srow + (c0 + 8) * 2) = o[1];
+                } else if (a.out_ld % 16 == 0) {
+                    // one 256-bit store: the whole 32-byte sector of this row chunk
+                    ptx::st_global_v8(dst, o[0], o[1]);
+                    if (a.up_w) {
+                        ptx::st_global_v8(dst + a.out_ld, o[0], o[1]);
+                        ptx::st_global_v8(dst + up_dy, o[0], o[1]);
+                        ptx::st_global_v8(dst + up_dy + a.out_ld, o[0], o[1]);
+                    }
+                } else {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        *reinterpret_cast<uint4*>(dst + 8 * h) = o[h];
                         if (a.up_w) {
-                            *reinterpret_cast<uint4*>(dst + a.out_ld + j) = o;
-                            *reinterpret_cast<uint4*>(dst + up_dy + j) = o;
-                            *reinterpret_cast<uint4*>(dst + up_dy + a.out_ld + j) = o;
+                            *reinterpret_cast<uint4*>(dst + a.out_ld + 8 * h) = o[h];
+                            *reinterpret_cast<uint4*>(dst + up_dy + 8 * h) = o[h];
+                            *reinterpret_cast<uint4*>(dst + up_dy + a.out_ld + 8 * h) = o[h];
                         }
                     }
                 }
@@ -279,15 +321,68 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
     }
 }
 
-// kPair: CTA-pair (cta_group::2) variant, launched as clusters of 2.  The pair computes a
-// 256 x block_n tile: each CTA stages its own 128 A rows and half of the B rows, the leader
-// (rank 0) issues M=256 MMAs that read both CTAs' smem, and each CTA's TMEM receives its
-// own 128 rows, so the epilogue is unchanged.  Per SM this halves the B bytes staged and
-// read per MMA (the single-CTA kernel is shared-memory-bandwidth bound at block_n <= 256).
-template <bool kTF32, bool kPair>
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Attention S-GEMM epilogue (softmax in the epilogue, proj/src/tensor.cpp:163-199): one
+// 16-column chunk of row p of S = Q K^T -> P = 2^(S * sl2 - shift) with shift = the row's
+// max over the tile (so P <= 1), stored in the P element type (keys >= n_valid: not stored,
+// the P buffer's padding columns stay zero).
+template <bool kTF32>
+__device__ __forceinline__ void softmax_chunk(const GemmArgs& a, float* v, int n0, long long p,
+                                              bool valid, float sl2, float shift) {
+    if (!valid) return;
+    const bool full = n0 + 16 <= a.n_valid;
+    if (kTF32 || a.out_f32) {
+        float* dst = reinterpret_cast<float*>(a.out) + p * a.out_ld + n0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            v[j] = ex2_approx(fmaf(v[j], sl2, -shift));
+            if (a.round_tf32) v[j] = round_tf32(v[j]);
+        }
+        if (full && (a.out_ld % 8) == 0) {
+#pragma unroll
+            for (int j = 0; j < 16; j += 8) {
+                uint4 lo, hi;
+                lo = make_uint4(__float_as_uint(v[j]), __float_as_uint(v[j + 1]),
+                                __float_as_uint(v[j + 2]), __float_as_uint(v[j + 3]));
+                hi = make_uint4(__float_as_uint(v[j + 4]), __float_as_uint(v[j + 5]),
+                                __float_as_uint(v[j + 6]), __float_as_uint(v[j + 7]));
+                ptx::st_global_v8(dst + j, lo, hi);
+            }
+        } else {
+            for (int j = 0; j < 16; ++j)
+                if (n0 + j < a.n_valid) dst[j] = v[j];
+        }
+    } else {
+        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(a.out) + p * a.out_ld + n0;
+        uint4 o[2];
+        __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(o);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            o2[i] = __floats2bfloat162_rn(ex2_approx(fmaf(v[2 * i], sl2, -shift)),
+                                          ex2_approx(fmaf(v[2 * i + 1], sl2, -shift)));
+        if (full && (a.out_ld % 16) == 0) {
+            ptx::st_global_v8(dst, o[0], o[1]);
+        } else {
+            const __nv_bfloat16* ob = reinterpret_cast<const __nv_bfloat16*>(o);
+            for (int j = 0; j < 16; ++j)
+                if (n0 + j < a.n_valid) dst[j] = ob[j];
+        }
+    }
+}
+
+// kAttn: 0 = conv / linear (no attention code compiled in), 1 = attention S GEMM (softmax
+// epilogue), 2 = attention PV GEMM (1/l row scale; bf16: B operand MN-major, i.e. V [keys][d]
+// as staged by TMA, no transpose).
+template <bool kTF32, bool kPair, int kAttn>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmD, const GemmArgs a) {
+    constexpr bool kBmn = kAttn == 2 && !kTF32;
     constexpr int P = kPair ? 2 : 1;   // CTAs per cluster
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte aligned base derived from smem_raw by pointer arithmetic (not an integer
@@ -397,8 +492,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (rank == 0)
                         ptx::mbar_arrive_expect_tx(&st.full_bar[i],
                                                    P * (nk * a_box_bytes + b_stage_bytes));
-                    load_b<kPair>(sb, &tmB, &st.full_bar[i], full_leader + uint32_t(i) * 8u, bcoord,
-                                  kb0 + i * kps, a);
+                    load_b<kPair, kBmn>(sb, &tmB, &st.full_bar[i], full_leader + uint32_t(i) * 8u,
+                                        bcoord, kb0 + i * kps, a, kel);
                 }
                 __syncwarp();
             }
@@ -500,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 }
                             }
                             if (!b_done) {
-                                load_b<kPair>(sb, &tmB, &st.full_bar[stage], fb, bcoord, kb, a);
+                                load_b<kPair, kBmn>(sb, &tmB, &st.full_bar[stage], fb, bcoord, kb, a, kel);
                             }
                         }
                     }
@@ -533,10 +628,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         // 16-element bf16 / 8-element tf32 step).
         const uint32_t smem0 = ptx::smem_u32(ring);
         const uint64_t desc_a0 = ptx::smem_desc_sw128(smem0);
-        const uint64_t desc_b0 = ptx::smem_desc_sw128(smem0 + a_stage_bytes);
+        // kBmn: each 128-byte N chunk of a stage's B box holds kps * kel K rows (LBO apart)
+        constexpr int kelB = kTF32 ? 32 : 64;
+        const uint64_t desc_b0 =
+            kBmn ? ptx::smem_desc_sw128_mn(smem0 + a_stage_bytes, uint32_t(kps * kelB * kBlockBytes))
+                 : ptx::smem_desc_sw128(smem0 + a_stage_bytes);
         const uint32_t slab0 = ptx::smem_u32(smem);   // slab mode: slot s at slab0 + s * slab_bytes
         const uint64_t desc_stride = stage_bytes >> 4;
-        const uint64_t a_next = a_slot >> 4, b_next = b_slot >> 4;
+        const uint64_t a_next = a_slot >> 4;
+        const uint64_t b_next = kBmn ? uint64_t(kelB * kBlockBytes) >> 4 : b_slot >> 4;
         // loop-invariant launch parameters, read once (the issue loop is on the critical path)
         const bool do_mma = !(dbg & 1);
         const bool slab = a.slab != 0;
@@ -622,7 +722,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (ptx::elect_one()) {
                     if (do_mma) {
                         const uint32_t acc0 = kb > kb0 ? 1u : 0u;
-                        if (kPair) {
+                        if (kPair && kBmn) {
+                            ptx::mma4_bf16_pair_bmn(d_tmem, da, db, idesc, acc0);
+                            if (two) ptx::mma4_bf16_pair_bmn(d_tmem, da + a_next, db + b_next, idesc, 1u);
+                        } else if (kPair) {
                             if (kTF32) {
                                 ptx::mma4_tf32_pair(d_tmem, da, db, idesc, acc0);
                                 if (two) ptx::mma4_tf32_pair(d_tmem, da + a_next, db + b_next, idesc, 1u);
@@ -630,6 +733,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 ptx::mma4_bf16_pair(d_tmem, da, db, idesc, acc0);
                                 if (two) ptx::mma4_bf16_pair(d_tmem, da + a_next, db + b_next, idesc, 1u);
                             }
+                        } else if (kBmn) {
+                            ptx::mma4_bf16_bmn(d_tmem, da, db, idesc, acc0);
+                            if (two) ptx::mma4_bf16_bmn(d_tmem, da + a_next, db + b_next, idesc, 1u);
                         } else {
                             if (kTF32) {
                                 ptx::mma4_tf32(d_tmem, da, db, idesc, acc0);
@@ -686,6 +792,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         int acc = 0;
         uint32_t acc_phase = 0;
+        // attention epilogues read what the previous kernel wrote (row norms, partial row
+        // sums) ahead of the accumulator: wait for it here (the loads then overlap the MMAs)
+        constexpr bool softmax = kAttn == 1;
+        constexpr bool pv = kAttn == 2;
+        if (pv) pdl_wait();   // row_scale comes from the previous kernel
+        const float sl2 = a.sm_scale * 1.4426950408889634f;   // scale * log2(e)
+        float* const s_row = st.gn;   // softmax: [3][128] partial row maxima
         for (int t = tile0; t < total_tiles; t += tile_step) {
             const int cur = acc;
             const uint32_t cur_phase = acc_phase;
@@ -717,6 +830,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint8_t* srow = stage_out ? smem + size_t(r) * a.block_n * eb_out : nullptr;
             for (int c = et; c < a.block_n; c += kEpiThreads)
                 sbias[c] = (a.bias && nbase + c < a.n_valid) ? a.bias[nbase + c] : 0.0f;
+            const float rinv = (pv && valid) ? __ldg(a.row_scale + p) : 1.0f;
             ptx::mbar_wait(&st.tfull_bar[cur], cur_phase);
             ptx::tc_fence_after();
             if ((dbg & 4) || (kPair && m_tile >= m_tiles)) {
@@ -726,6 +840,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             epi_bar();
             const uint32_t t_row = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(cur * 256);
+
             if (a.splits > 1) {
                 // 2-way split-K.  The split that finishes its main loop first publishes its
                 // fp32 partial tile; the second adds it to its own TMEM accumulator.  fp32
@@ -775,6 +890,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int j = 0; j < 16; ++j) v[j] = v[j] + o[j];
                     }
+                    if (pv) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) v[j] *= rinv;
+                    }
                     finish_chunk<kTF32>(a, v, sbias, c0, nbase + c0, p, valid, sgn_warp, lane, srow);
                 }
                 release(cur);
@@ -782,14 +901,70 @@ __global__ void __launch_bounds__(kThreads, 1)
                     *ticket = 0u;
                     *ready = 0u;
                 }
+            } else if (softmax) {
+                // pass 1: the row's max over this tile's keys (three chunk-interleaved warps
+                // per row, combined through smem); pass 2: P = 2^(S sl2 - max) <= 1.  Two
+                // TMEM loads in flight per wait.
+                const bool full_tile = nbase + a.block_n <= a.n_valid;
+                float mx = -INFINITY;
+                for (int c0 = half * 16; c0 < a.block_n; c0 += 2 * kCS) {
+                    float v0[16], v1[16];
+                    const bool two = c0 + kCS < a.block_n;
+                    ptx::tmem_ld16_nowait(t_row + c0, v0);
+                    if (two) ptx::tmem_ld16_nowait(t_row + c0 + kCS, v1);
+                    ptx::tmem_wait_ld();
+                    ptx::tmem_pin16(v0);
+                    if (two) ptx::tmem_pin16(v1);
+                    if (full_tile) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) mx = fmaxf(mx, v0[j]);
+                        if (two) {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) mx = fmaxf(mx, v1[j]);
+                        }
+                    } else {
+                        const int n0 = nbase + c0;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (n0 + j < a.n_valid) mx = fmaxf(mx, v0[j]);
+                        if (two) {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j)
+                                if (n0 + kCS + j < a.n_valid) mx = fmaxf(mx, v1[j]);
+                        }
+                    }
+                }
+                s_row[half * kTileM + r] = mx;
+                epi_bar();
+                mx = fmaxf(fmaxf(s_row[r], s_row[kTileM + r]), s_row[2 * kTileM + r]);
+                const float shift = mx * sl2;
+                for (int c0 = half * 16; c0 < a.block_n; c0 += 2 * kCS) {
+                    float v0[16], v1[16];
+                    const bool two = c0 + kCS < a.block_n;
+                    ptx::tmem_ld16_nowait(t_row + c0, v0);
+                    if (two) ptx::tmem_ld16_nowait(t_row + c0 + kCS, v1);
+                    ptx::tmem_wait_ld();
+                    ptx::tmem_pin16(v0);
+                    if (two) ptx::tmem_pin16(v1);
+                    softmax_chunk<kTF32>(a, v0, nbase + c0, p, valid, sl2, shift);
+                    if (two) softmax_chunk<kTF32>(a, v1, nbase + c0 + kCS, p, valid, sl2, shift);
+                }
+                release(cur);
+                if (half == 0 && valid) a.sm_rowmax[size_t(tc.nt) * a.sm_ld + p] = shift;
+                epi_bar();   // s_row is rewritten by the next tile
             } else {
                 for (int c0 = half * 16; c0 < a.block_n; c0 += kCS) {
                     float v[16];
                     ptx::tmem_ld16(t_row + c0, v);
+                    if (pv) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) v[j] *= rinv;
+                    }
                     finish_chunk<kTF32>(a, v, sbias, c0, nbase + c0, p, valid, sgn_warp, lane, srow);
                 }
                 release(cur);
             }
+
             if (stage_out) {
                 ptx::fence_proxy_async();   // staged rows -> visible to the TMA engine
                 epi_bar();
@@ -961,6 +1136,7 @@ void plan_output_map(GemmPlan& p, bool conv) {
     a.tma_store = 0;
     if ((uint64_t(a.out_ld) * eb) % 16 || (reinterpret_cast<uintptr_t>(a.out) % 16)) return;
     if (a.up_w) return;            // fused upsample: four row stores per output row
+    if (a.sm_rowmax) return;       // softmax epilogue: P rows stored directly
     if (conv) {
         uint64_t d[3] = {uint64_t(a.n_valid), uint64_t(a.out_w), uint64_t(a.out_rows)};
         uint64_t st[2] = {uint64_t(a.out_ld) * eb, uint64_t(a.out_w) * a.out_ld * eb};
@@ -975,8 +1151,9 @@ void plan_output_map(GemmPlan& p, bool conv) {
     a.tma_store = 1;
 }
 
-uint32_t make_idesc(Elem e, int n, int m) {
+uint32_t make_idesc(Elem e, int n, int m, bool b_mn = false) {
     uint32_t d = 0;
+    if (b_mn) d |= 1u << 16;                         // B MN-major
     d |= 1u << 4;                                    // D format f32
     const uint32_t fmt = e == Elem::BF16 ? 1u : 2u;  // BF16 / TF32
     d |= fmt << 7;                                   // A format
@@ -1022,7 +1199,8 @@ double tile_eff(int pair, int bn) {
 // over SM pairs); split-K pays a partial write + read.
 //   force_splits: bits 0-3 = splits (0 auto), bit 4 = force pair, bit 5 = force single CTA
 void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int gn_cpg, int force_splits,
-                   int force_block_n, int& block_n, int& splits, int& pair, bool gemm = false) {
+                   int force_block_n, int& block_n, int& splits, int& pair, bool gemm = false,
+                   int bn_mult = 16) {
     double best = 1e300;
     block_n = 16;
     splits = 1;
@@ -1037,7 +1215,7 @@ void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int gn_cpg
         const int units = (m_tiles + P - 1) / P;
         for (int bn = 256; bn >= 16; bn -= 16) {
             if (force_block_n && bn != force_block_n) continue;
-            if (n_pad % bn) continue;
+            if (n_pad % bn || bn % (bn_mult * (bn_mult > 16 ? P : 1))) continue;
             if (gn_cpg && bn % gn_cpg) continue;
             const int nt = n_pad / bn;
             for (int s : {1, 2}) {
@@ -1069,7 +1247,7 @@ void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int gn_cpg
         double lbest = 1e300;
         int lbn = 0;
         for (int bn = 256; bn >= 64; bn -= 16) {   // >= 64: the measured range
-            if (n_pad % bn) continue;
+            if (n_pad % bn || bn % bn_mult) continue;
             const long long tiles = (long long)m_tiles * (n_pad / bn);
             if (tiles > num_sms) continue;
             const double cost = double(k_blocks) * 2.0 * bn + 2500.0;
@@ -1087,11 +1265,13 @@ void choose_tiling(int m_tiles, int n_pad, int k_blocks, int num_sms, int gn_cpg
 }
 
 void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const EpilogueSpec& ep,
-                 const GemmScratch& sc, int num_sms, int force_splits, int force_block_n) {
+                 const GemmScratch& sc, int num_sms, int force_splits, int force_block_n,
+                 bool b_mn = false) {
     GemmArgs& a = p.a;
-    const bool gn = ep.gn_groups > 0;
+    // the attention epilogues use the GroupNorm scratch region for their row values
+    const bool gn = ep.gn_groups > 0 || ep.sm_rowmax;
     int cpg = 0;
-    if (gn) {
+    if (ep.gn_groups > 0) {
         if (ep.n_valid % ep.gn_groups)
             throw std::invalid_argument("GroupNorm statistics: channels not divisible by groups");
         cpg = ep.n_valid / ep.gn_groups;
@@ -1100,9 +1280,16 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
     }
     int bn, splits, pair;
     if (force_block_n > 256) throw std::invalid_argument("GEMM: block_n must be <= 256");
+    // MN-major B: whole 128-byte N chunks per tile, single CTA; softmax epilogue: whole K per
+    // tile (no split-K)
+    // (a CTA pair stages block_n / 2 columns per CTA: block_n a multiple of two chunks)
+    const int bn_mult = b_mn ? int(kBlockBytes / elem_bytes(p.elem)) : 16;
+    if (b_mn && p.elem != Elem::BF16) throw std::invalid_argument("GEMM: MN-major B is bf16 only");
     choose_tiling(m_tiles, n_pad, k_blocks, num_sms, cpg, force_splits, force_block_n, bn, splits,
-                  pair, a.mode == 0);
-    if (gn && bn % cpg) throw std::invalid_argument("GroupNorm statistics: block_n not group aligned");
+                  pair, a.mode == 0, bn_mult);
+    if (ep.sm_rowmax) splits = 1;
+    if (bn % bn_mult) throw std::invalid_argument("GEMM: block_n must be a multiple of the B chunk");
+    if (cpg && bn % cpg) throw std::invalid_argument("GroupNorm statistics: block_n not group aligned");
     if (pair && bn % 16) throw std::invalid_argument("CTA-pair GEMM: block_n % 16 != 0");
     p.pair = pair;
     a.block_n = bn;
@@ -1137,7 +1324,12 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
             break;
         }
     }
-    a.idesc = make_idesc(p.elem, bn, pair ? 2 * kTileM : kTileM);
+    a.idesc = make_idesc(p.elem, bn, pair ? 2 * kTileM : kTileM, b_mn);
+    a.b_mn = b_mn ? 1 : 0;
+    a.sm_rowmax = ep.sm_rowmax;
+    a.sm_scale = ep.sm_scale;
+    a.sm_ld = ep.sm_ld;
+    a.row_scale = ep.row_scale;
     a.out = ep.out;
     a.out_ld = ep.out_ld;
     a.n_valid = ep.n_valid;
@@ -1149,7 +1341,7 @@ void finish_plan(GemmPlan& p, int m_tiles, int n_pad, int k_blocks, const Epilog
     a.scale = ep.scale;
     a.partial = a.splits > 1 ? sc.ws : nullptr;
     a.tile_ticket = sc.tickets;
-    if (gn) {
+    if (ep.gn_groups > 0) {
         if (size_t(m_tiles) * ep.gn_groups * 2 > sc.gn_part_len || !sc.gn_ticket)
             throw std::invalid_argument("GroupNorm statistics scratch too small");
         a.gn_groups = ep.gn_groups;
@@ -1286,7 +1478,44 @@ void plan_gemm(GemmPlan& p, Elem e, const void* A, int M, int K, long long lda, 
     a.b_bytes = b_static ? ((long long)(N - 1) * ldb + K) * (long long)eb / 16 * 16 : 0;
 }
 
-template <bool kTF32, bool kPair>
+void plan_gemm_bmn(GemmPlan& p, Elem e, const void* A, int M, int K, long long lda, const void* V,
+                   int v_rows, int N, long long ldv, const EpilogueSpec& ep, const GemmScratch& sc,
+                   int num_sms) {
+    std::memset(&p, 0, sizeof(p));
+    p.elem = e;
+    const size_t eb = elem_bytes(e);
+    const int kel = int(kBlockBytes / eb);
+    if (K % kel) throw std::invalid_argument("plan_gemm_bmn: K must fill 128-byte blocks");
+    if (N % kel) throw std::invalid_argument("plan_gemm_bmn: N must fill 128-byte chunks");
+    if (v_rows > K) throw std::invalid_argument("plan_gemm_bmn: more V rows than K");
+    GemmArgs& a = p.a;
+    a.mode = 0;
+    a.tiles_y = (M + kTileM - 1) / kTileM;
+    a.tiles_x = 1;
+    a.out_rows = M;
+    a.out_w = 1;
+    a.rows_box = kTileM;
+    a.w_box = 1;
+    a.cin_chunks = K / kel;
+    a.m_pix = M;
+    uint64_t ad[2] = {uint64_t(K), uint64_t(M)};
+    uint64_t as[1] = {uint64_t(lda) * eb};
+    uint32_t ab[2] = {uint32_t(kel), uint32_t(kTileM)};
+    encode(&p.tmA, e, 2, A, ad, as, ab);
+    finish_plan(p, a.tiles_y, N, K / kel, ep, sc, num_sms, 0, 0, /*b_mn=*/true);
+    // V [v_rows <= K][N] (row stride ldv) as {kel, K, N / kel}: a box {kel, kps * kel, block_n / kel}
+    // lands as block_n / kel consecutive [kps * kel rows][128 B] swizzled N chunks; rows >= K
+    // (the keys' padding) are zero-filled
+    uint64_t d[3] = {uint64_t(kel), uint64_t(v_rows), uint64_t(N / kel)};
+    uint64_t st[2] = {uint64_t(ldv) * eb, uint64_t(kBlockBytes)};
+    uint32_t b[3] = {uint32_t(kel), uint32_t(a.kps * kel), uint32_t(a.block_n / (p.pair ? 2 : 1) / kel)};
+    encode(&p.tmB, e, 3, V, d, st, b);
+    p.flops = 2.0 * double(M) * N * K;
+    a.b_static = 0;
+    plan_output_map(p, false);
+}
+
+template <bool kTF32, bool kPair, int kAttn = 0>
 void launch_variant(const GemmPlan& p, cudaStream_t s) {
     // the dynamic-smem attribute is per device: remember which devices have it
     static std::mutex mu;
@@ -1296,16 +1525,40 @@ void launch_variant(const GemmPlan& p, cudaStream_t s) {
     {
         std::lock_guard<std::mutex> lk(mu);
         if (!(done >> dev & 1ull)) {
-            CUDA_CHECK(cudaFuncSetAttribute(gemm_kernel<kTF32, kPair>,
+            CUDA_CHECK(cudaFuncSetAttribute(gemm_kernel<kTF32, kPair, kAttn>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
             done |= 1ull << dev;
         }
     }
-    launch_pdl(gemm_kernel<kTF32, kPair>, dim3(p.grid), dim3(kThreads), p.smem, s, kPair ? 2 : 1,
+    launch_pdl(gemm_kernel<kTF32, kPair, kAttn>, dim3(p.grid), dim3(kThreads), p.smem, s, kPair ? 2 : 1,
                p.tmA, p.tmB, p.tmD, p.a);
 }
 
 void launch_gemm(const GemmPlan& p, cudaStream_t s) {
+    const int attn = p.a.sm_rowmax ? 1 : p.a.row_scale ? 2 : 0;
+    if (p.a.b_mn && (attn != 2 || p.elem != Elem::BF16))
+        throw std::logic_error("GEMM: MN-major B is the bf16 attention PV GEMM only");
+    if (attn == 1) {
+        if (p.elem == Elem::F32) {
+            if (p.pair) launch_variant<true, true, 1>(p, s);
+            else launch_variant<true, false, 1>(p, s);
+        } else {
+            if (p.pair) launch_variant<false, true, 1>(p, s);
+            else launch_variant<false, false, 1>(p, s);
+        }
+        return;
+    }
+    if (attn == 2) {
+        if (p.elem == Elem::F32) {
+            if (p.pair) launch_variant<true, true, 2>(p, s);
+            else launch_variant<true, false, 2>(p, s);
+        } else {
+            if (!p.a.b_mn) throw std::logic_error("GEMM: bf16 attention PV GEMM reads V MN-major");
+            if (p.pair) launch_variant<false, true, 2>(p, s);
+            else launch_variant<false, false, 2>(p, s);
+        }
+        return;
+    }
     if (p.elem == Elem::F32) {
         if (p.pair) launch_variant<true, true>(p, s);
         else launch_variant<true, false>(p, s);

@@ -538,117 +538,6 @@ __global__ void upsample_kernel(const T* __restrict__ x, T* __restrict__ y, int 
 }
 
 // ---------------------------------------------------------------- attention helpers
-template <class T>
-__global__ void softmax_kernel(const float* __restrict__ S, int ns, long long lds, float scale,
-                               T* __restrict__ P, long long ldp) {
-    pdl_wait();
-    pdl_trigger();
-    const int row = blockIdx.x;
-    const float* s = S + (long long)row * lds;
-    __shared__ float red[32];
-    float mx = -INFINITY;
-    for (int j = threadIdx.x; j < ns; j += blockDim.x) mx = fmaxf(mx, s[j] * scale);
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : -INFINITY;
-        for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-        if (threadIdx.x == 0) red[0] = v;
-    }
-    __syncthreads();
-    mx = red[0];
-    __syncthreads();
-    float sum = 0.0f;
-    for (int j = threadIdx.x; j < ns; j += blockDim.x) sum += expf(s[j] * scale - mx);
-    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (threadIdx.x == 0) red[0] = v;
-    }
-    __syncthreads();
-    const float inv = 1.0f / red[0];
-    T* pr = P + (long long)row * ldp;
-    for (int j = threadIdx.x; j < ns; j += blockDim.x)
-        pr[j] = from_float<T>(expf(s[j] * scale - mx) * inv, true);
-}
-
-// Row softmax with the row held in registers: one read of S (float4, streaming) instead of
-// three, NV float4 per thread, 256 threads per row; same per-element formula as
-// softmax_kernel (expf(s * scale - max) * (1 / sum)).  Needs ns, lds, ldp % 4 == 0.
-template <int NV>
-__device__ __forceinline__ float block_reduce_256(float v, bool is_max, float* red) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        const float w = __shfl_xor_sync(0xffffffffu, v, o);
-        v = is_max ? fmaxf(v, w) : v + w;
-    }
-    __syncthreads();   // red may still be read from the previous reduction
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    v = red[0];
-#pragma unroll
-    for (int w = 1; w < 8; ++w) v = is_max ? fmaxf(v, red[w]) : v + red[w];
-    return v;
-}
-
-template <class T, int NV>
-__global__ void __launch_bounds__(256) softmax_reg_kernel(const float* __restrict__ S, int ns,
-                                                          long long lds, float scale,
-                                                          T* __restrict__ P, long long ldp) {
-    pdl_wait();
-    pdl_trigger();
-    __shared__ float red[8];
-    const int row = blockIdx.x;
-    const int n4 = ns >> 2;
-    const float4* s4 = reinterpret_cast<const float4*>(S + (long long)row * lds);
-    float4 v[NV];
-    float mx = -INFINITY;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        const int j = threadIdx.x + i * 256;
-        if (j < n4) {
-            v[i] = __ldcs(s4 + j);
-            v[i].x *= scale;
-            v[i].y *= scale;
-            v[i].z *= scale;
-            v[i].w *= scale;
-            mx = fmaxf(mx, fmaxf(fmaxf(v[i].x, v[i].y), fmaxf(v[i].z, v[i].w)));
-        }
-    }
-    mx = block_reduce_256<NV>(mx, true, red);
-    float sum = 0.0f;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        if (threadIdx.x + i * 256 < n4) {
-            v[i].x = expf(v[i].x - mx);
-            v[i].y = expf(v[i].y - mx);
-            v[i].z = expf(v[i].z - mx);
-            v[i].w = expf(v[i].w - mx);
-            sum += (v[i].x + v[i].y) + (v[i].z + v[i].w);
-        }
-    }
-    sum = block_reduce_256<NV>(sum, false, red);
-    const float inv = 1.0f / sum;
-    T* pr = P + (long long)row * ldp;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        const int j = threadIdx.x + i * 256;
-        if (j < n4) {
-            const T a = from_float<T>(v[i].x * inv, true), b = from_float<T>(v[i].y * inv, true);
-            const T c = from_float<T>(v[i].z * inv, true), d = from_float<T>(v[i].w * inv, true);
-            if constexpr (sizeof(T) == 2) {
-                __align__(8) T q[4] = {a, b, c, d};
-                *reinterpret_cast<uint2*>(pr + 4 * j) = *reinterpret_cast<const uint2*>(q);
-            } else {
-                *reinterpret_cast<float4*>(pr + 4 * j) = make_float4(a, b, c, d);
-            }
-        }
-    }
-}
 
 template <class T>
 __global__ void transpose_kernel(const T* __restrict__ V, int ns, int C, long long ldv,
@@ -825,6 +714,74 @@ __global__ void elem_to_f32_kernel(const T* __restrict__ s, float* __restrict__ 
         d[i] = to_float(s[i]);
 }
 
+
+// ---------------------------------------------------------------- attention (tcgen05 path)
+// attention (proj/src/tensor.cpp:163-199) runs as S GEMM -> P with the softmax in the GEMM
+// epilogue (P = exp(S scale - tile max) from the TMEM accumulator, tile max per row and key
+// tile) -> attn_rescale -> PV GEMM with 1/l in its epilogue (V read MN-major in bf16).
+// attn_rescale, one warp per query row: m = max over the key tiles' maxima, P of tile t *=
+// 2^(max_t - m) (the tile holding the row max is left as is), l = sum of the row's stored P
+// (what the PV GEMM multiplies; lanes sum fixed column residues, then a fixed xor tree ->
+// deterministic) -> row_scale = 1 / l.
+template <class T>
+__global__ void __launch_bounds__(256) attn_rescale_kernel(T* __restrict__ P, long long ldp, int m,
+                                                           int s, const float* __restrict__ rowmax,
+                                                           int n_tiles, int block_n, int ld_rm,
+                                                           float* __restrict__ row_scale,
+                                                           int round_tf32) {
+    constexpr int VEC = Vec<T>::N;
+    extern __shared__ float s_alpha[];   // [8 warps][n_tiles]
+    pdl_wait();
+    pdl_trigger();
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int r = blockIdx.x * 8 + wib;
+    if (r >= m) return;
+    float* alpha = s_alpha + wib * n_tiles;
+    float mx = -INFINITY;
+    for (int t = lane; t < n_tiles; t += 32) mx = fmaxf(mx, rowmax[(long long)t * ld_rm + r]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int t = lane; t < n_tiles; t += 32) {
+        const float d = rowmax[(long long)t * ld_rm + r] - mx;
+        float a;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(a) : "f"(d));
+        alpha[t] = d == 0.0f ? 1.0f : a;
+    }
+    __syncwarp();
+    T* row = P + (long long)r * ldp;
+    const int nv = (s + VEC - 1) / VEC;   // vectors holding keys (the padding stays zero)
+    float sum = 0.0f;
+    for (int v0 = lane; v0 < nv; v0 += 32 * 4) {
+        uint4 raw[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int v = v0 + u * 32;
+            if (v < nv) raw[u] = *reinterpret_cast<const uint4*>(row + (long long)v * VEC);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int v = v0 + u * 32;
+            if (v >= nv) continue;
+            const float a = alpha[(v * VEC) / block_n];
+            float f[VEC];
+            load_vec<T>(reinterpret_cast<const T*>(&raw[u]), f);
+            if (a != 1.0f) {
+#pragma unroll
+                for (int i = 0; i < VEC; ++i) f[i] *= a;
+                uint4 o;
+                store_vec<T>(reinterpret_cast<T*>(&o), f, round_tf32 != 0);
+                *reinterpret_cast<uint4*>(row + (long long)v * VEC) = o;
+                load_vec<T>(reinterpret_cast<const T*>(&o), f);   // the stored values
+            }
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) sum += f[i];
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) row_scale[r] = 1.0f / sum;
+}
+
 #define DISPATCH(e, ...)                          \
     do {                                          \
         if ((e) == Elem::BF16) {                  \
@@ -967,33 +924,24 @@ void upsample2x(Elem e, const void* x, void* y, int rows, int W, int ld, cudaStr
     CUDA_CHECK(cudaGetLastError());
 }
 
-void softmax_rows(Elem e, const float* S, int m, int ns, long long lds, float scale, void* P,
-                  long long ldp, cudaStream_t s) {
-    const bool vec = ns % 4 == 0 && lds % 4 == 0 && ldp % 4 == 0 && ns <= 16 * 1024 &&
-                     reinterpret_cast<uintptr_t>(S) % 16 == 0 && reinterpret_cast<uintptr_t>(P) % 16 == 0;
-    if (vec) {
-        const int per = (ns / 4 + 255) / 256;   // float4 per thread
-#define PP_SOFTMAX_REG(NV)                                                                          \
-    DISPATCH(e, launch_pdl(softmax_reg_kernel<T, NV>, dim3(m), dim3(256), 0, s, 1, S, ns, lds, scale, \
-                           static_cast<T*>(P), ldp))
-        if (per <= 1) PP_SOFTMAX_REG(1);
-        else if (per <= 2) PP_SOFTMAX_REG(2);
-        else if (per <= 4) PP_SOFTMAX_REG(4);
-        else if (per <= 8) PP_SOFTMAX_REG(8);
-        else PP_SOFTMAX_REG(16);
-#undef PP_SOFTMAX_REG
-    } else {
-        DISPATCH(e, launch_pdl(softmax_kernel<T>, dim3(m), dim3(256), 0, s, 1, S, ns, lds, scale,
-                               static_cast<T*>(P), ldp));
-    }
-    CUDA_CHECK(cudaGetLastError());
-}
 
 void transpose(Elem e, const void* V, int ns, int C, long long ldv, void* Vt, long long ldt,
                cudaStream_t s) {
     dim3 grid((ns + 31) / 32, (C + 31) / 32), block(32, 8);
     DISPATCH(e, launch_pdl(transpose_kernel<T>, dim3(grid), dim3(block), 0, s, 1, static_cast<const T*>(V), ns, C, ldv,
                                                           static_cast<T*>(Vt), ldt));
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void attn_rescale(Elem e, void* P, long long ldp, int m, int s, const float* rowmax, int n_tiles,
+                  int block_n, int ld_rm, float* row_scale, bool round_tf32, cudaStream_t st) {
+    const int VEC = e == Elem::BF16 ? 8 : 4;
+    if (block_n % VEC || ldp % VEC)
+        throw std::invalid_argument("attention: P tiles must hold whole 16-byte vectors");
+    const size_t smem = size_t(8) * n_tiles * sizeof(float);
+    DISPATCH(e, launch_pdl(attn_rescale_kernel<T>, dim3((m + 7) / 8), dim3(256), smem, st, 1,
+                           static_cast<T*>(P), ldp, m, s, rowmax, n_tiles, block_n, ld_rm,
+                           row_scale, round_tf32 ? 1 : 0));
     CUDA_CHECK(cudaGetLastError());
 }
 

@@ -65,10 +65,12 @@ void add_channel(Elem e, const void* x, const float* vec, const void* skip, void
 void upsample2x(Elem e, const void* x, void* y, int rows, int W, int ld, cudaStream_t s);
 
 // ---- attention helpers (proj/src/tensor.cpp:163-199) -------------------------------------
-// P[i][j] = softmax_j(S[i][j] * scale) written as T with row stride ldp (cols >= S zeroed).
-void softmax_rows(Elem e, const float* S, int m, int ns, long long lds, float scale, void* P,
-                  long long ldp, cudaStream_t s);
-// Vt[c][j] = V[j][c] for j < ns (ld of V = ldv, ld of Vt = ldt)
+// Attention between the two tcgen05 GEMMs (gemm.hpp sm_* / row_scale epilogues): P [m][ldp]
+// holds each key tile (block_n keys) scaled by its own row max (rowmax[t * ld_rm + r], log2
+// units); brings every tile to the row max and writes row_scale[r] = 1 / (sum of row r).
+void attn_rescale(Elem e, void* P, long long ldp, int m, int s, const float* rowmax, int n_tiles,
+                  int block_n, int ld_rm, float* row_scale, bool round_tf32, cudaStream_t st);
+// Vt[c][j] = V[j][c] for j < ns (ld of V = ldv, ld of Vt = ldt): the TF32 PV GEMM's B operand
 void transpose(Elem e, const void* V, int ns, int C, long long ldv, void* Vt, long long ldt,
                cudaStream_t s);
 

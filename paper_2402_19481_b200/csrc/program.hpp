@@ -94,7 +94,8 @@ struct Program {
     };
     std::vector<LayerX> lx;
     std::vector<Group> groups;
-    std::vector<std::array<GemmPlan, 2>> plans;    // per group, per step parity: conv / linear / PV
+    std::vector<std::array<GemmPlan, 2>> plans;    // per group, per step parity: conv / linear;
+                                                   // attention PV per K/V parity
     std::vector<std::array<GemmPlan, 2>> s_plans;  // attention S = Q K^T per K/V parity
     std::vector<char> fused_stats;                 // per GN layer: stats come from the conv epilogue
     std::vector<char> merged_into_prev;            // per group: computed by the previous group
@@ -102,10 +103,16 @@ struct Program {
     // scratch
     double* gn_partial = nullptr;
     unsigned int* gn_ticket = nullptr;
-    float* S = nullptr;
+    // attention: P = softmax numerators [m][s_pad] (padding columns stay zero), per key tile
+    // row maxima [n_tiles][m], 1 / row sums [m]; fp32 mode: V^T [C][s_pad] for the PV GEMM
     void* P = nullptr;
-    void* Vt = nullptr;
     int s_pad = 0;
+    float* attn_rowmax = nullptr;
+    float* attn_rscale = nullptr;
+    void* Vt = nullptr;
+    int attn_c = 0;   // attention channels
+    // V read MN-major by the PV GEMM (bf16, whole 128-byte channel chunks); else V^T
+    bool attn_v_mn() const { return e == Elem::BF16 && attn_c % 64 == 0; }
     // time embedding
     std::vector<float*> temb_out;   // per layer (nullptr unless AddTimeEmb)
     TembLayer* temb_dev = nullptr;

@@ -327,6 +327,29 @@ __device__ __forceinline__ void mma4_tf32_pair(uint32_t d_tmem, uint64_t a_desc,
                                                uint32_t idesc, uint32_t acc0) {
     PP_MMA4("2", "tf32");
 }
+// B operand MN-major (attention V): the K steps of a 128-byte block advance the B start by
+// B1, B2, B3 (multiples of 16 bf16 / 8 tf32 K rows of 128 bytes: 2048 / 1024 bytes, >> 4).
+#define PP_MMA4_BMN(GROUP, KIND, B1, B2, B3)                                                    \
+    asm volatile(                                                                          \
+        "{\n\t.reg .pred p;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"                      \
+        "setp.ne.b32 p, %4, 0;\n\t"                                                         \
+        "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"               \
+        "add.s64 b1, %2, " B1 ";\n\tadd.s64 b2, %2, " B2 ";\n\tadd.s64 b3, %2, " B3 ";\n\t" \
+        "tcgen05.mma.cta_group::" GROUP ".kind::" KIND " [%0], %1, %2, %3, p;\n\t"         \
+        "tcgen05.mma.cta_group::" GROUP ".kind::" KIND " [%0], a1, b1, %3, 1;\n\t"         \
+        "tcgen05.mma.cta_group::" GROUP ".kind::" KIND " [%0], a2, b2, %3, 1;\n\t"         \
+        "tcgen05.mma.cta_group::" GROUP ".kind::" KIND " [%0], a3, b3, %3, 1;\n\t}" ::"r"(d_tmem), \
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(acc0)                                    \
+        : "memory")
+__device__ __forceinline__ void mma4_bf16_bmn(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                              uint32_t idesc, uint32_t acc0) {
+    PP_MMA4_BMN("1", "f16", "128", "256", "384");
+}
+__device__ __forceinline__ void mma4_bf16_pair_bmn(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                                   uint32_t idesc, uint32_t acc0) {
+    PP_MMA4_BMN("2", "f16", "128", "256", "384");
+}
+#undef PP_MMA4_BMN
 #undef PP_MMA4
 
 // Arrive on an mbarrier when all previously issued tcgen05 ops of this thread finish.
@@ -381,6 +404,21 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, float* v) {
 __device__ __forceinline__ void tmem_wait_ld() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// One 256-bit global store (sm_100): a whole 32-byte sector per lane, so the row-strided
+// epilogue stores of a warp (32 rows) write full sectors in one instruction.  dst 32-byte
+// aligned.
+__device__ __forceinline__ void st_global_v8(void* dst, const uint4& lo, const uint4& hi) {
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "r"(lo.x),
+                 "r"(lo.y), "r"(lo.z), "r"(lo.w), "r"(hi.x), "r"(hi.y), "r"(hi.z), "r"(hi.w)
+                 : "memory");
+}
+
+// After tmem_wait_ld: ties the registers of a tmem_ld16_nowait to a point after the wait, so
+// no use is scheduled between the load and its wait.
+__device__ __forceinline__ void tmem_pin16(float* v) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) asm volatile("" : "+f"(v[i]));
+}
 // 32 lanes x 16 consecutive 32-bit columns (one row per thread).
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
     uint32_t r[16];
@@ -405,6 +443,19 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
     d |= uint64_t(1024 >> 4) << 32;         // SBO
     d |= uint64_t(1) << 46;                 // version
     d |= uint64_t(2) << 61;                 // SWIZZLE_128B
+    return d;
+}
+
+// MN-major operand, 128-byte swizzle (canonical ((8,n),(8,k)) : ((1,LBO),(8,SBO)) in 16-byte
+// units): rows of 128 bytes hold consecutive N elements of one K index, 8-row swizzle atoms
+// are 1024 bytes apart along K (SBO), and the next 128 bytes of N start lbo_bytes further.
+__device__ __forceinline__ uint64_t smem_desc_sw128_mn(uint32_t saddr, uint32_t lbo_bytes) {
+    uint64_t d = 0;
+    d |= uint64_t((saddr >> 4) & 0x3FFF);
+    d |= uint64_t((lbo_bytes >> 4) & 0x3FFF) << 16;   // LBO: next 128 bytes of N
+    d |= uint64_t(1024 >> 4) << 32;                    // SBO: next 8 K rows
+    d |= uint64_t(1) << 46;                            // version
+    d |= uint64_t(2) << 61;                            // SWIZZLE_128B
     return d;
 }
 

@@ -340,10 +340,15 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
         const Region& ri = spec.layer_in[g.first];
         const int ns = ri.full_h * ri.full_w;
         s_pad = round_up(ns, 64);
-        const int npad = round_up(in.C, 16);
-        S = static_cast<float*>(alloc(size_t(in.pix()) * s_pad * 4));
         P = alloc(size_t(in.pix()) * s_pad * eb);
-        Vt = alloc(size_t(npad) * s_pad * eb);
+        CUDA_CHECK(cudaMemset(P, 0, size_t(in.pix()) * s_pad * eb));   // key padding: P = 0
+        attn_rscale = static_cast<float*>(alloc(size_t(in.pix()) * 4));
+        attn_c = in.C;
+        if (!attn_v_mn()) {   // TF32 MMAs take B K-major only: V^T by the transpose kernel
+            const size_t vt = size_t(round_up(in.C, 16)) * s_pad * eb;
+            Vt = alloc(vt);
+            CUDA_CHECK(cudaMemset(Vt, 0, vt));
+        }
     }
 
     // SelfAttn(+AddSkip) followed by CrossAttn+AddSkip of that output: CrossAttn's output is
@@ -435,18 +440,36 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
                     e2.out_ld = act[gc.last].ld;
                     e2.bias = wts->L[gc.first].cross_v;
                 }
+                // S = Q K^T with the softmax in the epilogue (P, per-tile row maxima), then
+                // O = P V with V MN-major straight from the K/V map (bf16) and 1/l in the
+                // epilogue
                 const Region& ri = spec.layer_in[g.first];
                 const int ns = ri.full_h * ri.full_w;
+                const int m_rows = int(in.pix());
                 EpilogueSpec es;
-                es.out = S;
+                es.out = P;
                 es.out_ld = s_pad;
-                es.out_f32 = true;
+                es.out_f32 = e == Elem::F32;
+                es.round_tf32 = rnd;
                 es.n_valid = ns;
+                // (non-null marks the softmax epilogue; the table is sized by the tiling below)
+                es.sm_rowmax = static_cast<float*>(P);
+                es.sm_scale = float(1.0 / std::sqrt(double(d.in_ch)));
+                es.sm_ld = m_rows;
                 const void* kv = nb > 1 ? lx[g.first].kv[p] : in.interior(eb);
-                plan_gemm(s_plans[gi][p], e, in.interior(eb), int(in.pix()), in.ld, in.ld, kv, ns,
-                          in.ld, es, sc, sms);
-                plan_gemm(plans[gi][p], e, P, int(in.pix()), s_pad, s_pad, Vt, in.C, s_pad, e2, sc,
-                          sms);
+                GemmPlan& sp = s_plans[gi][p];
+                plan_gemm(sp, e, in.interior(eb), m_rows, in.ld, in.ld, kv, ns, in.ld, es, sc, sms);
+                if (!attn_rowmax)
+                    attn_rowmax = static_cast<float*>(alloc(size_t(sp.a.n_tiles) * m_rows * 4));
+                else if (p == 1 && sp.a.n_tiles != s_plans[gi][0].a.n_tiles)
+                    throw std::logic_error("attention: S tilings differ between parities");
+                sp.a.sm_rowmax = attn_rowmax;
+                e2.row_scale = attn_rscale;
+                if (attn_v_mn())
+                    plan_gemm_bmn(plans[gi][p], e, P, m_rows, s_pad, s_pad, kv, ns, in.C, in.ld, e2,
+                                  sc, sms);
+                else
+                    plan_gemm(plans[gi][p], e, P, m_rows, s_pad, s_pad, Vt, in.C, s_pad, e2, sc, sms);
             }
         }
         if (fuse_gn) fused_stats[next] = 1;
@@ -605,16 +628,21 @@ void Program::attention(const Group& g, int par, int par_out) {
     const Region& ri = spec.layer_in[g.first];
     const int ns = ri.full_h * ri.full_w;
     const GemmPlan& sp = s_plans[gi][par];
+    const GemmPlan& pv = plans[gi][par];   // V = the K/V map of this parity
+    (void)par_out;
     const void* kv = nb > 1 ? lx[g.first].kv[par] : in.interior(eb);
-    const float scale = float(1.0 / std::sqrt(double(m->layers[g.first].in_ch)));
+    const int m_rows = int(in.pix());
+    if (!attn_v_mn()) {
+        run_timed(CAT_OTHER, 0, [&] { transpose(e, kv, ns, in.C, in.ld, Vt, s_pad, cs); });
+        count(1);
+    }
     run_timed(CAT_GEMM, sp.flops, [&] { launch_gemm(sp, cs); });
     run_timed(CAT_OTHER, 0, [&] {
-        softmax_rows(e, S, int(in.pix()), ns, s_pad, scale, P, s_pad, cs);
-        transpose(e, kv, ns, in.C, in.ld, Vt, s_pad, cs);
+        attn_rescale(e, P, s_pad, m_rows, ns, attn_rowmax, sp.a.n_tiles, sp.a.block_n, m_rows,
+                     attn_rscale, rnd, cs);
     });
-    const GemmPlan& pv = plans[gi][par_out];
     run_timed(CAT_GEMM, pv.flops, [&] { launch_gemm(pv, cs); });
-    count(4);
+    count(3);
 }
 
 void Program::gn_stats(const Group& g, int par) {

@@ -96,7 +96,8 @@ def test_linear_vs_oracle(dtype):
 
 
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
-@pytest.mark.parametrize("m,s,d", [(1, 1, 8), (6, 10, 8), (128, 256, 64), (64, 1024, 1280)])
+@pytest.mark.parametrize("m,s,d", [(1, 1, 8), (6, 10, 8), (128, 256, 64), (64, 1024, 1280),
+                                   (200, 1000, 96), (128, 14400, 1280)])
 def test_attention_vs_oracle(dtype, m, s, d):
     # test_tensor.cpp:148-175 (single token, oracle); d=1280 is the SDXL-shape head
     rng = np.random.default_rng(m + s + d)
@@ -110,6 +111,32 @@ def test_attention_vs_oracle(dtype, m, s, d):
     assert O.rel_l2(out, ref) <= TOL[dtype] * 2, O.rel_l2(out, ref)
     if s == 1:
         assert np.allclose(out, np.broadcast_to(v[:, :, :1], out.shape), rtol=1e-2)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_attention_extreme_logit_ranges(dtype):
+    # The softmax runs in the S-GEMM epilogue against each key tile's own row max; attn_rescale
+    # brings the tiles to the row max.  One huge key puts the rows aligned with it ~50 above
+    # every other logit (one tile dominates, the others are scaled by ~e^-50) while the
+    # orthogonal rows see only O(1) logits: both must match the fp64 oracle.
+    rng = np.random.default_rng(5)
+    m, s, d = 64, 256, 64
+    k = rng.standard_normal((1, 1, s, d)).astype(np.float32)
+    k[0, 0, 3] = 0.0
+    k[0, 0, 3, 0] = 400.0
+    q = rng.standard_normal((1, 1, m, d)).astype(np.float32)
+    q[0, 0, ::2, 0] = 0.0                      # orthogonal to the big key
+    q[0, 0, 1::2] *= 0.05
+    q[0, 0, 1::2, 0] = 1.0                     # aligned with it: one dominant logit
+    v = rng.standard_normal((1, 1, s, d)).astype(np.float32)
+    scale = float(np.float32(1.0 / np.sqrt(d)))
+    out = np.zeros((1, 1, m, d), np.float32)
+    N.check(N.lib().pp_attention(N.DTYPES[dtype], _p(q), _p(k), _p(v), 1, m, s, d, d, scale, _p(out)))
+    ref = O.attention(q, k, v, scale)
+    assert np.isfinite(out).all()
+    for rows in (slice(0, None, 2), slice(1, None, 2)):
+        err = O.rel_l2(out[0, 0, rows], ref[0, 0, rows])
+        assert err <= TOL[dtype] * 2, (rows, err)
 
 
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
