@@ -376,13 +376,15 @@ __device__ __forceinline__ void softmax_chunk(const GemmArgs& a, float* v, int n
 }
 
 // kAttn: 0 = conv / linear (no attention code compiled in), 1 = attention S GEMM (softmax
-// epilogue), 2 = attention PV GEMM (1/l row scale; bf16: B operand MN-major, i.e. V [keys][d]
-// as staged by TMA, no transpose).
+// epilogue), 2 = attention PV GEMM (1/l row scale) with the B operand MN-major (bf16: V
+// [keys][d] as staged by TMA, no transpose), 3 = PV GEMM with B = V^T K-major (TF32, or
+// channel counts that do not fill 128-byte chunks).
 template <bool kTF32, bool kPair, int kAttn>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmD, const GemmArgs a) {
-    constexpr bool kBmn = kAttn == 2 && !kTF32;
+    constexpr bool kBmn = kAttn == 2;
+    static_assert(!(kBmn && kTF32), "MN-major B is bf16 only");
     constexpr int P = kPair ? 2 : 1;   // CTAs per cluster
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte aligned base derived from smem_raw by pointer arithmetic (not an integer
@@ -795,7 +797,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // attention epilogues read what the previous kernel wrote (row norms, partial row
         // sums) ahead of the accumulator: wait for it here (the loads then overlap the MMAs)
         constexpr bool softmax = kAttn == 1;
-        constexpr bool pv = kAttn == 2;
+        constexpr bool pv = kAttn >= 2;
         if (pv) pdl_wait();   // row_scale comes from the previous kernel
         const float sl2 = a.sm_scale * 1.4426950408889634f;   // scale * log2(e)
         float* const s_row = st.gn;   // softmax: [3][128] partial row maxima
@@ -1549,13 +1551,15 @@ void launch_gemm(const GemmPlan& p, cudaStream_t s) {
         return;
     }
     if (attn == 2) {
-        if (p.elem == Elem::F32) {
-            if (p.pair) launch_variant<true, true, 2>(p, s);
-            else launch_variant<true, false, 2>(p, s);
-        } else {
-            if (!p.a.b_mn) throw std::logic_error("GEMM: bf16 attention PV GEMM reads V MN-major");
+        if (p.a.b_mn) {
             if (p.pair) launch_variant<false, true, 2>(p, s);
             else launch_variant<false, false, 2>(p, s);
+        } else if (p.elem == Elem::F32) {
+            if (p.pair) launch_variant<true, true, 3>(p, s);
+            else launch_variant<true, false, 3>(p, s);
+        } else {
+            if (p.pair) launch_variant<false, true, 3>(p, s);
+            else launch_variant<false, false, 3>(p, s);
         }
         return;
     }

@@ -782,6 +782,42 @@ __global__ void __launch_bounds__(256) attn_rescale_kernel(T* __restrict__ P, lo
     if (lane == 0) row_scale[r] = 1.0f / sum;
 }
 
+// ---------------------------------------------------------------- stem im2col
+// The stem conv (conv2d_region, proj/src/tensor.cpp:79-130, 4 -> 320 channels) as a plain
+// tcgen05 GEMM with K = 9 taps x 4 channels in ONE 128-byte K block: this kernel gathers the
+// 36 values of every output pixel (tap-major, channel-minor; zero outside the image, the halo
+// rows come from the padded band) into out[pixel][kpad] (the padding columns stay zero).
+template <class T>
+__global__ void __launch_bounds__(256) stem_im2col_kernel(const T* __restrict__ in, int rows, int W,
+                                                          int ld_in, int C_in, T* __restrict__ out,
+                                                          int kpad) {
+    pdl_wait();
+    pdl_trigger();
+    const long long n = (long long)rows * W * 9;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long p = i / 9;
+        const int tap = int(i - p * 9), ky = tap / 3, kx = tap - 3 * ky;
+        const int y = int(p / W), x = int(p - (long long)y * W);
+        const int xx = x + kx - 1;
+        T v[4];
+        if (xx >= 0 && xx < W) {
+            const T* src = in + ((long long)(y + ky) * W + xx) * ld_in;   // padded row y + ky
+#pragma unroll
+            for (int c = 0; c < 4; ++c) v[c] = c < C_in ? src[c] : from_float<T>(0.0f, false);
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) v[c] = from_float<T>(0.0f, false);
+        }
+        T* dst = out + p * kpad + tap * 4;
+        if constexpr (sizeof(T) == 2) {
+            *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(v);
+        } else {
+            *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(v);
+        }
+    }
+}
+
 #define DISPATCH(e, ...)                          \
     do {                                          \
         if ((e) == Elem::BF16) {                  \
@@ -942,6 +978,15 @@ void attn_rescale(Elem e, void* P, long long ldp, int m, int s, const float* row
     DISPATCH(e, launch_pdl(attn_rescale_kernel<T>, dim3((m + 7) / 8), dim3(256), smem, st, 1,
                            static_cast<T*>(P), ldp, m, s, rowmax, n_tiles, block_n, ld_rm,
                            row_scale, round_tf32 ? 1 : 0));
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void stem_im2col(Elem e, const void* in, int rows, int W, int ld_in, int C_in, void* out, int kpad,
+                 cudaStream_t s) {
+    if (C_in > 4 || kpad < 36) throw std::invalid_argument("stem_im2col: <= 4 channels, kpad >= 36");
+    DISPATCH(e, launch_pdl(stem_im2col_kernel<T>, dim3(grid_for((long long)rows * W * 9, 256)),
+                           dim3(256), 0, s, 1, static_cast<const T*>(in), rows, W, ld_in, C_in,
+                           static_cast<T*>(out), kpad));
     CUDA_CHECK(cudaGetLastError());
 }
 

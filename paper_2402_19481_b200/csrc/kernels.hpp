@@ -74,6 +74,12 @@ void attn_rescale(Elem e, void* P, long long ldp, int m, int s, const float* row
 void transpose(Elem e, const void* V, int ns, int C, long long ldv, void* Vt, long long ldt,
                cudaStream_t s);
 
+// ---- stem im2col (conv2d_region, tensor.cpp:79-130, C_in <= 4) ------------------------------
+// in = halo-padded band [rows + 2][W][ld_in]; out[p][tap * 4 + c] for the 9 taps (zero outside
+// the image); columns 36..kpad-1 are left untouched (zero).
+void stem_im2col(Elem e, const void* in, int rows, int W, int ld_in, int C_in, void* out, int kpad,
+                 cudaStream_t s);
+
 // ---- context exchange (displaced patch parallelism) ----------------------------------------
 // A batch of exchange copies in ONE launch (in-process transport: every band's halo rows,
 // K/V band and GroupNorm statistics of a batch of layers): chunk i = {src, dst, bytes},

@@ -30,6 +30,8 @@ struct LayerWeights {
     float* temb_w = nullptr;  // AddTimeEmb: [C][time_dim] fp32 (reference layout)
     float* temb_b = nullptr;
     float* cross_v = nullptr; // CrossAttn: projected value vector [ld] fp32
+    // stem conv with in_ch <= 4 as one-K-block GEMM: [n_pad][kStemK] (tap-major, 4 channels)
+    void* w_stem = nullptr;
 };
 
 struct DeviceWeights {
@@ -99,6 +101,8 @@ struct Program {
     std::vector<std::array<GemmPlan, 2>> s_plans;  // attention S = Q K^T per K/V parity
     std::vector<char> fused_stats;                 // per GN layer: stats come from the conv epilogue
     std::vector<char> merged_into_prev;            // per group: computed by the previous group
+    std::vector<char> stem_gemm;                   // per group: stem conv as im2col + GEMM
+    void* stem_cols = nullptr;                     // [pix][kStemK] im2col of the stem input
     GemmScratch sc;
     // scratch
     double* gn_partial = nullptr;

@@ -38,6 +38,12 @@ uint16_t f2bf(float f) {
     u += 0x7fffu + ((u >> 16) & 1u);
     return uint16_t(u >> 16);
 }
+float bf2f(uint16_t h) {
+    const uint32_t u = uint32_t(h) << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
 float tf32_rna(float f) {
     uint32_t u;
     std::memcpy(&u, &f, 4);
@@ -61,6 +67,9 @@ void upload_elem(void* dst, const std::vector<float>& src, Elem e) {
 }
 
 int act_ld(int C, Elem e) { return round_up(C, e == Elem::BF16 ? 64 : 32); }
+
+// K of the stem GEMM: 9 taps x 4 channels padded to whole 128-byte blocks (bf16: one block)
+constexpr int kStemK = 64;
 
 }  // namespace
 
@@ -106,6 +115,16 @@ DeviceWeights::DeviceWeights(const Model& m, const std::vector<float>& cond, int
                 w.w = alloc(pk.size() * eb);
                 upload_elem(w.w, pk, e);
                 w.bias = up_f32(d.bias, w.n_pad);
+                if (d.kind == Kind::Conv && d.in_ch <= 4) {
+                    // the stem as a one-K-block GEMM over its im2col: [n_pad][kStemK], k = tap * 4 + ci
+                    std::vector<float> st(size_t(w.n_pad) * kStemK, 0.0f);
+                    for (int co = 0; co < d.out_ch; ++co)
+                        for (int ci = 0; ci < d.in_ch; ++ci)
+                            for (int t9 = 0; t9 < 9; ++t9)
+                                st[size_t(co) * kStemK + t9 * 4 + ci] = t.data[(size_t(co) * d.in_ch + ci) * 9 + t9];
+                    w.w_stem = alloc(st.size() * eb);
+                    upload_elem(w.w_stem, st, e);
+                }
                 break;
             }
             case Kind::Linear: {
@@ -379,6 +398,7 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
     const int sms = device_sm_count();
     plans.resize(groups.size());
     s_plans.resize(groups.size());
+    stem_gemm.assign(groups.size(), 0);
     for (size_t gi = 0; gi < groups.size(); ++gi) {
         const Group& g = groups[gi];
         const Layer& d = m->layers[g.first];
@@ -419,7 +439,20 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
                 e2.gn_groups = m->layers[next].groups;
                 e2.gn_out = lx[next].stats[p] + size_t(band) * e2.gn_groups * 2;
             }
-            if (d.kind == Kind::Conv || d.kind == Kind::DownConv) {
+            if (d.kind == Kind::Conv && lw.w_stem && d.stride == 1) {
+                // the stem (<= 4 input channels): im2col with K = 36 in one 128-byte K block +
+                // a plain GEMM, instead of a 9-tap implicit GEMM over channels padded 16x
+                e2.bias = lw.bias;
+                if (!stem_cols) {
+                    const size_t bytes = size_t(in.pix()) * kStemK * eb;
+                    stem_cols = alloc(bytes);
+                    CUDA_CHECK(cudaMemset(stem_cols, 0, bytes));
+                }
+                plan_gemm(plans[gi][p], e, stem_cols, int(in.pix()), kStemK, kStemK, lw.w_stem,
+                          d.out_ch, kStemK, e2, sc, sms, 0, 0, /*b_static=*/true);
+                plans[gi][p].flops = 2.0 * double(in.pix()) * d.out_ch * 9.0 * d.in_ch;
+                stem_gemm[gi] = 1;
+            } else if (d.kind == Kind::Conv || d.kind == Kind::DownConv) {
                 e2.bias = lw.bias;
                 plan_conv(plans[gi][p], e, in.base, in.rows, in.w, in.ld, d.stride, lw.w, lw.n_pad,
                           e2, sc, sms);
@@ -601,6 +634,13 @@ void Program::halo_rows(const Group& g, int par_pack, int par_unpack) {
 void Program::conv(const Group& g, int par) {
     const size_t gi = size_t(&g - groups.data());
     const GemmPlan& p = plans[gi][par];
+    if (stem_gemm[gi]) {
+        const Act& in = input_of(g.first);
+        run_timed(CAT_OTHER, 0, [&] {
+            stem_im2col(e, in.base, in.rows, in.w, in.ld, in.C, stem_cols, kStemK, cs);
+        });
+        count(1);
+    }
     run_timed(CAT_CONV, p.flops, [&] { launch_gemm(p, cs); });
     count(1);
 }
