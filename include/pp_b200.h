@@ -150,6 +150,10 @@ typedef struct {
                        * exchange (halo rows, K/V, GroupNorm statistics) is skipped and each
                        * band normalises with its own statistics; compute is identical, the
                        * results are NOT the reference's.  Default 0. */
+    int stress;       /* --stress-sched (proj/src/collectives.cpp:45-56): perturb the device
+                       * schedule around every exchange with seeded sleep kernels on the
+                       * compute and exchange streams; results must not change.  Default 0. */
+    unsigned long long stress_seed;   /* default 0xC0FFEE */
 } pp_runner_opts;
 PP_API void pp_runner_opts_default(pp_runner_opts* o);
 

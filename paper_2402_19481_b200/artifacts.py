@@ -114,3 +114,57 @@ def load_weights(cfg: "P.ModelConfig", path: str) -> "P.Model":
             raise
         raise P.InvalidArgument(f"load_weights: file holds {m.group(1)} values, model expects "
                                 f"{m.group(2)}") from None
+
+
+def similarity_report(trajectory):
+    """input_similarity_report (proj/src/sampler.cpp:97-127): per consecutive pair of step
+    inputs the mean |x_t - x_{t-1}| (fp64), their mean, the observed range over every state,
+    and ratio = mean / range (0 when the range is 0).  trajectory: [steps, ...] array."""
+    traj = np.asarray(trajectory)
+    if traj.shape[0] == 0:
+        return {"per_step_mean_abs_diff": [], "mean_abs_diff": 0.0, "range_min": 0.0,
+                "range_max": 0.0, "ratio": 0.0}
+    lo = float(np.min(traj).astype(np.float64))
+    hi = float(np.max(traj).astype(np.float64))
+    per = [float(np.mean(np.abs(traj[i].astype(np.float64) - traj[i - 1].astype(np.float64))))
+           for i in range(1, traj.shape[0])]
+    mean = float(np.mean(per)) if per else 0.0
+    rng = hi - lo
+    return {"per_step_mean_abs_diff": per, "mean_abs_diff": mean, "range_min": lo,
+            "range_max": hi, "ratio": mean / rng if rng > 0.0 else 0.0}
+
+
+COST_KEYS = ("compute_rate", "link_bandwidth", "link_latency", "comm_uses_compute_fraction")
+
+
+def parse_cost_profile(path: str) -> dict:
+    """parse_cost_profile (proj/src/io.cpp:110-131) + CostParams::validate
+    (proj/src/costmodel.cpp:13-19): 'key = value' lines, '#' comments, unknown keys and bad
+    values are InvalidArgument."""
+    p = {"compute_rate": 1000.0, "link_bandwidth": 100.0, "link_latency": 5.0,
+         "comm_uses_compute_fraction": 0.15}
+    try:
+        f = open(path)
+    except OSError:
+        raise P.InvalidArgument(f"cost profile: cannot open {path}") from None
+    with f:
+        for line in f:
+            t = line.strip()
+            if not t or t.startswith("#"):
+                continue
+            if "=" not in t:
+                raise P.InvalidArgument(f"cost profile: expected 'key = value', got '{t}'")
+            k, v = (s.strip() for s in t.split("=", 1))
+            if k not in COST_KEYS:
+                raise P.InvalidArgument(f"cost profile: unknown key '{k}'")
+            try:
+                p[k] = float(v)
+            except ValueError:
+                raise P.InvalidArgument(f"cost profile: bad value '{v}'") from None
+    if p["compute_rate"] <= 0.0 or p["link_bandwidth"] <= 0.0:
+        raise P.InvalidArgument("CostParams: rates must be positive")
+    if p["link_latency"] < 0.0:
+        raise P.InvalidArgument("CostParams: negative latency")
+    if not (0.0 <= p["comm_uses_compute_fraction"] < 1.0):
+        raise P.InvalidArgument("CostParams: comm_uses_compute_fraction must be in [0,1)")
+    return p

@@ -57,6 +57,8 @@ pp::RunnerOptions opts_of(const pp_runner_opts* o) {
     r.device = o->device;
     r.profile = o->profile != 0;
     r.no_comm = o->no_comm != 0;
+    r.stress = o->stress != 0;
+    r.stress_seed = o->stress_seed;
     return r;
 }
 
@@ -299,6 +301,8 @@ PP_API void pp_runner_opts_default(pp_runner_opts* o) {
     o->profile = 0;
     o->transport = PP_TRANSPORT_NCCL;
     o->no_comm = 0;
+    o->stress = 0;
+    o->stress_seed = 0xC0FFEEull;
 }
 
 PP_API int pp_runner_create(const pp_model* m, const float* cond, int cond_dim, int h, int w,

@@ -818,6 +818,11 @@ __global__ void __launch_bounds__(256) stem_im2col_kernel(const T* __restrict__ 
     }
 }
 
+// --stress-sched: a single thread sleeping `us` microseconds on the stream (scheduling noise)
+__global__ void sleep_kernel(unsigned int us) {
+    for (unsigned int i = 0; i < us; ++i) __nanosleep(1000);
+}
+
 #define DISPATCH(e, ...)                          \
     do {                                          \
         if ((e) == Elem::BF16) {                  \
@@ -987,6 +992,11 @@ void stem_im2col(Elem e, const void* in, int rows, int W, int ld_in, int C_in, v
     DISPATCH(e, launch_pdl(stem_im2col_kernel<T>, dim3(grid_for((long long)rows * W * 9, 256)),
                            dim3(256), 0, s, 1, static_cast<const T*>(in), rows, W, ld_in, C_in,
                            static_cast<T*>(out), kpad));
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void stream_sleep(unsigned int us, cudaStream_t s) {
+    sleep_kernel<<<1, 1, 0, s>>>(us);
     CUDA_CHECK(cudaGetLastError());
 }
 

@@ -80,6 +80,9 @@ void transpose(Elem e, const void* V, int ns, int C, long long ldv, void* Vt, lo
 void stem_im2col(Elem e, const void* in, int rows, int W, int ld_in, int C_in, void* out, int kpad,
                  cudaStream_t s);
 
+// --stress-sched: one thread sleeping `us` microseconds on stream s
+void stream_sleep(unsigned int us, cudaStream_t s);
+
 // ---- context exchange (displaced patch parallelism) ----------------------------------------
 // A batch of exchange copies in ONE launch (in-process transport: every band's halo rows,
 // K/V band and GroupNorm statistics of a batch of layers): chunk i = {src, dst, bytes},

@@ -1016,6 +1016,23 @@ void Runner::record_trace(int s, int kind) {
     }
 }
 
+// --stress-sched (CollectiveHub::maybe_stress, proj/src/collectives.cpp:45-56): per band, a
+// seeded draw r = state % 3 -- 0: nothing (the reference yields), 1: sleep state % 200 us, 2:
+// nothing -- applied to the compute and the exchange stream before every exchanging layer.
+// The results must be bitwise unchanged (the exchange is ordered by events, not by timing).
+void Runner::stress_jitter(Program& b, int band) {
+    if (stress_state_.empty()) {
+        for (int d = 0; d < n_dev_; ++d)
+            stress_state_.push_back(substream_seed(o_.stress_seed, uint64_t(d), 0xC0FFEE));
+    }
+    for (cudaStream_t s : {b.cs, b.xs}) {
+        SplitMix64 rng(stress_state_[band]);
+        stress_state_[band] = rng.next();
+        const uint64_t v = stress_state_[band];
+        if (v % 3 == 1) stream_sleep(unsigned(v % 200), s);
+    }
+}
+
 void Runner::run_bands(std::vector<std::unique_ptr<Program>>& progs, int t, int s, bool displaced) {
     const bool exchanging = &progs == &bands_;   // naive patch programs never exchange or post
     if (displaced) check_displaced_ready(s);
@@ -1045,6 +1062,14 @@ void Runner::run_bands(std::vector<std::unique_ptr<Program>>& progs, int t, int 
                 fn(*b, b->groups[gi]);
             }
         };
+        if (o_.stress && exchanging &&
+            (d.kind == Kind::Conv || d.kind == Kind::DownConv || d.kind == Kind::SelfAttn ||
+             d.kind == Kind::GroupNorm)) {
+            for (auto& b : progs) {
+                DeviceGuard g(b->dev);
+                stress_jitter(*b, b->band);
+            }
+        }
         if (d.kind == Kind::Conv || d.kind == Kind::DownConv) {
             if (multi && displaced) {
                 // the halo rows of step s-1 were exchanged a step ago: wait for them, then

@@ -43,6 +43,8 @@ struct RunnerOptions {
     int device = 0;                   // CUDA device of every local band / of this rank
     bool profile = false;
     bool no_comm = false;             // ablation ("No Comm."): exchanges skipped, local GN stats
+    bool stress = false;              // scheduling noise around the exchanges (determinism check)
+    uint64_t stress_seed = 0xC0FFEE;
 };
 
 struct CommVolumes {
@@ -138,6 +140,8 @@ private:
     cudaEvent_t nev_ = nullptr; // naive: end of the previous naive step's work
     std::unique_ptr<Transport> transport_;
     std::vector<int> posted_;      // per layer: last step whose gather exchange was posted
+    std::vector<uint64_t> stress_state_;   // --stress-sched: per band splitmix64 state
+    void stress_jitter(Program& b, int band);
     std::vector<int> gn_posted_;   // per layer: last step whose GN stats were posted
     uint64_t total_macs_ = 0;
     // RawTrace mirror (record_trace): per device events + the reference's cache-step state

@@ -187,6 +187,8 @@ class RunnerOptions:
     profile: bool = False
     transport: str = "nccl"          # world > 1: "nccl" or "ipc" (CUDA IPC + copy engines)
     no_comm: bool = False            # ablation only ("No Comm."): exchanges skipped
+    stress: bool = False             # --stress-sched: scheduling noise (results unchanged)
+    stress_seed: int = 0xC0FFEE
 
 
 class PatchRunner:
@@ -215,6 +217,8 @@ class PatchRunner:
             raise InvalidArgument(f"unknown transport '{opts.transport}'")
         o.transport = N.TRANSPORTS[opts.transport]
         o.no_comm = int(opts.no_comm)
+        o.stress = int(opts.stress)
+        o.stress_seed = int(opts.stress_seed)
         h_ = C.c_void_p()
         N.check(N.lib().pp_runner_create(model._h, _p(cond), cond.size, h, w, C.byref(o),
                                          C.byref(h_)))

@@ -136,3 +136,87 @@ def test_psnr_shape_mismatch_message():
     b = np.zeros((1, 4, 6, 8), np.float32)
     with pytest.raises(P.InvalidArgument, match=r"^psnr: shape mismatch \(1,4,6,9\) vs \(1,4,6,8\)$"):
         A.psnr(a, b, 1.0)
+
+
+def test_similarity_report_matches_reference_rule():
+    # input_similarity_report (sampler.cpp:97-127): mean |x_t - x_{t-1}| over the pairs, range
+    # over every state, ratio = mean / range
+    traj = np.stack([np.full((1, 1, 2, 2), v, np.float32) for v in (0.0, 1.0, 3.0)])
+    r = A.similarity_report(traj)
+    assert r["per_step_mean_abs_diff"] == [1.0, 2.0]
+    assert r["mean_abs_diff"] == 1.5 and (r["range_min"], r["range_max"]) == (0.0, 3.0)
+    assert r["ratio"] == 0.5
+    assert A.similarity_report(np.zeros((0, 1)))["ratio"] == 0.0
+    assert A.similarity_report(np.zeros((3, 1, 2)))["ratio"] == 0.0
+
+
+def test_cost_profile_parsing(tmp_path):
+    # parse_cost_profile (io.cpp:110-131) + CostParams::validate (costmodel.cpp:13-19)
+    f = tmp_path / "cost.txt"
+    f.write_text("# comment\ncompute_rate = 2000\n\nlink_latency=1.5\n")
+    p = A.parse_cost_profile(str(f))
+    assert p == {"compute_rate": 2000.0, "link_bandwidth": 100.0, "link_latency": 1.5,
+                 "comm_uses_compute_fraction": 0.15}
+    for text, msg in (("bogus = 1", "unknown key 'bogus'"), ("compute_rate 3", "expected 'key = value'"),
+                      ("link_bandwidth = 0", "rates must be positive"),
+                      ("link_latency = -1", "negative latency"),
+                      ("comm_uses_compute_fraction = 1", r"must be in \[0,1\)")):
+        f.write_text(text + "\n")
+        with pytest.raises(P.InvalidArgument, match=msg):
+            A.parse_cost_profile(str(f))
+    with pytest.raises(P.InvalidArgument, match="cannot open"):
+        A.parse_cost_profile(str(tmp_path / "none.txt"))
+
+
+def test_cli_config_and_matrix_files_are_validated(tmp_path):
+    # --config 'key = value' mirroring the flags (cli.cpp:70), --matrix key=value rows
+    # (cli.cpp:39-64): bad files are usage errors (exit 2) before any GPU work
+    cfgf = tmp_path / "exp.cfg"
+    cfgf.write_text("# base experiment\nmode = displaced\ndevices = 2\nsize = 32x32\nsteps = 4\n")
+    assert cli.parse_config_file(str(cfgf)) == {"mode": "displaced", "devices": "2",
+                                                "size": "32x32", "steps": "4"}
+    cfgf.write_text("mode = displaced\nframes = 3\n")
+    assert cli.run(["--config", str(cfgf), "--out", str(tmp_path)]) == 2
+    base = {"mode": "reference", "devices": 1, "steps": 4, "warmup": 1, "size": "32x32",
+            "model-seed": 42, "noise-seed": 1234, "cond-seed": 7, "gn-scheme": "corrected",
+            "model": "toy", "dtype": "bf16"}
+    mf = tmp_path / "runs.txt"
+    mf.write_text("mode=displaced devices=2  # two bands\n\n# nothing\nmode=sync-pp devices=4 warmup=0\n")
+    rows = cli.parse_matrix_file(base, str(mf))
+    assert [(r["mode"], r["devices"]) for r in rows] == [("displaced", "2"), ("sync-pp", "4")]
+    assert rows[1]["warmup"] == "0" and rows[0]["steps"] == 4
+    for text, msg in (("mode=displaced frames=2", "unknown key 'frames'"),
+                      ("displaced", "expected key=value"),
+                      ("mode=sync-pp devices=3", "divisible")):
+        mf.write_text(text + "\n")
+        with pytest.raises(P.InvalidArgument, match=msg):
+            cli.parse_matrix_file(base, str(mf))
+        assert cli.run(["--matrix", str(mf), "--size", "32x32", "--out", str(tmp_path)]) == 2
+    cost = tmp_path / "cost.txt"
+    cost.write_text("link_bandwidth = -2\n")
+    assert cli.run(["--cost-profile", str(cost), "--out", str(tmp_path)]) == 2
+
+
+@pytest.mark.gpu
+def test_cli_matrix_and_stress_sched(tmp_path):
+    # run_matrix (io.cpp:288-328): one metrics row per experiment, psnr vs the matching
+    # reference-mode run (inf for the reference row); --stress-sched must not change results
+    mf = tmp_path / "runs.txt"
+    mf.write_text("mode=reference\nmode=displaced devices=2 warmup=1\nmode=sync-pp devices=2\n")
+    code = cli.run(["--matrix", str(mf), "--size", "32x32", "--steps", "4", "--out", str(tmp_path)])
+    assert code == 0
+    lines = open(tmp_path / "metrics.csv").read().splitlines()
+    assert lines[0] == ("mode,N,steps,warmup,psnr_db_vs_reference,total_macs,per_device_macs,"
+                        "comm_bytes,stall_us,makespan_us,similarity_ratio")
+    rows = [l.split(",") for l in lines[1:]]
+    assert [r[0] for r in rows] == ["reference", "displaced", "sync-pp"]
+    assert rows[0][4] == "inf" and float(rows[1][4]) > 30.0 and float(rows[2][4]) > 40.0
+    assert int(rows[0][7]) == 0 and int(rows[1][7]) > 0
+    assert all(float(r[9]) > 0 and 0.0 < float(r[10]) < 1.0 for r in rows)
+    outs = []
+    for flag in ([], ["--stress-sched"]):
+        d = tmp_path / ("s" if flag else "n")
+        assert cli.run(["--mode", "displaced", "--devices", "2", "--steps", "4", "--warmup", "1",
+                        "--size", "32x32", "--out", str(d), "--emit", "tensor"] + flag) == 0
+        outs.append(A.read_tnsr(str(d / "x0.tnsr")))
+    assert np.array_equal(outs[0], outs[1])

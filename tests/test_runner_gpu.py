@@ -135,6 +135,28 @@ def test_graph_replay_is_bit_identical(mode, n):
     assert rel(g2, ref) <= TOL["bf16"]
 
 
+@pytest.mark.parametrize("mode,n", [("displaced", 4), ("sync-pp", 2)])
+def test_stress_sched_does_not_change_results(mode, n):
+    # --stress-sched (CollectiveHub::maybe_stress, collectives.cpp:45-56): seeded sleep kernels
+    # on the compute and exchange streams around every exchange perturb the schedule; the
+    # exchange is ordered by events, so x0 (eager and graph-replayed) is bitwise unchanged
+    cfg = TOY
+    m = P.build_model(cfg, 42)
+    cond = O.random_condition(cfg.cond_dim, 7)
+    x = O.random_normal(1, cfg.in_channels, 32, 32, 1234)
+    abar = O.make_schedule()
+    plan = O.make_plan(1000, 6)
+    outs = []
+    for stress, seed in ((False, 0xC0FFEE), (True, 0xC0FFEE), (True, 99)):
+        r = P.PatchRunner(m, cond, 32, 32, mode=mode, n_devices=n, warmup_steps=1, dtype="bf16",
+                          stress=stress, stress_seed=seed)
+        eager, _ = r.sample(x, plan, abar, trajectory=True)
+        g, _ = r.sample(x, plan, abar)
+        outs += [eager, g]
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+
+
 def test_graph_replay_after_other_plan_uses_its_own_time_embeddings():
     # sample(A) captures the graph; an eager sample(B) (trajectory=True) rewrites the per-plan
     # time-embedding table in place; the next sample(A) replays the graph and must see A's
