@@ -154,6 +154,14 @@ typedef struct {
                        * schedule around every exchange with seeded sleep kernels on the
                        * compute and exchange streams; results must not change.  Default 0. */
     unsigned long long stress_seed;   /* default 0xC0FFEE */
+    /* classifier-free guidance (beyond the reference API): cfg_scale != 0 runs a second,
+     * unconditional U-Net pass per step (condition `uncond`, cond_dim floats; NULL = zeros)
+     * concurrently with the conditional one and denoises with
+     * eps = eps_u + cfg_scale (eps_c - eps_u).  world > 1 with NCCL: cfg_nccl_id = a second
+     * ncclUniqueId for the unconditional pass.  Default 0 (off). */
+    double cfg_scale;
+    const float* uncond;
+    const void* cfg_nccl_id;
 } pp_runner_opts;
 PP_API void pp_runner_opts_default(pp_runner_opts* o);
 

@@ -59,6 +59,13 @@ pp::RunnerOptions opts_of(const pp_runner_opts* o) {
     r.no_comm = o->no_comm != 0;
     r.stress = o->stress != 0;
     r.stress_seed = o->stress_seed;
+    r.cfg_scale = o->cfg_scale;
+    if (!std::isfinite(r.cfg_scale)) throw std::invalid_argument("pp_runner_create: cfg_scale not finite");
+    if (r.cfg_scale != 0.0 && r.world > 1 && r.transport == PP_TRANSPORT_NCCL) {
+        need(o->cfg_nccl_id, "pp_runner_create(cfg_nccl_id)");
+        const uint8_t* p = static_cast<const uint8_t*>(o->cfg_nccl_id);
+        r.cfg_nccl_id.assign(p, p + 128);
+    }
     return r;
 }
 
@@ -303,6 +310,9 @@ PP_API void pp_runner_opts_default(pp_runner_opts* o) {
     o->no_comm = 0;
     o->stress = 0;
     o->stress_seed = 0xC0FFEEull;
+    o->cfg_scale = 0.0;
+    o->uncond = nullptr;
+    o->cfg_nccl_id = nullptr;
 }
 
 PP_API int pp_runner_create(const pp_model* m, const float* cond, int cond_dim, int h, int w,
@@ -314,7 +324,9 @@ PP_API int pp_runner_create(const pp_model* m, const float* cond, int cond_dim, 
         auto r = std::make_unique<pp_runner>();
         r->graph = m->m;
         std::vector<float> c(cond, cond + (cond ? cond_dim : 0));
-        r->r = std::make_unique<pp::Runner>(r->graph, c, h, w, opts_of(opts));
+        pp::RunnerOptions ro = opts_of(opts);
+        if (ro.cfg_scale != 0.0 && opts->uncond) ro.uncond.assign(opts->uncond, opts->uncond + cond_dim);
+        r->r = std::make_unique<pp::Runner>(r->graph, c, h, w, ro);
         for (auto& t : r->graph.weights) std::vector<float>().swap(t.data);
         *out = r.release();
     });

@@ -828,6 +828,73 @@ Runner::Runner(const Model& m, const std::vector<float>& cond, int h, int w, con
             }
         }
     }
+    if (o_.cfg_scale != 0.0) {
+        // classifier-free guidance: the unconditional pass is a second runner over the same
+        // bands (own streams, caches and exchange), stepped alongside this one
+        if (o_.mode == MODE_NAIVE)
+            throw std::invalid_argument("classifier-free guidance: naive mode is not supported");
+        if (!o_.uncond.empty() && o_.uncond.size() != cond_.size())
+            throw std::invalid_argument("classifier-free guidance: uncond length " +
+                                        std::to_string(o_.uncond.size()) + " != condition length " +
+                                        std::to_string(cond_.size()));
+        RunnerOptions u = o_;
+        u.cfg_scale = 0.0;
+        u.uncond.clear();
+        if (o_.world > 1 && o_.transport == 0) {
+            if (o_.cfg_nccl_id.size() != 128)
+                throw std::invalid_argument("classifier-free guidance: cfg_nccl_id required (world > 1, NCCL)");
+            u.nccl_id = o_.cfg_nccl_id;
+        }
+        const std::vector<float> unc = o_.uncond.empty() ? std::vector<float>(cond_.size(), 0.0f) : o_.uncond;
+        cfg_ = std::make_unique<Runner>(m_, unc, h, w, u);
+        for (auto& b : bands_) {
+            DeviceGuard g(b->dev);
+            for (int k = 0; k < 2; ++k) {
+                cudaEvent_t ev;
+                CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                cfg_ev_.push_back(ev);
+            }
+        }
+    }
+}
+
+void Runner::cfg_combine() {
+    for (size_t d = 0; d < bands_.size(); ++d) {
+        Program& b = *bands_[d];
+        Program& u = *cfg_->bands_[d];
+        DeviceGuard g(b.dev);
+        CUDA_CHECK(cudaEventRecord(cfg_ev_[2 * d], u.cs));
+        CUDA_CHECK(cudaStreamWaitEvent(b.cs, cfg_ev_[2 * d], 0));
+        cfg_combine_eps(b.eps, u.eps, (long long)b.stem.rows * w_ * m_.cfg.in_channels, o_.cfg_scale, b.cs);
+        launches_ += 1;
+    }
+}
+
+void Runner::cfg_refresh_stem() {
+    for (size_t d = 0; d < bands_.size(); ++d) {
+        Program& b = *bands_[d];
+        Program& u = *cfg_->bands_[d];
+        DeviceGuard g(b.dev);
+        CUDA_CHECK(cudaMemcpyAsync(u.stem.interior(u.eb), b.stem.interior(b.eb),
+                                   size_t(b.stem.rows) * b.stem.w * b.stem.ld * b.eb,
+                                   cudaMemcpyDeviceToDevice, b.cs));
+        CUDA_CHECK(cudaEventRecord(cfg_ev_[2 * d + 1], b.cs));
+        CUDA_CHECK(cudaStreamWaitEvent(u.cs, cfg_ev_[2 * d + 1], 0));
+    }
+}
+
+CommVolumes Runner::volumes() const {
+    CommVolumes v = volumes_;
+    if (cfg_) {
+        const CommVolumes u = cfg_->volumes();
+        v.allgather_recv += u.allgather_recv;
+        v.allgather_sent += u.allgather_sent;
+        v.halo_recv += u.halo_recv;
+        v.halo_sent += u.halo_sent;
+        v.statreduce_recv += u.statreduce_recv;
+        v.statreduce_sent += u.statreduce_sent;
+    }
+    return v;
 }
 
 std::vector<uint8_t> Runner::ipc_export() {
@@ -850,6 +917,8 @@ const DeviceWeights* Runner::weights_for(int dev) {
 }
 
 Runner::~Runner() {
+    cfg_.reset();
+    for (auto ev : cfg_ev_) cudaEventDestroy(ev);
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     for (auto ev : graph_events_) cudaEventDestroy(ev);
     transport_.reset();   // uses the bands' streams and buffers
@@ -1429,8 +1498,15 @@ void Runner::step(int entry, const float* x, int t, int s, float* eps) {
     if (o_.profile) begin_profile();
     const bool displaced = e == STEP_DISPLACED;
     if (displaced) check_displaced_ready(s);
+    if (cfg_ && displaced) cfg_->check_displaced_ready(s);
     load_x(x);
     run_bands(t, s, displaced);
+    if (cfg_) {
+        cfg_->load_x(x);
+        cfg_->run_bands(t, s, displaced);
+        cfg_->count_macs(s, false);
+        cfg_combine();
+    }
     store_eps(eps);
     count_macs(s, false);
     record_trace(s, e == STEP_REFERENCE ? 0 : displaced ? 2 : 1);
@@ -1464,6 +1540,10 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
     launches_ = 0;
     if (o_.profile) begin_profile();
     load_x(x_T);
+    if (cfg_) {
+        cfg_->launches_ = 0;
+        cfg_->load_x(x_T);
+    }
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
     for (auto& b : bands_) {
         DeviceGuard g(b->dev);
@@ -1477,6 +1557,11 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
     // ~80 launches and ~30 exchange copies per step become one graph launch.
     bool same_dev = true;
     for (auto& b : bands_) same_dev &= b->dev == bands_[0]->dev;
+    // every band stream taking part in the loop (with guidance: the unconditional pass too)
+    std::vector<Program*> all;
+    for (auto& b : bands_) all.push_back(b.get());
+    if (cfg_)
+        for (auto& b : cfg_->bands_) all.push_back(b.get());
     // (the IPC transport's flag sequence numbers advance per exchange: not capturable)
     const bool use_graph = !traj && !o_.profile && graphs_enabled_ && (o_.world > 1 || same_dev) &&
                            !(o_.world > 1 && o_.transport == 1);
@@ -1488,8 +1573,8 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
     // (x_T upload) before the launch and fork them again after it.
     auto join_to_b0 = [&]() {
         Program& b0 = *bands_[0];
-        for (auto& b : bands_) {
-            if (b.get() == &b0) continue;
+        for (Program* b : all) {
+            if (b == &b0) continue;
             CUDA_CHECK(cudaEventRecord(b->ready[0], b->cs));
             CUDA_CHECK(cudaStreamWaitEvent(b0.cs, b->ready[0], 0));
         }
@@ -1497,13 +1582,13 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
     auto fork_from_b0 = [&]() {
         Program& b0 = *bands_[0];
         CUDA_CHECK(cudaEventRecord(b0.ready[0], b0.cs));
-        for (auto& b : bands_)
-            if (b.get() != &b0) CUDA_CHECK(cudaStreamWaitEvent(b->cs, b0.ready[0], 0));
+        for (Program* b : all)
+            if (b != &b0) CUDA_CHECK(cudaStreamWaitEvent(b->cs, b0.ready[0], 0));
     };
     // The per-plan time-embedding table is read by the captured graph: refresh it for this
     // plan before any replay (a no-op when it already holds these timesteps; an eager run of
     // another plan may have rewritten it in place since the capture).
-    for (auto& b : bands_) b->prepare_temb_plan(ts, n);
+    for (Program* b : all) b->prepare_temb_plan(ts, n);
     if (use_graph && graph_exec_ && key == graph_key_) {
         Program& b0 = *bands_[0];
         DeviceGuard g(b0.dev);
@@ -1522,12 +1607,14 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
         volumes_.statreduce_recv += graph_vol_.statreduce_recv;
         volumes_.statreduce_sent += graph_vol_.statreduce_sent;
         launches_ += graph_launches_;
+        if (cfg_) cfg_->total_macs_ += cfg_graph_macs_;
         for (int i = 0; i < n; ++i)
             record_trace(i, o_.mode == MODE_REFERENCE                          ? 0
                             : (o_.mode == MODE_DISPLACED && i >= 1 + o_.warmup) ? 2
                                                                                 : 1);
     } else {
     const uint64_t macs0 = total_macs_;
+    const uint64_t cfg_macs0 = cfg_ ? cfg_->total_macs_ : 0;
     const auto step_macs0 = step_device_macs_;
     const CommVolumes vol0 = volumes_;
     const long launches0 = launches_;
@@ -1543,8 +1630,8 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
         cudaEvent_t fork;
         CUDA_CHECK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
         CUDA_CHECK(cudaEventRecord(fork, b0.cs));
-        for (auto& b : bands_) {
-            if (b.get() != &b0) others.push_back(b->cs);
+        for (Program* b : all) {
+            if (b != &b0) others.push_back(b->cs);
             others.push_back(b->xs);
         }
         for (cudaStream_t s : others) CUDA_CHECK(cudaStreamWaitEvent(s, fork, 0));
@@ -1581,9 +1668,14 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
         }
         bool displaced = false;
         if (o_.mode == MODE_DISPLACED) displaced = i >= 1 + o_.warmup;
-        for (auto& b : bands_) b->use_temb_step(i);
+        for (Program* b : all) b->use_temb_step(i);
         run_bands(t, i, displaced);
-        for (auto& b : bands_) b->use_temb_step(-1);
+        if (cfg_) {
+            cfg_->run_bands(t, i, displaced);
+            cfg_->count_macs(i, false);
+            cfg_combine();
+        }
+        for (Program* b : all) b->use_temb_step(-1);
         count_macs(i, false);
         record_trace(i, o_.mode == MODE_REFERENCE ? 0 : displaced ? 2 : 1);
         const int t_next = i + 1 < n ? ts[i + 1] : -1;
@@ -1594,6 +1686,7 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
                         b->e, b->stem.interior(b->eb), b->stem.ld, b->cs);
             launches_ += 1;
         }
+        if (cfg_) cfg_refresh_stem();
     }
     if (use_graph) {
         Program& b0 = *bands_[0];
@@ -1610,7 +1703,7 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
         CUDA_CHECK(cudaGraphInstantiate(&graph_exec_, graph, 0));
         CUDA_CHECK(cudaGraphDestroy(graph));
         // events recorded inside the capture are re-armed as ordinary (completed) events
-        for (auto& b : bands_) {
+        for (Program* b : all) {
             DeviceGuard gb(b->dev);
             for (auto ev : b->ready)
                 if (ev) CUDA_CHECK(cudaEventRecord(ev, b->cs));
@@ -1630,7 +1723,8 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
         graph_vol_.halo_sent = volumes_.halo_sent - vol0.halo_sent;
         graph_vol_.statreduce_recv = volumes_.statreduce_recv - vol0.statreduce_recv;
         graph_vol_.statreduce_sent = volumes_.statreduce_sent - vol0.statreduce_sent;
-        graph_launches_ = launches_ - launches0;
+        graph_launches_ = launches_ - launches0 + (cfg_ ? cfg_->launches_ : 0);
+        cfg_graph_macs_ = cfg_ ? cfg_->total_macs_ - cfg_macs0 : 0;
         join_to_b0();
         CUDA_CHECK(cudaGraphLaunch(graph_exec_, b0.cs));
         fork_from_b0();
@@ -1669,6 +1763,7 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
         }
     }
     launches_ += long(bands_.size());
+    if (cfg_) launches_ += cfg_->launches_;
     last_device_ms_ = 0;
     for (size_t k = 0; k < bands_.size(); ++k) {
         DeviceGuard g(bands_[k]->dev);

@@ -45,6 +45,14 @@ struct RunnerOptions {
     bool no_comm = false;             // ablation ("No Comm."): exchanges skipped, local GN stats
     bool stress = false;              // scheduling noise around the exchanges (determinism check)
     uint64_t stress_seed = 0xC0FFEE;
+    // classifier-free guidance (beyond the reference API): cfg_scale != 0
+    // runs the U-Net a second time per step under the `uncond` condition (zeros if empty) on
+    // its own band streams, concurrently with the conditional pass, and denoises with
+    // eps = eps_u + cfg_scale (eps_c - eps_u).  world > 1 + NCCL: cfg_nccl_id = the id of the
+    // unconditional pass's communicator.
+    double cfg_scale = 0.0;
+    std::vector<float> uncond;
+    std::vector<uint8_t> cfg_nccl_id;
 };
 
 struct CommVolumes {
@@ -89,10 +97,10 @@ public:
 
     const PatchSpec& patch_spec(int device) const;
     long cached_input(int device, int layer, float* dst, int* nchw4);
-    uint64_t total_macs() const { return total_macs_; }
+    uint64_t total_macs() const { return total_macs_ + (cfg_ ? cfg_->total_macs() : 0); }
     const std::vector<TraceEvent>& trace(int device) const;
     std::vector<uint64_t> step_device_macs(int step) const;
-    CommVolumes volumes() const { return volumes_; }
+    CommVolumes volumes() const;
     ProfileTotals profile() const { return prof_; }
     long launches() const { return launches_; }
     // device time (CUDA events on the band compute streams, max over local bands) of the
@@ -141,6 +149,11 @@ private:
     std::unique_ptr<Transport> transport_;
     std::vector<int> posted_;      // per layer: last step whose gather exchange was posted
     std::vector<uint64_t> stress_state_;   // --stress-sched: per band splitmix64 state
+    std::unique_ptr<Runner> cfg_;          // classifier-free guidance: the unconditional pass
+    uint64_t cfg_graph_macs_ = 0;
+    std::vector<cudaEvent_t> cfg_ev_;      // per band: [2d] uncond eps ready, [2d+1] x_t refreshed
+    void cfg_combine();                    // eps of every band <- the guided eps
+    void cfg_refresh_stem();               // the unconditional pass's stem input <- x_t
     void stress_jitter(Program& b, int band);
     std::vector<int> gn_posted_;   // per layer: last step whose GN stats were posted
     uint64_t total_macs_ = 0;

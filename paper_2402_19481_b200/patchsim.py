@@ -189,6 +189,9 @@ class RunnerOptions:
     no_comm: bool = False            # ablation only ("No Comm."): exchanges skipped
     stress: bool = False             # --stress-sched: scheduling noise (results unchanged)
     stress_seed: int = 0xC0FFEE
+    cfg_scale: float = 0.0           # classifier-free guidance (beyond the reference API)
+    uncond: object = None            # unconditional condition (cond_dim floats; None = zeros)
+    cfg_nccl_id: bytes | None = None # world > 1 + NCCL: the unconditional pass's unique id
 
 
 class PatchRunner:
@@ -219,6 +222,16 @@ class PatchRunner:
         o.no_comm = int(opts.no_comm)
         o.stress = int(opts.stress)
         o.stress_seed = int(opts.stress_seed)
+        o.cfg_scale = float(opts.cfg_scale)
+        if opts.uncond is not None:
+            self._uncond = _f32(opts.uncond)
+            if self._uncond.size != cond.size:
+                raise InvalidArgument(f"classifier-free guidance: uncond length {self._uncond.size} "
+                                      f"!= condition length {cond.size}")
+            o.uncond = self._uncond.ctypes.data
+        if opts.cfg_nccl_id is not None:
+            self._cfg_id = C.create_string_buffer(bytes(opts.cfg_nccl_id), 128)
+            o.cfg_nccl_id = C.cast(self._cfg_id, C.c_void_p)
         h_ = C.c_void_p()
         N.check(N.lib().pp_runner_create(model._h, _p(cond), cond.size, h, w, C.byref(o),
                                          C.byref(h_)))

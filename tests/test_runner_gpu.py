@@ -413,3 +413,52 @@ def test_full_size_1024_properties():
     assert rel(sync2, ref) <= TOL["bf16"]
     disp = run("displaced", 2, warmup=1)
     assert rel(disp, ref) <= 5e-2                 # one stale step at 1024^2
+
+
+@pytest.mark.parametrize("mode,n,dtype", [("displaced", 2, "bf16"), ("sync-pp", 4, "fp32"),
+                                          ("reference", 1, "bf16")])
+def test_classifier_free_guidance_vs_oracle(mode, n, dtype):
+    # cfg_scale (beyond the reference API): a second, unconditional
+    # U-Net pass per step on its own band streams, eps = eps_u + s (eps_c - eps_u); per-step
+    # latents against the oracle's two lockstep reference runners (run_sampling_cfg), graph
+    # replay bitwise equal to the eager loop, both passes' MACs counted
+    cfg = TOY
+    m = P.build_model(cfg, 42)
+    cond = O.random_condition(cfg.cond_dim, 7)
+    unc = O.random_condition(cfg.cond_dim, 99)
+    x = O.random_normal(1, cfg.in_channels, 32, 32, 1234)
+    abar = O.make_schedule()
+    plan = O.make_plan(1000, 4)
+    r = P.PatchRunner(m, cond, 32, 32, mode=mode, n_devices=n, warmup_steps=1, dtype=dtype,
+                      cfg_scale=3.0, uncond=unc)
+    eager, traj = r.sample(x, plan, abar, trajectory=True)
+    g, _ = r.sample(x, plan, abar)
+    assert np.array_equal(g, eager)
+    ref = O.run_sampling_cfg(ocfg(cfg), mode, n, 32, 32, 4, 1, cfg_scale=3.0, uncond=unc)
+    for i in range(4):
+        assert rel(traj[i], ref["trajectory"][i]) <= TOL[dtype], i
+    assert rel(g, ref["x0"]) <= TOL[dtype]
+    plain = O.run_sampling(ocfg(cfg), mode, n, 32, 32, 4, 1)["x0"]
+    assert rel(plain, ref["x0"]) > 0.05                     # guidance really applied (7.8 %)
+    assert r.total_macs() == 2 * ref["total_macs"]          # two sample() calls
+
+
+def test_classifier_free_guidance_step_api_and_errors():
+    # run_step with guidance returns the guided eps of the two passes (oracle: the two
+    # reference runners' eps combined in fp64); uncond length and naive mode are checked
+    cfg = TOY
+    m = P.build_model(cfg, 42)
+    cond = O.random_condition(cfg.cond_dim, 7)
+    x = O.random_normal(1, cfg.in_channels, 32, 32, 1234)
+    r = P.PatchRunner(m, cond, 32, 32, mode="sync-pp", n_devices=2, dtype="fp32", cfg_scale=2.5)
+    eps = r.run_step(x, 700, 0)
+    om = O.build_model(ocfg(cfg), 42)
+    ec = O.PatchRunner(om, cond, 32, 32, "sync-pp", 2, 4, "corrected").run_step(x, 700, 0)
+    eu = O.PatchRunner(om, np.zeros_like(cond), 32, 32, "sync-pp", 2, 4, "corrected").run_step(x, 700, 0)
+    ref = (eu.astype(np.float64) + 2.5 * (ec.astype(np.float64) - eu)).astype(np.float32)
+    assert rel(eps, ref) <= EPS_TOL["fp32"]
+    with pytest.raises(P.InvalidArgument, match="uncond length"):
+        P.PatchRunner(m, cond, 32, 32, mode="displaced", n_devices=2, cfg_scale=2.0,
+                      uncond=np.zeros(cond.size + 1, np.float32))
+    with pytest.raises(P.InvalidArgument, match="naive mode"):
+        P.PatchRunner(m, cond, 32, 32, mode="naive", n_devices=2, cfg_scale=2.0)
