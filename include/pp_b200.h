@@ -162,6 +162,10 @@ typedef struct {
     double cfg_scale;
     const float* uncond;
     const void* cfg_nccl_id;
+    /* condition tokens (beyond the reference API, which projects one): cond (and uncond) hold
+     * cond_tokens x model cond_dim floats and every CrossAttn layer attends over the
+     * cond_tokens projected rows; default 1 (the reference's layer_cross_attn exactly) */
+    int cond_tokens;
 } pp_runner_opts;
 PP_API void pp_runner_opts_default(pp_runner_opts* o);
 

@@ -77,7 +77,8 @@ class RunnerOpts(C.Structure):
                 ("rank", C.c_int), ("nccl_id", C.c_void_p), ("device", C.c_int),
                 ("profile", C.c_int), ("transport", C.c_int), ("no_comm", C.c_int),
                 ("stress", C.c_int), ("stress_seed", C.c_ulonglong),
-                ("cfg_scale", C.c_double), ("uncond", C.c_void_p), ("cfg_nccl_id", C.c_void_p)]
+                ("cfg_scale", C.c_double), ("uncond", C.c_void_p), ("cfg_nccl_id", C.c_void_p),
+                ("cond_tokens", C.c_int)]
 
 
 _V, _I, _L, _D, _U64, _F = C.c_void_p, C.c_int, C.c_long, C.c_double, C.c_uint64, C.c_float

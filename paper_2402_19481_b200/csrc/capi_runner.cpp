@@ -60,6 +60,8 @@ pp::RunnerOptions opts_of(const pp_runner_opts* o) {
     r.stress = o->stress != 0;
     r.stress_seed = o->stress_seed;
     r.cfg_scale = o->cfg_scale;
+    r.cond_tokens = o->cond_tokens;
+    if (r.cond_tokens < 1) throw std::invalid_argument("pp_runner_create: cond_tokens must be >= 1");
     if (!std::isfinite(r.cfg_scale)) throw std::invalid_argument("pp_runner_create: cfg_scale not finite");
     if (r.cfg_scale != 0.0 && r.world > 1 && r.transport == PP_TRANSPORT_NCCL) {
         need(o->cfg_nccl_id, "pp_runner_create(cfg_nccl_id)");
@@ -313,6 +315,7 @@ PP_API void pp_runner_opts_default(pp_runner_opts* o) {
     o->cfg_scale = 0.0;
     o->uncond = nullptr;
     o->cfg_nccl_id = nullptr;
+    o->cond_tokens = 1;
 }
 
 PP_API int pp_runner_create(const pp_model* m, const float* cond, int cond_dim, int h, int w,

@@ -29,7 +29,14 @@ struct LayerWeights {
     float* beta = nullptr;
     float* temb_w = nullptr;  // AddTimeEmb: [C][time_dim] fp32 (reference layout)
     float* temb_b = nullptr;
-    float* cross_v = nullptr; // CrossAttn: projected value vector [ld] fp32
+    float* cross_v = nullptr; // CrossAttn: projected value vector [ld] fp32 (one token)
+    // CrossAttn over T > 1 condition tokens (beyond the reference API): the projected keys and
+    // values in the element type, [T][ld] each (K: the S GEMM's B; V: the PV GEMM's B, read
+    // MN-major), and V^T [ld][T_pad] for the TF32 PV GEMM
+    void* cross_k_tok = nullptr;
+    void* cross_v_tok = nullptr;
+    void* cross_vt_tok = nullptr;
+    int tokens = 1, tokens_pad = 0;
     // stem conv with in_ch <= 4 as one-K-block GEMM: [n_pad][kStemK] (tap-major, 4 channels)
     void* w_stem = nullptr;
 };
@@ -39,7 +46,8 @@ struct DeviceWeights {
     Elem e = Elem::BF16;
     std::vector<LayerWeights> L;
     std::vector<void*> allocs;
-    DeviceWeights(const Model& m, const std::vector<float>& cond, int dev, Elem e);
+    // cond = tokens x cond_dim floats (tokens > 1: multi-token cross-attention)
+    DeviceWeights(const Model& m, const std::vector<float>& cond, int dev, Elem e, int tokens = 1);
     ~DeviceWeights();
     void* alloc(size_t bytes);
 };
@@ -114,6 +122,10 @@ struct Program {
     float* attn_rowmax = nullptr;
     float* attn_rscale = nullptr;
     void* Vt = nullptr;
+    // multi-token cross-attention scratch: P [m][tokens_pad], row maxima, 1/l
+    void* Pc = nullptr;
+    float* rowmax_c = nullptr;
+    float* rscale_c = nullptr;
     int attn_c = 0;   // attention channels
     // V read MN-major by the PV GEMM (bf16, whole 128-byte channel chunks); else V^T
     bool attn_v_mn() const { return e == Elem::BF16 && attn_c % 64 == 0; }
@@ -171,6 +183,8 @@ struct Program {
     void conv(const Group& g, int par);
     void own_kv(const Group& g, int par_post, int par_use);
     void attention(const Group& g, int par, int par_out);
+    // CrossAttn over T > 1 condition tokens: S GEMM (softmax epilogue) -> rescale -> PV GEMM
+    void cross_attention(const Group& g);
     void gn_stats(const Group& g, int par);
     void gn_apply(const Group& g, int combine_mode, int par_cur, int par_prev);
     void simple(const Group& g, int par);

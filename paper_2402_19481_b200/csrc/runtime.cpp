@@ -82,8 +82,10 @@ void* DeviceWeights::alloc(size_t bytes) {
     return p;
 }
 
-DeviceWeights::DeviceWeights(const Model& m, const std::vector<float>& cond, int dev_, Elem e_)
+DeviceWeights::DeviceWeights(const Model& m, const std::vector<float>& cond, int dev_, Elem e_,
+                             int tokens)
     : dev(dev_), e(e_) {
+    if (tokens < 1) throw std::invalid_argument("condition: tokens must be >= 1");
     DeviceGuard g(dev);
     const size_t eb = elem_bytes(e);
     L.resize(m.layers.size());
@@ -154,18 +156,41 @@ DeviceWeights::DeviceWeights(const Model& m, const std::vector<float>& cond, int
             case Kind::CrossAttn: {
                 // project_condition (model.cpp:252-263): only the value half reaches the
                 // output -- softmax over a single key is exactly 1 (test_model.cpp:216-232).
-                if (int(cond.size()) != d.cond_dim)
-                    throw std::invalid_argument("condition: expected " + std::to_string(d.cond_dim) +
+                if (int(cond.size()) != d.cond_dim * tokens)
+                    throw std::invalid_argument("condition: expected " + std::to_string(d.cond_dim * tokens) +
                                                 " values, got " + std::to_string(cond.size()));
                 if (!d_cond) {
                     d_cond = static_cast<float*>(alloc(cond.size() * 4));
                     CUDA_CHECK(cudaMemcpy(d_cond, cond.data(), cond.size() * 4, cudaMemcpyHostToDevice));
                 }
                 const int ld = act_ld(d.out_ch, e);
-                w.cross_v = static_cast<float*>(alloc(size_t(ld) * 4));
                 float* wv = up_f32(d.weight2, d.out_ch * d.cond_dim);
                 float* bv = up_f32(d.bias2, d.out_ch);
-                gemv_f64(wv, bv, d_cond, d.out_ch, d.cond_dim, w.cross_v, 0);
+                if (tokens == 1) {
+                    w.cross_v = static_cast<float*>(alloc(size_t(ld) * 4));
+                    gemv_f64(wv, bv, d_cond, d.out_ch, d.cond_dim, w.cross_v, 0);
+                    break;
+                }
+                // project_condition (model.cpp:252-263) over `tokens` condition rows: K and V
+                // [T][C] (fp64 accumulate -> fp32 -> element type), padded to [T][ld]
+                float* wk = up_f32(d.weight, d.out_ch * d.cond_dim);
+                float* bk = up_f32(d.bias, d.out_ch);
+                float* kf = static_cast<float*>(alloc(size_t(tokens) * ld * 4));
+                float* vf = static_cast<float*>(alloc(size_t(tokens) * ld * 4));
+                for (int j = 0; j < tokens; ++j) {
+                    gemv_f64(wk, bk, d_cond + size_t(j) * d.cond_dim, d.out_ch, d.cond_dim, kf + size_t(j) * ld, 0);
+                    gemv_f64(wv, bv, d_cond + size_t(j) * d.cond_dim, d.out_ch, d.cond_dim, vf + size_t(j) * ld, 0);
+                }
+                w.tokens = tokens;
+                w.tokens_pad = round_up(tokens, 64);
+                w.cross_k_tok = alloc(size_t(tokens) * ld * eb);
+                w.cross_v_tok = alloc(size_t(tokens) * ld * eb);
+                f32_to_elem(kf, e, w.cross_k_tok, (long long)tokens * ld, e == Elem::F32, 0);
+                f32_to_elem(vf, e, w.cross_v_tok, (long long)tokens * ld, e == Elem::F32, 0);
+                if (!(e == Elem::BF16 && d.out_ch % 64 == 0)) {   // the PV GEMM takes V^T K-major
+                    w.cross_vt_tok = alloc(size_t(ld) * w.tokens_pad * eb);
+                    transpose(e, w.cross_v_tok, tokens, ld, ld, w.cross_vt_tok, w.tokens_pad, 0);
+                }
                 break;
             }
             default: break;
@@ -173,11 +198,19 @@ DeviceWeights::DeviceWeights(const Model& m, const std::vector<float>& cond, int
     }
     // PatchRunner::cond_k/cond_v (runtime.cpp:145-163) caches the FIRST CrossAttn layer's
     // projection and uses it for every CrossAttn layer; forward_collect does the same.
-    float* first = nullptr;
+    const LayerWeights* first = nullptr;
     for (const Layer& d : m.layers)
         if (d.kind == Kind::CrossAttn) {
-            if (!first) first = L[d.id].cross_v;
-            else L[d.id].cross_v = first;
+            if (!first) {
+                first = &L[d.id];
+            } else {
+                L[d.id].cross_v = first->cross_v;
+                L[d.id].cross_k_tok = first->cross_k_tok;
+                L[d.id].cross_v_tok = first->cross_v_tok;
+                L[d.id].cross_vt_tok = first->cross_vt_tok;
+                L[d.id].tokens = first->tokens;
+                L[d.id].tokens_pad = first->tokens_pad;
+            }
         }
     CUDA_CHECK(cudaDeviceSynchronize());
 }
@@ -384,7 +417,7 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
             const Group& g = groups[gi];
             const Group& gc = groups[gi + 1];
             if (g.kind == Kind::SelfAttn && gc.kind == Kind::CrossAttn && gc.skip == g.last &&
-                srcs_count.count(g.last) == 1 && gc.last != L - 1)
+                srcs_count.count(g.last) == 1 && gc.last != L - 1 && wts->L[gc.first].tokens == 1)
                 merged_into_prev[gi + 1] = 1;
             // Linear / GroupNorm group -> Upsample of its output: the producer stores the
             // nearest-2x upsample directly (its own output is not materialised)
@@ -503,6 +536,36 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
                                   sc, sms);
                 else
                     plan_gemm(plans[gi][p], e, P, m_rows, s_pad, s_pad, Vt, in.C, s_pad, e2, sc, sms);
+            } else if (d.kind == Kind::CrossAttn && lw.tokens > 1) {
+                // layer_cross_attn (model.cpp:265-271) over T condition tokens: q = the band's
+                // tokens, K / V = the T projected condition rows (the same for every band)
+                const int m_rows = int(in.pix());
+                const int tp = lw.tokens_pad;
+                if (!Pc) {
+                    Pc = alloc(size_t(m_rows) * tp * eb);
+                    CUDA_CHECK(cudaMemset(Pc, 0, size_t(m_rows) * tp * eb));
+                    rscale_c = static_cast<float*>(alloc(size_t(m_rows) * 4));
+                }
+                EpilogueSpec es;
+                es.out = Pc;
+                es.out_ld = tp;
+                es.out_f32 = e == Elem::F32;
+                es.round_tf32 = rnd;
+                es.n_valid = lw.tokens;
+                es.sm_rowmax = static_cast<float*>(Pc);   // marks the softmax epilogue
+                es.sm_scale = float(1.0 / std::sqrt(double(d.in_ch)));
+                es.sm_ld = m_rows;
+                GemmPlan& sp = s_plans[gi][p];
+                plan_gemm(sp, e, in.interior(eb), m_rows, in.ld, in.ld, lw.cross_k_tok, lw.tokens, in.ld,
+                          es, sc, sms);
+                if (!rowmax_c) rowmax_c = static_cast<float*>(alloc(size_t(sp.a.n_tiles) * m_rows * 4));
+                sp.a.sm_rowmax = rowmax_c;
+                e2.row_scale = rscale_c;
+                if (lw.cross_vt_tok)
+                    plan_gemm(plans[gi][p], e, Pc, m_rows, tp, tp, lw.cross_vt_tok, d.out_ch, tp, e2, sc, sms);
+                else
+                    plan_gemm_bmn(plans[gi][p], e, Pc, m_rows, tp, tp, lw.cross_v_tok, lw.tokens, d.out_ch,
+                                  in.ld, e2, sc, sms);
             }
         }
         if (fuse_gn) fused_stats[next] = 1;
@@ -685,6 +748,21 @@ void Program::attention(const Group& g, int par, int par_out) {
     count(3);
 }
 
+void Program::cross_attention(const Group& g) {
+    const size_t gi = size_t(&g - groups.data());
+    const LayerWeights& lw = wts->L[g.first];
+    const GemmPlan& sp = s_plans[gi][0];
+    const GemmPlan& pv = plans[gi][0];
+    const int m_rows = int(input_of(g.first).pix());
+    run_timed(CAT_GEMM, sp.flops, [&] { launch_gemm(sp, cs); });
+    run_timed(CAT_OTHER, 0, [&] {
+        attn_rescale(e, Pc, lw.tokens_pad, m_rows, lw.tokens, rowmax_c, sp.a.n_tiles, sp.a.block_n,
+                     m_rows, rscale_c, rnd, cs);
+    });
+    run_timed(CAT_GEMM, pv.flops, [&] { launch_gemm(pv, cs); });
+    count(3);
+}
+
 void Program::gn_stats(const Group& g, int par) {
     const Act& in = input_of(g.first);
     const LayerX& x = lx[g.first];
@@ -738,6 +816,10 @@ void Program::gn_apply(const Group& g, int mode, int par_cur, int par_prev) {
 
 void Program::simple(const Group& g, int par) {
     const Layer& d = m->layers[g.first];
+    if (d.kind == Kind::CrossAttn && wts->L[g.first].tokens > 1) {
+        cross_attention(g);
+        return;
+    }
     const Act& in = input_of(g.first);
     const int L = int(m->layers.size());
     if (g.last == L - 1) throw std::invalid_argument("unsupported final layer kind");
@@ -912,7 +994,7 @@ void Runner::ipc_connect(const uint8_t* blobs, size_t per_rank) {
 const DeviceWeights* Runner::weights_for(int dev) {
     for (auto& wp : weights_)
         if (wp->dev == dev) return wp.get();
-    weights_.push_back(std::make_unique<DeviceWeights>(m_, cond_, dev, o_.elem));
+    weights_.push_back(std::make_unique<DeviceWeights>(m_, cond_, dev, o_.elem, o_.cond_tokens));
     return weights_.back().get();
 }
 
@@ -972,7 +1054,8 @@ void Runner::count_macs(int s, bool naive) {
             uint64_t macs = 0;
             for (const Layer& ld : m_.layers) {
                 const int lh = ph / ld.scale_in, lw = pw / ld.scale_in;
-                macs += macs_of_layer(ld, Region{0, lh, lh, lw});
+                macs += macs_of_layer(ld, Region{0, lh, lh, lw}) *
+                        (ld.kind == Kind::CrossAttn ? uint64_t(o_.cond_tokens) : 1u);
             }
             step_device_macs_[s][d] += macs;
             total_macs_ += macs;
@@ -982,7 +1065,10 @@ void Runner::count_macs(int s, bool naive) {
     for (int d = 0; d < n_dev_; ++d) {
         const PatchSpec& sp = specs_[std::min<size_t>(d, specs_.size() - 1)];
         uint64_t macs = 0;
-        for (const Layer& ld : m_.layers) macs += macs_of_layer(ld, sp.layer_in[ld.id]);
+        // CrossAttn over T condition tokens: 2 m T d (costmodel.cpp:50-54 has T = 1)
+        for (const Layer& ld : m_.layers)
+            macs += macs_of_layer(ld, sp.layer_in[ld.id]) *
+                    (ld.kind == Kind::CrossAttn ? uint64_t(o_.cond_tokens) : 1u);
         step_device_macs_[s][d] += macs;
         total_macs_ += macs;
     }

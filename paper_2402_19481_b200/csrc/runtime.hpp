@@ -52,6 +52,9 @@ struct RunnerOptions {
     // unconditional pass's communicator.
     double cfg_scale = 0.0;
     std::vector<float> uncond;
+    // condition tokens (beyond the reference API, which has one): cond holds cond_tokens x
+    // cond_dim floats and every CrossAttn layer attends over the cond_tokens projected rows
+    int cond_tokens = 1;
     std::vector<uint8_t> cfg_nccl_id;
 };
 

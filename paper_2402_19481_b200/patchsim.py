@@ -202,6 +202,9 @@ class PatchRunner:
         self.opts = opts
         self.model = model
         self.h, self.w = h, w
+        # a 2-D cond [T][cond_dim] is T condition tokens (multi-token cross-attention, beyond
+        # the reference API); 1-D is the reference's single condition vector
+        tokens = int(np.asarray(cond).shape[0]) if np.asarray(cond).ndim == 2 else 1
         cond = _f32(cond)
         o = N.RunnerOpts()
         N.lib().pp_runner_opts_default(C.byref(o))
@@ -223,6 +226,7 @@ class PatchRunner:
         o.stress = int(opts.stress)
         o.stress_seed = int(opts.stress_seed)
         o.cfg_scale = float(opts.cfg_scale)
+        o.cond_tokens = tokens
         if opts.uncond is not None:
             self._uncond = _f32(opts.uncond)
             if self._uncond.size != cond.size:

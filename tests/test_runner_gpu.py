@@ -462,3 +462,55 @@ def test_classifier_free_guidance_step_api_and_errors():
                       uncond=np.zeros(cond.size + 1, np.float32))
     with pytest.raises(P.InvalidArgument, match="naive mode"):
         P.PatchRunner(m, cond, 32, 32, mode="naive", n_devices=2, cfg_scale=2.0)
+
+
+def _oracle_run(cfg, cond, mode, n, hw, steps, warmup, seeds=(42, 1234)):
+    """run_sampling (runtime.cpp:494-526) on the oracle with an explicit condition."""
+    om = O.build_model(ocfg(cfg), seeds[0])
+    r = O.PatchRunner(om, cond, hw, hw, mode, 1 if mode == "reference" else n, warmup, "corrected")
+    counter = [0]
+
+    def ex(x, t):
+        e = r.run_step(x, t, counter[0])
+        counter[0] += 1
+        return e
+
+    return O.sample(ex, O.make_plan(1000, steps), O.make_schedule(), 1, cfg.in_channels, hw, hw,
+                    seeds[1])
+
+
+@pytest.mark.parametrize("mode,n,dtype,tokens", [("displaced", 2, "bf16", 5), ("sync-pp", 4, "fp32", 77),
+                                                 ("reference", 1, "bf16", 3)])
+def test_multi_token_cross_attention_vs_oracle(mode, n, dtype, tokens):
+    # layer_cross_attn (model.cpp:265-271) over T condition tokens (beyond the reference API,
+    # which projects one): a 2-D condition [T][cond_dim]; the CrossAttn layer becomes a real
+    # attention (S GEMM + softmax epilogue, rescale, PV GEMM) against the T projected rows
+    cfg = TOY
+    m = P.build_model(cfg, 42)
+    cond = np.random.default_rng(tokens).standard_normal((tokens, cfg.cond_dim)).astype(np.float32)
+    x = O.random_normal(1, cfg.in_channels, 32, 32, 1234)
+    r = P.PatchRunner(m, cond, 32, 32, mode=mode, n_devices=n, warmup_steps=1, dtype=dtype)
+    got, traj = r.sample(x, O.make_plan(1000, 4), O.make_schedule(), trajectory=True)
+    g, _ = r.sample(x, O.make_plan(1000, 4), O.make_schedule())
+    assert np.array_equal(g, got)
+    ref, rtraj = _oracle_run(cfg, cond, mode, n, 32, 4, 1)
+    for i in range(4):
+        assert rel(traj[i], rtraj[i]) <= TOL[dtype], i
+    assert rel(got, ref) <= TOL[dtype]
+    single = _oracle_run(cfg, cond[0], mode, n, 32, 4, 1)[0]
+    assert rel(single, ref) > 5e-3                    # the extra tokens matter
+
+
+def test_multi_token_single_token_is_the_reference_path():
+    # a [1][cond_dim] condition is exactly the reference's single-vector path
+    cfg = TOY
+    m = P.build_model(cfg, 42)
+    cond = O.random_condition(cfg.cond_dim, 7)
+    x = O.random_normal(1, cfg.in_channels, 32, 32, 1234)
+    a = P.PatchRunner(m, cond, 32, 32, mode="displaced", n_devices=2, warmup_steps=1, dtype="bf16")
+    b = P.PatchRunner(m, cond[None, :], 32, 32, mode="displaced", n_devices=2, warmup_steps=1,
+                      dtype="bf16")
+    plan, abar = O.make_plan(1000, 4), O.make_schedule()
+    assert np.array_equal(a.sample(x, plan, abar)[0], b.sample(x, plan, abar)[0])
+    with pytest.raises(P.InvalidArgument, match="condition: expected"):
+        P.PatchRunner(m, np.zeros((3, cfg.cond_dim + 1), np.float32), 32, 32, mode="reference")
