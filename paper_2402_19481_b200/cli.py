@@ -54,7 +54,7 @@ def parse_size(s: str):
 
 CONFIG_KEYS = ("mode", "devices", "steps", "warmup", "size", "model-seed", "noise-seed",
                "cond-seed", "out", "compare-against", "cost-profile", "emit", "gn-scheme",
-               "stress-sched", "matrix", "model", "dtype", "weights")
+               "stress-sched", "matrix", "model", "dtype", "weights", "cfg-scale", "cond-tokens")
 MATRIX_KEYS = ("mode", "devices", "steps", "warmup", "size", "model-seed", "noise-seed",
                "cond-seed", "gn-scheme")
 
@@ -213,6 +213,10 @@ def build_parser():
     ap.add_argument("--stress-sched", action="store_true",
                     help="inject scheduling noise around the exchanges (determinism check)")
     ap.add_argument("--matrix", default="", help="experiment list; each line key=value overrides")
+    ap.add_argument("--cfg-scale", type=float, default=0.0,
+                    help="classifier-free guidance scale (0 = off; unconditional = zeros)")
+    ap.add_argument("--cond-tokens", type=int, default=1,
+                    help="condition tokens (random_condition over tokens x cond_dim)")
     return ap
 
 
@@ -234,6 +238,7 @@ def run(argv) -> int:
         args.devices, args.steps, args.warmup = int(args.devices), int(args.steps), int(args.warmup)
         args.model_seed, args.noise_seed = int(args.model_seed), int(args.noise_seed)
         args.cond_seed = int(args.cond_seed)
+        args.cfg_scale, args.cond_tokens = float(args.cfg_scale), int(args.cond_tokens)
     except SystemExit as e:
         return 0 if e.code == 0 else 2
     except ValueError as e:
@@ -271,13 +276,17 @@ def run(argv) -> int:
 
         model = (A.load_weights(mcfg, args.weights) if args.weights
                  else P.build_model(mcfg, args.model_seed))
-        cond = P.random_condition(mcfg.cond_dim, args.cond_seed)
+        if args.cond_tokens < 1:
+            raise P.InvalidArgument("--cond-tokens must be >= 1")
+        cond = P.random_condition(mcfg.cond_dim * args.cond_tokens, args.cond_seed)
+        if args.cond_tokens > 1:
+            cond = cond.reshape(args.cond_tokens, mcfg.cond_dim)
         x_T = P.random_normal(1, mcfg.in_channels, h, w, args.noise_seed)
         abar = P.make_schedule(rc.schedule_steps, rc.beta_start, rc.beta_end)
         plan = P.make_plan(rc.schedule_steps, args.steps)
         runner = P.PatchRunner(model, cond, h, w, mode=args.mode, n_devices=args.devices,
                                warmup_steps=args.warmup, gn_scheme=args.gn_scheme,
-                               dtype=args.dtype, stress=args.stress_sched)
+                               dtype=args.dtype, stress=args.stress_sched, cfg_scale=args.cfg_scale)
         x0, traj = runner.sample(x_T, plan, abar, trajectory="tensor" in emit)
         device_ms = runner.last_device_ms()
 
