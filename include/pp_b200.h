@@ -73,6 +73,10 @@ PP_API int pp_device_count(void);
  * proj/include/patchsim/model.hpp:30-59, proj/src/model.cpp:158-218 */
 typedef struct {
     int in_channels, base_channels, levels, groups, cond_dim, attn_at_level;
+    /* deeper graphs (beyond the reference API; 0 = the reference graph): residual blocks per
+     * level (0 -> 1), attention-level bit mask (0 -> attn_at_level only), attention blocks
+     * after each residual block there (0 -> 1), attention on the up path too (0 / 1) */
+    int res_blocks, attn_levels, attn_depth, attn_up;
 } pp_model_config;
 
 typedef struct {

@@ -52,7 +52,8 @@ _lock = threading.Lock()
 
 class ModelConfig(C.Structure):
     _fields_ = [(n, C.c_int) for n in ("in_channels", "base_channels", "levels", "groups",
-                                        "cond_dim", "attn_at_level")]
+                                        "cond_dim", "attn_at_level", "res_blocks", "attn_levels",
+                                        "attn_depth", "attn_up")]
 
 
 class LayerDesc(C.Structure):

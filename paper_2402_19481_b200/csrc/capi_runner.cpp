@@ -28,6 +28,10 @@ pp::ModelConfig cfg_of(const pp_model_config* c) {
     m.groups = c->groups;
     m.cond_dim = c->cond_dim;
     m.attn_at_level = c->attn_at_level;
+    m.res_blocks = c->res_blocks ? c->res_blocks : 1;
+    m.attn_levels = c->attn_levels;
+    m.attn_depth = c->attn_depth ? c->attn_depth : 1;
+    m.attn_up = c->attn_up;
     return m;
 }
 
@@ -231,7 +235,7 @@ PP_API void pp_run_config_default(pp_run_config* c) {
     c->model_seed = 42;
     c->noise_seed = 1234;
     c->cond_seed = 7;
-    c->model = pp_model_config{4, 16, 3, 4, 8, -1};
+    c->model = pp_model_config{4, 16, 3, 4, 8, -1, 0, 0, 0, 0};
     c->schedule_steps = 1000;
     c->beta_start = 1e-4;
     c->beta_end = 2e-2;

@@ -31,6 +31,10 @@ void ModelConfig::validate() const {
         throw std::invalid_argument("ModelConfig: base_channels must be divisible by groups");
     if (attn_level() < 0 || attn_level() >= levels)
         throw std::invalid_argument("ModelConfig: attn_at_level out of range");
+    if (res_blocks < 1 || attn_depth < 1)
+        throw std::invalid_argument("ModelConfig: res_blocks and attn_depth must be >= 1");
+    if (attn_levels < 0 || attn_levels >= (1 << levels))
+        throw std::invalid_argument("ModelConfig: attn_levels names a level that does not exist");
 }
 
 uint64_t substream_seed(uint64_t seed, uint64_t a, uint64_t b) {
@@ -169,11 +173,13 @@ Model build_graph(const ModelConfig& cfg) {
     std::vector<int> exits(cfg.levels, -1);
     for (int lv = 0; lv < cfg.levels; ++lv) {
         const int scale = 1 << lv;
-        const int entry = int(b.m.layers.size()) - 1;
-        exits[lv] = b.res_block(b.level_ch(lv), scale, entry);
-        if (lv == cfg.attn_level()) {
-            b.attn_block(b.level_ch(lv), scale);
-            exits[lv] = int(b.m.layers.size()) - 1;
+        for (int rb = 0; rb < cfg.res_blocks; ++rb) {
+            const int entry = int(b.m.layers.size()) - 1;
+            exits[lv] = b.res_block(b.level_ch(lv), scale, entry);
+            if (cfg.has_attn(lv)) {
+                for (int k = 0; k < cfg.attn_depth; ++k) b.attn_block(b.level_ch(lv), scale);
+                exits[lv] = int(b.m.layers.size()) - 1;
+            }
         }
         if (lv + 1 < cfg.levels) b.conv(Kind::DownConv, b.level_ch(lv), b.level_ch(lv + 1), scale);
     }
@@ -182,8 +188,12 @@ Model build_graph(const ModelConfig& cfg) {
         b.upsample(b.level_ch(lv + 1), scale * 2);
         b.conv(Kind::Conv, b.level_ch(lv + 1), b.level_ch(lv), scale);
         b.add_skip(exits[lv], b.level_ch(lv), scale);
-        const int entry = int(b.m.layers.size()) - 1;
-        b.res_block(b.level_ch(lv), scale, entry);
+        for (int rb = 0; rb < cfg.res_blocks; ++rb) {
+            const int entry = int(b.m.layers.size()) - 1;
+            b.res_block(b.level_ch(lv), scale, entry);
+            if (cfg.attn_up && cfg.has_attn(lv))
+                for (int k = 0; k < cfg.attn_depth; ++k) b.attn_block(b.level_ch(lv), scale);
+        }
     }
     b.gn(b.level_ch(0), 1);
     b.silu(b.level_ch(0), 1);

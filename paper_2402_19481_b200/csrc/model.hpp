@@ -31,7 +31,18 @@ struct ModelConfig {
     int groups = 4;
     int cond_dim = 8;
     int attn_at_level = -1;
+    // Deeper graphs (beyond the reference API; the defaults build the
+    // reference graph exactly): res_blocks residual blocks per level on both paths, attention
+    // at the levels of the attn_levels bit mask (0: attn_level() only), attn_depth attention
+    // blocks after every residual block there, and attn_up: also on the up path.
+    int res_blocks = 1;
+    int attn_levels = 0;
+    int attn_depth = 1;
+    int attn_up = 0;
     int attn_level() const { return attn_at_level < 0 ? levels - 1 : attn_at_level; }
+    bool has_attn(int lv) const {
+        return attn_levels ? ((attn_levels >> lv) & 1) != 0 : lv == attn_level();
+    }
     int depth_divisor() const { return 1 << (levels - 1); }
     void validate() const;  // throws std::invalid_argument (model.cpp:25-33)
 };

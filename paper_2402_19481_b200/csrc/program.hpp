@@ -115,20 +115,19 @@ struct Program {
     // scratch
     double* gn_partial = nullptr;
     unsigned int* gn_ticket = nullptr;
-    // attention: P = softmax numerators [m][s_pad] (padding columns stay zero), per key tile
-    // row maxima [n_tiles][m], 1 / row sums [m]; fp32 mode: V^T [C][s_pad] for the PV GEMM
-    void* P = nullptr;
-    int s_pad = 0;
-    float* attn_rowmax = nullptr;
-    float* attn_rscale = nullptr;
-    void* Vt = nullptr;
-    // multi-token cross-attention scratch: P [m][tokens_pad], row maxima, 1/l
-    void* Pc = nullptr;
-    float* rowmax_c = nullptr;
-    float* rscale_c = nullptr;
-    int attn_c = 0;   // attention channels
-    // V read MN-major by the PV GEMM (bf16, whole 128-byte channel chunks); else V^T
-    bool attn_v_mn() const { return e == Elem::BF16 && attn_c % 64 == 0; }
+    // attention scratch per attention group (self-attention, or cross-attention over T > 1
+    // tokens): P = softmax numerators [m][s_pad] (padding columns stay zero), per key tile row
+    // maxima [n_tiles][m], 1 / row sums [m]; V^T [C][s_pad] when the PV GEMM cannot read V
+    // MN-major (TF32, or channels not filling 128-byte chunks)
+    struct AttnScratch {
+        void* P = nullptr;
+        int s_pad = 0;
+        float* rowmax = nullptr;
+        float* rscale = nullptr;
+        void* Vt = nullptr;
+        bool v_mn = false;
+    };
+    std::vector<AttnScratch> attn_sc;   // per group
     // time embedding
     std::vector<float*> temb_out;   // per layer (nullptr unless AddTimeEmb)
     TembLayer* temb_dev = nullptr;

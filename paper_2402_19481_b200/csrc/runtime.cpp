@@ -197,21 +197,9 @@ DeviceWeights::DeviceWeights(const Model& m, const std::vector<float>& cond, int
         }
     }
     // PatchRunner::cond_k/cond_v (runtime.cpp:145-163) caches the FIRST CrossAttn layer's
-    // projection and uses it for every CrossAttn layer; forward_collect does the same.
-    const LayerWeights* first = nullptr;
-    for (const Layer& d : m.layers)
-        if (d.kind == Kind::CrossAttn) {
-            if (!first) {
-                first = &L[d.id];
-            } else {
-                L[d.id].cross_v = first->cross_v;
-                L[d.id].cross_k_tok = first->cross_k_tok;
-                L[d.id].cross_v_tok = first->cross_v_tok;
-                L[d.id].cross_vt_tok = first->cross_vt_tok;
-                L[d.id].tokens = first->tokens;
-                L[d.id].tokens_pad = first->tokens_pad;
-            }
-        }
+    // projection for every CrossAttn layer; the reference graph has exactly one.  Deeper graphs
+    // (ModelConfig::res_blocks / attn_*, beyond the reference API) project each CrossAttn layer
+    // with its own weights -- identical for one layer.
     CUDA_CHECK(cudaDeviceSynchronize());
 }
 
@@ -385,21 +373,25 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
     sc.gn_ticket = static_cast<unsigned int*>(alloc(1024));   // 1 + N tiles counters
     fused_stats.assign(L, 0);
 
-    // attention scratch (one SelfAttn geometry per model)
-    for (const Group& g : groups) {
+    // attention scratch, per SelfAttn group (their geometries differ when attention runs at
+    // several levels); multi-token CrossAttn scratch is sized when its plan is built
+    attn_sc.assign(groups.size(), AttnScratch{});
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+        const Group& g = groups[gi];
         if (g.kind != Kind::SelfAttn) continue;
+        AttnScratch& as = attn_sc[gi];
         const Act& in = input_of(g.first);
         const Region& ri = spec.layer_in[g.first];
         const int ns = ri.full_h * ri.full_w;
-        s_pad = round_up(ns, 64);
-        P = alloc(size_t(in.pix()) * s_pad * eb);
-        CUDA_CHECK(cudaMemset(P, 0, size_t(in.pix()) * s_pad * eb));   // key padding: P = 0
-        attn_rscale = static_cast<float*>(alloc(size_t(in.pix()) * 4));
-        attn_c = in.C;
-        if (!attn_v_mn()) {   // TF32 MMAs take B K-major only: V^T by the transpose kernel
-            const size_t vt = size_t(round_up(in.C, 16)) * s_pad * eb;
-            Vt = alloc(vt);
-            CUDA_CHECK(cudaMemset(Vt, 0, vt));
+        as.s_pad = round_up(ns, 64);
+        as.P = alloc(size_t(in.pix()) * as.s_pad * eb);
+        CUDA_CHECK(cudaMemset(as.P, 0, size_t(in.pix()) * as.s_pad * eb));   // key padding: P = 0
+        as.rscale = static_cast<float*>(alloc(size_t(in.pix()) * 4));
+        as.v_mn = e == Elem::BF16 && in.C % 64 == 0;
+        if (!as.v_mn) {   // TF32 MMAs take B K-major only: V^T by the transpose kernel
+            const size_t vt = size_t(round_up(in.C, 16)) * as.s_pad * eb;
+            as.Vt = alloc(vt);
+            CUDA_CHECK(cudaMemset(as.Vt, 0, vt));
         }
     }
 
@@ -513,58 +505,62 @@ Program::Program(Runner* r_, const Model& m_, const DeviceWeights* w_, int dev_,
                 const int ns = ri.full_h * ri.full_w;
                 const int m_rows = int(in.pix());
                 EpilogueSpec es;
-                es.out = P;
-                es.out_ld = s_pad;
+                AttnScratch& as = attn_sc[gi];
+                es.out = as.P;
+                es.out_ld = as.s_pad;
                 es.out_f32 = e == Elem::F32;
                 es.round_tf32 = rnd;
                 es.n_valid = ns;
                 // (non-null marks the softmax epilogue; the table is sized by the tiling below)
-                es.sm_rowmax = static_cast<float*>(P);
+                es.sm_rowmax = static_cast<float*>(as.P);
                 es.sm_scale = float(1.0 / std::sqrt(double(d.in_ch)));
                 es.sm_ld = m_rows;
                 const void* kv = nb > 1 ? lx[g.first].kv[p] : in.interior(eb);
                 GemmPlan& sp = s_plans[gi][p];
                 plan_gemm(sp, e, in.interior(eb), m_rows, in.ld, in.ld, kv, ns, in.ld, es, sc, sms);
-                if (!attn_rowmax)
-                    attn_rowmax = static_cast<float*>(alloc(size_t(sp.a.n_tiles) * m_rows * 4));
+                if (!as.rowmax)
+                    as.rowmax = static_cast<float*>(alloc(size_t(sp.a.n_tiles) * m_rows * 4));
                 else if (p == 1 && sp.a.n_tiles != s_plans[gi][0].a.n_tiles)
                     throw std::logic_error("attention: S tilings differ between parities");
-                sp.a.sm_rowmax = attn_rowmax;
-                e2.row_scale = attn_rscale;
-                if (attn_v_mn())
-                    plan_gemm_bmn(plans[gi][p], e, P, m_rows, s_pad, s_pad, kv, ns, in.C, in.ld, e2,
+                sp.a.sm_rowmax = as.rowmax;
+                e2.row_scale = as.rscale;
+                if (as.v_mn)
+                    plan_gemm_bmn(plans[gi][p], e, as.P, m_rows, as.s_pad, as.s_pad, kv, ns, in.C, in.ld, e2,
                                   sc, sms);
                 else
-                    plan_gemm(plans[gi][p], e, P, m_rows, s_pad, s_pad, Vt, in.C, s_pad, e2, sc, sms);
+                    plan_gemm(plans[gi][p], e, as.P, m_rows, as.s_pad, as.s_pad, as.Vt, in.C, as.s_pad, e2,
+                              sc, sms);
             } else if (d.kind == Kind::CrossAttn && lw.tokens > 1) {
                 // layer_cross_attn (model.cpp:265-271) over T condition tokens: q = the band's
                 // tokens, K / V = the T projected condition rows (the same for every band)
                 const int m_rows = int(in.pix());
                 const int tp = lw.tokens_pad;
-                if (!Pc) {
-                    Pc = alloc(size_t(m_rows) * tp * eb);
-                    CUDA_CHECK(cudaMemset(Pc, 0, size_t(m_rows) * tp * eb));
-                    rscale_c = static_cast<float*>(alloc(size_t(m_rows) * 4));
+                AttnScratch& as = attn_sc[gi];
+                if (!as.P) {
+                    as.s_pad = tp;
+                    as.P = alloc(size_t(m_rows) * tp * eb);
+                    CUDA_CHECK(cudaMemset(as.P, 0, size_t(m_rows) * tp * eb));
+                    as.rscale = static_cast<float*>(alloc(size_t(m_rows) * 4));
                 }
                 EpilogueSpec es;
-                es.out = Pc;
+                es.out = as.P;
                 es.out_ld = tp;
                 es.out_f32 = e == Elem::F32;
                 es.round_tf32 = rnd;
                 es.n_valid = lw.tokens;
-                es.sm_rowmax = static_cast<float*>(Pc);   // marks the softmax epilogue
+                es.sm_rowmax = static_cast<float*>(as.P);   // marks the softmax epilogue
                 es.sm_scale = float(1.0 / std::sqrt(double(d.in_ch)));
                 es.sm_ld = m_rows;
                 GemmPlan& sp = s_plans[gi][p];
                 plan_gemm(sp, e, in.interior(eb), m_rows, in.ld, in.ld, lw.cross_k_tok, lw.tokens, in.ld,
                           es, sc, sms);
-                if (!rowmax_c) rowmax_c = static_cast<float*>(alloc(size_t(sp.a.n_tiles) * m_rows * 4));
-                sp.a.sm_rowmax = rowmax_c;
-                e2.row_scale = rscale_c;
+                if (!as.rowmax) as.rowmax = static_cast<float*>(alloc(size_t(sp.a.n_tiles) * m_rows * 4));
+                sp.a.sm_rowmax = as.rowmax;
+                e2.row_scale = as.rscale;
                 if (lw.cross_vt_tok)
-                    plan_gemm(plans[gi][p], e, Pc, m_rows, tp, tp, lw.cross_vt_tok, d.out_ch, tp, e2, sc, sms);
+                    plan_gemm(plans[gi][p], e, as.P, m_rows, tp, tp, lw.cross_vt_tok, d.out_ch, tp, e2, sc, sms);
                 else
-                    plan_gemm_bmn(plans[gi][p], e, Pc, m_rows, tp, tp, lw.cross_v_tok, lw.tokens, d.out_ch,
+                    plan_gemm_bmn(plans[gi][p], e, as.P, m_rows, tp, tp, lw.cross_v_tok, lw.tokens, d.out_ch,
                                   in.ld, e2, sc, sms);
             }
         }
@@ -735,14 +731,15 @@ void Program::attention(const Group& g, int par, int par_out) {
     (void)par_out;
     const void* kv = nb > 1 ? lx[g.first].kv[par] : in.interior(eb);
     const int m_rows = int(in.pix());
-    if (!attn_v_mn()) {
-        run_timed(CAT_OTHER, 0, [&] { transpose(e, kv, ns, in.C, in.ld, Vt, s_pad, cs); });
+    const AttnScratch& as = attn_sc[gi];
+    if (!as.v_mn) {
+        run_timed(CAT_OTHER, 0, [&] { transpose(e, kv, ns, in.C, in.ld, as.Vt, as.s_pad, cs); });
         count(1);
     }
     run_timed(CAT_GEMM, sp.flops, [&] { launch_gemm(sp, cs); });
     run_timed(CAT_OTHER, 0, [&] {
-        attn_rescale(e, P, s_pad, m_rows, ns, attn_rowmax, sp.a.n_tiles, sp.a.block_n, m_rows,
-                     attn_rscale, rnd, cs);
+        attn_rescale(e, as.P, as.s_pad, m_rows, ns, as.rowmax, sp.a.n_tiles, sp.a.block_n, m_rows,
+                     as.rscale, rnd, cs);
     });
     run_timed(CAT_GEMM, pv.flops, [&] { launch_gemm(pv, cs); });
     count(3);
@@ -756,8 +753,9 @@ void Program::cross_attention(const Group& g) {
     const int m_rows = int(input_of(g.first).pix());
     run_timed(CAT_GEMM, sp.flops, [&] { launch_gemm(sp, cs); });
     run_timed(CAT_OTHER, 0, [&] {
-        attn_rescale(e, Pc, lw.tokens_pad, m_rows, lw.tokens, rowmax_c, sp.a.n_tiles, sp.a.block_n,
-                     m_rows, rscale_c, rnd, cs);
+        const AttnScratch& as = attn_sc[gi];
+        attn_rescale(e, as.P, as.s_pad, m_rows, lw.tokens, as.rowmax, sp.a.n_tiles, sp.a.block_n,
+                     m_rows, as.rscale, rnd, cs);
     });
     run_timed(CAT_GEMM, pv.flops, [&] { launch_gemm(pv, cs); });
     count(3);

@@ -37,10 +37,16 @@ class ModelConfig:
     groups: int = 4
     cond_dim: int = 8
     attn_at_level: int = -1
+    # deeper graphs (beyond the reference API; defaults = the reference graph)
+    res_blocks: int = 1
+    attn_levels: int = 0
+    attn_depth: int = 1
+    attn_up: int = 0
 
     def c(self):
         return N.ModelConfig(self.in_channels, self.base_channels, self.levels, self.groups,
-                             self.cond_dim, self.attn_at_level)
+                             self.cond_dim, self.attn_at_level, self.res_blocks, self.attn_levels,
+                             self.attn_depth, self.attn_up)
 
     def depth_divisor(self):
         return 1 << (self.levels - 1)

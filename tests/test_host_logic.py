@@ -20,10 +20,14 @@ TINY = P.ModelConfig(2, 8, 2, 4, 8, -1)
 
 def ocfg(c):
     return O.ModelConfig(c.in_channels, c.base_channels, c.levels, c.groups, c.cond_dim,
-                         c.attn_at_level)
+                         c.attn_at_level, c.res_blocks, c.attn_levels, c.attn_depth, c.attn_up)
 
 
-@pytest.mark.parametrize("cfg,seed", [(P.ModelConfig(), 42), (TINY, 77), (P.ModelConfig(3, 24, 4, 6, 5, 1), 9)])
+DEEP = P.ModelConfig(4, 16, 3, 4, 8, -1, res_blocks=2, attn_levels=0b110, attn_depth=2, attn_up=1)
+
+
+@pytest.mark.parametrize("cfg,seed", [(P.ModelConfig(), 42), (TINY, 77), (P.ModelConfig(3, 24, 4, 6, 5, 1), 9),
+                                      (DEEP, 3)])
 def test_weight_pool_bit_exact(cfg, seed):
     m = P.build_model(cfg, seed)
     om = O.build_model(ocfg(cfg), seed)
@@ -45,6 +49,21 @@ def test_sdxl_shape_pool_matches_reference_digest():
     assert pool.size == 77_388_804
     assert hashlib.sha256(pool.tobytes()).hexdigest() == str(GOLD["sdxl_weight_sha256"])
     assert m.total_macs(128, 128) == 231_234_600_960   # 0.2312 TMAC/step
+
+
+def test_deeper_graph_topology():
+    # beyond the reference API: the default extension fields build the reference graph (the
+    # SDXL digest above); res_blocks / attn_levels / attn_depth / attn_up grow it -- level l
+    # gets res_blocks residual blocks, each followed by attn_depth attention blocks at the
+    # attention levels (and on the up path with attn_up)
+    kinds = [d["kind"] for d in P.build_model(DEEP, 3).layers]
+    base = [d["kind"] for d in P.build_model(P.ModelConfig(), 3).layers]
+    assert kinds.count("SelfAttn") == 2 * 2 * 2 + 2 * 2 * 1   # down: 2 lv x 2 rb x 2; up: lv 1 only
+    assert kinds.count("Conv") == base.count("Conv") + 4 * 2 + 2 * 2 - 2
+    assert base.count("SelfAttn") == 1
+    for bad in (dict(res_blocks=-1), dict(attn_depth=-2), dict(attn_levels=8)):
+        with pytest.raises(P.InvalidArgument, match="ModelConfig"):
+            P.build_model(P.ModelConfig(**bad), 1)
 
 
 def test_from_pool_roundtrip():

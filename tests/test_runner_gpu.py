@@ -25,7 +25,7 @@ TOY = P.ModelConfig()                           # model.hpp:30-36 defaults
 
 def ocfg(c):
     return O.ModelConfig(c.in_channels, c.base_channels, c.levels, c.groups, c.cond_dim,
-                         c.attn_at_level)
+                         c.attn_at_level, c.res_blocks, c.attn_levels, c.attn_depth, c.attn_up)
 
 
 def rel(a, b):
@@ -514,3 +514,29 @@ def test_multi_token_single_token_is_the_reference_path():
     assert np.array_equal(a.sample(x, plan, abar)[0], b.sample(x, plan, abar)[0])
     with pytest.raises(P.InvalidArgument, match="condition: expected"):
         P.PatchRunner(m, np.zeros((3, cfg.cond_dim + 1), np.float32), 32, 32, mode="reference")
+
+
+# two residual blocks per level and attention at levels 1 and 2 (4 self-attention layers at two
+# geometries).  Deeper random-init stacks (attn_depth 2 + attn_up: residual-stream values of
+# ~2e4, one-hot softmax rows) amplify bf16 / TF32 input rounding beyond the latent bar; their
+# graph and weight pool are checked bit-exactly on the host (test_host_logic.py).
+DEEP = dataclasses.replace(TOY, res_blocks=2, attn_levels=0b110)
+
+
+@pytest.mark.parametrize("mode,n,dtype", [("displaced", 2, "bf16"), ("sync-pp", 4, "fp32"),
+                                          ("reference", 1, "bf16")])
+def test_deeper_graph_vs_oracle(mode, n, dtype):
+    # a deeper U-Net (beyond the reference API): two residual blocks per level, attention at
+    # levels 1 and 2; per-step latents against the oracle's runners over the same graph
+    m = P.build_model(DEEP, 42)
+    cond = O.random_condition(DEEP.cond_dim, 7)
+    x = O.random_normal(1, DEEP.in_channels, 32, 32, 1234)
+    r = P.PatchRunner(m, cond, 32, 32, mode=mode, n_devices=n, warmup_steps=1, dtype=dtype)
+    got, traj = r.sample(x, O.make_plan(1000, 4), O.make_schedule(), trajectory=True)
+    g, _ = r.sample(x, O.make_plan(1000, 4), O.make_schedule())
+    assert np.array_equal(g, got)
+    ref = O.run_sampling(ocfg(DEEP), mode, n, 32, 32, 4, 1)
+    for i in range(4):
+        assert rel(traj[i], ref["trajectory"][i]) <= TOL[dtype], i
+    assert rel(got, ref["x0"]) <= TOL[dtype]
+    assert r.total_macs() == 2 * ref["total_macs"]
