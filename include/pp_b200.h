@@ -170,6 +170,15 @@ typedef struct {
      * cond_tokens x model cond_dim floats and every CrossAttn layer attends over the
      * cond_tokens projected rows; default 1 (the reference's layer_cross_attn exactly) */
     int cond_tokens;
+    /* CFG batch split across two GPU groups (beyond the reference API):
+     * cfg_pair_role 0 / 1 = this rank runs only the conditional / unconditional pass of its
+     * band (conditioned on cond / uncond -- both ranks of a pair pass the same two) and swaps
+     * eps bands with its partner after every pass; both then hold the same guided latent.
+     * cfg_pair_transport: PP_TRANSPORT_NCCL (a two-rank communicator per pair, cfg_nccl_id =
+     * its ncclUniqueId; graph-captured) or PP_TRANSPORT_IPC (pp_runner_pair_export / _connect;
+     * eager).  One band per process.  Default -1: both passes in this runner (cfg_scale). */
+    int cfg_pair_role;
+    int cfg_pair_transport;
 } pp_runner_opts;
 PP_API void pp_runner_opts_default(pp_runner_opts* o);
 
@@ -216,6 +225,11 @@ PP_API double pp_runner_last_device_ms(const pp_runner* r);
 /* switch per-kernel CUDA-event timing on/off (resets the pp_runner_profile totals) */
 PP_API int pp_runner_set_profile(pp_runner* r, int on);
 /* ncclGetUniqueId for the multi-process (one rank per GPU) layout */
+/* CFG pair link over CUDA IPC (cfg_pair_transport == PP_TRANSPORT_IPC): this rank's handle
+ * blob (call with out = NULL for the size), then connect with the partner's blob before the
+ * first step.  Replaces nothing in the reference (beyond its API). */
+PP_API int pp_runner_pair_export(pp_runner* r, void* out, long cap, long* size);
+PP_API int pp_runner_pair_connect(pp_runner* r, const void* blob, long size);
 PP_API int pp_nccl_unique_id(void* out128);
 /* PP_TRANSPORT_IPC: this rank's CUDA IPC handle blob (receive buffers + flags); *size = its
  * byte count, copied to out when cap suffices.  Replaces the hub registration of

@@ -79,7 +79,7 @@ class RunnerOpts(C.Structure):
                 ("profile", C.c_int), ("transport", C.c_int), ("no_comm", C.c_int),
                 ("stress", C.c_int), ("stress_seed", C.c_ulonglong),
                 ("cfg_scale", C.c_double), ("uncond", C.c_void_p), ("cfg_nccl_id", C.c_void_p),
-                ("cond_tokens", C.c_int)]
+                ("cond_tokens", C.c_int), ("cfg_pair_role", C.c_int), ("cfg_pair_transport", C.c_int)]
 
 
 _V, _I, _L, _D, _U64, _F = C.c_void_p, C.c_int, C.c_long, C.c_double, C.c_uint64, C.c_float
@@ -130,6 +130,8 @@ SIGNATURES = {
     "pp_nccl_unique_id": (_I, [_V]),
     "pp_runner_ipc_export": (_I, [_V, _V, _L, _V]),
     "pp_runner_ipc_connect": (_I, [_V, _V, _L]),
+    "pp_runner_pair_export": (_I, [_V, _V, _L, _V]),
+    "pp_runner_pair_connect": (_I, [_V, _V, _L]),
     "pp_assemble_bands": (_I, [_V, _I, _I, _I, _I, _V]),
     "pp_dev_gemm_bench": (_I, [_I, _I, _I, _I, _I, _I, _I, _I, _I, _V]),
     "pp_dev_gn_bench": (_I, [_I, _LL, _I, _I, _I, _I, _V]),

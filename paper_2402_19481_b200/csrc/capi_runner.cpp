@@ -67,7 +67,13 @@ pp::RunnerOptions opts_of(const pp_runner_opts* o) {
     r.cond_tokens = o->cond_tokens;
     if (r.cond_tokens < 1) throw std::invalid_argument("pp_runner_create: cond_tokens must be >= 1");
     if (!std::isfinite(r.cfg_scale)) throw std::invalid_argument("pp_runner_create: cfg_scale not finite");
-    if (r.cfg_scale != 0.0 && r.world > 1 && r.transport == PP_TRANSPORT_NCCL) {
+    r.cfg_pair_role = o->cfg_pair_role;
+    r.cfg_pair_transport = o->cfg_pair_transport;
+    if (r.cfg_pair_role < -1 || r.cfg_pair_role > 1)
+        throw std::invalid_argument("pp_runner_create: cfg_pair_role must be -1, 0 or 1");
+    const bool need_cfg_id = r.cfg_pair_role >= 0 ? r.cfg_pair_transport == PP_TRANSPORT_NCCL
+                                                  : r.world > 1 && r.transport == PP_TRANSPORT_NCCL;
+    if (r.cfg_scale != 0.0 && need_cfg_id) {
         need(o->cfg_nccl_id, "pp_runner_create(cfg_nccl_id)");
         const uint8_t* p = static_cast<const uint8_t*>(o->cfg_nccl_id);
         r.cfg_nccl_id.assign(p, p + 128);
@@ -320,6 +326,8 @@ PP_API void pp_runner_opts_default(pp_runner_opts* o) {
     o->uncond = nullptr;
     o->cfg_nccl_id = nullptr;
     o->cond_tokens = 1;
+    o->cfg_pair_role = -1;
+    o->cfg_pair_transport = PP_TRANSPORT_NCCL;
 }
 
 PP_API int pp_runner_create(const pp_model* m, const float* cond, int cond_dim, int h, int w,
@@ -472,6 +480,25 @@ PP_API int pp_runner_ipc_connect(pp_runner* r, const void* blobs, long per_rank)
         need(blobs, "pp_runner_ipc_connect");
         if (per_rank <= 0) throw std::invalid_argument("pp_runner_ipc_connect: bad blob size");
         r->r->ipc_connect(static_cast<const uint8_t*>(blobs), size_t(per_rank));
+    });
+}
+
+PP_API int pp_runner_pair_export(pp_runner* r, void* out, long cap, long* size) {
+    return pp::guard([&] {
+        need(r, "pp_runner_pair_export");
+        need(size, "pp_runner_pair_export(size)");
+        const auto blob = r->r->pair_export();
+        *size = long(blob.size());
+        if (out && cap >= *size) std::memcpy(out, blob.data(), blob.size());
+    });
+}
+
+PP_API int pp_runner_pair_connect(pp_runner* r, const void* blob, long size) {
+    return pp::guard([&] {
+        need(r, "pp_runner_pair_connect");
+        need(blob, "pp_runner_pair_connect");
+        if (size <= 0) throw std::invalid_argument("pp_runner_pair_connect: bad blob size");
+        r->r->pair_connect(static_cast<const uint8_t*>(blob), size_t(size));
     });
 }
 

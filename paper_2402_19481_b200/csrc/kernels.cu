@@ -818,14 +818,14 @@ __global__ void __launch_bounds__(256) stem_im2col_kernel(const T* __restrict__ 
     }
 }
 
-__global__ void cfg_combine_kernel(float* __restrict__ ec, const float* __restrict__ eu, long long n,
+__global__ void cfg_combine_kernel(float* out, const float* ec, const float* eu, long long n,
                                    double scale) {
     pdl_wait();
     pdl_trigger();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const double u = double(eu[i]);
-        ec[i] = float(__dadd_rn(u, __dmul_rn(scale, __dsub_rn(double(ec[i]), u))));
+        out[i] = float(__dadd_rn(u, __dmul_rn(scale, __dsub_rn(double(ec[i]), u))));
     }
 }
 
@@ -1006,8 +1006,9 @@ void stem_im2col(Elem e, const void* in, int rows, int W, int ld_in, int C_in, v
     CUDA_CHECK(cudaGetLastError());
 }
 
-void cfg_combine_eps(float* eps_c, const float* eps_u, long long n, double scale, cudaStream_t s) {
-    launch_pdl(cfg_combine_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, 1, eps_c, eps_u, n, scale);
+void cfg_combine_eps(float* out, const float* eps_c, const float* eps_u, long long n, double scale,
+                     cudaStream_t s) {
+    launch_pdl(cfg_combine_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, 1, out, eps_c, eps_u, n, scale);
     CUDA_CHECK(cudaGetLastError());
 }
 

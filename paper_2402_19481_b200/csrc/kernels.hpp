@@ -80,8 +80,10 @@ void transpose(Elem e, const void* V, int ns, int C, long long ldv, void* Vt, lo
 void stem_im2col(Elem e, const void* in, int rows, int W, int ld_in, int C_in, void* out, int kpad,
                  cudaStream_t s);
 
-// classifier-free guidance: eps_c[i] <- eps_u + scale (eps_c - eps_u), in fp64 (no contraction)
-void cfg_combine_eps(float* eps_c, const float* eps_u, long long n, double scale, cudaStream_t s);
+// classifier-free guidance: out[i] <- eps_u + scale (eps_c - eps_u), in fp64 (no contraction);
+// out may alias eps_c or eps_u
+void cfg_combine_eps(float* out, const float* eps_c, const float* eps_u, long long n, double scale,
+                     cudaStream_t s);
 
 // --stress-sched: one thread sleeping `us` microseconds on stream s
 void stream_sleep(unsigned int us, cudaStream_t s);

@@ -236,4 +236,24 @@ std::unique_ptr<Transport> make_ipc_transport(Program* band, int world, int rank
 std::vector<uint8_t> ipc_export(Transport& t);
 void ipc_connect(Transport& t, const uint8_t* blobs, size_t per_rank);
 
+// Classifier-free guidance batch split (beyond the reference API): the conditional and the
+// unconditional pass of one band run on two ranks (two GPU groups); after every U-Net pass
+// the pair swaps its eps bands.  role 0 = conditional rank, 1 = unconditional rank.
+class PairLink {
+public:
+    virtual ~PairLink() = default;
+    // Enqueue on s: send `mine` (the n floats of this rank's eps band) to the partner and
+    // receive the partner's.  Returns the device buffer that holds the partner's eps in stream
+    // order on s, valid until the next exchange call.
+    virtual const float* exchange(cudaStream_t s, const float* mine) = 0;
+    virtual bool capturable() const = 0;
+    virtual std::vector<uint8_t> export_blob() const;
+    virtual void connect(const uint8_t* blob, size_t size);
+};
+// two-rank NCCL communicator (rank = role): ncclSend / ncclRecv on the stream, graph-capturable
+std::unique_ptr<PairLink> make_nccl_pair(int dev, int role, const std::vector<uint8_t>& id, size_t n);
+// CUDA IPC: the partner pushes into one of two parity receive buffers with the copy engine and
+// bumps a flag with a stream memory operation (host sequence numbers: not graph-capturable)
+std::unique_ptr<PairLink> make_ipc_pair(int dev, int role, size_t n);
+
 }  // namespace pp

@@ -857,6 +857,14 @@ void Program::simple(const Group& g, int par) {
 // ------------------------------------------------------------------------------ runner
 Runner::Runner(const Model& m, const std::vector<float>& cond, int h, int w, const RunnerOptions& o)
     : m_(m), cond_(cond), o_(o), h_(h), w_(w) {
+    if (o_.cfg_pair_role == 1) {
+        // the unconditional half of a CFG batch split is conditioned on `uncond` (zeros if empty)
+        if (!o_.uncond.empty() && o_.uncond.size() != cond_.size())
+            throw std::invalid_argument("classifier-free guidance: uncond length " +
+                                        std::to_string(o_.uncond.size()) + " != condition length " +
+                                        std::to_string(cond_.size()));
+        cond_ = o_.uncond.empty() ? std::vector<float>(cond_.size(), 0.0f) : o_.uncond;
+    }
     if (o_.mode == MODE_REFERENCE) o_.n_devices = 1;
     if (o_.n_devices < 1) throw std::invalid_argument("PatchRunner: need at least one device");
     n_dev_ = o_.n_devices;
@@ -908,7 +916,29 @@ Runner::Runner(const Model& m, const std::vector<float>& cond, int h, int w, con
             }
         }
     }
-    if (o_.cfg_scale != 0.0) {
+    if (o_.cfg_pair_role >= 0) {
+        // CFG batch split: this rank runs one of the two passes of its band (the condition
+        // was chosen before the weights were projected, see below); the partner runs the other
+        if (o_.cfg_pair_role > 1) throw std::invalid_argument("classifier-free guidance: cfg_pair_role must be 0 or 1");
+        if (o_.cfg_scale == 0.0)
+            throw std::invalid_argument("classifier-free guidance: cfg_pair_role needs cfg_scale != 0");
+        if (o_.mode == MODE_NAIVE)
+            throw std::invalid_argument("classifier-free guidance: naive mode is not supported");
+        if (bands_.size() != 1)
+            throw std::invalid_argument("classifier-free guidance: the batch split runs one band per "
+                                        "process (world == n_devices, or one device)");
+        const Program& b = *bands_[0];
+        const size_t n = size_t(b.stem.rows) * w_ * m_.cfg.in_channels;
+        if (o_.cfg_pair_transport == 0) {
+            if (o_.cfg_nccl_id.size() != 128)
+                throw std::invalid_argument("classifier-free guidance: cfg_nccl_id required (NCCL pair link)");
+            pair_ = make_nccl_pair(b.dev, o_.cfg_pair_role, o_.cfg_nccl_id, n);
+        } else if (o_.cfg_pair_transport == 1) {
+            pair_ = make_ipc_pair(b.dev, o_.cfg_pair_role, n);
+        } else {
+            throw std::invalid_argument("classifier-free guidance: unknown cfg_pair_transport");
+        }
+    } else if (o_.cfg_scale != 0.0) {
         // classifier-free guidance: the unconditional pass is a second runner over the same
         // bands (own streams, caches and exchange), stepped alongside this one
         if (o_.mode == MODE_NAIVE)
@@ -945,7 +975,7 @@ void Runner::cfg_combine() {
         DeviceGuard g(b.dev);
         CUDA_CHECK(cudaEventRecord(cfg_ev_[2 * d], u.cs));
         CUDA_CHECK(cudaStreamWaitEvent(b.cs, cfg_ev_[2 * d], 0));
-        cfg_combine_eps(b.eps, u.eps, (long long)b.stem.rows * w_ * m_.cfg.in_channels, o_.cfg_scale, b.cs);
+        cfg_combine_eps(b.eps, b.eps, u.eps, (long long)b.stem.rows * w_ * m_.cfg.in_channels, o_.cfg_scale, b.cs);
         launches_ += 1;
     }
 }
@@ -961,6 +991,28 @@ void Runner::cfg_refresh_stem() {
         CUDA_CHECK(cudaEventRecord(cfg_ev_[2 * d + 1], b.cs));
         CUDA_CHECK(cudaStreamWaitEvent(u.cs, cfg_ev_[2 * d + 1], 0));
     }
+}
+
+void Runner::pair_combine() {
+    Program& b = *bands_[0];
+    DeviceGuard g(b.dev);
+    const long long n = (long long)b.stem.rows * w_ * m_.cfg.in_channels;
+    const float* other = pair_->exchange(b.cs, b.eps);
+    // both ranks evaluate eps_u + s (eps_c - eps_u) with the same operands in the same fp64
+    // order, so the two halves of the pair hold bit-identical latents
+    if (o_.cfg_pair_role == 0) cfg_combine_eps(b.eps, b.eps, other, n, o_.cfg_scale, b.cs);
+    else cfg_combine_eps(b.eps, other, b.eps, n, o_.cfg_scale, b.cs);
+    launches_ += 1;
+}
+
+std::vector<uint8_t> Runner::pair_export() {
+    if (!pair_) throw std::invalid_argument("pp_runner_pair_export: runner has no CFG pair link");
+    return pair_->export_blob();
+}
+
+void Runner::pair_connect(const uint8_t* blob, size_t size) {
+    if (!pair_) throw std::invalid_argument("pp_runner_pair_connect: runner has no CFG pair link");
+    pair_->connect(blob, size);
 }
 
 CommVolumes Runner::volumes() const {
@@ -999,6 +1051,7 @@ const DeviceWeights* Runner::weights_for(int dev) {
 Runner::~Runner() {
     cfg_.reset();
     for (auto ev : cfg_ev_) cudaEventDestroy(ev);
+    pair_.reset();
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     for (auto ev : graph_events_) cudaEventDestroy(ev);
     transport_.reset();   // uses the bands' streams and buffers
@@ -1591,6 +1644,7 @@ void Runner::step(int entry, const float* x, int t, int s, float* eps) {
         cfg_->count_macs(s, false);
         cfg_combine();
     }
+    if (pair_) pair_combine();
     store_eps(eps);
     count_macs(s, false);
     record_trace(s, e == STEP_REFERENCE ? 0 : displaced ? 2 : 1);
@@ -1648,7 +1702,7 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
         for (auto& b : cfg_->bands_) all.push_back(b.get());
     // (the IPC transport's flag sequence numbers advance per exchange: not capturable)
     const bool use_graph = !traj && !o_.profile && graphs_enabled_ && (o_.world > 1 || same_dev) &&
-                           !(o_.world > 1 && o_.transport == 1);
+                           !(o_.world > 1 && o_.transport == 1) && !(pair_ && !pair_->capturable());
     std::vector<double> key(ts, ts + n);
     for (int i = 0; i < n; ++i) key.push_back(abar_at(ts[i]));
     key.push_back(o_.mode);
@@ -1759,6 +1813,7 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
             cfg_->count_macs(i, false);
             cfg_combine();
         }
+        if (pair_) pair_combine();
         for (Program* b : all) b->use_temb_step(-1);
         count_macs(i, false);
         record_trace(i, o_.mode == MODE_REFERENCE ? 0 : displaced ? 2 : 1);

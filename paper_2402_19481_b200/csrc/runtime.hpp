@@ -56,6 +56,13 @@ struct RunnerOptions {
     // cond_dim floats and every CrossAttn layer attends over the cond_tokens projected rows
     int cond_tokens = 1;
     std::vector<uint8_t> cfg_nccl_id;
+    // CFG batch split across two GPU groups (beyond the reference API): cfg_pair_role 0 / 1 =
+    // this rank runs only the conditional / unconditional pass of its band (conditioned on
+    // `cond` / `uncond`) and swaps eps bands with its partner rank after every pass over
+    // cfg_pair_transport (0: a two-rank NCCL communicator, id cfg_nccl_id; 1: CUDA IPC,
+    // pair_export / pair_connect).  -1 (default): both passes in this runner.
+    int cfg_pair_role = -1;
+    int cfg_pair_transport = 0;
 };
 
 struct CommVolumes {
@@ -83,6 +90,7 @@ struct ProfileTotals {
 struct DeviceWeights;  // packed weights on one CUDA device
 struct Program;        // one band compiled for one CUDA device
 class Transport;
+class PairLink;
 struct XItem;
 
 class Runner {
@@ -114,6 +122,9 @@ public:
     // IPC transport (world > 1, transport 1): this rank's handle blob, then every rank's blob
     std::vector<uint8_t> ipc_export();
     void ipc_connect(const uint8_t* blobs, size_t per_rank);
+    // CFG pair link over CUDA IPC: this rank's handle blob, then the partner's
+    std::vector<uint8_t> pair_export();
+    void pair_connect(const uint8_t* blob, size_t size);
 
 private:
     friend struct Program;
@@ -157,6 +168,8 @@ private:
     std::vector<cudaEvent_t> cfg_ev_;      // per band: [2d] uncond eps ready, [2d+1] x_t refreshed
     void cfg_combine();                    // eps of every band <- the guided eps
     void cfg_refresh_stem();               // the unconditional pass's stem input <- x_t
+    std::unique_ptr<PairLink> pair_;       // CFG batch split: eps swap with the partner rank
+    void pair_combine();                   // own eps <- guided eps from own + partner's band
     void stress_jitter(Program& b, int band);
     std::vector<int> gn_posted_;   // per layer: last step whose GN stats were posted
     uint64_t total_macs_ = 0;

@@ -473,7 +473,129 @@ private:
     bool connected_ = false;
 };
 
+// ---------------------------------------------------------------- CFG pair links
+class NcclPair final : public PairLink {
+public:
+    NcclPair(int dev, int role, const std::vector<uint8_t>& id, size_t n) : dev_(dev), role_(role), n_(n) {
+        if (id.size() != sizeof(ncclUniqueId))
+            throw std::invalid_argument("CFG pair link needs the 128-byte ncclUniqueId (cfg_nccl_id)");
+        ncclUniqueId uid;
+        std::memcpy(&uid, id.data(), sizeof(uid));
+        DeviceGuard g(dev_);
+        CUDA_CHECK(cudaMalloc(&recv_, std::max<size_t>(n_, 1) * 4));
+        NCCL_CHECK(ncclCommInitRank(&comm_, 2, uid, role_));
+    }
+    ~NcclPair() override {
+        DeviceGuard g(dev_);
+        if (comm_) ncclCommDestroy(comm_);
+        cudaFree(recv_);
+    }
+    const float* exchange(cudaStream_t s, const float* mine) override {
+        DeviceGuard g(dev_);
+        NCCL_CHECK(ncclGroupStart());
+        NCCL_CHECK(ncclSend(mine, n_, ncclFloat32, 1 - role_, comm_, s));
+        NCCL_CHECK(ncclRecv(recv_, n_, ncclFloat32, 1 - role_, comm_, s));
+        NCCL_CHECK(ncclGroupEnd());
+        return recv_;
+    }
+    bool capturable() const override { return true; }
+
+private:
+    int dev_, role_;
+    size_t n_;
+    float* recv_ = nullptr;
+    ncclComm_t comm_ = nullptr;
+};
+
+constexpr uint32_t kPairMagic = 0x50504350u;   // "PPCP"
+
+// One allocation: two parity receive buffers of n floats, then the ARRIVED flag.  Exchange k
+// lands in parity k & 1.  No READY handshake is needed: the partner's push k follows (in its
+// stream) its wait for our push k-1, which follows (in ours) our read of exchange k-2, the
+// last use of the same parity buffer.
+class IpcPair final : public PairLink {
+public:
+    IpcPair(int dev, int role, size_t n) : dev_(dev), role_(role), n_(n) {
+        DeviceGuard g(dev_);
+        stride_ = (std::max<size_t>(n_, 1) * 4 + 255) / 256 * 256;
+        CUDA_CHECK(cudaMalloc(&buf_, 2 * stride_ + 256));
+        CUDA_CHECK(cudaMemset(buf_, 0, 2 * stride_ + 256));
+        wait_ = driver_fn<WaitValueFn>("cuStreamWaitValue32");
+        write_ = driver_fn<WriteValueFn>("cuStreamWriteValue32");
+    }
+    ~IpcPair() override {
+        DeviceGuard g(dev_);
+        cudaDeviceSynchronize();
+        if (peer_) cudaIpcCloseMemHandle(peer_);
+        cudaFree(buf_);
+    }
+    std::vector<uint8_t> export_blob() const override {
+        std::vector<uint8_t> out(32 + sizeof(cudaIpcMemHandle_t));
+        const uint64_t hdr[4] = {kPairMagic, uint64_t(role_), uint64_t(n_), uint64_t(stride_)};
+        std::memcpy(out.data(), hdr, 32);
+        DeviceGuard g(dev_);
+        cudaIpcMemHandle_t h;
+        CUDA_CHECK(cudaIpcGetMemHandle(&h, buf_));
+        std::memcpy(out.data() + 32, &h, sizeof(h));
+        return out;
+    }
+    void connect(const uint8_t* blob, size_t size) override {
+        if (size != 32 + sizeof(cudaIpcMemHandle_t))
+            throw std::invalid_argument("pp_runner_pair_connect: handle blob size mismatch");
+        uint64_t hdr[4];
+        std::memcpy(hdr, blob, 32);
+        if (hdr[0] != kPairMagic || hdr[1] != uint64_t(1 - role_) || hdr[2] != n_ || hdr[3] != stride_)
+            throw std::invalid_argument("pp_runner_pair_connect: blob is not the partner's (role " +
+                                        std::to_string(1 - role_) + ", same band shape) handle");
+        if (peer_) throw std::invalid_argument("pp_runner_pair_connect: already connected");
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, blob + 32, sizeof(h));
+        DeviceGuard g(dev_);
+        CUDA_CHECK(cudaIpcOpenMemHandle(&peer_, h, cudaIpcMemLazyEnablePeerAccess));
+    }
+    const float* exchange(cudaStream_t s, const float* mine) override {
+        if (!peer_) throw std::runtime_error("CFG pair link not connected (pp_runner_pair_connect)");
+        DeviceGuard g(dev_);
+        const uint32_t k = ++seq_;
+        const size_t off = (k & 1) * stride_;
+        CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(peer_) + off, mine, n_ * 4, cudaMemcpyDeviceToDevice, s));
+        CUresult r = write_(reinterpret_cast<CUstream>(s), flag(peer_), k, CU_STREAM_WRITE_VALUE_DEFAULT);
+        if (r != CUDA_SUCCESS) throw CudaError("cuStreamWriteValue32 failed (" + std::to_string(int(r)) + ")");
+        r = wait_(reinterpret_cast<CUstream>(s), flag(buf_), k, CU_STREAM_WAIT_VALUE_GEQ);
+        if (r != CUDA_SUCCESS) throw CudaError("cuStreamWaitValue32 failed (" + std::to_string(int(r)) + ")");
+        return reinterpret_cast<const float*>(static_cast<char*>(buf_) + off);
+    }
+    bool capturable() const override { return false; }
+
+private:
+    CUdeviceptr flag(void* base) const {
+        return reinterpret_cast<CUdeviceptr>(static_cast<char*>(base) + 2 * stride_);
+    }
+    int dev_, role_;
+    size_t n_, stride_ = 0;
+    void* buf_ = nullptr;
+    void* peer_ = nullptr;
+    uint32_t seq_ = 0;
+    WaitValueFn wait_ = nullptr;
+    WriteValueFn write_ = nullptr;
+};
+
 }  // namespace
+
+std::vector<uint8_t> PairLink::export_blob() const {
+    throw std::invalid_argument("pp_runner_pair_export: the CFG pair link does not use CUDA IPC");
+}
+void PairLink::connect(const uint8_t*, size_t) {
+    throw std::invalid_argument("pp_runner_pair_connect: the CFG pair link does not use CUDA IPC");
+}
+
+std::unique_ptr<PairLink> make_nccl_pair(int dev, int role, const std::vector<uint8_t>& id, size_t n) {
+    return std::make_unique<NcclPair>(dev, role, id, n);
+}
+
+std::unique_ptr<PairLink> make_ipc_pair(int dev, int role, size_t n) {
+    return std::make_unique<IpcPair>(dev, role, n);
+}
 
 std::unique_ptr<Transport> make_inproc_transport(std::vector<Program*> bands) {
     return std::make_unique<InProcTransport>(std::move(bands));

@@ -197,7 +197,10 @@ class RunnerOptions:
     stress_seed: int = 0xC0FFEE
     cfg_scale: float = 0.0           # classifier-free guidance (beyond the reference API)
     uncond: object = None            # unconditional condition (cond_dim floats; None = zeros)
-    cfg_nccl_id: bytes | None = None # world > 1 + NCCL: the unconditional pass's unique id
+    cfg_nccl_id: bytes | None = None # world > 1 + NCCL: the unconditional pass's unique id;
+                                     # batch split + NCCL: the pair communicator's unique id
+    cfg_pair_role: int = -1          # CFG batch split: 0 conditional / 1 unconditional rank
+    cfg_pair_transport: str = "nccl" # batch split eps swap: "nccl" or "ipc"
 
 
 class PatchRunner:
@@ -239,6 +242,10 @@ class PatchRunner:
                 raise InvalidArgument(f"classifier-free guidance: uncond length {self._uncond.size} "
                                       f"!= condition length {cond.size}")
             o.uncond = self._uncond.ctypes.data
+        o.cfg_pair_role = int(opts.cfg_pair_role)
+        if opts.cfg_pair_transport not in N.TRANSPORTS:
+            raise InvalidArgument(f"unknown transport '{opts.cfg_pair_transport}'")
+        o.cfg_pair_transport = N.TRANSPORTS[opts.cfg_pair_transport]
         if opts.cfg_nccl_id is not None:
             self._cfg_id = C.create_string_buffer(bytes(opts.cfg_nccl_id), 128)
             o.cfg_nccl_id = C.cast(self._cfg_id, C.c_void_p)
@@ -271,6 +278,29 @@ class PatchRunner:
         allb = [None] * dist.get_world_size(group)
         dist.all_gather_object(allb, mine, group=group)
         self.ipc_connect(allb)
+
+    def pair_handles(self) -> bytes:
+        """CFG batch split over CUDA IPC: this rank's pair-link handle blob."""
+        n = C.c_long()
+        N.check(N.lib().pp_runner_pair_export(self._r, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        N.check(N.lib().pp_runner_pair_export(self._r, buf, n.value, C.byref(n)))
+        return buf.raw
+
+    def pair_connect(self, blob) -> None:
+        """Open the partner rank's pair-link receive buffers."""
+        blob = bytes(blob)
+        buf = C.create_string_buffer(blob, len(blob))
+        N.check(N.lib().pp_runner_pair_connect(self._r, buf, len(blob)))
+
+    def connect_pair(self, partner: int, group=None) -> None:
+        """all-gather the pair blobs over torch.distributed and connect to `partner` (its rank
+        in `group`)."""
+        import torch.distributed as dist
+        mine = self.pair_handles()
+        allb = [None] * dist.get_world_size(group)
+        dist.all_gather_object(allb, mine, group=group)
+        self.pair_connect(allb[partner])
 
     def close(self):
         if getattr(self, "_r", None) and N._lib is not None:

@@ -50,3 +50,35 @@ def test_ipc_transport_matches_inprocess(tmp_path, world):
     assert res["bad_blob"].startswith("InvalidArgument"), res["bad_blob"]
     assert res["bad_transport"].startswith("InvalidArgument"), res["bad_transport"]
     assert res["not_connected"].startswith("RuntimeFailure") and "not connected" in res["not_connected"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_cfg_batch_split(tmp_path, world):
+    # classifier-free guidance split across two groups of world/2 ranks (conditional /
+    # unconditional pass), eps swapped over a CUDA IPC pair link: both halves must equal the
+    # in-process CFG runner bit for bit
+    out = tmp_path / "cfg.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tests", "_cfg_split_worker.py"), str(out)]
+    p = subprocess.Popen(cmd, cwd=ROOT, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True,
+                         start_new_session=True)
+    try:
+        log, _ = p.communicate(timeout=300)
+    except subprocess.TimeoutExpired:
+        os.killpg(p.pid, signal.SIGKILL)
+        log, _ = p.communicate()
+        pytest.fail(f"CFG split world-{world} run timed out:\n" + log[-3000:])
+    assert p.returncode == 0, log[-5000:]
+    res = json.loads(out.read_text())
+    keys = [k for k in res if "/" in k]
+    assert len(keys) >= 3
+    for key in keys:
+        r = res[key]
+        assert r["finite"], key
+        assert r["x0_equal"] and r["x0_replay_equal"] and r["traj_equal"] and r["eps_equal"], (key, r)
+        assert r["guided_rel"] > 1e-3, (key, r)
+    assert res["not_connected"].startswith("RuntimeFailure") and "not connected" in res["not_connected"]
+    assert res["bad_blob"].startswith("InvalidArgument"), res["bad_blob"]
+    assert res["no_scale"].startswith("InvalidArgument"), res["no_scale"]
