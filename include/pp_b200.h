@@ -149,7 +149,7 @@ typedef struct {
     int profile;      /* record per-kernel CUDA events (pp_runner_profile) */
     int transport;    /* world > 1: PP_TRANSPORT_NCCL (nccl_id) or PP_TRANSPORT_IPC (CUDA IPC
                        * peer mappings + copy engines; pp_runner_ipc_export / _connect before
-                       * the first step; no CUDA-graph capture) */
+                       * the first step; graph-captured like NCCL) */
     int no_comm;      /* ablation only, the paper's "No Comm." row: every
                        * exchange (halo rows, K/V, GroupNorm statistics) is skipped and each
                        * band normalises with its own statistics; compute is identical, the
@@ -175,8 +175,8 @@ typedef struct {
      * band (conditioned on cond / uncond -- both ranks of a pair pass the same two) and swaps
      * eps bands with its partner after every pass; both then hold the same guided latent.
      * cfg_pair_transport: PP_TRANSPORT_NCCL (a two-rank communicator per pair, cfg_nccl_id =
-     * its ncclUniqueId; graph-captured) or PP_TRANSPORT_IPC (pp_runner_pair_export / _connect;
-     * eager).  One band per process.  Default -1: both passes in this runner (cfg_scale). */
+     * its ncclUniqueId) or PP_TRANSPORT_IPC (pp_runner_pair_export / _connect); both
+     * graph-captured.  One band per process.  Default -1: both passes in this runner (cfg_scale). */
     int cfg_pair_role;
     int cfg_pair_transport;
 } pp_runner_opts;

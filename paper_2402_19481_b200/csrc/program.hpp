@@ -225,6 +225,10 @@ public:
     virtual void wait(Program& b, int l, int par) = 0;
     // All-gather equal float chunks (rank order) on band b's compute stream (NCCL only).
     virtual void gather_floats(Program& b, const float* send, float* recv, size_t count) = 0;
+    // End of a runner call (sample / step), eager, on band b's compute stream: a transport
+    // whose flags carry per-call sequence numbers returns them to zero here, so every call --
+    // and every replay of a graph captured in one -- starts from the same flag state.
+    virtual void epoch_end(Program& b) { (void)b; }
 };
 
 std::unique_ptr<Transport> make_inproc_transport(std::vector<Program*> bands);
@@ -247,13 +251,14 @@ public:
     // order on s, valid until the next exchange call.
     virtual const float* exchange(cudaStream_t s, const float* mine) = 0;
     virtual bool capturable() const = 0;
+    virtual void epoch_end(cudaStream_t s) { (void)s; }   // as Transport::epoch_end
     virtual std::vector<uint8_t> export_blob() const;
     virtual void connect(const uint8_t* blob, size_t size);
 };
 // two-rank NCCL communicator (rank = role): ncclSend / ncclRecv on the stream, graph-capturable
 std::unique_ptr<PairLink> make_nccl_pair(int dev, int role, const std::vector<uint8_t>& id, size_t n);
 // CUDA IPC: the partner pushes into one of two parity receive buffers with the copy engine and
-// bumps a flag with a stream memory operation (host sequence numbers: not graph-capturable)
+// bumps a flag with a stream memory operation (per-call sequence numbers, reset by epoch_end)
 std::unique_ptr<PairLink> make_ipc_pair(int dev, int role, size_t n);
 
 }  // namespace pp

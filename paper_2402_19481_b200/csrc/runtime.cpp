@@ -1005,6 +1005,12 @@ void Runner::pair_combine() {
     launches_ += 1;
 }
 
+void Runner::end_epoch() {
+    if (o_.world > 1 && transport_) transport_->epoch_end(*bands_[0]);
+    if (cfg_ && cfg_->o_.world > 1 && cfg_->transport_) cfg_->transport_->epoch_end(*cfg_->bands_[0]);
+    if (pair_) pair_->epoch_end(bands_[0]->cs);
+}
+
 std::vector<uint8_t> Runner::pair_export() {
     if (!pair_) throw std::invalid_argument("pp_runner_pair_export: runner has no CFG pair link");
     return pair_->export_blob();
@@ -1645,6 +1651,7 @@ void Runner::step(int entry, const float* x, int t, int s, float* eps) {
         cfg_combine();
     }
     if (pair_) pair_combine();
+    end_epoch();
     store_eps(eps);
     count_macs(s, false);
     record_trace(s, e == STEP_REFERENCE ? 0 : displaced ? 2 : 1);
@@ -1700,9 +1707,9 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
     for (auto& b : bands_) all.push_back(b.get());
     if (cfg_)
         for (auto& b : cfg_->bands_) all.push_back(b.get());
-    // (the IPC transport's flag sequence numbers advance per exchange: not capturable)
+    // (the IPC transports' flag sequence numbers restart in every call, see end_epoch)
     const bool use_graph = !traj && !o_.profile && graphs_enabled_ && (o_.world > 1 || same_dev) &&
-                           !(o_.world > 1 && o_.transport == 1) && !(pair_ && !pair_->capturable());
+                           !(pair_ && !pair_->capturable());
     std::vector<double> key(ts, ts + n);
     for (int i = 0; i < n; ++i) key.push_back(abar_at(ts[i]));
     key.push_back(o_.mode);
@@ -1873,6 +1880,7 @@ void Runner::sample(const float* x_T, const int* ts, int n, const double* abar, 
         DeviceGuard g(bands_[k]->dev);
         CUDA_CHECK(cudaEventRecord(evs[k].second, bands_[k]->cs));
     }
+    end_epoch();
     // x0 download (band -> NCHW)
     if (o_.world > 1) {
         Program& b = *bands_[0];

@@ -170,6 +170,7 @@ private:
     void cfg_refresh_stem();               // the unconditional pass's stem input <- x_t
     std::unique_ptr<PairLink> pair_;       // CFG batch split: eps swap with the partner rank
     void pair_combine();                   // own eps <- guided eps from own + partner's band
+    void end_epoch();                      // transports' per-call flag reset (epoch_end)
     void stress_jitter(Program& b, int band);
     std::vector<int> gn_posted_;   // per layer: last step whose GN stats were posted
     uint64_t total_macs_ = 0;

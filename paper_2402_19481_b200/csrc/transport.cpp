@@ -18,7 +18,10 @@
 //    and no SM polls.  Per layer and per peer two monotone counters: READY (the peer's compute
 //    stream reached this exchange, so it finished reading the parity buffer about to be
 //    overwritten -- the same ordering the in-process transport takes from the receivers'
-//    `ready` events) and ARRIVED (the peer's rows for exchange k have landed).
+//    `ready` events) and ARRIVED (the peer's rows for exchange k have landed).  The counters
+//    restart at zero in every runner call: epoch_end (a two-phase flag barrier at the end of
+//    the call) resets them once no peer can still write them, so the flag values a call uses
+//    depend only on its exchange sequence and a captured CUDA graph replays them unchanged.
 // All replace CollectiveHub (proj/src/collectives.cpp:62-232).
 #include "program.hpp"
 #include "util.hpp"
@@ -265,6 +268,7 @@ public:
         flags_ = static_cast<uint32_t*>(b->alloc(n_flags_ * 4));
         wait_ = driver_fn<WaitValueFn>("cuStreamWaitValue32");
         write_ = driver_fn<WriteValueFn>("cuStreamWriteValue32");
+        CUDA_CHECK(cudaEventCreateWithFlags(&xs_done_, cudaEventDisableTiming));
         seq_.assign(L_, 0);
         last_.assign(L_, {0u, 0u});
         senders_.assign(L_, {});
@@ -275,6 +279,7 @@ public:
         cudaStreamSynchronize(b_->xs);
         cudaStreamSynchronize(b_->cs);
         for (void* p : opened_) cudaIpcCloseMemHandle(p);
+        cudaEventDestroy(xs_done_);
     }
 
     // the receive buffers a peer pushes into, in a fixed order all ranks agree on
@@ -409,6 +414,31 @@ public:
             if (p != rank_) wait_ge(b.cs, flag(GARRIVED, 0, p), k);
     }
 
+    // Phase 1: every rank's pushes of this call have completed (its comm stream joined into
+    // the compute stream before it signals), so nothing more lands in our flags or buffers;
+    // reset the per-layer counters.  Phase 2: every rank has reset, so the next call's first
+    // READY / ARRIVED writes cannot be clobbered by a late reset.  Data exchanged in this call
+    // and read by the next (displaced steps through the step API) has landed by phase 1, so
+    // the next call's first wait of each (layer, parity) is a no-op (last_ = 0).
+    void epoch_end(Program& b) override {
+        need_connected();
+        DeviceGuard g(b.dev);
+        CUDA_CHECK(cudaEventRecord(xs_done_, b.xs));
+        CUDA_CHECK(cudaStreamWaitEvent(b.cs, xs_done_, 0));
+        const uint32_t k = ++gseq_;
+        for (int p = 0; p < world_; ++p)
+            if (p != rank_) write(b.cs, peer_flag(p, GREADY, 0, rank_), k);
+        for (int p = 0; p < world_; ++p)
+            if (p != rank_) wait_ge(b.cs, flag(GREADY, 0, p), k);
+        CUDA_CHECK(cudaMemsetAsync(flags_, 0, size_t(2) * L_ * world_ * 4, b.cs));
+        for (int p = 0; p < world_; ++p)
+            if (p != rank_) write(b.cs, peer_flag(p, GARRIVED, 0, rank_), k);
+        for (int p = 0; p < world_; ++p)
+            if (p != rank_) wait_ge(b.cs, flag(GARRIVED, 0, p), k);
+        std::fill(seq_.begin(), seq_.end(), 0u);
+        for (auto& a : last_) a = {0u, 0u};
+    }
+
 private:
     enum { READY = 0, ARRIVED = 1, GREADY = 2, GARRIVED = 3 };
     size_t flag_index(int kind, int l, int p) const {
@@ -470,6 +500,7 @@ private:
     std::vector<std::vector<void*>> peers_;
     std::vector<void*> opened_;
     uint32_t gseq_ = 0;
+    cudaEvent_t xs_done_ = nullptr;
     bool connected_ = false;
 };
 
@@ -509,10 +540,12 @@ private:
 
 constexpr uint32_t kPairMagic = 0x50504350u;   // "PPCP"
 
-// One allocation: two parity receive buffers of n floats, then the ARRIVED flag.  Exchange k
-// lands in parity k & 1.  No READY handshake is needed: the partner's push k follows (in its
-// stream) its wait for our push k-1, which follows (in ours) our read of exchange k-2, the
-// last use of the same parity buffer.
+// One allocation: two parity receive buffers of n floats, then the flags {ARRIVED, BAR1, BAR2}.
+// Exchange k lands in parity k & 1.  No READY handshake is needed: the partner's push k
+// follows (in its stream) its wait for our push k-1, which follows (in ours) our read of
+// exchange k-2, the last use of the same parity buffer.  ARRIVED restarts at zero in every
+// runner call (epoch_end: the IpcTransport's two-phase barrier on BAR1 / BAR2), so the pair
+// link is graph-capturable.
 class IpcPair final : public PairLink {
 public:
     IpcPair(int dev, int role, size_t n) : dev_(dev), role_(role), n_(n) {
@@ -565,17 +598,36 @@ public:
         if (r != CUDA_SUCCESS) throw CudaError("cuStreamWaitValue32 failed (" + std::to_string(int(r)) + ")");
         return reinterpret_cast<const float*>(static_cast<char*>(buf_) + off);
     }
-    bool capturable() const override { return false; }
+    bool capturable() const override { return true; }
+    void epoch_end(cudaStream_t s) override {
+        if (!peer_) throw std::runtime_error("CFG pair link not connected (pp_runner_pair_connect)");
+        DeviceGuard g(dev_);
+        const uint32_t k = ++bseq_;
+        signal(s, flag(peer_, 1), k);
+        await(s, flag(buf_, 1), k);
+        CUDA_CHECK(cudaMemsetAsync(reinterpret_cast<void*>(flag(buf_)), 0, 4, s));
+        signal(s, flag(peer_, 2), k);
+        await(s, flag(buf_, 2), k);
+        seq_ = 0;
+    }
 
 private:
-    CUdeviceptr flag(void* base) const {
-        return reinterpret_cast<CUdeviceptr>(static_cast<char*>(base) + 2 * stride_);
+    CUdeviceptr flag(void* base, int i = 0) const {
+        return reinterpret_cast<CUdeviceptr>(static_cast<char*>(base) + 2 * stride_ + 4 * i);
+    }
+    void signal(cudaStream_t s, CUdeviceptr a, uint32_t v) {
+        const CUresult r = write_(reinterpret_cast<CUstream>(s), a, v, CU_STREAM_WRITE_VALUE_DEFAULT);
+        if (r != CUDA_SUCCESS) throw CudaError("cuStreamWriteValue32 failed (" + std::to_string(int(r)) + ")");
+    }
+    void await(cudaStream_t s, CUdeviceptr a, uint32_t v) {
+        const CUresult r = wait_(reinterpret_cast<CUstream>(s), a, v, CU_STREAM_WAIT_VALUE_GEQ);
+        if (r != CUDA_SUCCESS) throw CudaError("cuStreamWaitValue32 failed (" + std::to_string(int(r)) + ")");
     }
     int dev_, role_;
     size_t n_, stride_ = 0;
     void* buf_ = nullptr;
     void* peer_ = nullptr;
-    uint32_t seq_ = 0;
+    uint32_t seq_ = 0, bseq_ = 0;
     WaitValueFn wait_ = nullptr;
     WriteValueFn write_ = nullptr;
 };

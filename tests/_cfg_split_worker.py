@@ -50,10 +50,11 @@ def main():
             r.connect_ipc(group=groups[role])
         r.connect_pair(partner)
         x0, _ = r.sample(x_T, plan, abar)
-        x0b, traj = r.sample(x_T, plan, abar, trajectory=True)
+        x0b, traj = r.sample(x_T, plan, abar, trajectory=True)   # eager
+        x0c, _ = r.sample(x_T, plan, abar)   # graph replay
         eps = r.run_step(x_T, int(plan[0]), 0)
         got = [None] * world
-        dist.all_gather_object(got, (x0, x0b, traj, eps))
+        dist.all_gather_object(got, (x0, x0b, traj, eps, x0c))
         dist.barrier()   # nobody frees an exported buffer while a peer still maps it
         r.close()
         dist.barrier()
@@ -70,7 +71,8 @@ def main():
             plain.close()
             res[f"{mode}/w{warmup}/{dtype}"] = {
                 "x0_equal": all(np.array_equal(g[0], rx0) for g in got),
-                "x0_replay_equal": all(np.array_equal(g[1], rx0) for g in got),
+                "x0_replay_equal": all(np.array_equal(g[1], rx0) and np.array_equal(g[4], rx0)
+                                       for g in got),
                 "traj_equal": all(np.array_equal(g[2], rtraj) for g in got),
                 "eps_equal": all(np.array_equal(g[3], reps) for g in got),
                 "finite": bool(np.isfinite(rx0).all()),

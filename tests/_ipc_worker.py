@@ -35,8 +35,11 @@ def main():
                               dtype=dtype, world=world, rank=rank, device=0, transport="ipc")
             r.connect_ipc()
             x0, _ = r.sample(x_T, plan, abar)
-            x0b, traj = r.sample(x_T, plan, abar, trajectory=True)   # per-step gathers
+            x0b, traj = r.sample(x_T, plan, abar, trajectory=True)   # per-step gathers, eager
+            x0c, _ = r.sample(x_T, plan, abar)   # replay of the graph captured by the first call
             eps = r.run_step(x_T, int(plan[0]), 0)
+            # step API: displaced steps read what the previous call exchanged
+            seq = [r.run_step(x_T, int(plan[i]), i) for i in range(steps)]
             vol = r.volumes()
             dist.barrier()   # nobody frees an exported buffer while a peer still maps it
             r.close()
@@ -46,11 +49,14 @@ def main():
                                     warmup_steps=warmup, dtype=dtype, device=0)
                 rx0, _ = ref.sample(x_T, plan, abar)
                 _, rtraj = ref.sample(x_T, plan, abar, trajectory=True)
+                ref.sample(x_T, plan, abar)   # same call sequence: same byte volumes
                 reps = ref.run_step(x_T, int(plan[0]), 0)
+                rseq = [ref.run_step(x_T, int(plan[i]), i) for i in range(steps)]
                 key = f"{mode}/w{warmup}/{dtype}"
                 res[key] = {
                     "x0_equal": bool(np.array_equal(x0, rx0)),
-                    "x0_replay_equal": bool(np.array_equal(x0, x0b)),
+                    "x0_replay_equal": bool(np.array_equal(x0, x0b) and np.array_equal(x0, x0c)),
+                    "step_seq_equal": all(np.array_equal(a, b) for a, b in zip(seq, rseq)),
                     "traj_equal": bool(np.array_equal(traj, rtraj)),
                     "eps_equal": bool(np.array_equal(eps, reps)),
                     "x0_rel": float(np.linalg.norm(x0 - rx0) / np.linalg.norm(rx0)),

@@ -45,7 +45,8 @@ def test_ipc_transport_matches_inprocess(tmp_path, world):
         r = res[key]
         assert r["finite"], key
         assert r["x0_equal"] and r["traj_equal"] and r["eps_equal"], (key, r)
-        assert r["x0_replay_equal"], (key, r)
+        assert r["x0_replay_equal"], (key, r)   # graph capture, replay and eager agree
+        assert r["step_seq_equal"], (key, r)
         assert r["volumes_equal"], (key, r)
     assert res["bad_blob"].startswith("InvalidArgument"), res["bad_blob"]
     assert res["bad_transport"].startswith("InvalidArgument"), res["bad_transport"]
