@@ -258,7 +258,12 @@ void* Program::alloc(size_t bytes) {
     void* p = nullptr;
     bytes = std::max<size_t>(bytes, 16);
     CUDA_CHECK(cudaMalloc(&p, bytes));
-    CUDA_CHECK(cudaMemset(p, 0, bytes));
+    // zeroed before return: a legacy-stream cudaMemset may still be pending when the
+    // non-blocking band streams (which do not wait for the legacy stream) first write the
+    // buffer -- a buffer allocated after construction, the per-plan time-embedding table, was
+    // zeroed after its first writer ran
+    CUDA_CHECK(cudaMemsetAsync(p, 0, bytes, cs));
+    CUDA_CHECK(cudaStreamSynchronize(cs));
     allocs.push_back(p);
     return p;
 }
@@ -643,7 +648,9 @@ void Program::prepare_temb_plan(const int* ts, int n) {
         temb_embs = static_cast<float*>(alloc(embs.size() * 4));
         temb_embs_cap = embs.size();
     }
-    CUDA_CHECK(cudaMemcpy(temb_embs, embs.data(), embs.size() * 4, cudaMemcpyHostToDevice));
+    // on the compute stream: a legacy-stream cudaMemcpy may return before its DMA lands, and
+    // the projection kernel below runs on the non-blocking compute stream
+    CUDA_CHECK(cudaMemcpyAsync(temb_embs, embs.data(), embs.size() * 4, cudaMemcpyHostToDevice, cs));
     time_projection_plan(temb_dev, n_temb, temb_max_c, temb_embs, n, dim, temb_plan, temb_ldt, cs);
     CUDA_CHECK(cudaStreamSynchronize(cs));
     temb_plan_key = std::move(key);
@@ -966,6 +973,10 @@ Runner::Runner(const Model& m, const std::vector<float>& cond, int h, int w, con
             }
         }
     }
+    // every upload (legacy-stream copies of weights and tables) and every zero-fill has landed
+    // before the first step is enqueued on the non-blocking band streams, and before a peer
+    // can map this runner's buffers (IPC)
+    CUDA_CHECK(cudaDeviceSynchronize());
 }
 
 void Runner::cfg_combine() {
@@ -1055,11 +1066,16 @@ const DeviceWeights* Runner::weights_for(int dev) {
 }
 
 Runner::~Runner() {
+    // the captured loop first: it holds NCCL work of this runner's communicators (and of the
+    // unconditional pass's), and ncclCommDestroy waits for every graph that captured them
+    if (graph_exec_) {
+        for (auto& b : bands_) cudaStreamSynchronize(b->cs);
+        cudaGraphExecDestroy(graph_exec_);
+    }
+    for (auto ev : graph_events_) cudaEventDestroy(ev);
     cfg_.reset();
     for (auto ev : cfg_ev_) cudaEventDestroy(ev);
     pair_.reset();
-    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
-    for (auto ev : graph_events_) cudaEventDestroy(ev);
     transport_.reset();   // uses the bands' streams and buffers
     bands_.clear();
     naive_rows_.clear();

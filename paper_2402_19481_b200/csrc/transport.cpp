@@ -146,7 +146,9 @@ private:
         }
         CopyChunk* dev = nullptr;
         CUDA_CHECK(cudaMalloc(&dev, std::max<size_t>(ch.size(), 1) * sizeof(CopyChunk)));
-        CUDA_CHECK(cudaMemcpy(dev, ch.data(), ch.size() * sizeof(CopyChunk), cudaMemcpyHostToDevice));
+        // ordered before the copy kernels on the comm stream (a legacy-stream copy is not)
+        CUDA_CHECK(cudaMemcpyAsync(dev, ch.data(), ch.size() * sizeof(CopyChunk), cudaMemcpyHostToDevice,
+                                   bands_[0]->xs));
         return tables_.emplace(key, Table{dev, int(ch.size())}).first->second;
     }
 

@@ -80,7 +80,8 @@ class Model:
         return cls(h, cfg)
 
     def __del__(self):
-        if getattr(self, "_h", None) and N._lib is not None:
+        # (module globals may already be None at interpreter shutdown)
+        if getattr(self, "_h", None) and N is not None and N._lib is not None:
             N._lib.pp_model_destroy(self._h)
             self._h = None
 
@@ -303,7 +304,7 @@ class PatchRunner:
         self.pair_connect(allb[partner])
 
     def close(self):
-        if getattr(self, "_r", None) and N._lib is not None:
+        if getattr(self, "_r", None) and N is not None and N._lib is not None:
             N._lib.pp_runner_destroy(self._r)
             self._r = None
 

@@ -2,12 +2,19 @@
 two process groups (beyond the reference API).  Ranks [0, G) run the conditional
 pass of bands 0..G-1, ranks [G, 2G) the unconditional pass of the same bands; inside a group the
 bands exchange over the copy-engine (CUDA IPC) transport, and rank r swaps eps bands with rank
-r +- G over a CUDA IPC pair link.  All processes share cuda:0 (one GPU per box).  Rank 0
+r +- G over a CUDA IPC pair link (argv[2] == "nccl": NCCL band transport and a two-rank NCCL
+pair communicator instead).  All processes share cuda:0 (one GPU per box).  Rank 0
 repeats the run with one in-process CFG runner (both passes, G bands in this process) and
 writes the comparison to argv[1]: the split must be bitwise identical to it, on both halves."""
 import json
 import os
 import sys
+
+TRANSPORT = sys.argv[2] if len(sys.argv) > 2 else "ipc"
+if TRANSPORT == "nccl":   # ranks sharing the one GPU: see _ipc_worker.py
+    os.environ["NCCL_HOSTID"] = "pp-test-host-" + os.environ.get("RANK", "0")
+    os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
+    os.environ.setdefault("NCCL_IB_DISABLE", "1")
 
 import numpy as np
 import torch
@@ -18,6 +25,8 @@ from paper_2402_19481_b200 import patchsim as P  # noqa: E402
 
 
 def main():
+    import faulthandler
+    faulthandler.dump_traceback_later(240, exit=True)   # a hang reports where it is, then exits
     out_path = sys.argv[1]
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
@@ -42,13 +51,21 @@ def main():
         cases.append(("reference", 0, "bf16"))
     for mode, warmup, dtype in cases:
         kw = dict(mode=mode, n_devices=G, warmup_steps=warmup, dtype=dtype, device=0,
-                  cfg_scale=scale, uncond=uncond, cfg_pair_role=role, cfg_pair_transport="ipc")
+                  cfg_scale=scale, uncond=uncond, cfg_pair_role=role, cfg_pair_transport=TRANSPORT)
         if G > 1:
-            kw.update(world=G, rank=band, transport="ipc")
+            kw.update(world=G, rank=band, transport=TRANSPORT)
+        if TRANSPORT == "nccl":
+            # one communicator per group (the bands) and one per pair (the eps swap)
+            ids = [[P.nccl_unique_id() for _ in range(2 + G)] if rank == 0 else None]
+            dist.broadcast_object_list(ids, 0)
+            kw["cfg_nccl_id"] = ids[0][2 + band]
+            if G > 1:
+                kw["nccl_id"] = ids[0][role]
         r = P.PatchRunner(model, cond, h, w, **kw)
-        if G > 1:
-            r.connect_ipc(group=groups[role])
-        r.connect_pair(partner)
+        if TRANSPORT == "ipc":
+            if G > 1:
+                r.connect_ipc(group=groups[role])
+            r.connect_pair(partner)
         x0, _ = r.sample(x_T, plan, abar)
         x0b, traj = r.sample(x_T, plan, abar, trajectory=True)   # eager
         x0c, _ = r.sample(x_T, plan, abar)   # graph replay
@@ -80,6 +97,12 @@ def main():
                 "guided_rel": float(np.linalg.norm(rx0 - px0) / np.linalg.norm(px0)),
             }
         dist.barrier()
+    if TRANSPORT != "ipc":
+        if rank == 0:
+            with open(out_path, "w") as f:
+                json.dump(res, f, indent=1)
+        dist.destroy_process_group()
+        return
     # misuse: a blob from the wrong rank (own role), a split without a scale
     r = P.PatchRunner(model, cond, h, w, mode="reference", device=0, cfg_scale=scale,
                       cfg_pair_role=role, cfg_pair_transport="ipc")

@@ -1,11 +1,21 @@
-"""Worker of tests/test_ipc_gpu.py: one rank of a world-2 run with the copy-engine (CUDA IPC)
-transport, both ranks on cuda:0 (the pool has one GPU per box; CUDA IPC maps a buffer of
-another process on the same device exactly as on a peer).  Rank 0 repeats the run in-process
+"""Worker of tests/test_ipc_gpu.py: one rank of a world-2 / world-4 run with the copy-engine
+(CUDA IPC) transport, or the NCCL transport when argv[2] == "nccl", all ranks on cuda:0 (the
+pool has one GPU per box; CUDA IPC maps a buffer of another process on the same device exactly
+as on a peer).  Rank 0 repeats the run in-process
 (world 1, two bands: the in-process transport, itself parity-tested against the oracle) and
 writes the comparison to argv[1]."""
 import json
 import os
 import sys
+
+TRANSPORT = sys.argv[2] if len(sys.argv) > 2 else "ipc"
+if TRANSPORT == "nccl":
+    # NCCL refuses two ranks of one host on one device ("Duplicate GPU"); a distinct
+    # NCCL_HOSTID per rank makes them look like separate hosts, so NCCL connects them over its
+    # socket transport (loopback): slow, but the NCCL transport's real code path runs
+    os.environ["NCCL_HOSTID"] = "pp-test-host-" + os.environ.get("RANK", "0")
+    os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
+    os.environ.setdefault("NCCL_IB_DISABLE", "1")
 
 import numpy as np
 import torch
@@ -16,6 +26,8 @@ from paper_2402_19481_b200 import patchsim as P  # noqa: E402
 
 
 def main():
+    import faulthandler
+    faulthandler.dump_traceback_later(240, exit=True)   # a hang reports where it is, then exits
     out_path = sys.argv[1]
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
@@ -31,9 +43,16 @@ def main():
     res = {}
     for mode, warmup in (("displaced", 1), ("sync-pp", 0), ("displaced", 0)):
         for dtype in ("bf16", "fp32"):
+            kw = {}
+            if TRANSPORT == "nccl":
+                ids = [P.nccl_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(ids, 0)
+                kw["nccl_id"] = ids[0]
             r = P.PatchRunner(model, cond, h, w, mode=mode, n_devices=world, warmup_steps=warmup,
-                              dtype=dtype, world=world, rank=rank, device=0, transport="ipc")
-            r.connect_ipc()
+                              dtype=dtype, world=world, rank=rank, device=0, transport=TRANSPORT,
+                              **kw)
+            if TRANSPORT == "ipc":
+                r.connect_ipc()
             x0, _ = r.sample(x_T, plan, abar)
             x0b, traj = r.sample(x_T, plan, abar, trajectory=True)   # per-step gathers, eager
             x0c, _ = r.sample(x_T, plan, abar)   # replay of the graph captured by the first call
@@ -65,6 +84,12 @@ def main():
                 }
                 ref.close()
             dist.barrier()
+    if TRANSPORT != "ipc":
+        if rank == 0:
+            with open(out_path, "w") as f:
+                json.dump(res, f, indent=1)
+        dist.destroy_process_group()
+        return
     # bad blob: wrong rank order is rejected with the reference's error class
     r = P.PatchRunner(model, cond, h, w, mode="displaced", n_devices=world, warmup_steps=1,
                       world=world, rank=rank, device=0, transport="ipc")
