@@ -375,6 +375,13 @@ def main():
     world, rank, local = dist_env()
     if world == 1 and args.gpus > 1:
         return relaunch_under_torchrun(args)
+    if world > 1 and os.environ.get("PP_BENCH_SHARED_GPU") == "1":
+        # validation of the N-rank path on a one-GPU box (never a reported number): every rank
+        # on cuda:0, each under its own NCCL_HOSTID so NCCL accepts two ranks on one device
+        local = 0
+        os.environ["NCCL_HOSTID"] = f"pp-bench-host-{rank}"
+        os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
+        os.environ.setdefault("NCCL_IB_DISABLE", "1")
     import torch
     torch.cuda.set_device(local)
     dist = None
@@ -384,11 +391,15 @@ def main():
     from paper_2402_19481_b200 import patchsim as P
 
     n = world if world > 1 else max(1, args.bands)
-    nccl_id = None
-    if world > 1 and args.transport == "nccl":
+
+    def fresh_nccl_id():
+        # one ncclUniqueId per communicator: every runner (and its unconditional pass) builds
+        # its own, and an id cannot be reused for a second ncclCommInitRank
+        if world == 1 or args.transport != "nccl":
+            return None
         obj = [P.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        return obj[0]
 
     model = P.build_model(P.ModelConfig(*SDXL), SEEDS[0])
     cond = P.random_condition(2048, SEEDS[2])
@@ -402,7 +413,7 @@ def main():
         nb = n if bands is None else bands
         r = P.PatchRunner(model, cond, h, w, mode=args.mode if nb > 1 else "displaced",
                           n_devices=nb, warmup_steps=args.warmup_steps, dtype=dtype,
-                          world=world, rank=rank, nccl_id=nccl_id, device=local,
+                          world=world, rank=rank, nccl_id=fresh_nccl_id(), device=local,
                           transport=args.transport, no_comm=no_comm)
         if world > 1 and args.transport == "ipc":
             r.connect_ipc()
