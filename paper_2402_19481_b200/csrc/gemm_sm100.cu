@@ -37,8 +37,9 @@ constexpr int kTileM = 128;
 constexpr int kBlockBytes = 128;   // K block = 128 bytes of each operand row
 constexpr int kTmemCols = 512;     // 2 accumulators x 256 columns
 constexpr int kSmemMax = 232448;
-// Kernel debug flags (GemmArgs::debug: 1 no MMA, 2 no TMA, 4 no epilogue, 1024 one K block)
-// exist for the micro-benchmarks only and are compiled out of the shipped library.
+// Kernel debug flags (GemmArgs::debug: 1 no MMA, 2 no TMA, 4 no epilogue, 1024 one K block; the
+// GroupNorm-statistics epilogue: 8 no column sums, 16 no per-tile section, 32 no fold, 64 relaxed
+// ticket) exist for the micro-benchmarks only and are compiled out of the shipped library.
 #ifdef PP_GEMM_DEBUG
 constexpr bool kGemmDebug = true;
 #else
@@ -286,7 +287,7 @@ __device__ __forceinline__ void finish_chunk(const GemmArgs& a, float* v, const 
             }
         }
     }
-    if (a.gn_groups) {
+    if (a.gn_groups && !(kGemmDebug && (a.debug & 8))) {
         // Column sums over the warp's 32 rows (invalid rows contribute 0) by a butterfly
         // transpose-reduce: each xor step halves the columns a lane keeps, so 16 columns
         // cost 16+8+4+2+1 shuffles per quantity instead of 16*5.  Lane l ends up with the
@@ -979,7 +980,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::bulk_wait_read();
                 }
             }
-            if (a.gn_groups) {
+            if (a.gn_groups && !(dbg & 16)) {
                 epi_bar();
                 const int cpg = a.gn_cpg;
                 const int g0 = nbase / cpg;
@@ -1015,11 +1016,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (et == 0) {
                     // release: cumulative over the partials stored before the barrier;
                     // acquire: the folding CTA sees every other tile's partials
-                    st.flags[2] = ptx::atom_add_acq_rel_gpu(a.gn_ticket + 1 + tc.nt, 1u) ==
+                    st.flags[2] = ((dbg & 64) ? atomicAdd(a.gn_ticket + 1 + tc.nt, 1u)
+                                              : ptx::atom_add_acq_rel_gpu(a.gn_ticket + 1 + tc.nt, 1u)) ==
                                   unsigned(m_tiles - 1);
                 }
                 epi_bar();
-                if (st.flags[2]) {
+                if (st.flags[2] && !(dbg & 32)) {
                     // P threads per group each sum a fixed residue class of M tiles (16 loads
                     // in flight), the P partials are added in order -> deterministic
                     const int G = a.gn_groups;

@@ -179,9 +179,11 @@ __device__ __forceinline__ uint32_t mapa(uint32_t local, uint32_t rank) {
     return r;
 }
 // Arrive on an mbarrier given by its shared::cluster address (possibly in the peer CTA).
+// Default .release.cta semantics: orders this thread's prior shared-memory / TMEM work (after
+// tcgen05.fence::before_thread_sync) without the gpu-scope MEMBAR that .release.cluster
+// compiles to (which waits for the thread's outstanding global stores: the epilogue's).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-                 : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
 // CTA-pair TMA: the box lands in the executing CTA's smem at `dst`, and its bytes are
