@@ -976,8 +976,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::tma_store_3d(&tmD, smem, nbase, tc.tx * a.w_box, tc.ty * a.rows_box);
                     else
                         ptx::tma_store_2d(&tmD, smem, nbase, tc.ty * kTileM);
-                    ptx::bulk_commit();
-                    ptx::bulk_wait_read();
+                    ptx::bulk_commit();   // read completion awaited before the CTA exits
                 }
             }
             if (a.gn_groups && !(dbg & 16)) {
@@ -1013,7 +1012,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 epi_bar();
                 // the last M tile of this N tile folds the N tile's groups (the N tiles fold
                 // disjoint groups in parallel); counter gn_ticket[1 + nt]
-                if (et == 0) {
+                // (a thread other than the one that issued the last tile's TMA store: its
+                // release fence would also wait for that store)
+                if (et == kEpiThreads - 1) {
                     // release: cumulative over the partials stored before the barrier;
                     // acquire: the folding CTA sees every other tile's partials
                     st.flags[2] = ((dbg & 64) ? atomicAdd(a.gn_ticket + 1 + tc.nt, 1u)
@@ -1063,6 +1064,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
+        // the last tile's TMA store must have read its staging smem before the CTA exits (not
+        // earlier: the GroupNorm section of that tile does not wait for it)
+        if (et == 0 && a.tma_store) ptx::bulk_wait_read();
     }
 
     ptx::tc_fence_before();
