@@ -1,6 +1,6 @@
 """Digest ncu --page raw --csv captures into one line per kernel launch.
 
-usage: python scripts/ncu_digest.py gpurun_out/r02d_*.raw.csv
+usage: python scripts/ncu_digest.py gpurun_out/r02g_*.raw.csv
 Columns: duration, DRAM bytes read+write, L2->SM (lts__t_bytes), tensor-pipe active % of
 elapsed, SM throughput %, DRAM throughput %, issued IPC.
 """
